@@ -1,0 +1,216 @@
+"""CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper around oracle/liboracle.so (plain C, fp64, -ffp-contract=off;
+see oracle.h / oracle.c for the paper citations).  Only tests/,
+__graft_entry__.smoke() and bench.py's CPU-baseline / --impl reference legs
+may import this package.  It shares no code with paper_2107_01243_b200.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+_lib = None
+
+_D = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_I = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C, no FMA contraction)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call([
+            "gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
+            "-Wall", "-o", _SO, _SRC, "-lm"])
+    return _SO
+
+
+class OMesh(C.Structure):
+    _fields_ = [("ex", C.c_int32), ("ey", C.c_int32), ("ez", C.c_int32),
+                ("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double),
+                ("y1", C.c_double), ("z0", C.c_double), ("z1", C.c_double),
+                ("periodic", C.c_int32 * 3), ("deform", C.c_int32),
+                ("deform_amp", C.c_double)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_SO)
+        L.oracle_legendre.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]
+        L.oracle_gll.argtypes = [C.c_int, _D, _D]
+        L.oracle_deriv.argtypes = [C.c_int, _D, _D]
+        L.oracle_ax_raw.argtypes = [C.c_int64, C.c_int, _D, _D, _D, _D]
+        L.oracle_diag_raw.argtypes = [C.c_int64, C.c_int, _D, _D, _D]
+        L.oracle_setup.argtypes = [C.POINTER(OMesh), C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_free.argtypes = [C.c_void_p]
+        L.oracle_free.restype = None
+        L.oracle_sizes.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 3
+        L.oracle_get.argtypes = [C.c_void_p, C.c_int, _D]
+        L.oracle_get_int.argtypes = [C.c_void_p, C.c_int, _I]
+        L.oracle_ax.argtypes = [C.c_void_p, _D, _D]
+        L.oracle_gs.argtypes = [C.c_void_p, _D]
+        L.oracle_mask_apply.argtypes = [C.c_void_p, _D]
+        L.oracle_apply.argtypes = [C.c_void_p, _D, _D]
+        L.oracle_rhs.argtypes = [C.c_void_p, _D, _D]
+        L.oracle_dot_c.argtypes = [C.c_void_p, _D, _D]
+        L.oracle_dot_c.restype = C.c_double
+        L.oracle_pcg.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int,
+                                 C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.c_void_p]
+        L.oracle_plan.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 3 + [C.c_void_p] * 3
+        L.oracle_shared.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64),
+                                    C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- 1-D rules
+def legendre(N: int, x: float):
+    L, dL = C.c_double(), C.c_double()
+    lib().oracle_legendre(N, x, C.byref(L), C.byref(dL))
+    return L.value, dL.value
+
+
+def gll(N: int):
+    xi, w = np.zeros(N + 1), np.zeros(N + 1)
+    assert lib().oracle_gll(N, xi, w) == 0
+    return xi, w
+
+
+def deriv(N: int, xi=None):
+    if xi is None:
+        xi, _ = gll(N)
+    D = np.zeros((N + 1) * (N + 1))
+    assert lib().oracle_deriv(N, _f64(xi), D) == 0
+    return D.reshape(N + 1, N + 1)
+
+
+def ax_raw(E: int, N: int, D, G, u):
+    w = np.zeros(E * (N + 1) ** 3)
+    assert lib().oracle_ax_raw(E, N, _f64(D).ravel(), _f64(G).ravel(), _f64(u).ravel(), w) == 0
+    return w
+
+
+def diag_raw(E: int, N: int, D, G):
+    d = np.zeros(E * (N + 1) ** 3)
+    assert lib().oracle_diag_raw(E, N, _f64(D).ravel(), _f64(G).ravel(), d) == 0
+    return d
+
+
+# ---------------------------------------------------------------- context
+class OracleError(RuntimeError):
+    pass
+
+
+_FIELDS = {"xi": 0, "w": 1, "D": 2, "X": 3, "Y": 4, "Z": 5, "G": 6, "B": 7, "dinv": 8, "c": 9}
+_INTS = {"gid": 0, "mult": 1, "mask": 2, "rank": 3}
+
+
+class Oracle:
+    """Mesh + GLL space + geometry + numbering + gs lists, all on the host."""
+
+    def __init__(self, spec, N: int, nranks: int = 1):
+        m = OMesh(spec.ex, spec.ey, spec.ez, spec.x0, spec.x1, spec.y0, spec.y1,
+                  spec.z0, spec.z1, (C.c_int32 * 3)(*spec.periodic), spec.deform,
+                  spec.deform_amp)
+        h = C.c_void_p()
+        st = lib().oracle_setup(C.byref(m), N, nranks, C.byref(h))
+        if st != 0:
+            raise OracleError(f"oracle_setup failed with status {st}")
+        self._h = h
+        self.spec, self.N, self.n, self.nranks = spec, N, N + 1, nranks
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        lib().oracle_sizes(h, C.byref(a), C.byref(b), C.byref(c))
+        self.nslots, self.E, self.nglob = a.value, b.value, c.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.oracle_free(h)
+            self._h = None
+
+    def get(self, name: str) -> np.ndarray:
+        n = self.n
+        size = {"xi": n, "w": n, "D": n * n, "G": 6 * self.nslots}.get(name, self.nslots)
+        out = np.zeros(size)
+        assert lib().oracle_get(self._h, _FIELDS[name], out) == 0
+        if name == "D":
+            out = out.reshape(n, n)
+        return out
+
+    def get_int(self, name: str) -> np.ndarray:
+        out = np.zeros(self.nslots, dtype=np.int64)
+        assert lib().oracle_get_int(self._h, _INTS[name], out) == 0
+        return out
+
+    def ax(self, u):
+        w = np.zeros(self.nslots)
+        assert lib().oracle_ax(self._h, _f64(u), w) == 0
+        return w
+
+    def gs(self, u):
+        v = np.array(u, dtype=np.float64, copy=True)
+        assert lib().oracle_gs(self._h, v) == 0
+        return v
+
+    def mask_apply(self, u):
+        v = np.array(u, dtype=np.float64, copy=True)
+        lib().oracle_mask_apply(self._h, v)
+        return v
+
+    def apply(self, u):
+        w = np.zeros(self.nslots)
+        assert lib().oracle_apply(self._h, _f64(u), w) == 0
+        return w
+
+    def rhs(self, f):
+        b = np.zeros(self.nslots)
+        assert lib().oracle_rhs(self._h, _f64(f), b) == 0
+        return b
+
+    def dot_c(self, a, b) -> float:
+        return lib().oracle_dot_c(self._h, _f64(a), _f64(b))
+
+    def pcg(self, b, tol: float, maxit: int):
+        x = np.zeros(self.nslots)
+        it, rf, rt = C.c_int(), C.c_double(), C.c_double()
+        hist = np.zeros(maxit + 1)
+        st = lib().oracle_pcg(self._h, _f64(b), x, tol, maxit, C.byref(it), C.byref(rf),
+                              C.byref(rt), hist.ctypes.data_as(C.c_void_p))
+        if st < 0:
+            raise OracleError(f"oracle_pcg failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
+                "status": st, "hist": hist[: it.value + 1]}
+
+    def plan(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        lib().oracle_plan(self._h, C.byref(a), C.byref(b), C.byref(c), None, None, None)
+        pairs = np.zeros(2 * a.value, dtype=np.int64)
+        off = np.zeros(b.value + 1, dtype=np.int64)
+        slots = np.zeros(c.value, dtype=np.int64)
+        assert lib().oracle_plan(self._h, C.byref(a), C.byref(b), C.byref(c),
+                                 pairs.ctypes.data_as(C.c_void_p),
+                                 off.ctypes.data_as(C.c_void_p),
+                                 slots.ctypes.data_as(C.c_void_p)) == 0
+        return pairs.reshape(-1, 2), off, slots
+
+    def shared(self, r: int, q: int) -> np.ndarray:
+        cnt = C.c_int64()
+        assert lib().oracle_shared(self._h, r, q, C.byref(cnt), None) == 0
+        g = np.zeros(cnt.value, dtype=np.int64)
+        assert lib().oracle_shared(self._h, r, q, C.byref(cnt),
+                                   g.ctypes.data_as(C.c_void_p)) == 0
+        return g

@@ -1,0 +1,661 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * A deliberately plain CPU implementation of what the hot path computes,
+ * written from the paper in its order and notation.  fp64 throughout,
+ * compiled with -O2 -ffp-contract=off (no FMA contraction).  No blocking,
+ * fusion or reordering beyond what each definition states.
+ *
+ *   P:L93-97   Eq. 7   GLL points xi_i, Legendre polynomials L_N, cardinal basis l_i
+ *   P:L97-99   Eq. 8   tensor-product nodal basis u_ijk
+ *   P:L101-105 Eq. 9   a(u,v) = sum_e v^T D^T G^e D u  (A^e = D^T G^e D)
+ *   P:L107-111 Eq. 10  w_L = Q Q^T A_L u_L, Q^T Boolean gather, Q scatter
+ *   P:L204-229 Alg. 1  gather-scatter split by processing element
+ *   P:L257     sec. 4  Jacobi-preconditioned CG
+ *
+ * Readings where the paper is silent or garbled (Q1..Q22) are in DESIGN.md.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_PI 3.14159265358979323846
+
+struct oracle_ctx {
+  oracle_mesh m;
+  int N, n, nranks, fully_periodic;
+  int64_t E, n3, nslots, nglob;
+  double *xi, *w, *D;          /* GLL rule and derivative matrix */
+  double *X, *Y, *Z;           /* node coordinates per slot */
+  double *G, *B;               /* geometric factors [E][6][n3], mass [E][n3] */
+  double *dinv, *c;            /* Jacobi inverse diagonal, c = 1/mult */
+  int64_t *gid;                /* global number per slot */
+  int32_t *mult;               /* multiplicity per slot */
+  uint8_t *mask;               /* 1 = Dirichlet slot */
+  int32_t *rank_elem;          /* owning rank per element */
+  int64_t *gs_off, *gs_slot;   /* slots of each gid, ascending (CSR) */
+};
+
+/* ------------------------------------------------------------------ */
+/* Eq. 7: Legendre polynomial L_N and derivative by the three-term     */
+/* recurrence (k+1) L_{k+1} = (2k+1) x L_k - k L_{k-1} and             */
+/* L'_{k+1} = L'_{k-1} + (2k+1) L_k.                                   */
+int oracle_legendre(int N, double x, double* L, double* dL) {
+  if (N < 0) return -1;
+  if (N == 0) { *L = 1.0; *dL = 0.0; return 0; }
+  double Lm = 1.0, Lc = x, dLm = 0.0, dLc = 1.0;
+  for (int k = 1; k < N; k++) {
+    double Lp = ((2.0 * k + 1.0) * x * Lc - k * Lm) / (k + 1.0);
+    double dLp = dLm + (2.0 * k + 1.0) * Lc;
+    Lm = Lc; Lc = Lp;
+    dLm = dLc; dLc = dLp;
+  }
+  *L = Lc; *dL = dLc;
+  return 0;
+}
+
+/* Eq. 7: GLL points are the roots of (1 - xi^2) L_N'(xi).  Interior roots
+   by Newton on L_N' from -cos(pi i/N) (reading Q1: seed, tolerance 1e-15,
+   50 iterations), L_N'' from Legendre's equation; symmetrised.
+   Weights w_i = 2 / (N (N+1) L_N(xi_i)^2). */
+int oracle_gll(int N, double* xi, double* w) {
+  if (N < 1) return -1;
+  xi[0] = -1.0;
+  xi[N] = 1.0;
+  for (int i = 1; i < N; i++) {
+    double x = -cos(ORACLE_PI * i / N);
+    for (int it = 0; it < 50; it++) {
+      double L, dL;
+      oracle_legendre(N, x, &L, &dL);
+      double d2L = (2.0 * x * dL - N * (N + 1.0) * L) / (1.0 - x * x);
+      double dx = dL / d2L;
+      x -= dx;
+      if (fabs(dx) < 1e-15) break;
+    }
+    xi[i] = x;
+  }
+  for (int i = 0; i <= N / 2; i++) {
+    double s = 0.5 * (xi[N - i] - xi[i]);
+    xi[i] = -s;
+    xi[N - i] = s;
+  }
+  if (N % 2 == 0) xi[N / 2] = 0.0;
+  for (int i = 0; i <= N; i++) {
+    double L, dL;
+    oracle_legendre(N, xi[i], &L, &dL);
+    w[i] = 2.0 / (N * (N + 1.0) * L * L);
+  }
+  return 0;
+}
+
+/* P:L105 "D the local derivatives of the operand at the GLL points":
+   D_ij = l_j'(xi_i) = L_N(xi_i) / (L_N(xi_j) (xi_i - xi_j)) for i != j,
+   D_ii = -sum_{j != i} D_ij (reading Q2, negative-sum diagonal). */
+int oracle_deriv(int N, const double* xi, double* D) {
+  if (N < 1) return -1;
+  int n = N + 1;
+  double* LN = (double*)malloc(sizeof(double) * n);
+  if (!LN) return -5;
+  for (int i = 0; i < n; i++) {
+    double dL;
+    oracle_legendre(N, xi[i], &LN[i], &dL);
+  }
+  for (int i = 0; i < n; i++) {
+    double s = 0.0;
+    for (int j = 0; j < n; j++) {
+      if (j == i) continue;
+      D[i * n + j] = LN[i] / (LN[j] * (xi[i] - xi[j]));
+      s += D[i * n + j];
+    }
+    D[i * n + i] = -s;
+  }
+  free(LN);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Eq. 9 per element, as plain loops:                                  */
+/*   ur = D_r u, us = D_s u, ut = D_t u                                 */
+/*   w_a = sum_b G_ab u_b           (G symmetric, 6 stored factors)     */
+/*   w   = D_r^T w_r + D_s^T w_s + D_t^T w_t                            */
+int oracle_ax_raw(int64_t E, int N, const double* D, const double* G,
+                  const double* u, double* w) {
+  if (E < 0 || N < 1) return -1;
+  const int n = N + 1;
+  const int64_t n3 = (int64_t)n * n * n;
+  int err = 0;
+#pragma omp parallel
+  {
+    double* ur = (double*)malloc(sizeof(double) * 3 * n3);
+    if (!ur) {
+#pragma omp atomic write
+      err = -5;
+    }
+#pragma omp for schedule(static)
+    for (int64_t e = 0; e < E; e++) {
+      if (!ur) continue;
+      double* us = ur + n3;
+      double* ut = us + n3;
+      const double* ue = u + e * n3;
+      const double* Ge = G + e * 6 * n3;
+      double* we = w + e * n3;
+      for (int k = 0; k < n; k++)
+        for (int j = 0; j < n; j++)
+          for (int i = 0; i < n; i++) {
+            int64_t p = i + n * j + n * n * k;
+            double r = 0.0, s = 0.0, t = 0.0;
+            for (int m = 0; m < n; m++) {
+              r += D[i * n + m] * ue[m + n * j + n * n * k];
+              s += D[j * n + m] * ue[i + n * m + n * n * k];
+              t += D[k * n + m] * ue[i + n * j + n * n * m];
+            }
+            const double grr = Ge[0 * n3 + p], gss = Ge[1 * n3 + p], gtt = Ge[2 * n3 + p];
+            const double grs = Ge[3 * n3 + p], grt = Ge[4 * n3 + p], gst = Ge[5 * n3 + p];
+            ur[p] = grr * r + grs * s + grt * t;
+            us[p] = grs * r + gss * s + gst * t;
+            ut[p] = grt * r + gst * s + gtt * t;
+          }
+      for (int k = 0; k < n; k++)
+        for (int j = 0; j < n; j++)
+          for (int i = 0; i < n; i++) {
+            double a = 0.0, b = 0.0, cc = 0.0;
+            for (int m = 0; m < n; m++) {
+              a += D[m * n + i] * ur[m + n * j + n * n * k];
+              b += D[m * n + j] * us[i + n * m + n * n * k];
+              cc += D[m * n + k] * ut[i + n * j + n * n * m];
+            }
+            we[i + n * j + n * n * k] = a + b + cc;
+          }
+    }
+    free(ur);
+  }
+  return err;
+}
+
+/* Diagonal of A^e = D^T G D at point (i,j,k) (reading Q14):
+   sum_l D_li^2 G_rr(ljk) + sum_l D_lj^2 G_ss(ilk) + sum_l D_lk^2 G_tt(ijl)
+   + 2 (G_rs D_ii D_jj + G_rt D_ii D_kk + G_st D_jj D_kk)(ijk). */
+int oracle_diag_raw(int64_t E, int N, const double* D, const double* G, double* d) {
+  if (E < 0 || N < 1) return -1;
+  const int n = N + 1;
+  const int64_t n3 = (int64_t)n * n * n;
+  for (int64_t e = 0; e < E; e++) {
+    const double* Ge = G + e * 6 * n3;
+    for (int k = 0; k < n; k++)
+      for (int j = 0; j < n; j++)
+        for (int i = 0; i < n; i++) {
+          int64_t p = i + n * j + n * n * k;
+          double s = 0.0;
+          for (int l = 0; l < n; l++)
+            s += D[l * n + i] * D[l * n + i] * Ge[0 * n3 + l + n * j + n * n * k];
+          for (int l = 0; l < n; l++)
+            s += D[l * n + j] * D[l * n + j] * Ge[1 * n3 + i + n * l + n * n * k];
+          for (int l = 0; l < n; l++)
+            s += D[l * n + k] * D[l * n + k] * Ge[2 * n3 + i + n * j + n * n * l];
+          s += 2.0 * (Ge[3 * n3 + p] * D[i * n + i] * D[j * n + j] +
+                      Ge[4 * n3 + p] * D[i * n + i] * D[k * n + k] +
+                      Ge[5 * n3 + p] * D[j * n + j] * D[k * n + k]);
+          d[e * n3 + p] = s;
+        }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* node coordinates (reading Q4): reference lattice, optional          */
+/* sinusoidal map after rescaling the box to (0, 2 pi)^3.               */
+static void node_xyz(const oracle_mesh* m, const double* xi, int64_t ex, int64_t ey,
+                     int64_t ez, int i, int j, int k, double* x, double* y, double* z) {
+  double hx = (m->x1 - m->x0) / m->ex;
+  double hy = (m->y1 - m->y0) / m->ey;
+  double hz = (m->z1 - m->z0) / m->ez;
+  double X = m->x0 + hx * (ex + 0.5 * (xi[i] + 1.0));
+  double Y = m->y0 + hy * (ey + 0.5 * (xi[j] + 1.0));
+  double Z = m->z0 + hz * (ez + 0.5 * (xi[k] + 1.0));
+  if (m->deform) {
+    double Xh = 2.0 * ORACLE_PI * (X - m->x0) / (m->x1 - m->x0);
+    double Yh = 2.0 * ORACLE_PI * (Y - m->y0) / (m->y1 - m->y0);
+    double Zh = 2.0 * ORACLE_PI * (Z - m->z0) / (m->z1 - m->z0);
+    double dlt = m->deform_amp * sin(Xh) * sin(Yh) * sin(Zh);
+    X += dlt * (m->x1 - m->x0) / (2.0 * ORACLE_PI);
+    Y += dlt * (m->y1 - m->y0) / (2.0 * ORACLE_PI);
+    Z += dlt * (m->z1 - m->z0) / (2.0 * ORACLE_PI);
+  }
+  *x = X; *y = Y; *z = Z;
+}
+
+/* P:L105 geometric factors (reading Q5): x_r etc. through D, J = det,
+   inverse metric by cofactors / J, G_ab = J w_i w_j w_k sum_m r_a,m r_b,m,
+   B = J w_i w_j w_k. */
+static int geometry(oracle_ctx* c) {
+  const int n = c->n;
+  const int64_t n3 = c->n3;
+  const double* D = c->D;
+  for (int64_t e = 0; e < c->E; e++) {
+    const double* xs[3] = {c->X + e * n3, c->Y + e * n3, c->Z + e * n3};
+    double* Ge = c->G + e * 6 * n3;
+    for (int k = 0; k < n; k++)
+      for (int j = 0; j < n; j++)
+        for (int i = 0; i < n; i++) {
+          int64_t p = i + n * j + n * n * k;
+          double M[3][3]; /* M[a][b] = d x_a / d r_b */
+          for (int a = 0; a < 3; a++) {
+            double dr = 0.0, ds = 0.0, dt = 0.0;
+            for (int q = 0; q < n; q++) {
+              dr += D[i * n + q] * xs[a][q + n * j + n * n * k];
+              ds += D[j * n + q] * xs[a][i + n * q + n * n * k];
+              dt += D[k * n + q] * xs[a][i + n * j + n * n * q];
+            }
+            M[a][0] = dr; M[a][1] = ds; M[a][2] = dt;
+          }
+          double J = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                     M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                     M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+          if (!(J > 0.0)) return -2;
+          double R[3][3]; /* R[b][a] = d r_b / d x_a */
+          R[0][0] = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) / J;
+          R[0][1] = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) / J;
+          R[0][2] = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) / J;
+          R[1][0] = (M[1][2] * M[2][0] - M[1][0] * M[2][2]) / J;
+          R[1][1] = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) / J;
+          R[1][2] = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) / J;
+          R[2][0] = (M[1][0] * M[2][1] - M[1][1] * M[2][0]) / J;
+          R[2][1] = (M[0][1] * M[2][0] - M[0][0] * M[2][1]) / J;
+          R[2][2] = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) / J;
+          double wq = c->w[i] * c->w[j] * c->w[k];
+          double Jw = J * wq;
+          const int ab[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};
+          for (int f = 0; f < 6; f++) {
+            int a = ab[f][0], b = ab[f][1];
+            double s = 0.0;
+            for (int q = 0; q < 3; q++) s += R[a][q] * R[b][q];
+            Ge[f * n3 + p] = Jw * s;
+          }
+          c->B[e * n3 + p] = Jw;
+        }
+  }
+  return 0;
+}
+
+/* P:L107 "Each degree of freedom ... is assigned a unique global number"
+   (reading Q6): lattice I = ex N + i (mod Ex N if periodic), likewise J, K;
+   gid = I + Nx (J + Ny K). Mask (reading Q8): lattice index at a
+   non-periodic box face. */
+static void numbering(oracle_ctx* c) {
+  const oracle_mesh* m = &c->m;
+  const int N = c->N, n = c->n;
+  int64_t Lx = (int64_t)m->ex * N, Ly = (int64_t)m->ey * N, Lz = (int64_t)m->ez * N;
+  int64_t Nx = Lx + (m->periodic[0] ? 0 : 1);
+  int64_t Ny = Ly + (m->periodic[1] ? 0 : 1);
+  int64_t Nz = Lz + (m->periodic[2] ? 0 : 1);
+  c->nglob = Nx * Ny * Nz;
+  for (int64_t e = 0; e < c->E; e++) {
+    int64_t ex = e % m->ex, ey = (e / m->ex) % m->ey, ez = e / ((int64_t)m->ex * m->ey);
+    for (int k = 0; k < n; k++)
+      for (int j = 0; j < n; j++)
+        for (int i = 0; i < n; i++) {
+          int64_t I = ex * N + i, J = ey * N + j, K = ez * N + k;
+          int msk = 0;
+          if (!m->periodic[0] && (I == 0 || I == Lx)) msk = 1;
+          if (!m->periodic[1] && (J == 0 || J == Ly)) msk = 1;
+          if (!m->periodic[2] && (K == 0 || K == Lz)) msk = 1;
+          if (m->periodic[0]) I %= Lx;
+          if (m->periodic[1]) J %= Ly;
+          if (m->periodic[2]) K %= Lz;
+          int64_t l = e * c->n3 + i + n * j + (int64_t)n * n * k;
+          c->gid[l] = I + Nx * (J + Ny * K);
+          c->mask[l] = (uint8_t)msk;
+        }
+  }
+}
+
+int oracle_setup(const oracle_mesh* m, int N, int nranks, oracle_ctx** out) {
+  *out = NULL;
+  if (!m || N < 1 || N > 11 || m->ex < 1 || m->ey < 1 || m->ez < 1) return -1;
+  for (int a = 0; a < 3; a++) {
+    int ea = a == 0 ? m->ex : (a == 1 ? m->ey : m->ez);
+    if (m->periodic[a] && ea < 2) return -1; /* reading Q7 */
+  }
+  if (!(m->x1 > m->x0) || !(m->y1 > m->y0) || !(m->z1 > m->z0)) return -1;
+  int64_t E = (int64_t)m->ex * m->ey * m->ez;
+  if (nranks < 1 || nranks > E) return -1;
+
+  oracle_ctx* c = (oracle_ctx*)calloc(1, sizeof(oracle_ctx));
+  if (!c) return -5;
+  c->m = *m;
+  c->N = N;
+  c->n = N + 1;
+  c->nranks = nranks;
+  c->E = E;
+  c->n3 = (int64_t)c->n * c->n * c->n;
+  c->nslots = E * c->n3;
+  c->fully_periodic = m->periodic[0] && m->periodic[1] && m->periodic[2];
+  int64_t ns = c->nslots;
+  c->xi = (double*)malloc(sizeof(double) * c->n);
+  c->w = (double*)malloc(sizeof(double) * c->n);
+  c->D = (double*)malloc(sizeof(double) * c->n * c->n);
+  c->X = (double*)malloc(sizeof(double) * ns);
+  c->Y = (double*)malloc(sizeof(double) * ns);
+  c->Z = (double*)malloc(sizeof(double) * ns);
+  c->G = (double*)malloc(sizeof(double) * 6 * ns);
+  c->B = (double*)malloc(sizeof(double) * ns);
+  c->dinv = (double*)malloc(sizeof(double) * ns);
+  c->c = (double*)malloc(sizeof(double) * ns);
+  c->gid = (int64_t*)malloc(sizeof(int64_t) * ns);
+  c->mult = (int32_t*)calloc(ns, sizeof(int32_t));
+  c->mask = (uint8_t*)malloc(ns);
+  c->rank_elem = (int32_t*)malloc(sizeof(int32_t) * E);
+  c->gs_slot = (int64_t*)malloc(sizeof(int64_t) * ns);
+  if (!c->xi || !c->w || !c->D || !c->X || !c->Y || !c->Z || !c->G || !c->B || !c->dinv ||
+      !c->c || !c->gid || !c->mult || !c->mask || !c->rank_elem || !c->gs_slot) {
+    oracle_free(c);
+    return -5;
+  }
+  oracle_gll(N, c->xi, c->w);
+  oracle_deriv(N, c->xi, c->D);
+
+  /* lexicographic element partition: rank r owns [r E / P, (r+1) E / P) */
+  for (int r = 0; r < nranks; r++) {
+    int64_t lo = (int64_t)r * E / nranks, hi = (int64_t)(r + 1) * E / nranks;
+    for (int64_t e = lo; e < hi; e++) c->rank_elem[e] = r;
+  }
+
+  for (int64_t e = 0; e < E; e++) {
+    int64_t ex = e % m->ex, ey = (e / m->ex) % m->ey, ez = e / ((int64_t)m->ex * m->ey);
+    for (int k = 0; k < c->n; k++)
+      for (int j = 0; j < c->n; j++)
+        for (int i = 0; i < c->n; i++) {
+          int64_t l = e * c->n3 + i + c->n * j + (int64_t)c->n * c->n * k;
+          node_xyz(m, c->xi, ex, ey, ez, i, j, k, &c->X[l], &c->Y[l], &c->Z[l]);
+        }
+  }
+  int st = geometry(c);
+  if (st) { oracle_free(c); return st; }
+  numbering(c);
+
+  /* slots of each gid in ascending slot order (counting sort) */
+  c->gs_off = (int64_t*)calloc(c->nglob + 1, sizeof(int64_t));
+  if (!c->gs_off) { oracle_free(c); return -5; }
+  for (int64_t l = 0; l < ns; l++) c->gs_off[c->gid[l] + 1]++;
+  for (int64_t g = 0; g < c->nglob; g++) c->gs_off[g + 1] += c->gs_off[g];
+  {
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * c->nglob);
+    if (!fill) { oracle_free(c); return -5; }
+    memcpy(fill, c->gs_off, sizeof(int64_t) * c->nglob);
+    for (int64_t l = 0; l < ns; l++) c->gs_slot[fill[c->gid[l]]++] = l;
+    free(fill);
+  }
+  for (int64_t l = 0; l < ns; l++) {
+    int64_t g = c->gid[l];
+    c->mult[l] = (int32_t)(c->gs_off[g + 1] - c->gs_off[g]);
+    c->c[l] = 1.0 / c->mult[l];
+  }
+
+  /* Jacobi: d = QQ^T diag(A_L), dinv = 0 on masked slots (reading Q14) */
+  oracle_diag_raw(E, N, c->D, c->G, c->dinv);
+  oracle_gs(c, c->dinv);
+  for (int64_t l = 0; l < ns; l++) c->dinv[l] = c->mask[l] ? 0.0 : 1.0 / c->dinv[l];
+  *out = c;
+  return 0;
+}
+
+void oracle_free(oracle_ctx* c) {
+  if (!c) return;
+  free(c->xi); free(c->w); free(c->D);
+  free(c->X); free(c->Y); free(c->Z);
+  free(c->G); free(c->B); free(c->dinv); free(c->c);
+  free(c->gid); free(c->mult); free(c->mask); free(c->rank_elem);
+  free(c->gs_off); free(c->gs_slot);
+  free(c);
+}
+
+int oracle_sizes(const oracle_ctx* c, int64_t* nslots, int64_t* E, int64_t* nglob) {
+  if (!c) return -1;
+  if (nslots) *nslots = c->nslots;
+  if (E) *E = c->E;
+  if (nglob) *nglob = c->nglob;
+  return 0;
+}
+
+int oracle_get(const oracle_ctx* c, int which, double* dst) {
+  if (!c || !dst) return -1;
+  int64_t ns = c->nslots;
+  switch (which) {
+    case 0: memcpy(dst, c->xi, sizeof(double) * c->n); break;
+    case 1: memcpy(dst, c->w, sizeof(double) * c->n); break;
+    case 2: memcpy(dst, c->D, sizeof(double) * c->n * c->n); break;
+    case 3: memcpy(dst, c->X, sizeof(double) * ns); break;
+    case 4: memcpy(dst, c->Y, sizeof(double) * ns); break;
+    case 5: memcpy(dst, c->Z, sizeof(double) * ns); break;
+    case 6: memcpy(dst, c->G, sizeof(double) * 6 * ns); break;
+    case 7: memcpy(dst, c->B, sizeof(double) * ns); break;
+    case 8: memcpy(dst, c->dinv, sizeof(double) * ns); break;
+    case 9: memcpy(dst, c->c, sizeof(double) * ns); break;
+    default: return -1;
+  }
+  return 0;
+}
+
+int oracle_get_int(const oracle_ctx* c, int which, int64_t* dst) {
+  if (!c || !dst) return -1;
+  for (int64_t l = 0; l < c->nslots; l++) {
+    switch (which) {
+      case 0: dst[l] = c->gid[l]; break;
+      case 1: dst[l] = c->mult[l]; break;
+      case 2: dst[l] = c->mask[l]; break;
+      case 3: dst[l] = c->rank_elem[l / c->n3]; break;
+      default: return -1;
+    }
+  }
+  return 0;
+}
+
+int oracle_ax(const oracle_ctx* c, const double* u, double* w) {
+  if (!c) return -1;
+  return oracle_ax_raw(c->E, c->N, c->D, c->G, u, w);
+}
+
+/* Eq. 10 + Alg. 1 (reading Q10): for each gid the slots are visited in
+   ascending slot order; each processing element first forms its partial sum
+   (Alg. 1 lines 6/8 "gather"), the partials are added in ascending rank
+   order, and the total is scattered to every slot (lines 9/18). Ranks own
+   contiguous element ranges, so ascending slots visit ranks in order. */
+int oracle_gs(const oracle_ctx* c, double* u) {
+  if (!c) return -1;
+  for (int64_t g = 0; g < c->nglob; g++) {
+    int64_t lo = c->gs_off[g], hi = c->gs_off[g + 1];
+    if (hi - lo < 2) continue;
+    int64_t s0 = c->gs_slot[lo];
+    int cur = c->rank_elem[s0 / c->n3];
+    double part = u[s0], total = 0.0;
+    int have_total = 0;
+    for (int64_t t = lo + 1; t < hi; t++) {
+      int64_t s = c->gs_slot[t];
+      int r = c->rank_elem[s / c->n3];
+      if (r == cur) {
+        part += u[s];
+      } else {
+        total = have_total ? total + part : part;
+        have_total = 1;
+        cur = r;
+        part = u[s];
+      }
+    }
+    total = have_total ? total + part : part;
+    for (int64_t t = lo; t < hi; t++) u[c->gs_slot[t]] = total;
+  }
+  return 0;
+}
+
+int oracle_mask_apply(const oracle_ctx* c, double* u) {
+  if (!c) return -1;
+  for (int64_t l = 0; l < c->nslots; l++)
+    if (c->mask[l]) u[l] = 0.0;
+  return 0;
+}
+
+/* P:L111 "w_L = QQ^T A_L u_L", then the Dirichlet mask (reading Q8). */
+int oracle_apply(const oracle_ctx* c, const double* u, double* w) {
+  int st = oracle_ax(c, u, w);
+  if (st) return st;
+  oracle_gs(c, w);
+  return oracle_mask_apply(c, w);
+}
+
+/* <a,b>_c = sum_l c_l a_l b_l, serial in slot order (c = 1/mult). */
+double oracle_dot_c(const oracle_ctx* c, const double* a, const double* b) {
+  double s = 0.0;
+  for (int64_t l = 0; l < c->nslots; l++) s += c->c[l] * a[l] * b[l];
+  return s;
+}
+
+/* Eq. 6 right-hand side with collocated quadrature (reading Q12):
+   b = mask(QQ^T (B .* f)); fully periodic: remove the unique-DOF mean
+   (reading Q13) so that b lies in range(A). */
+int oracle_rhs(const oracle_ctx* c, const double* f, double* b) {
+  if (!c) return -1;
+  for (int64_t l = 0; l < c->nslots; l++) b[l] = c->B[l] * f[l];
+  oracle_gs(c, b);
+  oracle_mask_apply(c, b);
+  if (c->fully_periodic) {
+    double sb = 0.0, sc = 0.0;
+    for (int64_t l = 0; l < c->nslots; l++) {
+      sb += c->c[l] * b[l];
+      sc += c->c[l];
+    }
+    double mean = sb / sc;
+    for (int64_t l = 0; l < c->nslots; l++) b[l] -= mean;
+  }
+  return 0;
+}
+
+/* P:L257 "preconditioned Conjugate Gradient (CG) ... with a block Jacobi
+   preconditioner", written step by step (readings Q14-Q17):
+   x0 = 0; r = b; z = M^-1 r; p = z; rho = <r,z>_c
+   for k = 1..maxit: w = A p; sigma = <p,w>_c; alpha = rho/sigma;
+     x += alpha p; r -= alpha w; gamma = <r,r>_c; stop if sqrt(gamma) <= tol;
+     z = M^-1 r; rho' = <r,z>_c; beta = rho'/rho; rho = rho'; p = z + beta p.
+   hist[k] = sqrt(gamma) after iteration k (hist[0] = ||b||_c). */
+int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+               int* iters, double* res_final, double* res_true, double* hist) {
+  if (!c || maxit < 0) return -1;
+  int64_t ns = c->nslots;
+  double* r = (double*)malloc(sizeof(double) * ns);
+  double* z = (double*)malloc(sizeof(double) * ns);
+  double* p = (double*)malloc(sizeof(double) * ns);
+  double* w = (double*)malloc(sizeof(double) * ns);
+  if (!r || !z || !p || !w) { free(r); free(z); free(p); free(w); return -5; }
+  int status = 1, k = 0;
+  for (int64_t l = 0; l < ns; l++) {
+    x[l] = 0.0;
+    r[l] = b[l];
+    z[l] = c->dinv[l] * r[l];
+    p[l] = z[l];
+  }
+  double rho = oracle_dot_c(c, r, z);
+  double gamma = oracle_dot_c(c, r, r);
+  if (hist) hist[0] = sqrt(gamma);
+  if (sqrt(gamma) <= tol) status = 0;
+  while (status == 1 && k < maxit) {
+    k++;
+    oracle_apply(c, p, w);
+    double sigma = oracle_dot_c(c, p, w);
+    if (!(sigma > 0.0)) { status = -6; break; }
+    double alpha = rho / sigma;
+    for (int64_t l = 0; l < ns; l++) {
+      x[l] += alpha * p[l];
+      r[l] -= alpha * w[l];
+    }
+    gamma = oracle_dot_c(c, r, r);
+    if (hist) hist[k] = sqrt(gamma);
+    if (sqrt(gamma) <= tol) { status = 0; break; }
+    for (int64_t l = 0; l < ns; l++) z[l] = c->dinv[l] * r[l];
+    double rho_new = oracle_dot_c(c, r, z);
+    double beta = rho_new / rho;
+    rho = rho_new;
+    for (int64_t l = 0; l < ns; l++) p[l] = z[l] + beta * p[l];
+  }
+  if (iters) *iters = k;
+  if (res_final) *res_final = sqrt(gamma);
+  if (res_true) {
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) w[l] = b[l] - w[l];
+    *res_true = sqrt(oracle_dot_c(c, w, w));
+  }
+  free(r); free(z); free(p); free(w);
+  return status;
+}
+
+/* ------------------------------------------------------------------ */
+/* canonical plan export (P:L231 sorted tuples + variable blocks)       */
+static int cmp_first(const void* a, const void* b) {
+  int64_t x = ((const int64_t*)a)[0], y = ((const int64_t*)b)[0];
+  return (x > y) - (x < y);
+}
+
+int oracle_plan(const oracle_ctx* c, int64_t* npairs, int64_t* nseg, int64_t* nsegslots,
+                int64_t* pairs, int64_t* seg_off, int64_t* seg_slot) {
+  if (!c) return -1;
+  int64_t np = 0, nsg = 0, nss = 0;
+  for (int64_t g = 0; g < c->nglob; g++) {
+    int64_t cnt = c->gs_off[g + 1] - c->gs_off[g];
+    if (cnt == 2) np++;
+    else if (cnt >= 3) { nsg++; nss += cnt; }
+  }
+  *npairs = np; *nseg = nsg; *nsegslots = nss;
+  if (!pairs || !seg_off || !seg_slot) return 0;
+  /* pairs: (l_a, l_b), sorted by l_a */
+  int64_t t = 0;
+  for (int64_t g = 0; g < c->nglob; g++) {
+    int64_t lo = c->gs_off[g];
+    if (c->gs_off[g + 1] - lo == 2) {
+      pairs[2 * t] = c->gs_slot[lo];
+      pairs[2 * t + 1] = c->gs_slot[lo + 1];
+      t++;
+    }
+  }
+  qsort(pairs, (size_t)np, 2 * sizeof(int64_t), cmp_first);
+  /* segments sorted by first slot: sort (first slot, gid) keys */
+  int64_t* key = (int64_t*)malloc(sizeof(int64_t) * 2 * (nsg ? nsg : 1));
+  if (!key) return -5;
+  t = 0;
+  for (int64_t g = 0; g < c->nglob; g++) {
+    int64_t lo = c->gs_off[g];
+    if (c->gs_off[g + 1] - lo >= 3) {
+      key[2 * t] = c->gs_slot[lo];
+      key[2 * t + 1] = g;
+      t++;
+    }
+  }
+  qsort(key, (size_t)nsg, 2 * sizeof(int64_t), cmp_first);
+  seg_off[0] = 0;
+  for (int64_t s = 0; s < nsg; s++) {
+    int64_t g = key[2 * s + 1];
+    int64_t lo = c->gs_off[g], hi = c->gs_off[g + 1];
+    for (int64_t q = lo; q < hi; q++) seg_slot[seg_off[s] + (q - lo)] = c->gs_slot[q];
+    seg_off[s + 1] = seg_off[s] + (hi - lo);
+  }
+  free(key);
+  return 0;
+}
+
+int oracle_shared(const oracle_ctx* c, int r, int q, int64_t* count, int64_t* gids) {
+  if (!c || r == q || r < 0 || q < 0 || r >= c->nranks || q >= c->nranks) return -1;
+  int64_t cnt = 0;
+  for (int64_t g = 0; g < c->nglob; g++) {
+    int hr = 0, hq = 0;
+    for (int64_t t = c->gs_off[g]; t < c->gs_off[g + 1]; t++) {
+      int rk = c->rank_elem[c->gs_slot[t] / c->n3];
+      if (rk == r) hr = 1;
+      if (rk == q) hq = 1;
+    }
+    if (hr && hq) {
+      if (gids) gids[cnt] = g;
+      cnt++;
+    }
+  }
+  *count = cnt;
+  return 0;
+}

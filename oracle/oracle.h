@@ -1,0 +1,80 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU reference for the matrix-free SEM
+ * pressure-Poisson hot path of Neko (arxiv 2107.01243).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library.  It shares no source with the CUDA product path
+ * (paper_2107_01243_b200/csrc, include/sem.h) and neither side includes the
+ * other.
+ *
+ * Citations: "P:L<n>" = /root/reference/PAPER.md line n; readings Q1..Q22 are
+ * listed in DESIGN.md section 3 (they follow SURVEY.md section 8(c)).
+ *
+ * Conventions (reading Q3, the paper leaves them free):
+ *   element  e = ex + Ex*(ey + Ey*ez)
+ *   slot     l = e*n^3 + i + n*j + n^2*k      (n = N+1, i along x fastest)
+ *   G        [E][6][n^3] in the order (rr, ss, tt, rs, rt, st)
+ *
+ * All functions return 0 on success, <0 on error:
+ *   -1 invalid argument, -2 non-positive Jacobian, -5 out of memory,
+ *   -6 CG breakdown (p^T A p <= 0); oracle_pcg returns 1 if not converged.
+ */
+#ifndef SEM_ORACLE_H
+#define SEM_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t ex, ey, ez;                 /* elements per axis */
+  double x0, x1, y0, y1, z0, z1;      /* box extents */
+  int32_t periodic[3];                /* 1 = periodic axis, 0 = homogeneous Dirichlet faces */
+  int32_t deform;                     /* 0 = Cartesian, 1 = sinusoidal map (reading Q4) */
+  double deform_amp;                  /* a in x_m = X_m + a sin X sin Y sin Z */
+} oracle_mesh;
+
+typedef struct oracle_ctx oracle_ctx;
+
+/* 1-D building blocks (Eq. 7) */
+int oracle_legendre(int N, double x, double* L, double* dL);
+int oracle_gll(int N, double* xi, double* w);
+int oracle_deriv(int N, const double* xi, double* D);        /* D[i*n+j] = l_j'(xi_i) */
+
+/* raw element kernels on caller arrays (used by the pins with random G) */
+int oracle_ax_raw(int64_t E, int N, const double* D, const double* G,
+                  const double* u, double* w);               /* Eq. 9, no gs, no mask */
+int oracle_diag_raw(int64_t E, int N, const double* D, const double* G,
+                    double* d);                               /* diag of A^e (reading Q14) */
+
+/* context: mesh + space + geometry + numbering + gs lists */
+int oracle_setup(const oracle_mesh* m, int N, int nranks, oracle_ctx** out);
+void oracle_free(oracle_ctx* c);
+int oracle_sizes(const oracle_ctx* c, int64_t* nslots, int64_t* E, int64_t* nglob);
+/* which: 0 xi, 1 w, 2 D, 3 X, 4 Y, 5 Z, 6 G, 7 B, 8 dinv, 9 c (=1/mult) */
+int oracle_get(const oracle_ctx* c, int which, double* dst);
+/* which: 0 gid, 1 mult, 2 mask, 3 rank of slot */
+int oracle_get_int(const oracle_ctx* c, int which, int64_t* dst);
+
+int oracle_ax(const oracle_ctx* c, const double* u, double* w);   /* w_L = A_L u_L */
+int oracle_gs(const oracle_ctx* c, double* u);                      /* u <- QQ^T u */
+int oracle_mask_apply(const oracle_ctx* c, double* u);
+int oracle_apply(const oracle_ctx* c, const double* u, double* w); /* mask(QQ^T A_L u) */
+int oracle_rhs(const oracle_ctx* c, const double* f, double* b);
+double oracle_dot_c(const oracle_ctx* c, const double* a, const double* b);
+int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+               int* iters, double* res_final, double* res_true, double* hist);
+
+/* canonical gs plan (reading Q11): pairs (l_a<l_b) sorted by l_a, segments
+   (>=3 slots, ascending) sorted by first slot. Call with NULL arrays to size. */
+int oracle_plan(const oracle_ctx* c, int64_t* npairs, int64_t* nseg, int64_t* nsegslots,
+                int64_t* pairs, int64_t* seg_off, int64_t* seg_slot);
+/* gids shared between ranks r and q (r != q), ascending; NULL list to size. */
+int oracle_shared(const oracle_ctx* c, int r, int q, int64_t* count, int64_t* gids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
