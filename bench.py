@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native SEM pressure-Poisson hot path.
+
+A "step" is one Jacobi-PCG iteration over the whole hot path:
+fused Ax+gs+mask with <p,Ap>, the NCCL exchange of shared
+entities (Alg. 1) and allreduce (N > 1), the x/r update with <r,z>_c and
+<r,r>_c, the convergence test and the p update.
+
+Workload (BASELINE.json configs[1]): the 8192-element Cartesian box (32x16x16
+elements, N=7, all 6 geometric factors stored and streamed, BP5 convention)
+per GPU; with N GPUs the box is stacked N times along z and partitioned into
+z-slabs (weak scaling, one slab of 8192 elements per GPU).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sem|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 Ax+gather-scatter GDOF/s and PCG iter/s at 1-8 B200; % HBM roofline"
+UNIT = "GDOF/s"
+E2E_ITERS = 20   # PCG iterations per end-to-end call (one host solve of b -> x)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="sem", choices=["sem", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg, P):
+    from sem_inputs import CONFIGS, weak_scaled
+    spec, N = CONFIGS[cfg]
+    return weak_scaled(spec, P), N, spec
+
+
+def bytes_model(N):
+    """SURVEY 8(d) per-point algorithmic bytes (paper Eq. 12 Q, cold cache)."""
+    fb = 1.0 - ((N - 1) / (N + 1)) ** 3           # fraction of slots on element faces
+    return {"f_b": fb, "ax": 64.0, "ax_gs": 64.0 + 20.0 * fb,
+            "pcg_iter_fused": 152.0 + 20.0 * fb, "flops_ax": 12 * (N + 1) + 15}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc = index, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return None
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[q] for r in self.rows for q in range(4)
+                          if r[5 + q].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------- oracle arm
+def oracle_pcg_rate(spec, N, target_s=15.0, max_iters=None):
+    """Time the CPU oracle (as it stands) doing PCG iterations on `spec`."""
+    import oracle as O
+    from sem_inputs import f_tgv
+    o = O.Oracle(spec, N)
+    s = 2 * math.pi
+    b = o.rhs(f_tgv(s * o.get("X"), s * o.get("Y"), s * o.get("Z")))
+    t0 = time.perf_counter()
+    o.pcg(b, 0.0, 1)
+    t1 = time.perf_counter() - t0
+    it = max(1, int(target_s / max(t1, 1e-3)))
+    if max_iters:
+        it = min(it, max_iters)
+    t0 = time.perf_counter()
+    r = o.pcg(b, 0.0, it)
+    dt = time.perf_counter() - t0
+    return {"iters": r["iters"], "seconds": dt, "n_p": o.nslots,
+            "gdofs": o.nslots * r["iters"] / dt / 1e9}
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    spec_g, N, spec1 = workload(args.config, 1)
+    from dataclasses import replace
+    # bounded sample: shrink the z extent so K+W oracle iterations stay ~minutes
+    probe = replace(spec1, ez=2, z1=spec1.z0 + (spec1.z1 - spec1.z0) * 2 / spec1.ez)
+    rp = oracle_pcg_rate(probe, N, target_s=2.0, max_iters=3)
+    per_elem_s = rp["seconds"] / rp["iters"] / probe.E
+    budget = 150.0 / max(args.steps + args.warmup, 1)     # seconds per step
+    ez = max(2, min(spec1.ez, int(budget / (per_elem_s * spec1.ex * spec1.ey))))
+    sample = replace(spec1, ez=ez, z1=spec1.z0 + (spec1.z1 - spec1.z0) * ez / spec1.ez)
+    import oracle as O
+    from sem_inputs import f_tgv
+    o = O.Oracle(sample, N)
+    s = 2 * math.pi
+    b = o.rhs(f_tgv(s * o.get("X"), s * o.get("Y"), s * o.get("Z")))
+    if args.warmup:
+        o.pcg(b, 0.0, args.warmup)
+    t0 = time.perf_counter()
+    r = o.pcg(b, 0.0, args.steps)
+    dt = time.perf_counter() - t0
+    value = o.nslots * args.steps / dt / 1e9
+    desc = (f"oracle PCG, {args.steps} iterations (tol=0) on a {sample.ex}x{sample.ey}x{sample.ez}"
+            f"-element slice of the {args.config} box, N={N}, {o.nslots} slots")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU, N={N}",
+                       "step": "one Jacobi-PCG iteration"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "iters": r["iters"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    import paper_2107_01243_b200 as sem
+    from paper_2107_01243_b200 import build as sem_build
+    from sem_inputs import f_tgv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    P = world
+    if args.gpus != P and P > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {P}")
+    torch.cuda.set_device(local)
+    dist = None
+    if P > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        sem_build.build()
+    if dist:
+        dist.barrier()
+    sem.load()
+
+    spec, N, spec1 = workload(args.config, P)
+    comm = None
+    if P > 1:
+        uid = [sem.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sem.nccl_comm_init(uid[0], rank, P)
+    stream = torch.cuda.current_stream()
+    ctx = sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm, stream=stream.cuda_stream)
+    nl = ctx.n_local
+    n_p_total = nl * P
+
+    # synthetic right-hand side: TGV pressure forcing on the unit box (x 2 pi)
+    X, Y, Z = ctx.coords()
+    s = 2 * math.pi
+    f = f_tgv(s * X, s * Y, s * Z, xp=torch)
+    b = ctx.zeros()
+    ctx.rhs(f, b)
+    x = ctx.zeros()
+    del X, Y, Z, f
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # ---- warm-up (W iterations)
+    ctx.pcg_solve(b, x, 0.0, max(args.warmup, 3))
+    barrier()
+
+    # ---- timed: exactly K PCG iterations (one solve, tol=0)
+    l0 = ctx.launch_count()
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record(stream)
+        res = ctx.pcg_solve(b, x, 0.0, args.steps)
+        ev1.record(stream)
+        barrier()
+    launches = ctx.launch_count() - l0
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    assert res["iters"] == args.steps, res
+    value = n_p_total * args.steps / (t_ms / 1e3) / 1e9
+
+    # ---- dominant kernel (fused Ax+gs), CUDA events on the context stream
+    ctx.timing(True)
+    ctx.pcg_solve(b, x, 0.0, args.steps)
+    k_ms, k_cnt = ctx.timing_read(0)
+    u_ms, u_cnt = ctx.timing_read(1)
+    p_ms, p_cnt = ctx.timing_read(2)
+    ctx.timing(False)
+    k_avg = max_over_ranks(k_ms / max(k_cnt, 1))
+    bm = bytes_model(N)
+    peak, peak_src = peaks()
+    achieved = nl * bm["ax_gs"] / (k_avg / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fjs:
+            tj = json.load(fjs)
+        key = f"{args.config}_N{N}_P1"
+        if key in tj:
+            traffic = tj[key]["dram_bytes_per_launch"]
+    except Exception:
+        pass
+
+    # ---- Ax+gs alone (sem_apply), and Ax alone, K repetitions each
+    u_rand = torch.empty(nl, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+    w = ctx.zeros()
+    for _ in range(3):
+        ctx.apply(u_rand, w)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ctx.apply(u_rand, w)
+    ev1.record(stream)
+    barrier()
+    apply_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ctx.ax(u_rand, w)
+    ev1.record(stream)
+    barrier()
+    ax_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    del u_rand, w
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), per step:
+    # H2D of b, E2E_ITERS PCG iterations, D2H of x
+    e2e = None
+    if not args.no_e2e:
+        bh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
+        bh.copy_(b)
+        xh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
+        bn, xn = bh.numpy(), xh.numpy()
+        ctx.pcg_solve_host(bn, xn, 0.0, E2E_ITERS)
+        e2e_steps = max(1, min(args.steps // 4, 10))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ctx.pcg_solve_host(bn, xn, 0.0, E2E_ITERS)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": n_p_total * E2E_ITERS * e2e_steps / e2e_s / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * n_p_total, "d2h_bytes_per_step": 8 * n_p_total,
+               "step": f"sem_pcg_solve_host: H2D b, {E2E_ITERS} PCG iterations, D2H x",
+               "steps": e2e_steps}
+
+    # ---- CPU baseline: the oracle as it stands, rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and P == 1 and not args.no_cpu_baseline:
+        from dataclasses import replace
+        sample = replace(spec1, ez=4, z1=spec1.z0 + (spec1.z1 - spec1.z0) * 4 / spec1.ez)
+        r = oracle_pcg_rate(sample, N, target_s=12.0)
+        cpu = {"value": r["gdofs"], "unit": UNIT, "cores": cores(), "kind": "oracle",
+               "sample": (f"oracle PCG (plain C, OpenMP Ax, serial gs/dots) {r['iters']} "
+                          f"iterations on a {sample.ex}x{sample.ey}x{sample.ez}-element slice of "
+                          f"the {args.config} box, N={N} ({r['n_p']} slots), {r['seconds']:.1f} s")}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": (f"{args.config}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU "
+                             f"(box stacked x{P} along z), N={N}, periodic, all 6 G stored"),
+                "N": N, "elements": spec.E, "n_p": n_p_total, "n_glob": ctx.n_glob,
+                "step": "one Jacobi-PCG iteration (fused Ax+gs+mask+<p,Ap>, update+dots, p)",
+                "l2": "no flush: per-iteration working set ~370 MB/GPU > 126 MB L2",
+                "parallelism": f"element z-slabs x{P}, NCCL gs exchange + allreduce",
+            },
+            "pcg_iter_per_s": args.steps / (t_ms / 1e3),
+            "ax_gs": {"gdofs": n_p_total / (apply_ms / 1e3) / 1e9, "ms": apply_ms,
+                      "frac_of_8TBps": nl * bm["ax_gs"] / (apply_ms / 1e3) / 8e12,
+                      "note": "sem_apply alone (fused Ax+gs+mask), random u"},
+            "ax_only": {"gdofs": n_p_total / (ax_ms / 1e3) / 1e9, "ms": ax_ms,
+                        "gbs_64B_per_pt": nl * 64 / (ax_ms / 1e3) / 1e9},
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": f"ax_kernel<{N + 1},AX_PCG> (fused Ax+gs+mask+sigma)",
+                "bytes_per_pt": bm["ax_gs"], "hbm_mandatory_bytes_per_pt": 64.0,
+                "avg_launch_ms": k_avg, "launches": k_cnt, "peak_source": peak_src,
+                "step_share": k_ms / max(k_ms + u_ms + p_ms, 1e-9),
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "res_final": res["res_final"],
+        }
+        print(json.dumps(line), flush=True)
+
+    ctx.close()
+    if comm is not None:
+        sem.nccl_comm_destroy(comm)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

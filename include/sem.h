@@ -1,0 +1,157 @@
+/*
+ * sem.h -- C ABI of the B200-native matrix-free SEM pressure-Poisson hot path
+ * (Neko, arxiv 2107.01243).  Implemented by paper_2107_01243_b200/libsem.so
+ * (hand-written CUDA for sm_100a + NCCL).  No torch types cross this boundary:
+ * plain pointers and sizes only.
+ *
+ * Citations "P:L<n>" are lines of the paper text;
+ * readings Q1..Q22 where the paper is silent or garbled are in DESIGN.md.
+ *
+ * Data layout (reading Q3, the paper leaves it free):
+ *   element e = ex + Ex*(ey + Ey*ez); rank r owns the contiguous element range
+ *   [r*E/P, (r+1)*E/P) (lexicographic partition); its local element index is
+ *   e - r*E/P.  A field is an E-vector u_L: n_local = E_local*(N+1)^3
+ *   fp64 values, slot l = e_local*n^3 + i + n*j + n^2*k with n = N+1 and i
+ *   running along x fastest.  Field pointers passed to hot calls are DEVICE
+ *   pointers, 16-byte aligned (a torch.cuda tensor satisfies this), caller
+ *   owned, at least n_local doubles.
+ *
+ * Status codes: every function returns one of the values below.  On an error
+ * sem_last_error() returns a thread-local message.  No exception crosses the ABI.
+ * All device work is ordered on sem_mesh.stream; sem_ax/sem_gs/sem_apply/
+ * sem_rhs are asynchronous with respect to the host, sem_setup and the PCG
+ * solves block.  Calls marked "collective" must be made by every rank in
+ * the same order.  One context per stream / host thread.
+ */
+#ifndef SEM_H
+#define SEM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEM_OK 0
+#define SEM_NOT_CONVERGED 1    /* PCG hit maxit; result filled */
+#define SEM_EINVAL (-1)        /* bad argument: counts, extents, N outside 1..11,
+                                  periodic axis with < 2 elements, P > E, NULL or
+                                  misaligned pointer */
+#define SEM_EGEOM (-2)         /* Jacobian <= 0 at some GLL point */
+#define SEM_ECUDA (-3)         /* CUDA runtime error (or no device) */
+#define SEM_ENCCL (-4)         /* NCCL error */
+#define SEM_ENOMEM (-5)        /* allocation failed */
+#define SEM_EBREAKDOWN (-6)    /* CG breakdown: p^T A p <= 0 or NaN */
+
+typedef struct sem_ctx sem_ctx; /* opaque; owns D, G, B, plan, dinv, work vectors */
+
+/* Hexahedral box mesh ("E non-overlapping hexahedral elements").
+   Non-periodic faces carry homogeneous Dirichlet conditions (Eq. 5). */
+typedef struct {
+  int32_t ex, ey, ez;                 /* elements per axis (>= 1; >= 2 if periodic) */
+  double x0, x1, y0, y1, z0, z1;      /* box extents, x1 > x0 etc. */
+  int32_t periodic[3];                /* 1 = periodic axis */
+  int32_t deform;                     /* 0 Cartesian; 1 x_m += a sin X sin Y sin Z on the
+                                         box rescaled to (0,2pi)^3 (reading Q4) */
+  double deform_amp;                  /* a */
+  int32_t rank, nranks;               /* this process and the element partition size */
+  void* nccl_comm;                    /* ncclComm_t for nranks > 1 (see sem_nccl_*), else NULL */
+  void* stream;                       /* cudaStream_t all work is ordered on (NULL = legacy) */
+} sem_mesh;
+
+/* ---- setup (GLL space, D, geometric factors G^e, numbering) ----
+   Builds the GLL rule and derivative matrix (Eq. 7), the node
+   coordinates and the six geometric factors G = J w_i w_j w_k (dr/dx)(dr/dx)^T
+   and mass B = J w_i w_j w_k (reading Q5) on the device, the gather-scatter plan
+   (element-local entities summed on this GPU, entities shared with
+   other ranks exchanged over NCCL), the Dirichlet mask and the Jacobi inverse
+   diagonal (reading Q14).  Collective, blocking.  N in 1..11. */
+int sem_setup(const sem_mesh* m, int N, sem_ctx** out);
+int sem_destroy(sem_ctx* c);
+/* n_local = local slots, e_local = local elements, n_glob = unique global DOF */
+int sem_sizes(const sem_ctx* c, int64_t* n_local, int64_t* e_local, int64_t* n_glob);
+
+/* ---- hot path ----
+   sem_ax:    w_L = A_L u_L, A^e = D^T G^e D per element (Eq. 9); no gs, no mask.
+   sem_gs:    u_L <- Q Q^T u_L in place (Eq. 10), sum over all slots
+              sharing a global number, in ascending slot order within a rank and
+              ascending rank order across ranks (reading Q10).  Collective.
+   sem_apply: w = mask(Q Q^T A_L u) -- the CG operator, fused in one
+              kernel pass plus the overlapped NCCL exchange (Alg. 1).  Collective.
+   u and w must not alias. */
+int sem_ax(sem_ctx* c, const double* u, double* w);
+int sem_gs(sem_ctx* c, double* u);
+int sem_apply(sem_ctx* c, const double* u, double* w);
+
+/* b = mask(Q Q^T (B .* f)) with f the nodal values of the forcing (Eq. 6 RHS,
+   collocated quadrature, reading Q12); on a fully periodic box the unique-DOF
+   mean is removed (reading Q13).  Collective. */
+int sem_rhs(sem_ctx* c, const double* f, double* b);
+/* device node coordinates (x, y, z per slot), for evaluating forcing terms */
+int sem_coords(sem_ctx* c, double* X, double* Y, double* Z);
+
+/* ---- Jacobi-preconditioned CG (readings Q14-Q17) ----
+   x0 = 0; stops when sqrt(<r,r>_c) <= tol (absolute, c = 1/multiplicity) or
+   after maxit iterations (iterations = applications of A).  res_final is the
+   recursive residual, res_true = sqrt(<b - A x, b - A x>_c) computed once at the
+   end.  Returns SEM_OK, SEM_NOT_CONVERGED or an error.  Collective, blocking.
+   sem_pcg_solve takes device b, x; sem_pcg_solve_host takes HOST b, x and does
+   the host<->device copies itself (end-to-end entry point). */
+typedef struct {
+  int32_t iters;
+  int32_t status;
+  double res_final;
+  double res_true;
+} sem_pcg_result;
+int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                  sem_pcg_result* res);
+int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_host, double tol,
+                       int32_t maxit, sem_pcg_result* res);
+/* recursive residual history of the last solve: hist[k] after k iterations */
+int sem_pcg_history(const sem_ctx* c, double* host_dst, int32_t max_entries, int32_t* n);
+
+/* ---- exports for parity tests (host buffers, caller allocated) ----
+   which: 0 xi[n], 1 w[n], 2 D[n*n], 3 G[E_local*6*n^3], 4 B[n_local], 5 dinv[n_local] */
+int sem_export_field(const sem_ctx* c, int which, double* host_dst);
+/* which: 0 multiplicity[n_local], 1 mask[n_local] (1 = Dirichlet slot) */
+int sem_export_int(const sem_ctx* c, int which, int64_t* host_dst);
+
+/* ---- host-only planner (no device needed; used by CPU tests) ----
+   Exposes the gather-scatter plan a rank would build for this mesh: lattice
+   global numbering (reading Q6), multiplicity, mask, the injective pairs
+   (l_a < l_b) sorted by l_a and the non-injective segments sorted by first
+   slot, the neighbour ranks and, per neighbour, the shared global
+   numbers in ascending order (Alg. 1 buffers). */
+typedef struct sem_plan sem_plan;
+int sem_plan_create(const sem_mesh* m, int N, sem_plan** out);
+int sem_plan_destroy(sem_plan* p);
+int sem_plan_sizes(const sem_plan* p, int64_t* n_local, int64_t* npairs, int64_t* nseg,
+                   int64_t* nsegslots, int32_t* n_nbr);
+int sem_plan_slots(const sem_plan* p, int64_t* gid, int64_t* mult, int64_t* mask);
+int sem_plan_pairs(const sem_plan* p, int64_t* pairs, int64_t* seg_off, int64_t* seg_slot);
+int sem_plan_neighbors(const sem_plan* p, int32_t* ranks, int64_t* counts);
+int sem_plan_shared(const sem_plan* p, int32_t q, int64_t* gids);
+/* GLL nodes xi[n], weights w[n] and D[n*n] (row-major, D[i*n+j] = l_j'(xi_i)) */
+int sem_plan_space(const sem_plan* p, double* xi, double* w, double* D);
+
+/* ---- NCCL bootstrap (one process per GPU; the 128-byte unique id is
+   broadcast by the caller, e.g. with torch.distributed) ---- */
+int sem_nccl_unique_id(uint8_t id[128]);
+int sem_nccl_comm_init(const uint8_t id[128], int rank, int nranks, void** comm);
+int sem_nccl_comm_destroy(void* comm);
+
+/* ---- instrumentation ----
+   sem_timing(c, 1) records CUDA events on the context stream around every
+   launch of kernel class `which` (0 = fused Ax+gs apply kernel, 1 = CG
+   update, 2 = p update, 3 = Ax only); sem_timing_read returns the summed
+   device time in ms and the number of timed launches since the last reset.
+   sem_launch_count returns the number of kernels this context has launched. */
+int sem_timing(sem_ctx* c, int enable);
+int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t* count);
+int sem_launch_count(const sem_ctx* c, int64_t* n);
+
+const char* sem_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_H */

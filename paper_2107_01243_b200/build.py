@@ -1,0 +1,79 @@
+"""Build libsem.so in-tree: hand-written CUDA for sm_100a + host C++ planner,
+linked against the NCCL that ships with torch (one libnccl.so.2 per process)."""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_obj")
+SO = os.path.join(HERE, "libsem.so")
+ROOT = os.path.dirname(HERE)
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_SRCS = ["ax.cu", "kern.cu", "api.cu"]
+CXX_SRCS = ["plan.cpp"]
+
+
+def _nccl_dirs():
+    import nvidia.nccl  # torch's NCCL 2.28 (pip package)
+    base = list(nvidia.nccl.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def _nvcc():
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if c and (os.path.isabs(c) and os.path.exists(c) or not os.path.isabs(c)):
+            return c
+    return "nvcc"
+
+
+def _deps_mtime():
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    files.append(os.path.join(ROOT, "include", "sem.h"))
+    files.append(os.path.abspath(__file__))
+    return max(os.path.getmtime(f) for f in files)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _deps_mtime():
+        return SO
+    os.makedirs(OBJ, exist_ok=True)
+    inc, lib = _nccl_dirs()
+    nvcc = _nvcc()
+    common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc,
+              "-I", os.path.join(ROOT, "include")]
+    jobs = []
+    for f in CUDA_SRCS:
+        out = os.path.join(OBJ, f + ".o")
+        jobs.append([nvcc, *ARCH, *common, "-Xptxas", "-v", "-c", os.path.join(CSRC, f), "-o", out])
+    for f in CXX_SRCS:
+        out = os.path.join(OBJ, f + ".o")
+        jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I",
+                     os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", out])
+
+    def run(cmd):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+        return r.stdout + r.stderr
+
+    with cf.ThreadPoolExecutor(max_workers=4) as ex:
+        logs = list(ex.map(run, jobs))
+    with open(os.path.join(OBJ, "ptxas.log"), "w") as f:
+        f.write("\n".join(logs))
+    if verbose:
+        print("\n".join(logs))
+    objs = [os.path.join(OBJ, f + ".o") for f in CUDA_SRCS + CXX_SRCS]
+    run([nvcc, *ARCH, "-shared", "-o", SO + ".tmp", *objs, "-L", lib, "-l:libnccl.so.2",
+         "-Xlinker", "-rpath=" + lib, "-lcudart"])
+    os.replace(SO + ".tmp", SO)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(SO)

@@ -1,0 +1,661 @@
+// C ABI of libsem (include/sem.h): context setup, the hot-path entry points
+// (sem_ax, sem_gs, sem_apply, sem_pcg_solve) and the NCCL plumbing.
+//
+// Multi-GPU (Alg. 1, P:L367 allreduce): one process per GPU; the
+// element range of this rank is split into boundary elements (incident to an
+// entity shared with another rank) and interior elements.  sem_apply runs the
+// fused Ax+gs kernel on the boundary elements, packs the shared partials,
+// exchanges them with ncclSend/ncclRecv on a communication stream while the
+// interior elements are processed, then adds the partials in ascending rank
+// order and scatters.  The CG inner products are reduced with ncclAllReduce on
+// device-resident scalars (two per iteration); the host never synchronises
+// inside an iteration and polls a device "done" flag every kBatch iterations.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "sem_internal.h"
+
+namespace sem {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace sem
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      sem::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+      return SEM_ECUDA;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                   \
+  do {                                                                                   \
+    ncclResult_t _r = (expr);                                                            \
+    if (_r != ncclSuccess) {                                                             \
+      sem::set_error(std::string(#expr) + ": " + ncclGetErrorString(_r));                \
+      return SEM_ENCCL;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+#define SEM_TRY(expr)           \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != SEM_OK) return _s; \
+  } while (0)
+
+namespace {
+
+constexpr int kBatch = 8;            // iterations enqueued between host polls
+constexpr int kTimerClasses = 4;
+
+struct Timer {
+  std::vector<cudaEvent_t> pool;     // pairs
+  std::vector<int> cls;              // class of each recorded pair
+  size_t used = 0;
+};
+
+}  // namespace
+
+struct sem_ctx {
+  sem::HostPlan hp;
+  sem::DevPlan dp;
+  int dev = 0, num_sms = 148;
+  cudaStream_t stream = nullptr, comm = nullptr;
+  ncclComm_t nccl = nullptr;
+  // device data
+  double *d_xi = nullptr, *d_w = nullptr, *d_D = nullptr, *d_G = nullptr, *d_B = nullptr,
+         *d_dinv = nullptr;
+  uint8_t *d_mult = nullptr, *d_bmask = nullptr;
+  int32_t *d_eref = nullptr, *d_fb = nullptr, *d_eb = nullptr, *d_vb = nullptr;
+  uint8_t *d_fax = nullptr, *d_eax = nullptr, *d_enin = nullptr, *d_emask = nullptr,
+          *d_vnin = nullptr, *d_vmask = nullptr;
+  unsigned* d_cnt = nullptr;
+  int32_t *d_sslot = nullptr, *d_soff = nullptr;
+  uint8_t *d_snloc = nullptr, *d_snr = nullptr, *d_smask = nullptr, *d_smult = nullptr;
+  double *d_part = nullptr, *d_send = nullptr, *d_recv = nullptr;
+  // work
+  double *d_r = nullptr, *d_p = nullptr, *d_wv = nullptr, *d_tmp = nullptr;
+  double* d_partial = nullptr;        // reduction partials
+  unsigned* d_tickets = nullptr;      // misc tickets
+  double* d_scal = nullptr;           // misc scalars
+  sem::PcgState* d_st = nullptr;
+  sem::PcgState* h_st = nullptr;      // pinned
+  double* d_hist = nullptr;
+  int hist_cap = 0;
+  int last_hist = 0;
+  cudaEvent_t ev_pack = nullptr, ev_comm = nullptr, ev_poll = nullptr;
+  int ax_grid = 148;
+  int red_grid = 592;
+  int64_t launches = 0;
+  bool timing = false;
+  Timer timer;
+  double t_ms[kTimerClasses] = {0, 0, 0, 0};
+  int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0};
+};
+
+namespace {
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    sem::set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SEM_ENOMEM : SEM_ECUDA;
+  }
+  return SEM_OK;
+}
+
+template <typename T>
+int upload(T** p, const std::vector<T>& v, cudaStream_t s) {
+  SEM_TRY(dalloc(p, v.size()));
+  if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return SEM_OK;
+}
+
+// timing hooks around kernel launches (sem_timing)
+int timer_begin(sem_ctx* c, int cls) {
+  if (!c->timing) return -1;
+  Timer& t = c->timer;
+  if (t.used + 2 > t.pool.size()) {
+    for (int q = 0; q < 256; q++) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      t.pool.push_back(e);
+    }
+  }
+  int idx = (int)t.used;
+  t.used += 2;
+  t.cls.push_back(cls);
+  cudaEventRecord(t.pool[idx], c->stream);
+  return idx;
+}
+
+void timer_end(sem_ctx* c, int idx) {
+  if (idx < 0) return;
+  cudaEventRecord(c->timer.pool[idx + 1], c->stream);
+}
+
+void timer_collect(sem_ctx* c) {
+  Timer& t = c->timer;
+  if (t.used == 0) return;
+  cudaEventSynchronize(t.pool[t.used - 1]);
+  for (size_t q = 0; q < t.cls.size(); q++) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.pool[2 * q], t.pool[2 * q + 1]);
+    c->t_ms[t.cls[q]] += ms;
+    c->t_cnt[t.cls[q]] += 1;
+  }
+  t.used = 0;
+  t.cls.clear();
+}
+
+int check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    sem::set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return SEM_ECUDA;
+  }
+  return SEM_OK;
+}
+
+// ---- the operator ----------------------------------------------------------
+int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi, int r1lo,
+           int r1hi, double* red_out) {
+  sem::AxLaunch a{};
+  a.u = u;
+  a.w = w;
+  a.G = c->d_G;
+  a.r0lo = r0lo; a.r0hi = r0hi; a.r1lo = r1lo; a.r1hi = r1hi;
+  a.red_partial = c->d_partial;
+  a.red_ticket = &c->d_st->tickets[0];
+  a.red_out = red_out;
+  a.done = &c->d_st->done;
+  const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
+  int grid = std::min(c->ax_grid, std::max(ng, 1));
+  int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
+  cudaError_t e = sem::launch_ax(c->dp, a, mode, grid, c->stream);
+  timer_end(c, tk);
+  c->launches++;
+  return check(e, "ax kernel");
+}
+
+// exchange the shared partials (Alg. 1 lines 1-5, 7, 10-17) on the comm stream
+int exchange(sem_ctx* c) {
+  CUDA_TRY(cudaEventRecord(c->ev_pack, c->stream));
+  CUDA_TRY(cudaStreamWaitEvent(c->comm, c->ev_pack, 0));
+  NCCL_TRY(ncclGroupStart());
+  for (size_t q = 0; q < c->hp.nbr_rank.size(); q++) {
+    const int peer = c->hp.nbr_rank[q];
+    const size_t off = (size_t)c->hp.nbr_off[q], cnt = (size_t)c->hp.nbr_cnt[q];
+    NCCL_TRY(ncclSend(c->d_send + off, cnt, ncclDouble, peer, c->nccl, c->comm));
+    NCCL_TRY(ncclRecv(c->d_recv + off, cnt, ncclDouble, peer, c->nccl, c->comm));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm));
+  return SEM_OK;
+}
+
+// w = mask(QQ^T A_L u) (mode AX_APPLY) or the same plus sigma (AX_PCG)
+int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
+  const sem::HostPlan& h = c->hp;
+  sem::PcgState* st = c->d_st;
+  if (h.nranks == 1 || h.nS == 0) {
+    SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, &st->sigma));
+    return SEM_OK;
+  }
+  int nparts = 1;
+  if (h.ihi > h.ilo) {
+    SEM_TRY(run_ax(c, u, w, mode, (int)h.b0lo, (int)h.b0hi, (int)h.b1lo, (int)h.b1hi,
+                   &st->sigma_part[0]));
+    CUDA_TRY(sem::launch_gs_pack(c->dp, w, c->d_part, c->d_send, c->stream));
+    c->launches++;
+    SEM_TRY(exchange(c));
+    SEM_TRY(run_ax(c, u, w, mode, (int)h.ilo, (int)h.ihi, 0, 0, &st->sigma_part[1]));
+    nparts = 2;
+  } else {
+    SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, &st->sigma_part[0]));
+    CUDA_TRY(sem::launch_gs_pack(c->dp, w, c->d_part, c->d_send, c->stream));
+    c->launches++;
+    SEM_TRY(exchange(c));
+  }
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+  CUDA_TRY(sem::launch_gs_unpack(c->dp, w, c->d_part, c->d_recv, 1,
+                                 mode == sem::AX_PCG ? st : nullptr, nparts, c->stream));
+  c->launches++;
+  if (mode == sem::AX_PCG)
+    NCCL_TRY(ncclAllReduce(&st->sigma, &st->sigma, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+  return SEM_OK;
+}
+
+// standalone gs (no mask unless asked): local entities + shared exchange
+int gs_op(sem_ctx* c, double* u, int apply_mask) {
+  CUDA_TRY(sem::launch_gs_local(c->dp, u, apply_mask, c->stream));
+  c->launches++;
+  if (c->hp.nranks > 1 && c->hp.nS > 0) {
+    CUDA_TRY(sem::launch_gs_pack(c->dp, u, c->d_part, c->d_send, c->stream));
+    c->launches++;
+    SEM_TRY(exchange(c));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+    CUDA_TRY(sem::launch_gs_unpack(c->dp, u, c->d_part, c->d_recv, apply_mask, nullptr, 1, c->stream));
+    c->launches++;
+  }
+  return SEM_OK;
+}
+
+int allreduce(sem_ctx* c, double* p, size_t count) {
+  if (c->hp.nranks > 1)
+    NCCL_TRY(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->nccl, c->stream));
+  return SEM_OK;
+}
+
+int ensure_hist(sem_ctx* c, int maxit) {
+  if (maxit + 2 <= c->hist_cap) return SEM_OK;
+  if (c->d_hist) cudaFree(c->d_hist);
+  c->hist_cap = maxit + 2;
+  return dalloc(&c->d_hist, (size_t)c->hist_cap);
+}
+
+void free_ctx(sem_ctx* c) {
+  if (!c) return;
+  void* ptrs[] = {c->d_xi, c->d_w, c->d_D, c->d_G, c->d_B, c->d_dinv, c->d_mult, c->d_bmask,
+                  c->d_eref, c->d_fb, c->d_eb, c->d_vb, c->d_fax, c->d_eax, c->d_enin,
+                  c->d_emask, c->d_vnin, c->d_vmask, c->d_cnt, c->d_sslot, c->d_soff,
+                  c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
+                  c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
+                  c->d_scal, c->d_st, c->d_hist};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->ev_poll) cudaEventDestroy(c->ev_poll);
+  for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
+  if (c->comm) cudaStreamDestroy(c->comm);
+  delete c;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// =============================================================== C ABI
+extern "C" const char* sem_last_error(void) { return sem::g_err.c_str(); }
+
+extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
+  if (!m || !out) { sem::set_error("NULL argument"); return SEM_EINVAL; }
+  *out = nullptr;
+  if (m->nranks > 1 && !m->nccl_comm) { sem::set_error("nranks > 1 needs nccl_comm"); return SEM_EINVAL; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    sem::set_error("no CUDA device (libsem has no CPU fallback)");
+    return SEM_ECUDA;
+  }
+  sem_ctx* c = new (std::nothrow) sem_ctx();
+  if (!c) return SEM_ENOMEM;
+  int st = sem::build_plan(m, N, &c->hp);
+  if (st != SEM_OK) { delete c; return st; }
+  const sem::HostPlan& h = c->hp;
+  c->stream = static_cast<cudaStream_t>(m->stream);
+  c->nccl = static_cast<ncclComm_t>(m->nccl_comm);
+  auto fail = [&](int s) { free_ctx(c); return s; };
+#define SETUP_TRY(expr)             \
+  do {                              \
+    int _s = (expr);                \
+    if (_s != SEM_OK) return fail(_s); \
+  } while (0)
+#define SETUP_CUDA(expr) SETUP_TRY(check((expr), #expr))
+  SETUP_CUDA(cudaGetDevice(&c->dev));
+  SETUP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev));
+  SETUP_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+  SETUP_CUDA(cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+  SETUP_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+  SETUP_CUDA(cudaEventCreateWithFlags(&c->ev_poll, cudaEventDisableTiming));
+  cudaStream_t s = c->stream;
+
+  SETUP_TRY(upload(&c->d_xi, h.xi, s));
+  SETUP_TRY(upload(&c->d_w, h.w, s));
+  SETUP_TRY(upload(&c->d_D, h.D, s));
+  SETUP_TRY(upload(&c->d_bmask, h.bmask, s));
+  SETUP_TRY(upload(&c->d_eref, h.eref, s));
+  SETUP_TRY(upload(&c->d_fb, h.f_base, s));
+  SETUP_TRY(upload(&c->d_fax, h.f_axis, s));
+  SETUP_TRY(upload(&c->d_eb, h.e_base, s));
+  SETUP_TRY(upload(&c->d_eax, h.e_axis, s));
+  SETUP_TRY(upload(&c->d_enin, h.e_nin, s));
+  SETUP_TRY(upload(&c->d_emask, h.e_mask, s));
+  SETUP_TRY(upload(&c->d_vb, h.v_base, s));
+  SETUP_TRY(upload(&c->d_vnin, h.v_nin, s));
+  SETUP_TRY(upload(&c->d_vmask, h.v_mask, s));
+  SETUP_TRY(upload(&c->d_sslot, h.s_slot, s));
+  SETUP_TRY(upload(&c->d_soff, h.s_off, s));
+  SETUP_TRY(upload(&c->d_snloc, h.s_nloc, s));
+  SETUP_TRY(upload(&c->d_snr, h.s_nr, s));
+  SETUP_TRY(upload(&c->d_smask, h.s_mask, s));
+  SETUP_TRY(upload(&c->d_smult, h.s_mult, s));
+  const size_t nent = (size_t)(h.nF + h.nEd + h.nV);
+  SETUP_TRY(dalloc(&c->d_cnt, nent));
+  SETUP_CUDA(cudaMemsetAsync(c->d_cnt, 0, std::max<size_t>(nent, 1) * sizeof(unsigned), s));
+  SETUP_TRY(dalloc(&c->d_part, (size_t)h.nS));
+  SETUP_TRY(dalloc(&c->d_send, (size_t)h.nbuf));
+  SETUP_TRY(dalloc(&c->d_recv, (size_t)h.nbuf));
+  const size_t nl = (size_t)h.n_local;
+  SETUP_TRY(dalloc(&c->d_G, 6 * nl));
+  SETUP_TRY(dalloc(&c->d_B, nl));
+  SETUP_TRY(dalloc(&c->d_dinv, nl));
+  SETUP_TRY(dalloc(&c->d_mult, nl + 2));
+  SETUP_TRY(dalloc(&c->d_r, nl));
+  SETUP_TRY(dalloc(&c->d_p, nl));
+  SETUP_TRY(dalloc(&c->d_wv, nl));
+  SETUP_TRY(dalloc(&c->d_st, 1));
+  SETUP_CUDA(cudaMemsetAsync(c->d_st, 0, sizeof(sem::PcgState), s));
+  SETUP_CUDA(cudaMallocHost(&c->h_st, sizeof(sem::PcgState)));
+  SETUP_TRY(ensure_hist(c, 1000));
+
+  sem::DevPlan& P = c->dp;
+  P.N = h.N; P.n = h.n; P.nloc = (int)h.nloc; P.n_local = h.n_local;
+  P.nF = (int)h.nF; P.nEd = (int)h.nEd; P.nV = (int)h.nV; P.nS = (int)h.nS;
+  P.D = c->d_D; P.bmask = c->d_bmask; P.eref = c->d_eref;
+  P.f_base = c->d_fb; P.f_axis = c->d_fax;
+  P.e_base = c->d_eb; P.e_axis = c->d_eax; P.e_nin = c->d_enin; P.e_mask = c->d_emask;
+  P.v_base = c->d_vb; P.v_nin = c->d_vnin; P.v_mask = c->d_vmask;
+  P.cnt = c->d_cnt;
+  P.s_slot = c->d_sslot; P.s_off = c->d_soff; P.s_nloc = c->d_snloc; P.s_nr = c->d_snr;
+  P.s_mask = c->d_smask; P.s_mult = c->d_smult;
+
+  // launch geometry (persistent grids sized to the SM count x residency)
+  c->ax_grid = c->num_sms * sem::ax_occupancy(h.N, sem::AX_PCG);
+  c->red_grid = sem::cg_grid(c->num_sms);
+  SETUP_TRY(dalloc(&c->d_partial, (size_t)2 * std::max(c->ax_grid, c->red_grid)));
+  SETUP_TRY(dalloc(&c->d_tickets, 8));
+  SETUP_CUDA(cudaMemsetAsync(c->d_tickets, 0, 8 * sizeof(unsigned), s));
+  SETUP_TRY(dalloc(&c->d_scal, 8));
+
+  // geometry on the device
+  int* d_bad = nullptr;
+  SETUP_TRY(dalloc(&d_bad, 1));
+  SETUP_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+  const double box[6] = {m->x0, m->x1, m->y0, m->y1, m->z0, m->z1};
+  SETUP_CUDA(sem::launch_geom(P, c->d_xi, c->d_w, h.e_lo, m->ex, m->ey, m->ez, box, m->deform,
+                              m->deform_amp, c->d_G, c->d_B, d_bad, s));
+  int bad = 0;
+  SETUP_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SETUP_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_bad);
+  // all ranks must agree on a geometry failure before returning
+  if (h.nranks > 1) {
+    double flag = bad ? 1.0 : 0.0;
+    SETUP_CUDA(cudaMemcpyAsync(c->d_scal, &flag, sizeof(double), cudaMemcpyHostToDevice, s));
+    if (ncclAllReduce(c->d_scal, c->d_scal, 1, ncclDouble, ncclSum, c->nccl, s) != ncclSuccess) {
+      sem::set_error("ncclAllReduce in setup failed");
+      return fail(SEM_ENCCL);
+    }
+    SETUP_CUDA(cudaMemcpyAsync(&flag, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SETUP_CUDA(cudaStreamSynchronize(s));
+    bad = flag > 0.0;
+  }
+  if (bad) {
+    sem::set_error("non-positive Jacobian at some GLL point");
+    return fail(SEM_EGEOM);
+  }
+  // multiplicity and Jacobi: d = QQ^T diag(A_L); dinv = mask ? 0 : 1/d (reading Q14)
+  SETUP_CUDA(sem::launch_mult(P, c->d_mult, s));
+  SETUP_CUDA(sem::launch_diag(P, c->d_G, c->d_dinv, s));
+  SETUP_TRY(gs_op(c, c->d_dinv, 0));
+  SETUP_CUDA(sem::launch_invert_mask(P, c->d_dinv, s));
+  SETUP_CUDA(cudaStreamSynchronize(s));
+#undef SETUP_TRY
+#undef SETUP_CUDA
+  *out = c;
+  return SEM_OK;
+}
+
+extern "C" int sem_destroy(sem_ctx* c) {
+  if (c) {
+    cudaStreamSynchronize(c->stream);
+    free_ctx(c);
+  }
+  return SEM_OK;
+}
+
+extern "C" int sem_sizes(const sem_ctx* c, int64_t* n_local, int64_t* e_local, int64_t* n_glob) {
+  if (!c) { sem::set_error("NULL context"); return SEM_EINVAL; }
+  if (n_local) *n_local = c->hp.n_local;
+  if (e_local) *e_local = c->hp.nloc;
+  if (n_glob) *n_glob = c->hp.nglob;
+  return SEM_OK;
+}
+
+extern "C" int sem_ax(sem_ctx* c, const double* u, double* w) {
+  if (!c || !u || !w || !aligned16(u) || !aligned16(w) || u == w) {
+    sem::set_error("sem_ax: bad arguments (NULL, misaligned or aliased pointers)");
+    return SEM_EINVAL;
+  }
+  return run_ax(c, u, w, sem::AX_ONLY, 0, (int)c->hp.nloc, 0, 0, nullptr);
+}
+
+extern "C" int sem_gs(sem_ctx* c, double* u) {
+  if (!c || !u) { sem::set_error("sem_gs: NULL argument"); return SEM_EINVAL; }
+  return gs_op(c, u, 0);
+}
+
+extern "C" int sem_apply(sem_ctx* c, const double* u, double* w) {
+  if (!c || !u || !w || !aligned16(u) || !aligned16(w) || u == w) {
+    sem::set_error("sem_apply: bad arguments (NULL, misaligned or aliased pointers)");
+    return SEM_EINVAL;
+  }
+  return apply_op(c, u, w, sem::AX_APPLY);
+}
+
+extern "C" int sem_coords(sem_ctx* c, double* X, double* Y, double* Z) {
+  if (!c || !X || !Y || !Z) { sem::set_error("sem_coords: NULL argument"); return SEM_EINVAL; }
+  const sem_mesh& m = c->hp.m;
+  const double box[6] = {m.x0, m.x1, m.y0, m.y1, m.z0, m.z1};
+  CUDA_TRY(sem::launch_coords(c->dp, c->d_xi, c->hp.e_lo, m.ex, m.ey, m.ez, box, m.deform,
+                              m.deform_amp, X, Y, Z, c->stream));
+  c->launches++;
+  return SEM_OK;
+}
+
+extern "C" int sem_rhs(sem_ctx* c, const double* f, double* b) {
+  if (!c || !f || !b) { sem::set_error("sem_rhs: NULL argument"); return SEM_EINVAL; }
+  CUDA_TRY(sem::launch_scale(c->d_B, f, b, c->hp.n_local, c->stream));
+  c->launches++;
+  SEM_TRY(gs_op(c, b, 1));
+  if (c->hp.fully_periodic) {
+    CUDA_TRY(sem::launch_sum_c(c->dp, c->d_mult, b, c->d_partial, &c->d_tickets[0], c->d_scal,
+                               c->red_grid, c->stream));
+    SEM_TRY(allreduce(c, c->d_scal, 2));
+    CUDA_TRY(sem::launch_sub_scalar(b, c->d_scal, c->hp.n_local, c->stream));
+    c->launches += 2;
+  }
+  return SEM_OK;
+}
+
+static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                   sem_pcg_result* res) {
+  if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
+  SEM_TRY(ensure_hist(c, maxit));
+  cudaStream_t s = c->stream;
+  sem::PcgState* st = c->d_st;
+  // scalars: tol, maxit
+  sem::PcgState init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  std::memcpy(c->h_st, &init, sizeof(init));   // h_st is idle: every solve ends synchronised
+  CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, c->d_dinv, b, x, c->d_r, c->d_p, c->d_partial,
+                               st, c->red_grid, s));
+  SEM_TRY(allreduce(c, &st->rho_new, 2));
+  CUDA_TRY(sem::launch_cg_start(st, c->d_hist, s));
+  c->launches += 2;
+  int done = 0;
+  for (int k = 0; k < maxit && !done; k += kBatch) {
+    const int nb = std::min(kBatch, maxit - k);
+    for (int q = 0; q < nb; q++) {
+      SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
+      int tk = timer_begin(c, 1);
+      CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, x, c->d_r, c->d_p, c->d_wv,
+                                     c->d_partial, st, c->red_grid, s));
+      timer_end(c, tk);
+      SEM_TRY(allreduce(c, &st->rho_new, 2));
+      tk = timer_begin(c, 2);
+      CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, st, c->d_hist, c->red_grid, s));
+      timer_end(c, tk);
+      c->launches += 2;
+    }
+    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(c->ev_poll, s));
+    CUDA_TRY(cudaEventSynchronize(c->ev_poll));
+    done = c->h_st->done;
+  }
+  // true residual once at the end (reading Q17)
+  SEM_TRY(apply_op(c, x, c->d_wv, sem::AX_APPLY));
+  CUDA_TRY(sem::launch_cg_residual(c->dp, c->d_mult, b, c->d_wv, c->d_partial, st, c->red_grid, s));
+  c->launches++;
+  SEM_TRY(allreduce(c, &st->res_true, 1));
+  CUDA_TRY(cudaMemcpyAsync(c->h_st, st, sizeof(sem::PcgState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  timer_collect(c);
+  const sem::PcgState& hs = *c->h_st;
+  c->last_hist = hs.iters;
+  if (res) {
+    res->iters = hs.iters;
+    res->res_final = std::sqrt(hs.gamma);
+    res->res_true = std::sqrt(hs.res_true);
+  }
+  int status;
+  if (hs.done == 1) status = SEM_OK;
+  else if (hs.done == 2 || hs.done == 3) {
+    sem::set_error(hs.done == 2 ? "CG breakdown: p^T A p <= 0" : "CG produced NaN");
+    status = SEM_EBREAKDOWN;
+  } else status = SEM_NOT_CONVERGED;
+  if (res) res->status = status;
+  return status;
+}
+
+extern "C" int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                             sem_pcg_result* res) {
+  if (!c || !b || !x || !aligned16(b) || !aligned16(x) || b == x) {
+    sem::set_error("sem_pcg_solve: bad arguments");
+    return SEM_EINVAL;
+  }
+  return pcg_run(c, b, x, tol, maxit, res);
+}
+
+extern "C" int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_host, double tol,
+                                  int32_t maxit, sem_pcg_result* res) {
+  if (!c || !b_host || !x_host) { sem::set_error("sem_pcg_solve_host: NULL argument"); return SEM_EINVAL; }
+  const size_t bytes = (size_t)c->hp.n_local * sizeof(double);
+  if (!c->d_tmp) SEM_TRY(dalloc(&c->d_tmp, 2 * (size_t)c->hp.n_local));
+  double* db = c->d_tmp;
+  double* dx = c->d_tmp + c->hp.n_local;
+  CUDA_TRY(cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, c->stream));
+  int st = pcg_run(c, db, dx, tol, maxit, res);
+  if (st < 0) return st;
+  CUDA_TRY(cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return st;
+}
+
+extern "C" int sem_pcg_history(const sem_ctx* c, double* host_dst, int32_t max_entries, int32_t* n) {
+  if (!c || !host_dst) return SEM_EINVAL;
+  int cnt = std::min(max_entries, c->last_hist + 1);
+  if (cnt > 0)
+    CUDA_TRY(cudaMemcpy(host_dst, c->d_hist, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost));
+  if (n) *n = cnt;
+  return SEM_OK;
+}
+
+extern "C" int sem_export_field(const sem_ctx* c, int which, double* host_dst) {
+  if (!c || !host_dst) return SEM_EINVAL;
+  const sem::HostPlan& h = c->hp;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  switch (which) {
+    case 0: std::memcpy(host_dst, h.xi.data(), h.xi.size() * sizeof(double)); return SEM_OK;
+    case 1: std::memcpy(host_dst, h.w.data(), h.w.size() * sizeof(double)); return SEM_OK;
+    case 2: std::memcpy(host_dst, h.D.data(), h.D.size() * sizeof(double)); return SEM_OK;
+    case 3: CUDA_TRY(cudaMemcpy(host_dst, c->d_G, 6 * (size_t)h.n_local * 8, cudaMemcpyDeviceToHost)); return SEM_OK;
+    case 4: CUDA_TRY(cudaMemcpy(host_dst, c->d_B, (size_t)h.n_local * 8, cudaMemcpyDeviceToHost)); return SEM_OK;
+    case 5: CUDA_TRY(cudaMemcpy(host_dst, c->d_dinv, (size_t)h.n_local * 8, cudaMemcpyDeviceToHost)); return SEM_OK;
+  }
+  sem::set_error("sem_export_field: unknown field");
+  return SEM_EINVAL;
+}
+
+extern "C" int sem_export_int(const sem_ctx* c, int which, int64_t* host_dst) {
+  if (!c || !host_dst) return SEM_EINVAL;
+  const size_t nl = (size_t)c->hp.n_local;
+  std::vector<uint8_t> tmp(nl);
+  if (which == 0) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(tmp.data(), c->d_mult, nl, cudaMemcpyDeviceToHost));
+  } else if (which == 1) {
+    uint8_t* d = nullptr;
+    SEM_TRY(dalloc(&d, nl));
+    CUDA_TRY(sem::launch_export_mask(c->dp, d, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(tmp.data(), d, nl, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  } else {
+    sem::set_error("sem_export_int: unknown field");
+    return SEM_EINVAL;
+  }
+  for (size_t l = 0; l < nl; l++) host_dst[l] = tmp[l];
+  return SEM_OK;
+}
+
+extern "C" int sem_nccl_unique_id(uint8_t id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  NCCL_TRY(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, 128);
+  return SEM_OK;
+}
+
+extern "C" int sem_nccl_comm_init(const uint8_t id[128], int rank, int nranks, void** comm) {
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t cm;
+  NCCL_TRY(ncclCommInitRank(&cm, nranks, u, rank));
+  *comm = cm;
+  return SEM_OK;
+}
+
+extern "C" int sem_nccl_comm_destroy(void* comm) {
+  if (comm) NCCL_TRY(ncclCommDestroy(static_cast<ncclComm_t>(comm)));
+  return SEM_OK;
+}
+
+extern "C" int sem_timing(sem_ctx* c, int enable) {
+  if (!c) return SEM_EINVAL;
+  timer_collect(c);
+  c->timing = enable != 0;
+  for (int q = 0; q < kTimerClasses; q++) { c->t_ms[q] = 0.0; c->t_cnt[q] = 0; }
+  return SEM_OK;
+}
+
+extern "C" int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t* count) {
+  if (!c || which < 0 || which >= kTimerClasses) return SEM_EINVAL;
+  timer_collect(c);
+  if (total_ms) *total_ms = c->t_ms[which];
+  if (count) *count = c->t_cnt[which];
+  return SEM_OK;
+}
+
+extern "C" int sem_launch_count(const sem_ctx* c, int64_t* n) {
+  if (!c || !n) return SEM_EINVAL;
+  *n = c->launches;
+  return SEM_OK;
+}

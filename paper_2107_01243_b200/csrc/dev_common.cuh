@@ -1,0 +1,134 @@
+// Device-side helpers shared by the libsem kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sem {
+namespace dev {
+
+// ---------------------------------------------------------------- PTX: mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA / bulk copy) accesses to the same buffer
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completion on mbarrier.
+// dst, src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed butterfly + serial over warps); blockDim a
+// multiple of 32; result valid in thread 0.  `scratch` >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int q = 0; q < nw; q++) s += scratch[q];
+  return s;
+}
+
+// Two-level deterministic grid reduction of NV values: every block writes its
+// partials (partial[b*NV + q]); the last block to finish (atomic ticket)
+// reduces them in a fixed order and writes out[q]; resets the ticket.
+// Returns true in the last block (after out[] is written by thread 0).
+template <int NV>
+__device__ __forceinline__ bool grid_reduce(const double (&v)[NV], double* partial,
+                                            unsigned* ticket, double* out, double* scratch,
+                                            int* s_flag) {
+  double bs[NV];
+#pragma unroll
+  for (int q = 0; q < NV; q++) bs[q] = block_sum(v[q], scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; q++) partial[(size_t)blockIdx.x * NV + q] = bs[q];
+    __threadfence();
+    unsigned t = atomicAdd(ticket, 1u);
+    *s_flag = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!*s_flag) return false;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; q++) acc[q] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NV; q++) acc[q] += __ldcg(&partial[(size_t)b * NV + q]);
+#pragma unroll
+  for (int q = 0; q < NV; q++) {
+    double s = block_sum(acc[q], scratch);
+    if (threadIdx.x == 0) out[q] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+  return true;
+}
+
+// slot-mask from the element's 6-bit Dirichlet face code (reading Q8)
+__device__ __forceinline__ bool face_masked(unsigned bm, int i, int j, int k, int nm1) {
+  return ((i == 0) && (bm & 1u)) || ((i == nm1) && (bm & 2u)) || ((j == 0) && (bm & 4u)) ||
+         ((j == nm1) && (bm & 8u)) || ((k == 0) && (bm & 16u)) || ((k == nm1) && (bm & 32u));
+}
+
+}  // namespace dev
+}  // namespace sem

@@ -1,0 +1,629 @@
+// Setup, gather-scatter and Krylov-vector kernels of libsem (sm_100a).
+//   geometry       P:L105 "geometric factors for mapping to and from the reference element" (reading Q5)
+//   gather-scatter P:L107-111 Eq. 10, Alg. 1, P:L231 (readings Q10, Q11)
+//   Jacobi-PCG     P:L257 (readings Q14-Q17)
+#include <cmath>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+#include "sem_internal.h"
+
+namespace sem {
+namespace dev {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double c_of(unsigned m) { return __drcp_rn((double)m); }
+
+// ---------------------------------------------------------------- geometry
+struct Box {
+  double x0, x1, y0, y1, z0, z1;
+};
+
+// node coordinates (reading Q4)
+__device__ __forceinline__ void node_xyz(const double* xi, int ex, int ey, int ez, int64_t e,
+                                         int i, int j, int k, const Box& b, int deform,
+                                         double amp, double* x) {
+  const int64_t cx = e % ex, cy = (e / ex) % ey, cz = e / ((int64_t)ex * ey);
+  const double hx = (b.x1 - b.x0) / ex, hy = (b.y1 - b.y0) / ey, hz = (b.z1 - b.z0) / ez;
+  double X = b.x0 + hx * ((double)cx + 0.5 * (xi[i] + 1.0));
+  double Y = b.y0 + hy * ((double)cy + 0.5 * (xi[j] + 1.0));
+  double Z = b.z0 + hz * ((double)cz + 0.5 * (xi[k] + 1.0));
+  if (deform) {
+    const double tp = 6.283185307179586476925286766559;
+    const double s = amp * sin(tp * (X - b.x0) / (b.x1 - b.x0)) *
+                     sin(tp * (Y - b.y0) / (b.y1 - b.y0)) * sin(tp * (Z - b.z0) / (b.z1 - b.z0));
+    X += s * (b.x1 - b.x0) / tp;
+    Y += s * (b.y1 - b.y0) / tp;
+    Z += s * (b.z1 - b.z0) / tp;
+  }
+  x[0] = X; x[1] = Y; x[2] = Z;
+}
+
+// one thread per slot: dx_a/dr_b through D on the isoparametric coordinates,
+// J = det, dr/dx by cofactors, G_ab = J w w w (dr_a/dx . dr_b/dx), B = J w w w
+__global__ void geom_kernel(int n, int64_t nslots, const double* __restrict__ xi,
+                            const double* __restrict__ wq, const double* __restrict__ D,
+                            int64_t e_lo, int ex, int ey, int ez, Box b, int deform, double amp,
+                            double* __restrict__ G, double* __restrict__ B, int* bad) {
+  const int64_t n3 = (int64_t)n * n * n;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nslots;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = l / n3;
+    const int p = (int)(l - el * n3);
+    const int i = p % n, j = (p / n) % n, k = p / (n * n);
+    const int64_t e = e_lo + el;
+    double M[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int m = 0; m < n; m++) {
+      double xr[3], xs[3], xt[3];
+      node_xyz(xi, ex, ey, ez, e, m, j, k, b, deform, amp, xr);
+      node_xyz(xi, ex, ey, ez, e, i, m, k, b, deform, amp, xs);
+      node_xyz(xi, ex, ey, ez, e, i, j, m, b, deform, amp, xt);
+      const double di = D[i * n + m], dj = D[j * n + m], dk = D[k * n + m];
+      for (int a = 0; a < 3; a++) {
+        M[a][0] = fma(di, xr[a], M[a][0]);
+        M[a][1] = fma(dj, xs[a], M[a][1]);
+        M[a][2] = fma(dk, xt[a], M[a][2]);
+      }
+    }
+    const double c00 = M[1][1] * M[2][2] - M[1][2] * M[2][1];
+    const double c01 = M[1][2] * M[2][0] - M[1][0] * M[2][2];
+    const double c02 = M[1][0] * M[2][1] - M[1][1] * M[2][0];
+    const double J = M[0][0] * c00 + M[0][1] * c01 + M[0][2] * c02;
+    if (!(J > 0.0)) {
+      atomicMax(bad, 1);
+      continue;
+    }
+    const double iJ = 1.0 / J;
+    double R[3][3];  // R[b][a] = d r_b / d x_a = cof(M)[a][b] / J
+    R[0][0] = c00 * iJ;
+    R[1][0] = c01 * iJ;
+    R[2][0] = c02 * iJ;
+    R[0][1] = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) * iJ;
+    R[1][1] = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) * iJ;
+    R[2][1] = (M[0][1] * M[2][0] - M[0][0] * M[2][1]) * iJ;
+    R[0][2] = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) * iJ;
+    R[1][2] = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) * iJ;
+    R[2][2] = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * iJ;
+    const double Jw = J * wq[i] * wq[j] * wq[k];
+    const int ab[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};
+    double* Ge = G + el * 6 * n3;
+    for (int f = 0; f < 6; f++) {
+      const int x = ab[f][0], y = ab[f][1];
+      Ge[f * n3 + p] = Jw * (R[x][0] * R[y][0] + R[x][1] * R[y][1] + R[x][2] * R[y][2]);
+    }
+    B[l] = Jw;
+  }
+}
+
+__global__ void coords_kernel(int n, int64_t nslots, const double* __restrict__ xi, int64_t e_lo,
+                              int ex, int ey, int ez, Box b, int deform, double amp,
+                              double* X, double* Y, double* Z) {
+  const int64_t n3 = (int64_t)n * n * n;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nslots;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = l / n3;
+    const int p = (int)(l - el * n3);
+    double x[3];
+    node_xyz(xi, ex, ey, ez, e_lo + el, p % n, (p / n) % n, p / (n * n), b, deform, amp, x);
+    X[l] = x[0]; Y[l] = x[1]; Z[l] = x[2];
+  }
+}
+
+// element diagonal of D^T G D (reading Q14)
+__global__ void diag_kernel(int n, int64_t nslots, const double* __restrict__ D,
+                            const double* __restrict__ G, double* __restrict__ d) {
+  const int64_t n3 = (int64_t)n * n * n;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nslots;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = l / n3;
+    const int p = (int)(l - el * n3);
+    const int i = p % n, j = (p / n) % n, k = p / (n * n);
+    const double* Ge = G + el * 6 * n3;
+    double s = 0.0;
+    for (int m = 0; m < n; m++) {
+      const double a = D[m * n + i], b2 = D[m * n + j], c = D[m * n + k];
+      s = fma(a * a, Ge[0 * n3 + m + n * j + n * n * k], s);
+      s = fma(b2 * b2, Ge[1 * n3 + i + n * m + n * n * k], s);
+      s = fma(c * c, Ge[2 * n3 + i + n * j + n * n * m], s);
+    }
+    const double dii = D[i * n + i], djj = D[j * n + j], dkk = D[k * n + k];
+    s += 2.0 * (Ge[3 * n3 + p] * dii * djj + Ge[4 * n3 + p] * dii * dkk + Ge[5 * n3 + p] * djj * dkk);
+    d[l] = s;
+  }
+}
+
+__device__ __forceinline__ bool slot_mask(const DevPlan& P, int64_t l) {
+  const int n = P.n;
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t el = l / n3;
+  const int p = (int)(l - el * n3);
+  return face_masked(P.bmask[el], p % n, (p / n) % n, p / (n * n), n - 1);
+}
+
+__global__ void invert_mask_kernel(const DevPlan P, double* d) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < P.n_local;
+       l += (int64_t)gridDim.x * blockDim.x)
+    d[l] = slot_mask(P, l) ? 0.0 : 1.0 / d[l];
+}
+
+__global__ void mask_kernel(const DevPlan P, double* u) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < P.n_local;
+       l += (int64_t)gridDim.x * blockDim.x)
+    if (slot_mask(P, l)) u[l] = 0.0;
+}
+
+__global__ void export_mask_kernel(const DevPlan P, uint8_t* m) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < P.n_local;
+       l += (int64_t)gridDim.x * blockDim.x)
+    m[l] = slot_mask(P, l) ? 1 : 0;
+}
+
+__global__ void scale_kernel(const double* __restrict__ B, const double* __restrict__ f,
+                             double* __restrict__ b, int64_t n) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x)
+    b[l] = B[l] * f[l];
+}
+
+__global__ void sub_scalar_kernel(double* a, const double* scal, int64_t n) {
+  // scal[0] = sum_l c_l b_l, scal[1] = sum_l c_l  -> subtract the unique-DOF mean
+  const double mean = scal[0] / scal[1];
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x)
+    a[l] -= mean;
+}
+
+// ---------------------------------------------------------------- gather-scatter
+__device__ __forceinline__ int f_s1(int axis, int n) { return axis == 0 ? n : 1; }
+__device__ __forceinline__ int f_s2(int axis, int n) { return axis == 2 ? n : n * n; }
+__device__ __forceinline__ int e_sd(int axis, int n) { return axis == 0 ? 1 : (axis == 1 ? n : n * n); }
+
+// Multiplicity per slot (uint8): 1 everywhere, nin on entity points, the global
+// incidence count on shared points.
+__global__ void mult_kernel(const DevPlan P, uint8_t* mult) {
+  const int n = P.n, N = n - 1;
+  const int64_t nf = (int64_t)(N - 1) * (N - 1), ne = N - 1;
+  const int64_t tF = P.nF * nf, tE = P.nEd * ne, tot = tF + tE + P.nV + P.nS;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < tF) {
+      const int64_t f = t / nf;
+      const int p = (int)(t - f * nf);
+      const int ax = P.f_axis[f];
+      const int off = (1 + p % (N - 1)) * f_s1(ax, n) + (1 + p / (N - 1)) * f_s2(ax, n);
+      mult[P.f_base[2 * f] + off] = 2;
+      mult[P.f_base[2 * f + 1] + off] = 2;
+    } else if (t < tF + tE) {
+      const int64_t q = t - tF, e = q / ne;
+      const int p = (int)(q - e * ne);
+      const int off = (1 + p) * e_sd(P.e_axis[e], n);
+      for (int x = 0; x < P.e_nin[e]; x++) mult[P.e_base[4 * e + x] + off] = P.e_nin[e];
+    } else if (t < tF + tE + P.nV) {
+      const int64_t v = t - tF - tE;
+      for (int x = 0; x < P.v_nin[v]; x++) mult[P.v_base[8 * v + x]] = P.v_nin[v];
+    } else {
+      const int64_t s = t - tF - tE - P.nV;
+      for (int x = 0; x < P.s_nloc[s]; x++) mult[P.s_slot[(int64_t)x * P.nS + s]] = P.s_mult[s];
+    }
+  }
+}
+
+// standalone gs over the rank-local entities: one thread per entity point,
+// ascending-slot sum, broadcast write (no atomics)
+__global__ void gs_local_kernel(const DevPlan P, double* __restrict__ u, int apply_mask) {
+  const int n = P.n, N = n - 1;
+  const int64_t nf = (int64_t)(N - 1) * (N - 1), ne = N - 1;
+  const int64_t tF = P.nF * nf, tE = P.nEd * ne, tot = tF + tE + P.nV;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t base[8];
+    int nin, off;
+    bool mk = false;
+    if (t < tF) {
+      const int64_t f = t / nf;
+      const int p = (int)(t - f * nf);
+      const int ax = P.f_axis[f];
+      off = (1 + p % (N - 1)) * f_s1(ax, n) + (1 + p / (N - 1)) * f_s2(ax, n);
+      nin = 2;
+      base[0] = P.f_base[2 * f];
+      base[1] = P.f_base[2 * f + 1];
+    } else if (t < tF + tE) {
+      const int64_t q = t - tF, e = q / ne;
+      const int p = (int)(q - e * ne);
+      off = (1 + p) * e_sd(P.e_axis[e], n);
+      nin = P.e_nin[e];
+      for (int x = 0; x < 4; x++) base[x] = P.e_base[4 * e + x];
+      mk = P.e_mask[e];
+    } else {
+      const int64_t v = t - tF - tE;
+      off = 0;
+      nin = P.v_nin[v];
+      for (int x = 0; x < 8; x++) base[x] = P.v_base[8 * v + x];
+      mk = P.v_mask[v];
+    }
+    double s = u[base[0] + off];
+    for (int x = 1; x < nin; x++) s += u[base[x] + off];
+    if (apply_mask && mk) s = 0.0;
+    for (int x = 0; x < nin; x++) u[base[x] + off] = s;
+  }
+}
+
+// Alg. 1 lines 6-7: this rank's partial for every shared point (ascending local
+// slots), copied into the send buffer of every neighbour that shares it.
+__global__ void gs_pack_kernel(const DevPlan P, const double* __restrict__ u, double* part,
+                               double* sendbuf) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.nS;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int nl = P.s_nloc[s];
+    double v = u[P.s_slot[s]];
+    for (int x = 1; x < nl; x++) v += u[P.s_slot[(int64_t)x * P.nS + s]];
+    part[s] = v;
+    const int nr = P.s_nr[s];
+    for (int x = 0; x < nr; x++) {
+      const int o = P.s_off[(int64_t)x * P.nS + s];
+      if (o >= 0) sendbuf[o] = v;
+    }
+  }
+}
+
+// Alg. 1 lines 10-18: total = sum of the rank partials in ascending rank order
+// (reading Q10, deterministic), scattered to every local slot.  Thread 0 also
+// combines the split sigma partials of the PCG operator (fixed order).
+__global__ void gs_unpack_kernel(const DevPlan P, double* __restrict__ u, const double* part,
+                                 const double* recvbuf, int apply_mask, PcgState* st, int nparts) {
+  if (st && blockIdx.x == 0 && threadIdx.x == 0) {
+    double sg = st->sigma_part[0];
+    for (int q = 1; q < nparts; q++) sg += st->sigma_part[q];
+    st->sigma = sg;
+  }
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.nS;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int nr = P.s_nr[s];
+    double tot = 0.0;
+    for (int x = 0; x < nr; x++) {
+      const int o = P.s_off[(int64_t)x * P.nS + s];
+      const double v = o < 0 ? part[s] : recvbuf[o];
+      tot = x == 0 ? v : tot + v;
+    }
+    if (apply_mask && P.s_mask[s]) tot = 0.0;
+    const int nl = P.s_nloc[s];
+    for (int x = 0; x < nl; x++) u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
+  }
+}
+
+// ---------------------------------------------------------------- reductions
+__global__ void dot_c_kernel(int64_t n, const uint8_t* __restrict__ mult,
+                             const double* __restrict__ a, const double* __restrict__ b,
+                             double* partial, unsigned* ticket, double* out) {
+  __shared__ double scratch[32];
+  __shared__ int flag;
+  double s = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x)
+    s = fma(c_of(mult[l]) * a[l], b[l], s);
+  double v[1] = {s};
+  grid_reduce<1>(v, partial, ticket, out, scratch, &flag);
+}
+
+// out2[0] = sum_l c_l a_l, out2[1] = sum_l c_l
+__global__ void sum_c_kernel(int64_t n, const uint8_t* __restrict__ mult,
+                             const double* __restrict__ a, double* partial, unsigned* ticket,
+                             double* out2) {
+  __shared__ double scratch[32];
+  __shared__ int flag;
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double c = c_of(mult[l]);
+    s0 = fma(c, a[l], s0);
+    s1 += c;
+  }
+  double v[2] = {s0, s1};
+  grid_reduce<2>(v, partial, ticket, out2, scratch, &flag);
+}
+
+// ---------------------------------------------------------------- Jacobi-PCG
+// init: x = 0, r = b, p = z = dinv .* b; partials of <r,z>_c and <r,r>_c
+__global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint8_t* __restrict__ mult,
+                               const double* __restrict__ dinv, const double* __restrict__ b,
+                               double* __restrict__ x, double* __restrict__ r,
+                               double* __restrict__ p, double* partial, PcgState* st) {
+  __shared__ double scratch[32];
+  __shared__ int flag;
+  double rz = 0.0, rr = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double bl = b[l], z = dinv[l] * bl, c = c_of(mult[l]);
+    x[l] = 0.0;
+    r[l] = bl;
+    p[l] = z;
+    rz = fma(c * bl, z, rz);
+    rr = fma(c * bl, bl, rr);
+  }
+  double v[2] = {rz, rr};
+  grid_reduce<2>(v, partial, &st->tickets[1], &st->rho_new, scratch, &flag);
+}
+
+__global__ void cg_start_kernel(PcgState* st, double* hist) {
+  st->rho_old = st->rho_new;
+  st->it = 0;
+  const double g = sqrt(st->gamma);
+  hist[0] = g;
+  st->done = (g <= st->tol) ? 1 : (st->maxit == 0 ? 4 : 0);
+  st->iters = 0;
+}
+
+// alpha = rho / sigma; x += alpha p; r -= alpha w; partials of
+// rho' = <r, dinv r>_c and gamma = <r, r>_c (z is never stored)
+__global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
+                                 const double* __restrict__ dinv, double* __restrict__ x,
+                                 double* __restrict__ r, const double* __restrict__ p,
+                                 const double* __restrict__ w, double* partial, PcgState* st) {
+  __shared__ double scratch[32];
+  __shared__ int flag;
+  if (st->done) return;
+  const double sigma = st->sigma;
+  const bool ok = sigma > 0.0;   // breakdown guard (also catches NaN)
+  const double alpha = ok ? st->rho_old / sigma : 0.0;
+  double rz = 0.0, rr = 0.0;
+  if (ok) {
+    const int64_t n2 = n >> 1;
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    const double2* d2 = reinterpret_cast<const double2*>(dinv);
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const uchar2* m2 = reinterpret_cast<const uchar2*>(mult);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const double2 pv = __ldcs(&p2[q]);
+      const double2 wv = __ldcs(&w2[q]);
+      const double2 dv = __ldcs(&d2[q]);
+      double2 xv = __ldcs(&x2[q]);
+      double2 rv = __ldcs(&r2[q]);
+      const uchar2 mv = m2[q];
+      xv.x = fma(alpha, pv.x, xv.x);
+      xv.y = fma(alpha, pv.y, xv.y);
+      rv.x = fma(-alpha, wv.x, rv.x);
+      rv.y = fma(-alpha, wv.y, rv.y);
+      __stcs(&x2[q], xv);
+      __stcg(&r2[q], rv);
+      const double c0 = c_of(mv.x), c1 = c_of(mv.y);
+      rz = fma(c0 * rv.x, dv.x * rv.x, rz);
+      rz = fma(c1 * rv.y, dv.y * rv.y, rz);
+      rr = fma(c0 * rv.x, rv.x, rr);
+      rr = fma(c1 * rv.y, rv.y, rr);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t l = n - 1;
+      x[l] = fma(alpha, p[l], x[l]);
+      const double rl = fma(-alpha, w[l], r[l]);
+      r[l] = rl;
+      const double c = c_of(mult[l]);
+      rz = fma(c * rl, dinv[l] * rl, rz);
+      rr = fma(c * rl, rl, rr);
+    }
+  }
+  double v[2] = {rz, rr};
+  if (grid_reduce<2>(v, partial, &st->tickets[2], &st->rho_new, scratch, &flag)) {
+    if (threadIdx.x == 0 && !ok) {
+      st->done = 2;
+      st->iters = st->it + 1;
+    }
+  }
+}
+
+// convergence test on sqrt(gamma); p = dinv .* r + beta p with beta = rho'/rho
+__global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double* __restrict__ dinv,
+                            const double* __restrict__ r, double* __restrict__ p, PcgState* st,
+                            double* hist) {
+  __shared__ int flag;
+  if (st->done) return;
+  const double g = sqrt(st->gamma);
+  const bool conv = g <= st->tol;
+  const bool bad = !(g == g) || !(st->rho_new == st->rho_new);
+  if (!conv && !bad) {
+    const double beta = st->rho_new / st->rho_old;
+    const int64_t n2 = n >> 1;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const double2* d2 = reinterpret_cast<const double2*>(dinv);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const double2 rv = __ldcg(&r2[q]);
+      const double2 dv = __ldcs(&d2[q]);
+      double2 pv = __ldcs(&p2[q]);
+      pv.x = fma(beta, pv.x, dv.x * rv.x);
+      pv.y = fma(beta, pv.y, dv.y * rv.y);
+      p2[q] = pv;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t l = n - 1;
+      p[l] = fma(beta, p[l], dinv[l] * r[l]);
+    }
+  }
+  // last block advances the iteration state
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(&st->tickets[3], 1u);
+    flag = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (flag && threadIdx.x == 0) {
+    st->tickets[3] = 0u;
+    const int it = st->it + 1;
+    st->it = it;
+    hist[it] = g;
+    if (bad) {
+      st->done = 3;
+      st->iters = it;
+    } else if (conv) {
+      st->done = 1;
+      st->iters = it;
+    } else {
+      st->rho_old = st->rho_new;
+      if (it >= st->maxit) {
+        st->done = 4;
+        st->iters = it;
+      }
+    }
+  }
+}
+
+// true residual: sqrt(sum c (b - A x)^2) -> st->res_true (after allreduce by the host)
+__global__ void cg_residual_kernel(int64_t n, const uint8_t* __restrict__ mult,
+                                   const double* __restrict__ b, const double* __restrict__ w,
+                                   double* partial, PcgState* st) {
+  __shared__ double scratch[32];
+  __shared__ int flag;
+  double s = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double d = b[l] - w[l];
+    s = fma(c_of(mult[l]) * d, d, s);
+  }
+  double v[1] = {s};
+  grid_reduce<1>(v, partial, &st->tickets[4], &st->res_true, scratch, &flag);
+}
+
+inline int grid_for(int64_t work, int cap = 148 * 8) {
+  int64_t g = (work + kThreads - 1) / kThreads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace dev
+
+using dev::kThreads;
+using dev::grid_for;
+
+cudaError_t launch_geom(const DevPlan& P, const double* xi, const double* wq, int64_t e_lo, int ex,
+                        int ey, int ez, const double* box, int deform, double amp, double* G,
+                        double* B, int* bad, cudaStream_t s) {
+  dev::Box b{box[0], box[1], box[2], box[3], box[4], box[5]};
+  dev::geom_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P.n, P.n_local, xi, wq, P.D, e_lo, ex,
+                                                            ey, ez, b, deform, amp, G, B, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coords(const DevPlan& P, const double* xi, int64_t e_lo, int ex, int ey, int ez,
+                          const double* box, int deform, double amp, double* X, double* Y,
+                          double* Z, cudaStream_t s) {
+  dev::Box b{box[0], box[1], box[2], box[3], box[4], box[5]};
+  dev::coords_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P.n, P.n_local, xi, e_lo, ex, ey, ez,
+                                                              b, deform, amp, X, Y, Z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diag(const DevPlan& P, const double* G, double* d, cudaStream_t s) {
+  dev::diag_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P.n, P.n_local, P.D, G, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mult(const DevPlan& P, uint8_t* mult, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(mult, 1, (size_t)P.n_local, s);
+  if (e != cudaSuccess) return e;
+  const int64_t N = P.N;
+  const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV + P.nS;
+  if (tot == 0) return cudaSuccess;
+  dev::mult_kernel<<<grid_for(tot), kThreads, 0, s>>>(P, mult);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_invert_mask(const DevPlan& P, double* d, cudaStream_t s) {
+  dev::invert_mask_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask(const DevPlan& P, double* u, cudaStream_t s) {
+  dev::mask_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P, u);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_mask(const DevPlan& P, uint8_t* m, cudaStream_t s) {
+  dev::export_mask_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale(const double* B, const double* f, double* b, int64_t n, cudaStream_t s) {
+  dev::scale_kernel<<<grid_for(n), kThreads, 0, s>>>(B, f, b, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStream_t s) {
+  dev::sub_scalar_kernel<<<grid_for(n), kThreads, 0, s>>>(a, scal, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, cudaStream_t s) {
+  const int64_t N = P.N;
+  const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
+  if (tot == 0) return cudaSuccess;
+  dev::gs_local_kernel<<<grid_for(tot), kThreads, 0, s>>>(P, u, apply_mask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs_pack(const DevPlan& P, const double* u, double* part, double* sendbuf,
+                           cudaStream_t s) {
+  if (P.nS == 0) return cudaSuccess;
+  dev::gs_pack_kernel<<<grid_for(P.nS), kThreads, 0, s>>>(P, u, part, sendbuf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs_unpack(const DevPlan& P, double* u, const double* part, const double* recvbuf,
+                             int apply_mask, PcgState* st, int nparts, cudaStream_t s) {
+  dev::gs_unpack_kernel<<<grid_for(P.nS > 0 ? P.nS : 1), kThreads, 0, s>>>(P, u, part, recvbuf,
+                                                                          apply_mask, st, nparts);
+  return cudaGetLastError();
+}
+
+int cg_grid(int num_sms) { return num_sms * 4; }
+
+cudaError_t launch_dot_c(const DevPlan& P, const uint8_t* mult, const double* a, const double* b,
+                         double* partial, unsigned* ticket, double* out, int grid, cudaStream_t s) {
+  dev::dot_c_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, a, b, partial, ticket, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a, double* partial,
+                         unsigned* ticket, double* out2, int grid, cudaStream_t s) {
+  dev::sum_c_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, a, partial, ticket, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv, const double* b,
+                           double* x, double* r, double* p, double* partial, PcgState* st, int grid,
+                           cudaStream_t s) {
+  dev::cg_init_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, b, x, r, p, partial, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s) {
+  dev::cg_start_kernel<<<1, 1, 0, s>>>(st, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
+                             double* r, const double* p, const double* w, double* partial,
+                             PcgState* st, int grid, cudaStream_t s) {
+  dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, x, r, p, w, partial, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
+                        PcgState* st, double* hist, int grid, cudaStream_t s) {
+  dev::cg_p_kernel<<<grid, kThreads, 0, s>>>(P.n_local, dinv, r, p, st, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
+                               const double* w, double* partial, PcgState* st, int grid,
+                               cudaStream_t s) {
+  dev::cg_residual_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, b, w, partial, st);
+  return cudaGetLastError();
+}
+
+}  // namespace sem

@@ -1,0 +1,112 @@
+// Launchers for the libsem CUDA kernels (called from api.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sem {
+
+// kernel modes of the element operator
+enum AxMode { AX_ONLY = 0, AX_APPLY = 1, AX_PCG = 2 };
+
+// device view of the gather-scatter plan
+struct DevPlan {
+  int N = 0, n = 0, nloc = 0;
+  int64_t n_local = 0;
+  int nF = 0, nEd = 0, nV = 0, nS = 0;
+  const double* D = nullptr;        // [n*n]
+  const uint8_t* bmask = nullptr;   // [nloc]
+  const int32_t* eref = nullptr;    // [nloc*26]
+  const int32_t* f_base = nullptr;  // [nF][2]
+  const uint8_t* f_axis = nullptr;
+  const int32_t* e_base = nullptr;  // [nEd][4]
+  const uint8_t* e_axis = nullptr;
+  const uint8_t* e_nin = nullptr;
+  const uint8_t* e_mask = nullptr;
+  const int32_t* v_base = nullptr;  // [nV][8]
+  const uint8_t* v_nin = nullptr;
+  const uint8_t* v_mask = nullptr;
+  unsigned* cnt = nullptr;          // [nF + nEd + nV] last-arriver tickets
+  // shared points (P > 1)
+  const int32_t* s_slot = nullptr;  // [8][nS]
+  const int32_t* s_off = nullptr;   // [8][nS]
+  const uint8_t* s_nloc = nullptr;
+  const uint8_t* s_nr = nullptr;
+  const uint8_t* s_mask = nullptr;
+  const uint8_t* s_mult = nullptr;
+};
+
+// PCG scalars, resident on the device (no per-iteration host sync)
+struct PcgState {
+  double sigma;          // <p, A p>
+  double rho_old;        // <r, z>_c of the previous iteration
+  double rho_new;        // <r, z>_c   (rho_new, gamma adjacent: one allreduce)
+  double gamma;          // <r, r>_c
+  double tol;
+  double res_true;
+  double sigma_part[2];  // per Ax launch when the operator is split (Alg. 1 overlap)
+  int it;                // completed iterations
+  int done;              // 0 running, 1 converged, 2 breakdown, 3 NaN, 4 maxit
+  int iters;
+  int maxit;
+  unsigned tickets[8];   // last-block tickets
+};
+
+struct AxLaunch {
+  const double* u;
+  double* w;
+  const double* G;
+  int r0lo, r0hi, r1lo, r1hi;     // element ranges (local indices)
+  double* red_partial;            // PCG: per-block partials
+  unsigned* red_ticket;
+  double* red_out;
+  const int* done;
+};
+
+// returns max resident CTAs/SM for the Ax kernel of this N and mode
+int ax_occupancy(int N, int mode);
+cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s);
+int ax_groups(int N, int nelem);   // element groups processed per launch
+
+// setup
+cudaError_t launch_geom(const DevPlan& P, const double* xi, const double* wq, int64_t e_lo,
+                        int ex, int ey, int ez, const double* box, int deform, double amp,
+                        double* G, double* B, int* bad, cudaStream_t s);
+cudaError_t launch_coords(const DevPlan& P, const double* xi, int64_t e_lo, int ex, int ey, int ez,
+                          const double* box, int deform, double amp, double* X, double* Y,
+                          double* Z, cudaStream_t s);
+cudaError_t launch_diag(const DevPlan& P, const double* G, double* d, cudaStream_t s);
+cudaError_t launch_mult(const DevPlan& P, uint8_t* mult, cudaStream_t s);
+cudaError_t launch_invert_mask(const DevPlan& P, double* d, cudaStream_t s);
+cudaError_t launch_scale(const double* B, const double* f, double* b, int64_t n, cudaStream_t s);
+cudaError_t launch_mask(const DevPlan& P, double* u, cudaStream_t s);
+cudaError_t launch_export_mask(const DevPlan& P, uint8_t* m, cudaStream_t s);
+
+// gather-scatter (standalone)
+cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, cudaStream_t s);
+cudaError_t launch_gs_pack(const DevPlan& P, const double* u, double* part, double* sendbuf,
+                           cudaStream_t s);
+cudaError_t launch_gs_unpack(const DevPlan& P, double* u, const double* part,
+                             const double* recvbuf, int apply_mask, PcgState* st, int nparts,
+                             cudaStream_t s);
+
+// reductions / CG vector kernels
+int cg_grid(int num_sms);
+cudaError_t launch_dot_c(const DevPlan& P, const uint8_t* mult, const double* a, const double* b,
+                         double* partial, unsigned* ticket, double* out, int grid, cudaStream_t s);
+cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a, double* partial,
+                         unsigned* ticket, double* out2, int grid, cudaStream_t s);
+cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStream_t s);
+cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv,
+                           const double* b, double* x, double* r, double* p, double* partial,
+                           PcgState* st, int grid, cudaStream_t s);
+cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s);
+cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
+                             double* r, const double* p, const double* w, double* partial,
+                             PcgState* st, int grid, cudaStream_t s);
+cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
+                        PcgState* st, double* hist, int grid, cudaStream_t s);
+cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
+                               const double* w, double* partial, PcgState* st, int grid,
+                               cudaStream_t s);
+
+}  // namespace sem

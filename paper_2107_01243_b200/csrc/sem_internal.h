@@ -1,0 +1,62 @@
+// Internal declarations of libsem (B200-native SEM Poisson hot path).
+// Host planner (plan.cpp), device kernels (*.cu) and the C ABI (api.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sem.h"
+
+namespace sem {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+// ---------------------------------------------------------------- entities
+// The gather-scatter plan is entity based: every
+// element face, edge and vertex shared by >= 2 elements is one entity; its
+// points are the face/edge interior nodes (or the vertex).  All incidences
+// of an entity see the same point parametrisation (conforming, aligned hex
+// box mesh), so a point's slot in incidence t is base[t] + offset(kind, p).
+enum EntClass { CLS_FACE = 0, CLS_EDGE = 1, CLS_VERT = 2 };
+constexpr int kRefsPerElem = 26;   // 6 faces + 12 edges + 8 vertices
+constexpr int kClsShift = 28;      // ref = (cls << 28) | index
+
+struct HostPlan {
+  sem_mesh m{};
+  int N = 0, n = 0;
+  int64_t n3 = 0;
+  int64_t E = 0, e_lo = 0, e_hi = 0, nloc = 0, n_local = 0, nglob = 0;
+  int rank = 0, nranks = 1;
+  bool fully_periodic = false;
+  std::vector<double> xi, w, D;           // GLL rule, D[i*n+j] = l_j'(xi_i)
+  std::vector<uint8_t> bmask;             // [nloc] bit (2a+b): face (axis a, side b) Dirichlet
+  std::vector<int32_t> eref;              // [nloc*26] local-entity refs, -1 none
+  // local entities (all incidences on this rank), SoA
+  int64_t nF = 0, nEd = 0, nV = 0;
+  std::vector<int32_t> f_base;            // [2][nF]
+  std::vector<uint8_t> f_axis;            // [nF] face normal axis
+  std::vector<int32_t> e_base;            // [4][nEd]
+  std::vector<uint8_t> e_axis, e_nin, e_mask;
+  std::vector<int32_t> v_base;            // [8][nV]
+  std::vector<uint8_t> v_nin, v_mask;
+  // shared points (some incidence on another rank), ascending gid
+  int64_t nS = 0;
+  std::vector<int64_t> s_gid;
+  std::vector<int32_t> s_slot;            // [8][nS] local slots ascending (-1 pad)
+  std::vector<uint8_t> s_nloc, s_mult, s_mask, s_nr;
+  std::vector<int32_t> s_off;             // [8][nS] per involved rank (ascending): -1 self, else buffer index
+  std::vector<int32_t> nbr_rank;
+  std::vector<int64_t> nbr_off, nbr_cnt;
+  int64_t nbuf = 0;
+  // Alg. 1 overlap: boundary elements [b0lo,b0hi) U [b1lo,b1hi), interior [ilo,ihi)
+  int64_t b0lo = 0, b0hi = 0, b1lo = 0, b1hi = 0, ilo = 0, ihi = 0;
+};
+
+int build_plan(const sem_mesh* m, int N, HostPlan* p);   // returns SEM_* status
+void gll_rule(int N, std::vector<double>* xi, std::vector<double>* w);
+void deriv_matrix(int N, const std::vector<double>& xi, std::vector<double>* D);
+int64_t lattice_gid(const HostPlan& p, int64_t e_global, int i, int j, int k);
+bool slot_masked(const HostPlan& p, int64_t e_global, int i, int j, int k);
+
+}  // namespace sem

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  * integer / index work (multiplicity, mask): bit-exact;
+  * gather-scatter: bit-exact (both sides add the same operands in ascending
+    slot order, rank-ordered partials);
+  * Ax, apply, rhs, geometry: normwise relative ||y_gpu - y_ref||_inf /
+    ||y_ref||_inf <= 1e-12 (reading Q22);
+  * PCG: iteration count +-1, final residuals and solution within 1e-10 (abs).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from sem_inputs import (CONFIGS, MeshSpec, f_sin, f_tgv, random_field, tgv_box, unit_box,
+                        weak_scaled)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2107_01243_b200 import build
+    build.build()
+    torch.cuda.set_device(0)
+
+
+def sem():
+    import paper_2107_01243_b200 as s
+    return s
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def nrel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+MESHES = [
+    (CONFIGS["C1"][0], 3),                       # Dirichlet, 8 elements
+    (unit_box(3, 2, 5, periodic=(1, 0, 0)), 7),  # mixed BC, 30 elements
+    (tgv_box(4, 3, 5, deform=1), 7),             # curvilinear, all 6 G
+    (tgv_box(2, 2, 2), 1),                       # N=1: vertices only
+    (unit_box(5, 2, 1), 2),                      # ragged tail for NE=8 (n=3)
+    (tgv_box(3, 3, 3, deform=1), 4),
+    (unit_box(2, 3, 2, periodic=(0, 1, 1)), 5),
+    (tgv_box(2, 2, 3, deform=1), 11),            # maximum N
+    (unit_box(3, 3, 2), 9),
+]
+IDS = [f"{s.ex}x{s.ey}x{s.ez}-p{''.join(map(str, s.periodic))}-d{s.deform}-N{N}" for s, N in MESHES]
+
+
+@pytest.mark.parametrize("spec,N", MESHES, ids=IDS)
+def test_setup_exports(spec, N):
+    o = O.Oracle(spec, N)
+    with sem().sem_setup(spec, N) as c:
+        assert c.n_local == o.nslots and c.n_glob == o.nglob
+        assert np.array_equal(c.export_int("mult"), o.get_int("mult"))
+        assert np.array_equal(c.export_int("mask"), o.get_int("mask"))
+        assert nrel(c.export_field("G"), o.get("G")) < 1e-12
+        assert nrel(c.export_field("B"), o.get("B")) < 1e-12
+        assert nrel(c.export_field("dinv"), o.get("dinv")) < 1e-12
+        X, Y, Z = c.coords()
+        for t, name in zip((X, Y, Z), "XYZ"):
+            assert np.abs(host(t) - o.get(name)).max() < 1e-13
+
+
+@pytest.mark.parametrize("spec,N", MESHES, ids=IDS)
+def test_ax_gs_apply_parity(spec, N):
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=11)
+    with sem().sem_setup(spec, N) as c:
+        du, dw = dev(u), c.zeros()
+        c.ax(du, dw)
+        w_ax = host(dw)
+        assert nrel(w_ax, o.ax(u)) <= 1e-12
+        # gather-scatter: bit-exact (same operands, same ascending order)
+        dv = dev(u)
+        c.gs(dv)
+        assert np.array_equal(host(dv), o.gs(u))
+        # fused Ax + gs + mask
+        dw.zero_()
+        c.apply(du, dw)
+        w_ap, ref = host(dw), o.apply(u)
+        assert nrel(w_ap, ref) <= 1e-12
+        assert np.all(w_ap[o.get_int("mask") == 1] == 0.0)
+        # continuity: every slot of a gid holds the same value, exactly
+        gid = o.get_int("gid")
+        first = np.zeros(o.nglob)
+        first[gid] = w_ap
+        assert np.array_equal(first[gid], w_ap)
+
+
+def test_apply_is_deterministic_and_repeatable():
+    spec, N = tgv_box(6, 5, 4, deform=1), 7
+    u = random_field(spec.n_slots(N), seed=5)
+    with sem().sem_setup(spec, N) as c:
+        du = dev(u)
+        outs = []
+        for _ in range(3):
+            w = c.zeros()
+            c.apply(du, w)
+            outs.append(host(w))
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("cfg", ["C2"])
+def test_full_size_c2_apply(cfg):
+    """BASELINE configs[1] at full size (8192 elements, N=7), the bench workload."""
+    spec, N = CONFIGS[cfg]
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=0)
+    with sem().sem_setup(spec, N) as c:
+        du, dw = dev(u), c.zeros()
+        c.ax(du, dw)
+        assert nrel(host(dw), o.ax(u)) <= 1e-12
+        c.apply(du, dw)
+        assert nrel(host(dw), o.apply(u)) <= 1e-12
+
+
+@pytest.mark.parametrize("spec,N,fun", [(CONFIGS["C1"][0], 3, f_sin), (tgv_box(4, 4, 3), 5, f_tgv),
+                                        (tgv_box(3, 4, 3, deform=1), 6, f_tgv),
+                                        (unit_box(2, 3, 2, periodic=(0, 1, 1)), 5, f_sin)])
+def test_rhs_parity(spec, N, fun):
+    o = O.Oracle(spec, N)
+    f = fun(o.get("X"), o.get("Y"), o.get("Z"))
+    with sem().sem_setup(spec, N) as c:
+        b = c.zeros()
+        c.rhs(dev(f), b)
+        assert nrel(host(b), o.rhs(f)) <= 1e-12
+
+
+PCG_CASES = [
+    (CONFIGS["C1"][0], 3, f_sin, 1e-10),
+    (tgv_box(8, 8, 8), 7, f_tgv, 1e-10),           # reduced C3
+    (tgv_box(6, 6, 6, deform=1), 5, f_tgv, 1e-10),  # reduced C4 (curvilinear)
+    (unit_box(3, 2, 4, periodic=(1, 0, 0)), 6, f_sin, 1e-10),
+]
+
+
+@pytest.mark.parametrize("spec,N,fun,tol", PCG_CASES)
+def test_pcg_parity(spec, N, fun, tol):
+    o = O.Oracle(spec, N)
+    f = fun(o.get("X"), o.get("Y"), o.get("Z"))
+    b = o.rhs(f)
+    ref = o.pcg(b, tol, 5000)
+    with sem().sem_setup(spec, N) as c:
+        x = c.zeros()
+        r = c.pcg_solve(dev(b), x, tol, 5000)
+        xs = host(x)
+        assert r["status"] == 0 and ref["status"] == 0
+        assert abs(r["iters"] - ref["iters"]) <= 1
+        assert abs(r["res_final"] - ref["res_final"]) <= 1e-10
+        assert abs(r["res_true"] - ref["res_true"]) <= 1e-10
+        assert r["res_final"] <= tol
+        assert np.abs(xs - ref["x"]).max() <= 1e-10
+        # residual history: same trajectory while the iterates agree
+        h = c.pcg_history()
+        k = min(len(h), len(ref["hist"])) - 1
+        np.testing.assert_allclose(h[: k + 1], ref["hist"][: k + 1], rtol=1e-6, atol=1e-12)
+        # end-to-end host entry point gives the same answer
+        xh = np.zeros(c.n_local)
+        r2 = c.pcg_solve_host(np.ascontiguousarray(b), xh, tol, 5000)
+        assert r2["iters"] == r["iters"]
+        assert np.array_equal(xh, xs)
+
+
+def test_pcg_c3_fixed_20_iterations():
+    """Full-size C3 (32^3, N=7, TGV pressure): the oracle's 20 iterations."""
+    spec, N = CONFIGS["C3"]
+    o = O.Oracle(spec, N)
+    b = o.rhs(f_tgv(o.get("X"), o.get("Y"), o.get("Z")))
+    ref = o.pcg(b, 0.0, 20)
+    with sem().sem_setup(spec, N) as c:
+        x = c.zeros()
+        r = c.pcg_solve(dev(b), x, 0.0, 20)
+        assert r["iters"] == 20 and r["status"] == 1
+        assert abs(r["res_final"] - ref["res_final"]) <= 1e-10
+        assert np.abs(host(x) - ref["x"]).max() <= 1e-10
+        np.testing.assert_allclose(c.pcg_history(), ref["hist"], rtol=1e-9)
+
+
+def test_pcg_edge_cases():
+    spec, N = CONFIGS["C1"]
+    with sem().sem_setup(spec, N) as c:
+        x = c.zeros()
+        # zero right-hand side: converged before the first iteration
+        r = c.pcg_solve(c.zeros(), x, 1e-10, 100)
+        assert r["iters"] == 0 and r["status"] == 0
+        assert float(x.abs().max()) == 0.0
+        # maxit = 0
+        o = O.Oracle(spec, N)
+        b = dev(o.rhs(f_sin(o.get("X"), o.get("Y"), o.get("Z"))))
+        r = c.pcg_solve(b, x, 1e-10, 0)
+        assert r["iters"] == 0 and r["status"] == 1
+        # bad arguments are rejected loudly
+        with pytest.raises(sem().SemError):
+            c.pcg_solve(b, b, 1e-10, 10)
+        with pytest.raises(sem().SemError):
+            c.apply(b, b)
+
+
+def test_launch_counts_and_native_library_loaded():
+    import os
+    spec, N = CONFIGS["C1"]
+    with sem().sem_setup(spec, N) as c:
+        n0 = c.launch_count()
+        u = c.zeros()
+        w = c.zeros()
+        c.apply(u, w)
+        assert c.launch_count() == n0 + 1          # one fused kernel per apply (P=1)
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert "libsem.so" in maps
