@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 Ax+gather-scatter GDOF/s and PCG iter/s at 1-8 B200; % HBM roofline"
 UNIT = "GDOF/s"
 E2E_ITERS = 20   # PCG iterations per end-to-end call (one host solve of b -> x)
+FUSED = False    # operator variant timed (SEM_OPT_FUSED_GS); both are reported under ax_gs
 
 
 def parse():
@@ -224,6 +225,7 @@ def main():
         comm = sem.nccl_comm_init(uid[0], rank, P)
     stream = torch.cuda.current_stream()
     ctx = sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm, stream=stream.cuda_stream)
+    ctx.set_fused_gs(FUSED)
     nl = ctx.n_local
     n_p_total = nl * P
 
@@ -274,11 +276,13 @@ def main():
     k_ms, k_cnt = ctx.timing_read(0)
     u_ms, u_cnt = ctx.timing_read(1)
     p_ms, p_cnt = ctx.timing_read(2)
+    g_ms, g_cnt = ctx.timing_read(4)
     ctx.timing(False)
     k_avg = max_over_ranks(k_ms / max(k_cnt, 1))
     bm = bytes_model(N)
     peak, peak_src = peaks()
-    achieved = nl * bm["ax_gs"] / (k_avg / 1e3) / 1e9
+    kbytes = bm["ax_gs"] if FUSED else bm["ax"]
+    achieved = nl * kbytes / (k_avg / 1e3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fjs:
@@ -289,18 +293,22 @@ def main():
     except Exception:
         pass
 
-    # ---- Ax+gs alone (sem_apply), and Ax alone, K repetitions each
+    # ---- Ax+gs alone (sem_apply, both variants), and Ax alone, K repetitions each
     u_rand = torch.empty(nl, dtype=torch.float64, device="cuda").uniform_(-1, 1)
     w = ctx.zeros()
-    for _ in range(3):
-        ctx.apply(u_rand, w)
-    barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        ctx.apply(u_rand, w)
-    ev1.record(stream)
-    barrier()
-    apply_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    apply_ms = {}
+    for fused in (True, False):
+        ctx.set_fused_gs(fused)
+        for _ in range(3):
+            ctx.apply(u_rand, w)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.apply(u_rand, w)
+        ev1.record(stream)
+        barrier()
+        apply_ms[fused] = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    ctx.set_fused_gs(FUSED)
     ev0.record(stream)
     for _ in range(args.steps):
         ctx.ax(u_rand, w)
@@ -356,18 +364,24 @@ def main():
                 "parallelism": f"element z-slabs x{P}, NCCL gs exchange + allreduce",
             },
             "pcg_iter_per_s": args.steps / (t_ms / 1e3),
-            "ax_gs": {"gdofs": n_p_total / (apply_ms / 1e3) / 1e9, "ms": apply_ms,
-                      "frac_of_8TBps": nl * bm["ax_gs"] / (apply_ms / 1e3) / 8e12,
-                      "note": "sem_apply alone (fused Ax+gs+mask), random u"},
+            "ax_gs": {
+                variant: {"gdofs": n_p_total / (apply_ms[f] / 1e3) / 1e9, "ms": apply_ms[f],
+                          "frac_of_8TBps": nl * bm["ax_gs"] / (apply_ms[f] / 1e3) / 8e12,
+                          "frac_of_measured": nl * bm["ax_gs"] / (apply_ms[f] / 1e3) / 1e9 / peak}
+                for variant, f in (("fused", True), ("two_kernel", False))},
             "ax_only": {"gdofs": n_p_total / (ax_ms / 1e3) / 1e9, "ms": ax_ms,
                         "gbs_64B_per_pt": nl * 64 / (ax_ms / 1e3) / 1e9},
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": f"ax_kernel<{N + 1},AX_PCG> (fused Ax+gs+mask+sigma)",
-                "bytes_per_pt": bm["ax_gs"], "hbm_mandatory_bytes_per_pt": 64.0,
+                "kernel": (f"ax_kernel<{N + 1},AX_PCG,fused={FUSED}> "
+                           + ("(Ax+gs+mask+sigma)" if FUSED else "(Ax+mask+sigma)")),
+                "bytes_per_pt": kbytes, "hbm_mandatory_bytes_per_pt": 64.0,
                 "avg_launch_ms": k_avg, "launches": k_cnt, "peak_source": peak_src,
-                "step_share": k_ms / max(k_ms + u_ms + p_ms, 1e-9),
+                "step_share": k_ms / max(k_ms + u_ms + p_ms + g_ms, 1e-9),
+                "other_kernels_ms_per_step": {"gs": g_ms / max(g_cnt, 1),
+                                              "cg_update": u_ms / max(u_cnt, 1),
+                                              "cg_p": p_ms / max(p_cnt, 1)},
             },
             "cpu_baseline": cpu,
             "e2e": e2e,

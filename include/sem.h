@@ -141,13 +141,19 @@ int sem_nccl_comm_destroy(void* comm);
 
 /* ---- instrumentation ----
    sem_timing(c, 1) records CUDA events on the context stream around every
-   launch of kernel class `which` (0 = fused Ax+gs apply kernel, 1 = CG
-   update, 2 = p update, 3 = Ax only); sem_timing_read returns the summed
+   launch of kernel class `which` (0 = Ax kernel of apply/PCG, 1 = CG
+   update, 2 = p update, 3 = Ax only, 4 = gather-scatter kernel of apply/PCG); sem_timing_read returns the summed
    device time in ms and the number of timed launches since the last reset.
    sem_launch_count returns the number of kernels this context has launched. */
 int sem_timing(sem_ctx* c, int enable);
 int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t* count);
 int sem_launch_count(const sem_ctx* c, int64_t* n);
+/* Operator variants (both compute the same w; results are bit-identical):
+   SEM_OPT_FUSED_GS = 1 -> gather-scatter fused into the Ax kernel (last
+   arriver per face/edge/vertex sums it); 0 (default) -> Ax kernel with the
+   mask in its epilogue followed by one gather-scatter kernel. */
+#define SEM_OPT_FUSED_GS 1
+int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);
 

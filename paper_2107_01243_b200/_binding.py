@@ -69,6 +69,7 @@ _SIGS = {
     "sem_timing": [_P, C.c_int],
     "sem_timing_read": [_P, C.c_int, C.POINTER(C.c_double), _I64P],
     "sem_launch_count": [_P, _I64P],
+    "sem_set_option": [_P, C.c_int, C.c_int],
 }
 
 
@@ -240,6 +241,9 @@ class Context:
         ms, cnt = C.c_double(), C.c_int64()
         _check(load().sem_timing_read(self._h, which, C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
+
+    def set_fused_gs(self, on: bool):
+        _check(load().sem_set_option(self._h, 1, 1 if on else 0))
 
     def launch_count(self) -> int:
         n = C.c_int64()

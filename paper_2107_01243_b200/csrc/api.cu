@@ -57,7 +57,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 namespace {
 
 constexpr int kBatch = 8;            // iterations enqueued between host polls
-constexpr int kTimerClasses = 4;
+constexpr int kTimerClasses = 5;
 
 struct Timer {
   std::vector<cudaEvent_t> pool;     // pairs
@@ -100,8 +100,9 @@ struct sem_ctx {
   int64_t launches = 0;
   bool timing = false;
   Timer timer;
-  double t_ms[kTimerClasses] = {0, 0, 0, 0};
-  int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0};
+  double t_ms[kTimerClasses] = {0, 0, 0, 0, 0};
+  int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0, 0};
+  bool fuse_gs = false;   // SEM_OPT_FUSED_GS
 };
 
 namespace {
@@ -185,7 +186,7 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
   int grid = std::min(c->ax_grid, std::max(ng, 1));
   int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
-  cudaError_t e = sem::launch_ax(c->dp, a, mode, grid, c->stream);
+  cudaError_t e = sem::launch_ax(c->dp, a, mode, grid, c->stream, c->fuse_gs);
   timer_end(c, tk);
   c->launches++;
   return check(e, "ax kernel");
@@ -207,12 +208,24 @@ int exchange(sem_ctx* c) {
   return SEM_OK;
 }
 
+// rank-local gather-scatter pass of the two-kernel operator (masked slots are
+// already zero, so every masked entity point sums to zero)
+int gs_pass(sem_ctx* c, double* w) {
+  if (c->fuse_gs) return SEM_OK;
+  int tk = timer_begin(c, 4);
+  cudaError_t e = sem::launch_gs_local(c->dp, w, 0, c->stream);
+  timer_end(c, tk);
+  c->launches++;
+  return check(e, "gs kernel");
+}
+
 // w = mask(QQ^T A_L u) (mode AX_APPLY) or the same plus sigma (AX_PCG)
 int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   const sem::HostPlan& h = c->hp;
   sem::PcgState* st = c->d_st;
   if (h.nranks == 1 || h.nS == 0) {
     SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, &st->sigma));
+    SEM_TRY(gs_pass(c, w));
     return SEM_OK;
   }
   int nparts = 1;
@@ -230,6 +243,7 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
     c->launches++;
     SEM_TRY(exchange(c));
   }
+  SEM_TRY(gs_pass(c, w));
   CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
   CUDA_TRY(sem::launch_gs_unpack(c->dp, w, c->d_part, c->d_recv, 1,
                                  mode == sem::AX_PCG ? st : nullptr, nparts, c->stream));
@@ -652,6 +666,17 @@ extern "C" int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t*
   if (total_ms) *total_ms = c->t_ms[which];
   if (count) *count = c->t_cnt[which];
   return SEM_OK;
+}
+
+extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
+  if (!c) return SEM_EINVAL;
+  if (option == SEM_OPT_FUSED_GS) {
+    cudaStreamSynchronize(c->stream);
+    c->fuse_gs = value != 0;
+    return SEM_OK;
+  }
+  sem::set_error("sem_set_option: unknown option");
+  return SEM_EINVAL;
 }
 
 extern "C" int sem_launch_count(const sem_ctx* c, int64_t* n) {

@@ -86,14 +86,15 @@ __device__ __forceinline__ void sum_point(double* __restrict__ w, const int32_t*
     if (t < nin) __stcg(&w[base[t] + off], s);
 }
 
-template <int n, int MODE>
+template <int n, int MODE, bool FUSE>
 __global__ void __launch_bounds__(AxShape<n>::T)
     ax_kernel(const DevPlan P, const AxLaunch a) {
   using Sh = AxShape<n>;
   constexpr int NE = Sh::NE, n2 = Sh::n2, n3 = Sh::n3, T = Sh::T, S = Sh::S;
   constexpr int dp = Sh::dpad;
   constexpr bool kBulkU = Sh::kBulkU;
-  constexpr bool kGs = MODE != AX_ONLY;
+  constexpr bool kMask = MODE != AX_ONLY;   // Dirichlet mask in the epilogue
+  constexpr bool kGs = kMask && FUSE;         // last-arriver gather-scatter in-kernel
 
   if (MODE == AX_PCG && *a.done) return;
 
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(AxShape<n>::T)
       const double* sws = sG + n3;
       const int e = e0 + el;
       double* wg = a.w + (size_t)e * n3;
-      const unsigned bm = kGs ? P.bmask[e] : 0u;
+      const unsigned bm = kMask ? P.bmask[e] : 0u;
 #pragma unroll
       for (int k = 0; k < n; k++) {
         double v = rw[k];
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(AxShape<n>::T)
           v = fma(sDt[i * dp + m], swr[m + n * j + n2 * k], v);
           v = fma(sDt[j * dp + m], sws[i + n * m + n2 * k], v);
         }
-        if (kGs && face_masked(bm, i, j, k, n - 1)) v = 0.0;
+        if (kMask && face_masked(bm, i, j, k, n - 1)) v = 0.0;
         if (MODE == AX_PCG) acc = fma(ru[k], v, acc);
         wg[ij + n2 * k] = v;
       }
@@ -229,17 +230,17 @@ __global__ void __launch_bounds__(AxShape<n>::T)
       // ---- arrive on this group's entities; the last arriver sums them ----
       if (tid == 0) s_misc[0] = 0;
       __syncthreads();   // all w_e stores of the group issued; list reset visible
-      if (tid < cnt * kRefsPerElem) {
-        const int e = e0 + tid / kRefsPerElem;
-        const int ref = P.eref[(size_t)e * kRefsPerElem + tid % kRefsPerElem];
+      for (int q = tid; q < cnt * kRefsPerElem; q += T) {
+        const int e = e0 + q / kRefsPerElem;
+        const int ref = P.eref[(size_t)e * kRefsPerElem + q % kRefsPerElem];
         if (ref >= 0) {
           const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
           const unsigned nin = cls == CLS_FACE ? 2u : (cls == CLS_EDGE ? P.e_nin[idx] : P.v_nin[idx]);
           unsigned* tk = P.cnt + (cls == CLS_FACE ? idx : (cls == CLS_EDGE ? P.nF + idx : P.nF + P.nEd + idx));
-          __threadfence();                       // release: this CTA's w stores
-          const unsigned old = atomicAdd(tk, 1u);
+          // acq_rel: releases this CTA's w stores (ordered before by the barrier),
+          // acquires the other incidences' stores when this is the last arrival
+          const unsigned old = atom_add_acq_rel_gpu(tk, 1u);
           if (old == nin - 1u) {
-            __threadfence();                     // acquire: the other incidences' stores
             *tk = 0u;
             s_list[atomicAdd(&s_misc[0], 1)] = ref;
           }
@@ -297,10 +298,10 @@ __global__ void __launch_bounds__(AxShape<n>::T)
   }
 }
 
-template <int n, int MODE>
+template <int n, int MODE, bool FUSE>
 static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
   using Sh = AxShape<n>;
-  auto kern = ax_kernel<n, MODE>;
+  auto kern = ax_kernel<n, MODE, FUSE>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -315,7 +316,7 @@ static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int grid, cudaS
 template <int n, int MODE>
 static int occupancy_n() {
   using Sh = AxShape<n>;
-  auto kern = ax_kernel<n, MODE>;
+  auto kern = ax_kernel<n, MODE, true>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem_bytes);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Sh::T, Sh::smem_bytes) != cudaSuccess)
@@ -323,20 +324,20 @@ static int occupancy_n() {
   return std::max(nb, 1);
 }
 
-template <int MODE>
+template <int MODE, bool FUSE>
 static cudaError_t dispatch(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
   switch (P.n) {
-    case 2: return launch_n<2, MODE>(P, a, grid, s);
-    case 3: return launch_n<3, MODE>(P, a, grid, s);
-    case 4: return launch_n<4, MODE>(P, a, grid, s);
-    case 5: return launch_n<5, MODE>(P, a, grid, s);
-    case 6: return launch_n<6, MODE>(P, a, grid, s);
-    case 7: return launch_n<7, MODE>(P, a, grid, s);
-    case 8: return launch_n<8, MODE>(P, a, grid, s);
-    case 9: return launch_n<9, MODE>(P, a, grid, s);
-    case 10: return launch_n<10, MODE>(P, a, grid, s);
-    case 11: return launch_n<11, MODE>(P, a, grid, s);
-    case 12: return launch_n<12, MODE>(P, a, grid, s);
+    case 2: return launch_n<2, MODE, FUSE>(P, a, grid, s);
+    case 3: return launch_n<3, MODE, FUSE>(P, a, grid, s);
+    case 4: return launch_n<4, MODE, FUSE>(P, a, grid, s);
+    case 5: return launch_n<5, MODE, FUSE>(P, a, grid, s);
+    case 6: return launch_n<6, MODE, FUSE>(P, a, grid, s);
+    case 7: return launch_n<7, MODE, FUSE>(P, a, grid, s);
+    case 8: return launch_n<8, MODE, FUSE>(P, a, grid, s);
+    case 9: return launch_n<9, MODE, FUSE>(P, a, grid, s);
+    case 10: return launch_n<10, MODE, FUSE>(P, a, grid, s);
+    case 11: return launch_n<11, MODE, FUSE>(P, a, grid, s);
+    case 12: return launch_n<12, MODE, FUSE>(P, a, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -384,11 +385,15 @@ int ax_occupancy(int N, int mode) {
   return dev::occ_dispatch<AX_PCG>(n);
 }
 
-cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s) {
+cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
+                      bool fuse_gs) {
   if (grid < 1) grid = 1;
-  if (mode == AX_ONLY) return dev::dispatch<AX_ONLY>(P, a, grid, s);
-  if (mode == AX_APPLY) return dev::dispatch<AX_APPLY>(P, a, grid, s);
-  return dev::dispatch<AX_PCG>(P, a, grid, s);
+  if (mode == AX_ONLY) return dev::dispatch<AX_ONLY, false>(P, a, grid, s);
+  if (mode == AX_APPLY)
+    return fuse_gs ? dev::dispatch<AX_APPLY, true>(P, a, grid, s)
+                   : dev::dispatch<AX_APPLY, false>(P, a, grid, s);
+  return fuse_gs ? dev::dispatch<AX_PCG, true>(P, a, grid, s)
+                 : dev::dispatch<AX_PCG, false>(P, a, grid, s);
 }
 
 }  // namespace sem

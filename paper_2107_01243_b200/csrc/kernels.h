@@ -64,7 +64,8 @@ struct AxLaunch {
 
 // returns max resident CTAs/SM for the Ax kernel of this N and mode
 int ax_occupancy(int N, int mode);
-cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s);
+cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
+                      bool fuse_gs);
 int ax_groups(int N, int nelem);   // element groups processed per launch
 
 // setup

@@ -77,11 +77,13 @@ def test_setup_exports(spec, N):
             assert np.abs(host(t) - o.get(name)).max() < 1e-13
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["2kernel", "fused"])
 @pytest.mark.parametrize("spec,N", MESHES, ids=IDS)
-def test_ax_gs_apply_parity(spec, N):
+def test_ax_gs_apply_parity(spec, N, fused):
     o = O.Oracle(spec, N)
     u = random_field(o.nslots, seed=11)
     with sem().sem_setup(spec, N) as c:
+        c.set_fused_gs(fused)
         du, dw = dev(u), c.zeros()
         c.ax(du, dw)
         w_ax = host(dw)
@@ -103,22 +105,24 @@ def test_ax_gs_apply_parity(spec, N):
         assert np.array_equal(first[gid], w_ap)
 
 
-def test_apply_is_deterministic_and_repeatable():
+def test_apply_is_deterministic_and_variants_agree_bitwise():
     spec, N = tgv_box(6, 5, 4, deform=1), 7
     u = random_field(spec.n_slots(N), seed=5)
     with sem().sem_setup(spec, N) as c:
         du = dev(u)
         outs = []
-        for _ in range(3):
+        for fused in (False, True, False, True):
+            c.set_fused_gs(fused)
             w = c.zeros()
             c.apply(du, w)
             outs.append(host(w))
-        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+        for o in outs[1:]:
+            assert np.array_equal(outs[0], o)
 
 
-@pytest.mark.parametrize("cfg", ["C2"])
-def test_full_size_c2_apply(cfg):
-    """BASELINE configs[1] at full size (8192 elements, N=7), the bench workload."""
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_full_size_apply(cfg):
+    """BASELINE configs[1] (the bench workload) and configs[2] at full size."""
     spec, N = CONFIGS[cfg]
     o = O.Oracle(spec, N)
     u = random_field(o.nslots, seed=0)
@@ -126,8 +130,12 @@ def test_full_size_c2_apply(cfg):
         du, dw = dev(u), c.zeros()
         c.ax(du, dw)
         assert nrel(host(dw), o.ax(u)) <= 1e-12
-        c.apply(du, dw)
-        assert nrel(host(dw), o.apply(u)) <= 1e-12
+        ref = o.apply(u)
+        for fused in (False, True):
+            c.set_fused_gs(fused)
+            dw.zero_()
+            c.apply(du, dw)
+            assert nrel(host(dw), ref) <= 1e-12
 
 
 @pytest.mark.parametrize("spec,N,fun", [(CONFIGS["C1"][0], 3, f_sin), (tgv_box(4, 4, 3), 5, f_tgv),
@@ -150,13 +158,15 @@ PCG_CASES = [
 ]
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["2kernel", "fused"])
 @pytest.mark.parametrize("spec,N,fun,tol", PCG_CASES)
-def test_pcg_parity(spec, N, fun, tol):
+def test_pcg_parity(spec, N, fun, tol, fused):
     o = O.Oracle(spec, N)
     f = fun(o.get("X"), o.get("Y"), o.get("Z"))
     b = o.rhs(f)
     ref = o.pcg(b, tol, 5000)
     with sem().sem_setup(spec, N) as c:
+        c.set_fused_gs(fused)
         x = c.zeros()
         r = c.pcg_solve(dev(b), x, tol, 5000)
         xs = host(x)
@@ -216,10 +226,12 @@ def test_launch_counts_and_native_library_loaded():
     import os
     spec, N = CONFIGS["C1"]
     with sem().sem_setup(spec, N) as c:
-        n0 = c.launch_count()
         u = c.zeros()
         w = c.zeros()
-        c.apply(u, w)
-        assert c.launch_count() == n0 + 1          # one fused kernel per apply (P=1)
+        for fused, k in ((True, 1), (False, 2)):   # kernels per apply at P=1
+            c.set_fused_gs(fused)
+            n0 = c.launch_count()
+            c.apply(u, w)
+            assert c.launch_count() == n0 + k
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libsem.so" in maps
