@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -183,6 +184,7 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.red_ticket = &c->d_st->tickets[0];
   a.red_out = red_out;
   a.done = &c->d_st->done;
+  std::copy(c->hp.D.begin(), c->hp.D.end(), a.Dm);
   const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
   int grid = std::min(c->ax_grid, std::max(ng, 1));
   int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
@@ -600,7 +602,17 @@ extern "C" int sem_export_field(const sem_ctx* c, int which, double* host_dst) {
     case 0: std::memcpy(host_dst, h.xi.data(), h.xi.size() * sizeof(double)); return SEM_OK;
     case 1: std::memcpy(host_dst, h.w.data(), h.w.size() * sizeof(double)); return SEM_OK;
     case 2: std::memcpy(host_dst, h.D.data(), h.D.size() * sizeof(double)); return SEM_OK;
-    case 3: CUDA_TRY(cudaMemcpy(host_dst, c->d_G, 6 * (size_t)h.n_local * 8, cudaMemcpyDeviceToHost)); return SEM_OK;
+    case 3: {  // export in the factor-major [E][6][n^3] order
+      std::vector<double> tmp(6 * (size_t)h.n_local);
+      CUDA_TRY(cudaMemcpy(tmp.data(), c->d_G, tmp.size() * 8, cudaMemcpyDeviceToHost));
+      const int n = h.n;
+      const int64_t n3 = h.n3;
+      for (int64_t el = 0; el < h.nloc; el++)
+        for (int f = 0; f < 6; f++)
+          for (int64_t p = 0; p < n3; p++)
+            host_dst[el * 6 * n3 + f * n3 + p] = tmp[sem::g_index_host(el, f, (int)p, n)];
+      return SEM_OK;
+    }
     case 4: CUDA_TRY(cudaMemcpy(host_dst, c->d_B, (size_t)h.n_local * 8, cudaMemcpyDeviceToHost)); return SEM_OK;
     case 5: CUDA_TRY(cudaMemcpy(host_dst, c->d_dinv, (size_t)h.n_local * 8, cudaMemcpyDeviceToHost)); return SEM_OK;
   }

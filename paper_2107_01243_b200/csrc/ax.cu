@@ -1,26 +1,26 @@
 // Element stiffness operator  w_L = A_L u_L,  A^e = D^T G^e D  (Eq. 9),
-// optionally fused with the gather-scatter QQ^T (Eq. 10), the
-// Dirichlet mask and the CG inner product <p, A p>.
+// optionally with the Dirichlet mask, the CG inner product <p, A p>
+// and the gather-scatter QQ^T (Eq. 10) fused in.
 //
-// Design, sm_100a, fp64 on the CUDA cores:
-//  * persistent grid; each CTA walks element groups (NE elements of n^3 points)
-//    with a 2-stage ring: the 6 geometric factors of the next group (and u when
-//    n is even) are fetched by the TMA bulk-copy engine (cp.async.bulk ->
-//    UBLKCP) into shared memory, completion tracked on mbarriers, while the
-//    current group is computed;
+// Design, sm_100a, fp64 on the CUDA cores (the
+// contraction is HBM-bound: 1.7 flop/B at N=7, far below the fp64 ridge):
+//  * warp-specialised persistent CTAs: one producer warp drives the TMA
+//    bulk-copy engine (cp.async.bulk -> UBLKCP), the compute warps only
+//    compute.  The producer streams, for the CTA's element sequence, each
+//    element's u block and then its k-planes of geometric factors (plane-major
+//    layout G[e][k][f][ij]: one 48 n^2-byte copy per plane) into two mbarrier
+//    rings (full/empty), so ~tens of KB per SM are in flight without holding
+//    registers and the compute warps never issue a global load;
 //  * thread (i,j) owns the k-column of its element: u_(i,j,:) and the
-//    t-direction contributions live in registers; the r and s contractions read
-//    shared memory (padded D to avoid bank conflicts); w_r, w_s overwrite the
-//    consumed G_rr, G_ss slots of the stage in place (no extra smem);
-//  * AX_APPLY / AX_PCG: after writing w_e, the CTA "arrives" on each face /
-//    edge / vertex entity of the element (one atomic ticket per entity per
-//    call); the last arriver sums the entity's slots in ascending slot order
-//    (reading Q10) while they are still L2-resident, writes the sum (or 0 on
-//    Dirichlet points) to every slot, and resets the ticket.  The gather-
-//    scatter therefore costs no separate pass over HBM;
-//  * AX_PCG also accumulates sigma = sum_l p_l (A_L p)_l = p^T A p (valid for a
-//    continuous p that vanishes on Dirichlet slots) and reduces it
-//    deterministically (fixed element->CTA map, fixed-order final sum).
+//    t-direction accumulation live in registers; the r and s contractions read
+//    shared memory (padded D and padded w_r/w_s scratch avoid bank conflicts);
+//  * epilogue: mask (per-thread precomputed bits), sigma = sum_l p_l (A_L p)_l
+//    (= p^T A p for a continuous p vanishing on Dirichlet slots), store w;
+//  * FUSE: after storing w_e the compute warps "arrive" on each face / edge /
+//    vertex entity of their elements (one atomic ticket per entity per call);
+//    the last arriver sums the entity's slots in ascending slot order (reading
+//    Q10) while they are L2-resident and resets the ticket.  Otherwise a
+//    separate gather-scatter kernel (kern.cu) follows.
 #include <algorithm>
 
 #include "dev_common.cuh"
@@ -32,41 +32,75 @@ namespace dev {
 
 template <int n>
 struct AxCfg;
-// elements per CTA group: keep ~64-160 threads per CTA and the 2-stage ring
-// inside shared memory
-template <> struct AxCfg<2> { static constexpr int NE = 16; };
-template <> struct AxCfg<3> { static constexpr int NE = 8; };
-template <> struct AxCfg<4> { static constexpr int NE = 4; };
-template <> struct AxCfg<5> { static constexpr int NE = 2; };
-template <> struct AxCfg<6> { static constexpr int NE = 2; };
-template <> struct AxCfg<7> { static constexpr int NE = 1; };
-template <> struct AxCfg<8> { static constexpr int NE = 1; };
-template <> struct AxCfg<9> { static constexpr int NE = 1; };
-template <> struct AxCfg<10> { static constexpr int NE = 1; };
-template <> struct AxCfg<11> { static constexpr int NE = 1; };
-template <> struct AxCfg<12> { static constexpr int NE = 1; };
+// NE: elements computed together by one CTA (64-160 compute threads)
+// NSG: depth of the G plane ring (planes in flight per CTA)
+// PPC: k-planes per bulk copy (divides n).  n=8 tuned with tools/ubench_ax.cu
+// on B200 (NSG=3, PPC=4: 6.2 TB/s on 32^3 elements); the others follow the same
+// rule of ~2 copies per element and a 2-3 slot ring within ~60 KB of smem.
+#ifndef SEM_AX8_NE
+#define SEM_AX8_NE 1
+#endif
+#ifndef SEM_AX8_NSG
+#define SEM_AX8_NSG 3
+#endif
+#ifndef SEM_AX8_PPC
+#define SEM_AX8_PPC 4
+#endif
+template <> struct AxCfg<2> { static constexpr int NE = 16, NSG = 3, PPC = 2; };
+template <> struct AxCfg<3> { static constexpr int NE = 8, NSG = 3, PPC = 3; };
+template <> struct AxCfg<4> { static constexpr int NE = 4, NSG = 3, PPC = 2; };
+template <> struct AxCfg<5> { static constexpr int NE = 2, NSG = 3, PPC = 5; };
+template <> struct AxCfg<6> { static constexpr int NE = 2, NSG = 3, PPC = 3; };
+template <> struct AxCfg<7> { static constexpr int NE = 1, NSG = 3, PPC = 7; };
+template <> struct AxCfg<8> {
+  static constexpr int NE = SEM_AX8_NE, NSG = SEM_AX8_NSG, PPC = SEM_AX8_PPC;
+};
+template <> struct AxCfg<9> { static constexpr int NE = 1, NSG = 3, PPC = 3; };
+template <> struct AxCfg<10> { static constexpr int NE = 1, NSG = 3, PPC = 5; };
+template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = 6, PPC = 1; };
+template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = 3, PPC = 3; };
 
 template <int n>
 struct AxShape {
-  static constexpr int NE = AxCfg<n>::NE;
+  static constexpr int NE = AxCfg<n>::NE, NSG = AxCfg<n>::NSG, PPC = AxCfg<n>::PPC;
+  static_assert(n % PPC == 0, "planes per copy must divide n");
   static constexpr int n2 = n * n, n3 = n2 * n;
   static constexpr int TC = NE * n2;               // computing threads
-  static constexpr int T = (TC + 31) / 32 * 32;    // launched threads
-  static constexpr int S = 2;                      // ring stages
+  static constexpr int TCW = (TC + 31) / 32 * 32;  // compute warps x 32
+  static constexpr int NWC = TCW / 32;             // compute warps
+  static constexpr int T = TCW + 32;               // + one producer warp
+  static constexpr int NSU = 2;                    // u ring depth
   static constexpr bool kBulkU = (n % 2) == 0;     // u block 16-B aligned for any element
-  static constexpr int stage_dbl = NE * 6 * n3 + (kBulkU ? NE * n3 : 0);
-  static constexpr int plainu_dbl = kBulkU ? 0 : NE * n3;
+  static constexpr int uslot = NE * n3;            // doubles per u slot
+  static constexpr int gslot = NE * PPC * 6 * n2;  // doubles per G slot (PPC planes x NE)
+  static constexpr int rp = n + 1;                 // padded row pitch of w_r / w_s
+  static constexpr int wpl = n * rp;               // padded plane pitch
+  static constexpr int wel = n * wpl;              // per element
   static constexpr int dpad = n + 1;
   static constexpr int kMaxList = NE * kRefsPerElem;
+  static constexpr int nbar = 2 * NSG + 2 * NSU;
   static constexpr size_t smem_bytes =
-      sizeof(double) * ((size_t)S * stage_dbl + plainu_dbl + 2 * n * dpad + 32) +
-      sizeof(uint64_t) * S + sizeof(int) * (kMaxList + 8);
+      sizeof(double) * ((size_t)NSU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32) +
+      sizeof(uint64_t) * nbar + sizeof(int) * (kMaxList + 8);
+  // CTAs per SM the shared memory allows; the register budget is sized to match
+  static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
+  static constexpr int MINB = MINB0 < 1 ? 1 : (MINB0 > 8 ? 8 : MINB0);
 };
 
 __device__ __forceinline__ int face_s1(int axis, int n) { return axis == 0 ? n : 1; }
 __device__ __forceinline__ int face_s2(int axis, int n) { return axis == 2 ? n : n * n; }
 __device__ __forceinline__ int edge_stride(int axis, int n) {
   return axis == 0 ? 1 : (axis == 1 ? n : n * n);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barrier over the compute warps only (the producer warp never joins)
+template <int NT>
+__device__ __forceinline__ void compute_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
 // Sum one entity point over its incidences (ascending slots), write the total.
@@ -87,208 +121,255 @@ __device__ __forceinline__ void sum_point(double* __restrict__ w, const int32_t*
 }
 
 template <int n, int MODE, bool FUSE>
-__global__ void __launch_bounds__(AxShape<n>::T)
+__global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     ax_kernel(const DevPlan P, const AxLaunch a) {
   using Sh = AxShape<n>;
-  constexpr int NE = Sh::NE, n2 = Sh::n2, n3 = Sh::n3, T = Sh::T, S = Sh::S;
-  constexpr int dp = Sh::dpad;
+  constexpr int NE = Sh::NE, n2 = Sh::n2, n3 = Sh::n3, TCW = Sh::TCW;
+  constexpr int NSG = Sh::NSG, NSU = Sh::NSU, PPC = Sh::PPC;
+  constexpr int dp = Sh::dpad, rp = Sh::rp, wpl = Sh::wpl;
   constexpr bool kBulkU = Sh::kBulkU;
   constexpr bool kMask = MODE != AX_ONLY;   // Dirichlet mask in the epilogue
   constexpr bool kGs = kMask && FUSE;         // last-arriver gather-scatter in-kernel
+  constexpr bool kDreg = n <= 9;              // D rows in registers (else shared memory)
 
   if (MODE == AX_PCG && *a.done) return;
 
   extern __shared__ __align__(128) double smem[];
-  double* stage0 = smem;
-  double* su_plain = smem + S * Sh::stage_dbl;
-  double* sD = su_plain + Sh::plainu_dbl;   // sD[i*dp+m]  = D[i][m]
-  double* sDt = sD + n * dp;                // sDt[i*dp+m] = D[m][i]
-  double* s_red = sDt + n * dp;             // 32 doubles
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_red + 32);
-  int* s_list = reinterpret_cast<int*>(bar + S);
-  int* s_misc = s_list + Sh::kMaxList;      // [0] list length, [1] last-block flag
+  double* sU = smem;                                   // [NSU][NE*n3]
+  double* sG = sU + NSU * Sh::uslot;                   // [NSG][NE][6][n2]
+  double* sWr = sG + NSG * Sh::gslot;                  // [NE][n][n][rp]
+  double* sWs = sWr + NE * Sh::wel;
+  double* sD = sWs + NE * Sh::wel;                     // sD[i*dp+m]  = D[i][m]
+  double* sDt = sD + n * dp;                           // sDt[i*dp+m] = D[m][i]
+  double* s_red = sDt + n * dp;                        // 32 doubles
+  uint64_t* fullG = reinterpret_cast<uint64_t*>(s_red + 32);
+  uint64_t* emptyG = fullG + NSG;
+  uint64_t* fullU = emptyG + NSG;
+  uint64_t* emptyU = fullU + NSU;
+  int* s_list = reinterpret_cast<int*>(emptyU + NSU);
+  int* s_misc = s_list + Sh::kMaxList;                 // [0] list length, [1] last-block flag
 
   const int tid = threadIdx.x;
-  const int el = tid / n2, ij = tid - (tid / n2) * n2;
-  const int i = ij % n, j = ij / n;
+  const bool producer = tid >= TCW;
 
-  for (int q = tid; q < n2; q += T) {
+  for (int q = tid; q < n2; q += Sh::T) {
     const int r = q / n, c = q % n;
     const double d = P.D[q];
     sD[r * dp + c] = d;
     sDt[c * dp + r] = d;
   }
   if (tid == 0) {
-    for (int s = 0; s < S; s++) mbar_init(&bar[s], 1);
+    for (int s = 0; s < NSG; s++) {
+      mbar_init(&fullG[s], 1);
+      mbar_init(&emptyG[s], Sh::NWC);
+    }
+    for (int s = 0; s < NSU; s++) {
+      mbar_init(&fullU[s], kBulkU ? 1 : 32);
+      mbar_init(&emptyU[s], Sh::NWC);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
-  const int n0 = a.r0hi - a.r0lo, n1 = a.r1hi - a.r1lo;
-  const int ng0 = (n0 + NE - 1) / NE, ng1 = (n1 + NE - 1) / NE, ng = ng0 + ng1;
-  auto group = [&](int g, int& e0, int& cnt) {
+  const int r0lo = a.r0lo, r0hi = a.r0hi, r1lo = a.r1lo, r1hi = a.r1hi;
+  const int ng0 = (r0hi - r0lo + NE - 1) / NE, ng1 = (r1hi - r1lo + NE - 1) / NE, ng = ng0 + ng1;
+  auto group = [=](int g, int& e0, int& cnt) {
     if (g < ng0) {
-      e0 = a.r0lo + g * NE;
-      cnt = min(NE, a.r0hi - e0);
+      e0 = r0lo + g * NE;
+      cnt = min(NE, r0hi - e0);
     } else {
-      e0 = a.r1lo + (g - ng0) * NE;
-      cnt = min(NE, a.r1hi - e0);
+      e0 = r1lo + (g - ng0) * NE;
+      cnt = min(NE, r1hi - e0);
     }
   };
-  const uint64_t pol_G = policy_evict_first();
-  auto issue = [&](int g, int s) {
-    int e0, cnt;
-    group(g, e0, cnt);
-    double* st = stage0 + s * Sh::stage_dbl;
-    const uint32_t bG = (uint32_t)cnt * 6u * n3 * 8u;
-    const uint32_t bU = kBulkU ? (uint32_t)cnt * n3 * 8u : 0u;
-    mbar_arrive_expect_tx(&bar[s], bG + bU);
-    bulk_g2s_hint(st, a.G + (size_t)e0 * 6 * n3, bG, &bar[s], pol_G);
-    if (kBulkU) bulk_g2s(st + NE * 6 * n3, a.u + (size_t)e0 * n3, bU, &bar[s]);
-  };
-  if (tid == 0)
-    for (int s = 0; s < S; s++) {
-      const int g = blockIdx.x + s * gridDim.x;
-      if (g < ng) issue(g, s);
-    }
 
   double acc = 0.0;  // sigma partial (AX_PCG)
-  int it = 0;
-  for (int g = blockIdx.x; g < ng; g += gridDim.x, ++it) {
-    const int s = it % S;
-    const uint32_t ph = (uint32_t)(it / S) & 1u;
-    int e0, cnt;
-    group(g, e0, cnt);
-    const bool active = el < cnt;
-    double* st = stage0 + s * Sh::stage_dbl;
-    double* sG = st + el * 6 * n3;
-    const double* sU;
-    if (kBulkU) {
-      sU = st + NE * 6 * n3 + el * n3;
-    } else {
-      double* su = su_plain + el * n3;
-      if (active) {
-        const double* ug = a.u + (size_t)(e0 + el) * n3;
-#pragma unroll
-        for (int k = 0; k < n; k++) su[ij + n2 * k] = ug[ij + n2 * k];
-      }
-      __syncthreads();
-      sU = su;
-    }
-    mbar_wait(&bar[s], ph);
 
-    double ru[n], rw[n];
-    if (active) {
+  if (producer) {
+    // ======================= producer warp: TMA bulk copies =======================
+    const int lane = tid - TCW;
+    const uint64_t pol = policy_evict_first();
+    int su = 0, sg = 0;
+    uint32_t phu = 0, phg = 0;
+    for (int g = blockIdx.x; g < ng; g += gridDim.x) {
+      int e0, cnt;
+      group(g, e0, cnt);
+      // u block of the group
+      mbar_wait(&emptyU[su], phu ^ 1u);
+      if (kBulkU) {
+        if (lane == 0) {
+          const uint32_t bU = (uint32_t)cnt * n3 * 8u;
+          mbar_arrive_expect_tx(&fullU[su], bU);
+          bulk_g2s(sU + su * Sh::uslot, a.u + (size_t)e0 * n3, bU, &fullU[su]);
+        }
+      } else {
+        double* dst = sU + su * Sh::uslot;
+        const double* src = a.u + (size_t)e0 * n3;
+        for (int q = lane; q < cnt * n3; q += 32) dst[q] = src[q];
+        mbar_arrive(&fullU[su]);   // release: this lane's stores
+      }
+      if (++su == NSU) { su = 0; phu ^= 1u; }
+      // k-planes of the geometric factors
+      for (int kb = 0; kb < n / PPC; kb++) {
+        mbar_wait(&emptyG[sg], phg ^ 1u);
+        if (lane == 0) {
+          const uint32_t bP = PPC * 6u * n2 * 8u;
+          mbar_arrive_expect_tx(&fullG[sg], bP * (uint32_t)cnt);
+          for (int x = 0; x < cnt; x++)
+            bulk_g2s_hint(sG + sg * Sh::gslot + x * PPC * 6 * n2,
+                          a.G + ((size_t)(e0 + x) * n + kb * PPC) * 6 * n2, bP, &fullG[sg], pol);
+        }
+        if (++sg == NSG) { sg = 0; phg ^= 1u; }
+      }
+    }
+  } else {
+    // ======================= compute warps =======================
+    const int el = tid / n2, ij = tid - (tid / n2) * n2;
+    const int i = ij % n, j = ij / n;
+    const int lane = tid & 31;
+    // D rows/columns this thread contracts with, in registers (the uniform
+    // D[k][m] operands come straight from the kernel-parameter constant bank)
+    double Di[n], Dj[n], Dti[n], Dtj[n];
+#pragma unroll
+    for (int m = 0; m < n; m++) {
+      Di[m] = kDreg ? a.Dm[i * n + m] : 0.0;
+      Dj[m] = kDreg ? a.Dm[j * n + m] : 0.0;
+      Dti[m] = kDreg ? a.Dm[m * n + i] : 0.0;
+      Dtj[m] = kDreg ? a.Dm[m * n + j] : 0.0;
+    }
+    int su = 0, sg = 0;
+    uint32_t phu = 0, phg = 0;
+    for (int g = blockIdx.x; g < ng; g += gridDim.x) {
+      int e0, cnt;
+      group(g, e0, cnt);
+      const bool active = el < cnt;
+      const double* sUe = sU + su * Sh::uslot + el * n3;
+      double* wr_s = sWr + el * Sh::wel;
+      double* ws_s = sWs + el * Sh::wel;
+      mbar_wait(&fullU[su], phu);
+
+      double ru[n], rw[n];
 #pragma unroll
       for (int k = 0; k < n; k++) {
-        ru[k] = sU[ij + n2 * k];
+        ru[k] = active ? sUe[ij + n2 * k] : 0.0;
         rw[k] = 0.0;
       }
 #pragma unroll
       for (int k = 0; k < n; k++) {
-        double ur = 0.0, us = 0.0, ut = 0.0;
+        if (k % PPC == 0) mbar_wait(&fullG[sg], phg);
+        const double* gp = sG + sg * Sh::gslot + (el * PPC + k % PPC) * 6 * n2 + ij;
+        double gk[6];
 #pragma unroll
-        for (int m = 0; m < n; m++) {
-          ur = fma(sD[i * dp + m], sU[m + n * j + n2 * k], ur);
-          us = fma(sD[j * dp + m], sU[i + n * m + n2 * k], us);
-          ut = fma(sD[k * dp + m], ru[m], ut);
+        for (int f = 0; f < 6; f++) gk[f] = active ? gp[f * n2] : 0.0;
+        if (k % PPC == PPC - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&emptyG[sg]);
+          if (++sg == NSG) { sg = 0; phg ^= 1u; }
         }
-        const int pt = ij + n2 * k;
-        const double grr = sG[0 * n3 + pt], gss = sG[1 * n3 + pt], gtt = sG[2 * n3 + pt];
-        const double grs = sG[3 * n3 + pt], grt = sG[4 * n3 + pt], gst = sG[5 * n3 + pt];
-        const double wr = grr * ur + grs * us + grt * ut;
-        const double ws = grs * ur + gss * us + gst * ut;
-        const double wt = grt * ur + gst * us + gtt * ut;
-        sG[0 * n3 + pt] = wr;   // own point only: safe without a barrier
-        sG[1 * n3 + pt] = ws;
+        if (active) {
+          double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
-        for (int m = 0; m < n; m++) rw[m] = fma(sD[k * dp + m], wt, rw[m]);
-      }
-    }
-    __syncthreads();
-    if (active) {
-      const double* swr = sG;
-      const double* sws = sG + n3;
-      const int e = e0 + el;
-      double* wg = a.w + (size_t)e * n3;
-      const unsigned bm = kMask ? P.bmask[e] : 0u;
-#pragma unroll
-      for (int k = 0; k < n; k++) {
-        double v = rw[k];
-#pragma unroll
-        for (int m = 0; m < n; m++) {
-          v = fma(sDt[i * dp + m], swr[m + n * j + n2 * k], v);
-          v = fma(sDt[j * dp + m], sws[i + n * m + n2 * k], v);
-        }
-        if (kMask && face_masked(bm, i, j, k, n - 1)) v = 0.0;
-        if (MODE == AX_PCG) acc = fma(ru[k], v, acc);
-        wg[ij + n2 * k] = v;
-      }
-    }
-
-    if (kGs) {
-      // ---- arrive on this group's entities; the last arriver sums them ----
-      if (tid == 0) s_misc[0] = 0;
-      __syncthreads();   // all w_e stores of the group issued; list reset visible
-      for (int q = tid; q < cnt * kRefsPerElem; q += T) {
-        const int e = e0 + q / kRefsPerElem;
-        const int ref = P.eref[(size_t)e * kRefsPerElem + q % kRefsPerElem];
-        if (ref >= 0) {
-          const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
-          const unsigned nin = cls == CLS_FACE ? 2u : (cls == CLS_EDGE ? P.e_nin[idx] : P.v_nin[idx]);
-          unsigned* tk = P.cnt + (cls == CLS_FACE ? idx : (cls == CLS_EDGE ? P.nF + idx : P.nF + P.nEd + idx));
-          // acq_rel: releases this CTA's w stores (ordered before by the barrier),
-          // acquires the other incidences' stores when this is the last arrival
-          const unsigned old = atom_add_acq_rel_gpu(tk, 1u);
-          if (old == nin - 1u) {
-            *tk = 0u;
-            s_list[atomicAdd(&s_misc[0], 1)] = ref;
+          for (int m = 0; m < n; m++) {
+            ur = fma(kDreg ? Di[m] : sD[i * dp + m], sUe[m + n * j + n2 * k], ur);
+            us = fma(kDreg ? Dj[m] : sD[j * dp + m], sUe[i + n * m + n2 * k], us);
+            ut = fma(a.Dm[k * n + m], ru[m], ut);
           }
+          // G order (rr, ss, tt, rs, rt, st)
+          const double wr = gk[0] * ur + gk[3] * us + gk[4] * ut;
+          const double ws = gk[3] * ur + gk[1] * us + gk[5] * ut;
+          const double wt = gk[4] * ur + gk[5] * us + gk[2] * ut;
+          wr_s[i + rp * j + wpl * k] = wr;
+          ws_s[i + rp * j + wpl * k] = ws;
+#pragma unroll
+          for (int m = 0; m < n; m++) rw[m] = fma(a.Dm[k * n + m], wt, rw[m]);
         }
       }
-      __syncthreads();
-      const int nl = s_misc[0];
-      if (nl > 0) {
-        constexpr int NW = T / 32;
-        const int lane = tid & 31, wid = tid >> 5;
-        const int N = n - 1, nf = (N - 1) * (N - 1), ne = N - 1;
-        for (int q = wid; q < nl; q += NW) {
-          const int ref = s_list[q];
-          const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
-          int32_t base[8];
-          if (n > 2 && cls == CLS_FACE) {
-            base[0] = P.f_base[2 * idx];
-            base[1] = P.f_base[2 * idx + 1];
-            const int ax = P.f_axis[idx];
-            const int s1 = face_s1(ax, n), s2 = face_s2(ax, n);
-            constexpr int Nm1 = n > 2 ? n - 2 : 1;
-            for (int p = lane; p < nf; p += 32) {
-              const int off = (1 + p % Nm1) * s1 + (1 + p / Nm1) * s2;
-              sum_point(a.w, base, 2, off, false);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyU[su]);   // u slot consumed
+      if (++su == NSU) { su = 0; phu ^= 1u; }
+      compute_sync<TCW>();                       // w_r / w_s of the group complete
+      if (active) {
+        const int e = e0 + el;
+        double* wg = a.w + (size_t)e * n3;
+        uint32_t kmask = 0u;   // bit k set: slot (i,j,k) is a Dirichlet slot
+        if (kMask) {
+          const unsigned bm = P.bmask[e];
+          const bool mij = ((i == 0) && (bm & 1u)) || ((i == n - 1) && (bm & 2u)) ||
+                           ((j == 0) && (bm & 4u)) || ((j == n - 1) && (bm & 8u));
+          kmask = mij ? 0xffffffffu
+                      : (((bm & 16u) ? 1u : 0u) | ((bm & 32u) ? (1u << (n - 1)) : 0u));
+        }
+#pragma unroll
+        for (int k = 0; k < n; k++) {
+          double v = rw[k];
+#pragma unroll
+          for (int m = 0; m < n; m++) {
+            v = fma(kDreg ? Dti[m] : sDt[i * dp + m], wr_s[m + rp * j + wpl * k], v);
+            v = fma(kDreg ? Dtj[m] : sDt[j * dp + m], ws_s[i + rp * m + wpl * k], v);
+          }
+          if (kMask && ((kmask >> k) & 1u)) v = 0.0;
+          if (MODE == AX_PCG) acc = fma(ru[k], v, acc);
+          wg[ij + n2 * k] = v;
+        }
+      }
+
+      if (kGs) {
+        // ---- arrive on this group's entities; the last arriver sums them ----
+        if (tid == 0) s_misc[0] = 0;
+        compute_sync<TCW>();   // all w_e stores of the group issued; list reset visible
+        for (int q = tid; q < cnt * kRefsPerElem; q += TCW) {
+          const int e = e0 + q / kRefsPerElem;
+          const int ref = P.eref[(size_t)e * kRefsPerElem + q % kRefsPerElem];
+          if (ref >= 0) {
+            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
+            const unsigned nin = cls == CLS_FACE ? 2u : (cls == CLS_EDGE ? P.e_nin[idx] : P.v_nin[idx]);
+            unsigned* tk = P.cnt + (cls == CLS_FACE ? idx : (cls == CLS_EDGE ? P.nF + idx : P.nF + P.nEd + idx));
+            // acq_rel: releases this CTA's w stores (ordered before by the barrier),
+            // acquires the other incidences' stores when this is the last arrival
+            const unsigned old = atom_add_acq_rel_gpu(tk, 1u);
+            if (old == nin - 1u) {
+              *tk = 0u;
+              s_list[atomicAdd(&s_misc[0], 1)] = ref;
             }
-          } else if (n > 2 && cls == CLS_EDGE) {
-            const int nin = P.e_nin[idx];
+          }
+        }
+        compute_sync<TCW>();
+        const int nl = s_misc[0];
+        if (nl > 0) {
+          constexpr int NW = Sh::NWC;
+          const int wid = tid >> 5;
+          constexpr int nf = (n - 2) * (n - 2), ne = n - 2;
+          constexpr int Nm1 = n > 2 ? n - 2 : 1;
+          for (int q = wid; q < nl; q += NW) {
+            const int ref = s_list[q];
+            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
+            int32_t base[8];
+            if (n > 2 && cls == CLS_FACE) {
+              base[0] = P.f_base[2 * idx];
+              base[1] = P.f_base[2 * idx + 1];
+              const int ax = P.f_axis[idx];
+              const int s1 = face_s1(ax, n), s2 = face_s2(ax, n);
+              for (int p = lane; p < nf; p += 32) {
+                const int off = (1 + p % Nm1) * s1 + (1 + p / Nm1) * s2;
+                sum_point(a.w, base, 2, off, false);
+              }
+            } else if (n > 2 && cls == CLS_EDGE) {
+              const int nin = P.e_nin[idx];
 #pragma unroll
-            for (int t = 0; t < 4; t++) base[t] = P.e_base[4 * idx + t];
-            const int sd = edge_stride(P.e_axis[idx], n);
-            const bool mk = P.e_mask[idx];
-            for (int p = lane; p < ne; p += 32) sum_point(a.w, base, nin, (1 + p) * sd, mk);
-          } else if (cls == CLS_VERT) {
-            const int nin = P.v_nin[idx];
+              for (int t = 0; t < 4; t++) base[t] = P.e_base[4 * idx + t];
+              const int sd = edge_stride(P.e_axis[idx], n);
+              const bool mk = P.e_mask[idx];
+              for (int p = lane; p < ne; p += 32) sum_point(a.w, base, nin, (1 + p) * sd, mk);
+            } else if (cls == CLS_VERT) {
+              const int nin = P.v_nin[idx];
 #pragma unroll
-            for (int t = 0; t < 8; t++) base[t] = P.v_base[8 * idx + t];
-            if (lane == 0) sum_point(a.w, base, nin, 0, P.v_mask[idx]);
+              for (int t = 0; t < 8; t++) base[t] = P.v_base[8 * idx + t];
+              if (lane == 0) sum_point(a.w, base, nin, 0, P.v_mask[idx]);
+            }
           }
         }
       }
-    }
-
-    // release the stage to the bulk-copy engine (WAW with the in-place w_r/w_s)
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      const int gn = g + S * gridDim.x;
-      if (gn < ng) issue(gn, s);
+      compute_sync<TCW>();   // w_r / w_s scratch free for the next group
     }
   }
 
@@ -316,7 +397,7 @@ static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int grid, cudaS
 template <int n, int MODE>
 static int occupancy_n() {
   using Sh = AxShape<n>;
-  auto kern = ax_kernel<n, MODE, true>;
+  auto kern = ax_kernel<n, MODE, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem_bytes);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Sh::T, Sh::smem_bytes) != cudaSuccess)
@@ -326,6 +407,10 @@ static int occupancy_n() {
 
 template <int MODE, bool FUSE>
 static cudaError_t dispatch(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
+#ifdef SEM_AX_ONLY_N8
+  if (P.n == 8) return launch_n<8, MODE, FUSE>(P, a, grid, s);
+  return cudaErrorInvalidValue;
+#endif
   switch (P.n) {
     case 2: return launch_n<2, MODE, FUSE>(P, a, grid, s);
     case 3: return launch_n<3, MODE, FUSE>(P, a, grid, s);
@@ -344,6 +429,9 @@ static cudaError_t dispatch(const DevPlan& P, const AxLaunch& a, int grid, cudaS
 
 template <int MODE>
 static int occ_dispatch(int n) {
+#ifdef SEM_AX_ONLY_N8
+  return occupancy_n<8, MODE>();
+#endif
   switch (n) {
     case 2: return occupancy_n<2, MODE>();
     case 3: return occupancy_n<3, MODE>();

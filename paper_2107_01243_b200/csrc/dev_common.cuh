@@ -131,6 +131,14 @@ __device__ __forceinline__ bool grid_reduce(const double (&v)[NV], double* parti
   return true;
 }
 
+// Geometric factors are stored element-blocked and plane-major,
+// G[e][k][f][i + n j] with f in (rr, ss, tt, rs, rt, st): one k-plane of all six
+// factors is a contiguous 48 n^2-byte block, the unit the Ax kernel streams.
+__host__ __device__ __forceinline__ int64_t g_index(int64_t el, int f, int p, int n) {
+  const int n2 = n * n, k = p / n2, ij = p - k * n2;
+  return el * 6 * n2 * n + (int64_t)(k * 6 + f) * n2 + ij;
+}
+
 // slot-mask from the element's 6-bit Dirichlet face code (reading Q8)
 __device__ __forceinline__ bool face_masked(unsigned bm, int i, int j, int k, int nm1) {
   return ((i == 0) && (bm & 1u)) || ((i == nm1) && (bm & 2u)) || ((j == 0) && (bm & 4u)) ||

@@ -87,10 +87,9 @@ __global__ void geom_kernel(int n, int64_t nslots, const double* __restrict__ xi
     R[2][2] = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * iJ;
     const double Jw = J * wq[i] * wq[j] * wq[k];
     const int ab[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};
-    double* Ge = G + el * 6 * n3;
     for (int f = 0; f < 6; f++) {
       const int x = ab[f][0], y = ab[f][1];
-      Ge[f * n3 + p] = Jw * (R[x][0] * R[y][0] + R[x][1] * R[y][1] + R[x][2] * R[y][2]);
+      G[g_index(el, f, p, n)] = Jw * (R[x][0] * R[y][0] + R[x][1] * R[y][1] + R[x][2] * R[y][2]);
     }
     B[l] = Jw;
   }
@@ -119,16 +118,16 @@ __global__ void diag_kernel(int n, int64_t nslots, const double* __restrict__ D,
     const int64_t el = l / n3;
     const int p = (int)(l - el * n3);
     const int i = p % n, j = (p / n) % n, k = p / (n * n);
-    const double* Ge = G + el * 6 * n3;
     double s = 0.0;
     for (int m = 0; m < n; m++) {
       const double a = D[m * n + i], b2 = D[m * n + j], c = D[m * n + k];
-      s = fma(a * a, Ge[0 * n3 + m + n * j + n * n * k], s);
-      s = fma(b2 * b2, Ge[1 * n3 + i + n * m + n * n * k], s);
-      s = fma(c * c, Ge[2 * n3 + i + n * j + n * n * m], s);
+      s = fma(a * a, G[g_index(el, 0, m + n * j + n * n * k, n)], s);
+      s = fma(b2 * b2, G[g_index(el, 1, i + n * m + n * n * k, n)], s);
+      s = fma(c * c, G[g_index(el, 2, i + n * j + n * n * m, n)], s);
     }
     const double dii = D[i * n + i], djj = D[j * n + j], dkk = D[k * n + k];
-    s += 2.0 * (Ge[3 * n3 + p] * dii * djj + Ge[4 * n3 + p] * dii * dkk + Ge[5 * n3 + p] * djj * dkk);
+    s += 2.0 * (G[g_index(el, 3, p, n)] * dii * djj + G[g_index(el, 4, p, n)] * dii * dkk +
+                G[g_index(el, 5, p, n)] * djj * dkk);
     d[l] = s;
   }
 }
@@ -210,42 +209,58 @@ __global__ void mult_kernel(const DevPlan P, uint8_t* mult) {
 }
 
 // standalone gs over the rank-local entities: one thread per entity point,
-// ascending-slot sum, broadcast write (no atomics)
-__global__ void gs_local_kernel(const DevPlan P, double* __restrict__ u, int apply_mask) {
-  const int n = P.n, N = n - 1;
-  const int64_t nf = (int64_t)(N - 1) * (N - 1), ne = N - 1;
-  const int64_t tF = P.nF * nf, tE = P.nEd * ne, tot = tF + tE + P.nV;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-       t += (int64_t)gridDim.x * blockDim.x) {
+// ascending-slot sum, broadcast write (no atomics).  Templated on n so the
+// point -> (entity, offset) decomposition is a constant division.
+template <int n>
+__global__ void __launch_bounds__(256) gs_local_kernel(const DevPlan P, double* __restrict__ u,
+                                                       int apply_mask) {
+  constexpr int N = n - 1;
+  constexpr int nf = (N - 1) * (N - 1), ne = N - 1;
+  constexpr int Nm1 = N > 1 ? N - 1 : 1;
+  const int tF = P.nF * nf, tE = P.nEd * ne, tot = tF + tE + P.nV;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
     int32_t base[8];
     int nin, off;
     bool mk = false;
-    if (t < tF) {
-      const int64_t f = t / nf;
-      const int p = (int)(t - f * nf);
+    if (nf > 0 && t < tF) {
+      const int f = t / (nf > 0 ? nf : 1);
+      const int p = t - f * nf;
       const int ax = P.f_axis[f];
-      off = (1 + p % (N - 1)) * f_s1(ax, n) + (1 + p / (N - 1)) * f_s2(ax, n);
+      off = (1 + p % Nm1) * f_s1(ax, n) + (1 + p / Nm1) * f_s2(ax, n);
       nin = 2;
-      base[0] = P.f_base[2 * f];
-      base[1] = P.f_base[2 * f + 1];
-    } else if (t < tF + tE) {
-      const int64_t q = t - tF, e = q / ne;
-      const int p = (int)(q - e * ne);
+      const int2 b2 = reinterpret_cast<const int2*>(P.f_base)[f];
+      base[0] = b2.x;
+      base[1] = b2.y;
+    } else if (ne > 0 && t < tF + tE) {
+      const int q = t - tF, e = q / (ne > 0 ? ne : 1);
+      const int p = q - e * ne;
       off = (1 + p) * e_sd(P.e_axis[e], n);
       nin = P.e_nin[e];
-      for (int x = 0; x < 4; x++) base[x] = P.e_base[4 * e + x];
+      const int4 b4 = reinterpret_cast<const int4*>(P.e_base)[e];
+      base[0] = b4.x; base[1] = b4.y; base[2] = b4.z; base[3] = b4.w;
       mk = P.e_mask[e];
     } else {
-      const int64_t v = t - tF - tE;
+      const int v = t - tF - tE;
       off = 0;
       nin = P.v_nin[v];
-      for (int x = 0; x < 8; x++) base[x] = P.v_base[8 * v + x];
+      const int4 b0 = reinterpret_cast<const int4*>(P.v_base)[2 * v];
+      const int4 b1 = reinterpret_cast<const int4*>(P.v_base)[2 * v + 1];
+      base[0] = b0.x; base[1] = b0.y; base[2] = b0.z; base[3] = b0.w;
+      base[4] = b1.x; base[5] = b1.y; base[6] = b1.z; base[7] = b1.w;
       mk = P.v_mask[v];
     }
-    double s = u[base[0] + off];
-    for (int x = 1; x < nin; x++) s += u[base[x] + off];
+    double v[8];
+#pragma unroll
+    for (int x = 0; x < 8; x++)
+      if (x < nin) v[x] = u[base[x] + off];
+    double s = v[0];
+#pragma unroll
+    for (int x = 1; x < 8; x++)
+      if (x < nin) s += v[x];
     if (apply_mask && mk) s = 0.0;
-    for (int x = 0; x < nin; x++) u[base[x] + off] = s;
+#pragma unroll
+    for (int x = 0; x < 8; x++)
+      if (x < nin) u[base[x] + off] = s;
   }
 }
 
@@ -562,7 +577,21 @@ cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, cudaStr
   const int64_t N = P.N;
   const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
   if (tot == 0) return cudaSuccess;
-  dev::gs_local_kernel<<<grid_for(tot), kThreads, 0, s>>>(P, u, apply_mask);
+  const int g = grid_for(tot, 148 * 16);
+  switch (P.n) {
+    case 2: dev::gs_local_kernel<2><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 3: dev::gs_local_kernel<3><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 4: dev::gs_local_kernel<4><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 5: dev::gs_local_kernel<5><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 6: dev::gs_local_kernel<6><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 7: dev::gs_local_kernel<7><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 8: dev::gs_local_kernel<8><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 9: dev::gs_local_kernel<9><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 10: dev::gs_local_kernel<10><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 11: dev::gs_local_kernel<11><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    case 12: dev::gs_local_kernel<12><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -60,6 +60,7 @@ struct AxLaunch {
   unsigned* red_ticket;
   double* red_out;
   const int* done;
+  double Dm[144];                 // D (row-major n x n), read from the constant bank
 };
 
 // returns max resident CTAs/SM for the Ax kernel of this N and mode

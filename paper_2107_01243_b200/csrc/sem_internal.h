@@ -54,6 +54,11 @@ struct HostPlan {
 };
 
 int build_plan(const sem_mesh* m, int N, HostPlan* p);   // returns SEM_* status
+// device G layout (see dev_common.cuh g_index): G[e][k][f][i + n j]
+inline int64_t g_index_host(int64_t el, int f, int p, int n) {
+  const int n2 = n * n, k = p / n2, ij = p - k * n2;
+  return el * 6 * n2 * n + (int64_t)(k * 6 + f) * n2 + ij;
+}
 void gll_rule(int N, std::vector<double>* xi, std::vector<double>* w);
 void deriv_matrix(int N, const std::vector<double>& xi, std::vector<double>* D);
 int64_t lattice_gid(const HostPlan& p, int64_t e_global, int i, int j, int k);

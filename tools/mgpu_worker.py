@@ -1,0 +1,108 @@
+"""Multi-GPU parity worker (launched by tests/test_multigpu.py under torchrun).
+
+Every rank builds its z-slab (lexicographic element range) of the mesh through
+the C ABI with an NCCL communicator; rank 0 gathers the local E-vectors and
+compares them with the oracle run with the SAME number of ranks (so the
+gather-scatter summation order -- ascending slots within a rank, ascending
+ranks across -- is identical):
+  * gs: bit-exact;  apply / rhs: normwise 1e-12;  PCG: iterations +-1, x within 1e-10.
+Exits non-zero on any mismatch.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2107_01243_b200 as sem  # noqa: E402
+from sem_inputs import f_sin, f_tgv, random_field, tgv_box, unit_box  # noqa: E402
+
+CASES = [
+    (tgv_box(4, 4, 8), 5, f_tgv),                    # z-slabs, periodic: 2 planes shared
+    (unit_box(3, 2, 5), 4, f_sin),                   # Dirichlet, slabs cut mid-layer
+    (tgv_box(4, 4, 8, deform=1), 7, f_tgv),          # curvilinear, overlap path
+    (unit_box(4, 3, 8, periodic=(1, 0, 0)), 3, f_sin),
+]
+
+
+def main():
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = [sem.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = sem.nccl_comm_init(uid[0], rank, P)
+    fails = []
+    for ci, (spec, N, fun) in enumerate(CASES):
+        E, n3 = spec.E, (N + 1) ** 3
+        lo, hi = rank * E // P, (rank + 1) * E // P
+        o = None
+        if rank == 0:
+            import oracle as O
+            o = O.Oracle(spec, N, nranks=P)
+        u = random_field(E * n3, seed=100 + ci)
+        ul = np.ascontiguousarray(u[lo * n3:hi * n3])
+        for fused in (False, True):
+            with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm) as c:
+                c.set_fused_gs(fused)
+                assert c.n_local == (hi - lo) * n3
+                du = torch.from_numpy(ul).cuda()
+                w = c.zeros()
+                c.apply(du, w)
+                g = du.clone()
+                c.gs(g)
+                X, Y, Z = c.coords()
+                fv = fun(X, Y, Z, xp=torch)
+                b = c.zeros()
+                c.rhs(fv, b)
+                x = c.zeros()
+                r = c.pcg_solve(b, x, 1e-10, 3000)
+                torch.cuda.synchronize()
+                parts = [None] * P
+                dist.all_gather_object(parts, (w.cpu().numpy(), g.cpu().numpy(), b.cpu().numpy(),
+                                               x.cpu().numpy(), r))
+                if rank == 0:
+                    W = np.concatenate([p[0] for p in parts])
+                    Gs = np.concatenate([p[1] for p in parts])
+                    B = np.concatenate([p[2] for p in parts])
+                    Xs = np.concatenate([p[3] for p in parts])
+                    ref_w = o.apply(u)
+                    tag = f"case{ci} P={P} fused={fused}"
+                    e = np.abs(W - ref_w).max() / np.abs(ref_w).max()
+                    if not e <= 1e-12:
+                        fails.append(f"{tag}: apply rel err {e:.2e}")
+                    if not np.array_equal(Gs, o.gs(u)):
+                        fails.append(f"{tag}: gs not bit-exact "
+                                     f"(max diff {np.abs(Gs - o.gs(u)).max():.2e})")
+                    fo = fun(o.get("X"), o.get("Y"), o.get("Z"))
+                    ref_b = o.rhs(fo)
+                    e = np.abs(B - ref_b).max() / np.abs(ref_b).max()
+                    if not e <= 1e-12:
+                        fails.append(f"{tag}: rhs rel err {e:.2e}")
+                    ref = o.pcg(ref_b, 1e-10, 3000)
+                    if abs(r["iters"] - ref["iters"]) > 1 or r["status"] != 0:
+                        fails.append(f"{tag}: pcg iters {r['iters']} vs {ref['iters']} st {r['status']}")
+                    dx = np.abs(Xs - ref["x"]).max()
+                    if not dx <= 1e-10:
+                        fails.append(f"{tag}: pcg x diff {dx:.2e}")
+                    if not abs(r["res_final"] - ref["res_final"]) <= 1e-10:
+                        fails.append(f"{tag}: pcg res {r['res_final']:.3e} vs {ref['res_final']:.3e}")
+                    print(f"{tag}: ok-check iters {r['iters']} (oracle {ref['iters']}) "
+                          f"dx {dx:.2e}", flush=True)
+    sem.nccl_comm_destroy(comm)
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        for f in fails:
+            print("FAIL", f, flush=True)
+        print("RESULT", "FAIL" if fails else "PASS", flush=True)
+        sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
