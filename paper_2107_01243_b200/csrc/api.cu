@@ -251,7 +251,7 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
                                  mode == sem::AX_PCG ? st : nullptr, nparts, c->stream));
   c->launches++;
   if (mode == sem::AX_PCG)
-    NCCL_TRY(ncclAllReduce(&st->sigma, &st->sigma, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    NCCL_TRY(ncclAllReduce(&st->loc[2], &st->sigma, 1, ncclDouble, ncclSum, c->nccl, c->stream));
   return SEM_OK;
 }
 
@@ -273,6 +273,15 @@ int gs_op(sem_ctx* c, double* u, int apply_mask) {
 int allreduce(sem_ctx* c, double* p, size_t count) {
   if (c->hp.nranks > 1)
     NCCL_TRY(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->nccl, c->stream));
+  return SEM_OK;
+}
+
+// out-of-place reduction of this rank's partials into the global scalars: safe
+// to repeat (kernels of converged iterations are no-ops but the collectives
+// still run, re-reducing the same partials)
+int allreduce_to(sem_ctx* c, const double* loc, double* glob, size_t count) {
+  if (c->hp.nranks > 1)
+    NCCL_TRY(ncclAllReduce(loc, glob, count, ncclDouble, ncclSum, c->nccl, c->stream));
   return SEM_OK;
 }
 
@@ -511,9 +520,11 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   init.maxit = maxit;
   std::memcpy(c->h_st, &init, sizeof(init));   // h_st is idle: every solve ends synchronised
   CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
+  const bool dist = c->hp.nranks > 1;
+  double* rg_out = dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, c->d_dinv, b, x, c->d_r, c->d_p, c->d_partial,
-                               st, c->red_grid, s));
-  SEM_TRY(allreduce(c, &st->rho_new, 2));
+                               st, rg_out, c->red_grid, s));
+  SEM_TRY(allreduce_to(c, &st->loc[0], &st->rho_new, 2));
   CUDA_TRY(sem::launch_cg_start(st, c->d_hist, s));
   c->launches += 2;
   int done = 0;
@@ -523,9 +534,9 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
       SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
       int tk = timer_begin(c, 1);
       CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, x, c->d_r, c->d_p, c->d_wv,
-                                     c->d_partial, st, c->red_grid, s));
+                                     c->d_partial, st, rg_out, c->red_grid, s));
       timer_end(c, tk);
-      SEM_TRY(allreduce(c, &st->rho_new, 2));
+      SEM_TRY(allreduce_to(c, &st->loc[0], &st->rho_new, 2));
       tk = timer_begin(c, 2);
       CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, st, c->d_hist, c->red_grid, s));
       timer_end(c, tk);
@@ -538,9 +549,10 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   }
   // true residual once at the end (reading Q17)
   SEM_TRY(apply_op(c, x, c->d_wv, sem::AX_APPLY));
-  CUDA_TRY(sem::launch_cg_residual(c->dp, c->d_mult, b, c->d_wv, c->d_partial, st, c->red_grid, s));
+  CUDA_TRY(sem::launch_cg_residual(c->dp, c->d_mult, b, c->d_wv, c->d_partial, st,
+                                   dist ? &st->loc[3] : &st->res_true, c->red_grid, s));
   c->launches++;
-  SEM_TRY(allreduce(c, &st->res_true, 1));
+  SEM_TRY(allreduce_to(c, &st->loc[3], &st->res_true, 1));
   CUDA_TRY(cudaMemcpyAsync(c->h_st, st, sizeof(sem::PcgState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   timer_collect(c);

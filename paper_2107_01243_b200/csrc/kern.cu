@@ -290,7 +290,7 @@ __global__ void gs_unpack_kernel(const DevPlan P, double* __restrict__ u, const 
   if (st && blockIdx.x == 0 && threadIdx.x == 0) {
     double sg = st->sigma_part[0];
     for (int q = 1; q < nparts; q++) sg += st->sigma_part[q];
-    st->sigma = sg;
+    st->loc[2] = sg;   // this rank's sigma; allreduced out-of-place into st->sigma
   }
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.nS;
        s += (int64_t)gridDim.x * blockDim.x) {
@@ -343,7 +343,8 @@ __global__ void sum_c_kernel(int64_t n, const uint8_t* __restrict__ mult,
 __global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                const double* __restrict__ dinv, const double* __restrict__ b,
                                double* __restrict__ x, double* __restrict__ r,
-                               double* __restrict__ p, double* partial, PcgState* st) {
+                               double* __restrict__ p, double* partial, PcgState* st,
+                               double* out2) {
   __shared__ double scratch[32];
   __shared__ int flag;
   double rz = 0.0, rr = 0.0;
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint
     rr = fma(c * bl, bl, rr);
   }
   double v[2] = {rz, rr};
-  grid_reduce<2>(v, partial, &st->tickets[1], &st->rho_new, scratch, &flag);
+  grid_reduce<2>(v, partial, &st->tickets[1], out2, scratch, &flag);
 }
 
 __global__ void cg_start_kernel(PcgState* st, double* hist) {
@@ -374,7 +375,8 @@ __global__ void cg_start_kernel(PcgState* st, double* hist) {
 __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                  const double* __restrict__ dinv, double* __restrict__ x,
                                  double* __restrict__ r, const double* __restrict__ p,
-                                 const double* __restrict__ w, double* partial, PcgState* st) {
+                                 const double* __restrict__ w, double* partial, PcgState* st,
+                                 double* out2) {
   __shared__ double scratch[32];
   __shared__ int flag;
   if (st->done) return;
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
     }
   }
   double v[2] = {rz, rr};
-  if (grid_reduce<2>(v, partial, &st->tickets[2], &st->rho_new, scratch, &flag)) {
+  if (grid_reduce<2>(v, partial, &st->tickets[2], out2, scratch, &flag)) {
     if (threadIdx.x == 0 && !ok) {
       st->done = 2;
       st->iters = st->it + 1;
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double*
 // true residual: sqrt(sum c (b - A x)^2) -> st->res_true (after allreduce by the host)
 __global__ void cg_residual_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                    const double* __restrict__ b, const double* __restrict__ w,
-                                   double* partial, PcgState* st) {
+                                   double* partial, PcgState* st, double* out1) {
   __shared__ double scratch[32];
   __shared__ int flag;
   double s = 0.0;
@@ -500,7 +502,7 @@ __global__ void cg_residual_kernel(int64_t n, const uint8_t* __restrict__ mult,
     s = fma(c_of(mult[l]) * d, d, s);
   }
   double v[1] = {s};
-  grid_reduce<1>(v, partial, &st->tickets[4], &st->res_true, scratch, &flag);
+  grid_reduce<1>(v, partial, &st->tickets[4], out1, scratch, &flag);
 }
 
 inline int grid_for(int64_t work, int cap = 148 * 8) {
@@ -624,9 +626,9 @@ cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a,
 }
 
 cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv, const double* b,
-                           double* x, double* r, double* p, double* partial, PcgState* st, int grid,
-                           cudaStream_t s) {
-  dev::cg_init_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, b, x, r, p, partial, st);
+                           double* x, double* r, double* p, double* partial, PcgState* st,
+                           double* out2, int grid, cudaStream_t s) {
+  dev::cg_init_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, b, x, r, p, partial, st, out2);
   return cudaGetLastError();
 }
 
@@ -637,8 +639,9 @@ cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s) {
 
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
                              double* r, const double* p, const double* w, double* partial,
-                             PcgState* st, int grid, cudaStream_t s) {
-  dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, x, r, p, w, partial, st);
+                             PcgState* st, double* out2, int grid, cudaStream_t s) {
+  dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, x, r, p, w, partial, st,
+                                                  out2);
   return cudaGetLastError();
 }
 
@@ -649,9 +652,9 @@ cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, d
 }
 
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
-                               const double* w, double* partial, PcgState* st, int grid,
-                               cudaStream_t s) {
-  dev::cg_residual_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, b, w, partial, st);
+                               const double* w, double* partial, PcgState* st, double* out1,
+                               int grid, cudaStream_t s) {
+  dev::cg_residual_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, b, w, partial, st, out1);
   return cudaGetLastError();
 }
 

@@ -44,6 +44,8 @@ struct PcgState {
   double tol;
   double res_true;
   double sigma_part[2];  // per Ax launch when the operator is split (Alg. 1 overlap)
+  double loc[4];         // P > 1: this rank's rho_new, gamma, sigma, res_true partial sums;
+                         // the allreduce is out-of-place loc -> global, hence idempotent
   int it;                // completed iterations
   int done;              // 0 running, 1 converged, 2 breakdown, 3 NaN, 4 maxit
   int iters;
@@ -100,15 +102,15 @@ cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a,
 cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStream_t s);
 cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv,
                            const double* b, double* x, double* r, double* p, double* partial,
-                           PcgState* st, int grid, cudaStream_t s);
+                           PcgState* st, double* out2, int grid, cudaStream_t s);
 cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s);
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
                              double* r, const double* p, const double* w, double* partial,
-                             PcgState* st, int grid, cudaStream_t s);
+                             PcgState* st, double* out2, int grid, cudaStream_t s);
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
                         PcgState* st, double* hist, int grid, cudaStream_t s);
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
-                               const double* w, double* partial, PcgState* st, int grid,
-                               cudaStream_t s);
+                               const double* w, double* partial, PcgState* st, double* out1,
+                               int grid, cudaStream_t s);
 
 }  // namespace sem
