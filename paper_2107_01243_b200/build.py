@@ -38,6 +38,16 @@ def _deps_mtime():
     return max(os.path.getmtime(f) for f in files)
 
 
+def _check_spills(log: str, limit: int = 16):
+    """Warn when a hot-path kernel at N=7 (n=8) spills: the register allocation at
+    the 168-register cap is fragile and a spill costs ~20% of Ax throughput."""
+    import re
+    for m in re.finditer(r"Compiling entry function '(_ZN3sem3dev9ax_kernelILi8E[^']*)'[^\n]*\n"
+                         r"[^\n]*?(\d+) bytes spill stores", log):
+        if int(m.group(2)) > limit:
+            print(f"WARNING: {m.group(1)} spills {m.group(2)} bytes", file=sys.stderr)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _deps_mtime():
         return SO
@@ -65,6 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         logs = list(ex.map(run, jobs))
     with open(os.path.join(OBJ, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
+    _check_spills("\n".join(logs))
     if verbose:
         print("\n".join(logs))
     objs = [os.path.join(OBJ, f + ".o") for f in CUDA_SRCS + CXX_SRCS]

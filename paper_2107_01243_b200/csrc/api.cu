@@ -88,6 +88,8 @@ struct sem_ctx {
   // work
   double *d_r = nullptr, *d_p = nullptr, *d_wv = nullptr, *d_tmp = nullptr;
   double* d_partial = nullptr;        // reduction partials
+  double* d_partial_ax = nullptr;     // per-CTA sigma partials of the Ax kernel
+  int* d_nsig = nullptr;              // their count
   unsigned* d_tickets = nullptr;      // misc tickets
   double* d_scal = nullptr;           // misc scalars
   sem::PcgState* d_st = nullptr;
@@ -180,7 +182,8 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.w = w;
   a.G = c->d_G;
   a.r0lo = r0lo; a.r0hi = r0hi; a.r1lo = r1lo; a.r1hi = r1hi;
-  a.red_partial = c->d_partial;
+  a.red_partial = red_out ? c->d_partial : c->d_partial_ax;
+  a.red_count = c->d_nsig;
   a.red_ticket = &c->d_st->tickets[0];
   a.red_out = red_out;
   a.done = &c->d_st->done;
@@ -226,7 +229,9 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   const sem::HostPlan& h = c->hp;
   sem::PcgState* st = c->d_st;
   if (h.nranks == 1 || h.nS == 0) {
-    SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, &st->sigma));
+    // single rank: the CG update kernel sums the per-CTA sigma partials itself
+    SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0,
+                   (mode == sem::AX_PCG && h.nranks == 1) ? nullptr : &st->sigma));
     SEM_TRY(gs_pass(c, w));
     return SEM_OK;
   }
@@ -299,7 +304,7 @@ void free_ctx(sem_ctx* c) {
                   c->d_emask, c->d_vnin, c->d_vmask, c->d_cnt, c->d_sslot, c->d_soff,
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
-                  c->d_scal, c->d_st, c->d_hist};
+                  c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -403,6 +408,8 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   c->ax_grid = c->num_sms * sem::ax_occupancy(h.N, sem::AX_PCG);
   c->red_grid = sem::cg_grid(c->num_sms);
   SETUP_TRY(dalloc(&c->d_partial, (size_t)2 * std::max(c->ax_grid, c->red_grid)));
+  SETUP_TRY(dalloc(&c->d_partial_ax, (size_t)c->ax_grid + 8));
+  SETUP_TRY(dalloc(&c->d_nsig, 1));
   SETUP_TRY(dalloc(&c->d_tickets, 8));
   SETUP_CUDA(cudaMemsetAsync(c->d_tickets, 0, 8 * sizeof(unsigned), s));
   SETUP_TRY(dalloc(&c->d_scal, 8));
@@ -534,7 +541,8 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
       SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
       int tk = timer_begin(c, 1);
       CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, x, c->d_r, c->d_p, c->d_wv,
-                                     c->d_partial, st, rg_out, c->red_grid, s));
+                                     c->d_partial, st, rg_out, dist ? nullptr : c->d_partial_ax,
+                                     c->d_nsig, c->red_grid, s));
       timer_end(c, tk);
       SEM_TRY(allreduce_to(c, &st->loc[0], &st->rho_new, 2));
       tk = timer_begin(c, 2);

@@ -131,6 +131,10 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
   constexpr bool kMask = MODE != AX_ONLY;   // Dirichlet mask in the epilogue
   constexpr bool kGs = kMask && FUSE;         // last-arriver gather-scatter in-kernel
   constexpr bool kDreg = n <= 9;              // D rows in registers (else shared memory)
+#ifndef SEM_DT_REG
+#define SEM_DT_REG 1
+#endif
+  constexpr bool kDtreg = kDreg && SEM_DT_REG; // transposed-contraction D columns in registers
 
   if (MODE == AX_PCG && *a.done) return;
 
@@ -234,8 +238,8 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     for (int m = 0; m < n; m++) {
       Di[m] = kDreg ? a.Dm[i * n + m] : 0.0;
       Dj[m] = kDreg ? a.Dm[j * n + m] : 0.0;
-      Dti[m] = kDreg ? a.Dm[m * n + i] : 0.0;
-      Dtj[m] = kDreg ? a.Dm[m * n + j] : 0.0;
+      Dti[m] = kDtreg ? a.Dm[m * n + i] : 0.0;
+      Dtj[m] = kDtreg ? a.Dm[m * n + j] : 0.0;
     }
     int su = 0, sg = 0;
     uint32_t phu = 0, phg = 0;
@@ -304,8 +308,8 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
           double v = rw[k];
 #pragma unroll
           for (int m = 0; m < n; m++) {
-            v = fma(kDreg ? Dti[m] : sDt[i * dp + m], wr_s[m + rp * j + wpl * k], v);
-            v = fma(kDreg ? Dtj[m] : sDt[j * dp + m], ws_s[i + rp * m + wpl * k], v);
+            v = fma(kDtreg ? Dti[m] : sDt[i * dp + m], wr_s[m + rp * j + wpl * k], v);
+            v = fma(kDtreg ? Dtj[m] : sDt[j * dp + m], ws_s[i + rp * m + wpl * k], v);
           }
           if (kMask && ((kmask >> k) & 1u)) v = 0.0;
           if (MODE == AX_PCG) acc = fma(ru[k], v, acc);
@@ -374,8 +378,16 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
   }
 
   if (MODE == AX_PCG) {
-    double v[1] = {acc};
-    grid_reduce<1>(v, a.red_partial, a.red_ticket, a.red_out, s_red, &s_misc[1]);
+    if (a.red_out) {
+      double v[1] = {acc};
+      grid_reduce<1>(v, a.red_partial, a.red_ticket, a.red_out, s_red, &s_misc[1]);
+    } else {   // partials only; the consumer kernel sums them (no last-block tail)
+      const double bs = block_sum(acc, s_red);
+      if (tid == 0) {
+        a.red_partial[blockIdx.x] = bs;
+        if (blockIdx.x == 0) *a.red_count = gridDim.x;
+      }
+    }
   }
 }
 

@@ -208,30 +208,57 @@ __global__ void mult_kernel(const DevPlan P, uint8_t* mult) {
   }
 }
 
-// standalone gs over the rank-local entities: one thread per entity point,
-// ascending-slot sum, broadcast write (no atomics).  Templated on n so the
-// point -> (entity, offset) decomposition is a constant division.
+// standalone gs over the rank-local entities: ascending-slot sum, broadcast
+// write, no atomics.  Templated on n so the point -> (entity, offset)
+// decomposition is a constant division.  Face points (2 incidences, ~85% of
+// the points) are processed F per thread with all 2F loads issued before any
+// use (the kernel is L2-latency bound); edges and vertices one per thread.
 template <int n>
 __global__ void __launch_bounds__(256) gs_local_kernel(const DevPlan P, double* __restrict__ u,
                                                        int apply_mask) {
   constexpr int N = n - 1;
   constexpr int nf = (N - 1) * (N - 1), ne = N - 1;
   constexpr int Nm1 = N > 1 ? N - 1 : 1;
+  constexpr int F = 4;
   const int tF = P.nF * nf, tE = P.nEd * ne, tot = tF + tE + P.nV;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+  const int nth = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (nf > 0) {
+    for (int t0 = tid; t0 < tF; t0 += nth * F) {
+      int a0[F], a1[F];
+      bool ok[F];
+#pragma unroll
+      for (int q = 0; q < F; q++) {
+        const int t = t0 + q * nth;
+        ok[q] = t < tF;
+        const int f = ok[q] ? t / (nf > 0 ? nf : 1) : 0;
+        const int p = t - f * nf;
+        const int ax = P.f_axis[f];
+        const int off = (1 + p % Nm1) * f_s1(ax, n) + (1 + p / Nm1) * f_s2(ax, n);
+        const int2 b2 = reinterpret_cast<const int2*>(P.f_base)[f];
+        a0[q] = b2.x + off;
+        a1[q] = b2.y + off;
+      }
+      double v0[F], v1[F];
+#pragma unroll
+      for (int q = 0; q < F; q++)
+        if (ok[q]) {
+          v0[q] = u[a0[q]];
+          v1[q] = u[a1[q]];
+        }
+#pragma unroll
+      for (int q = 0; q < F; q++)
+        if (ok[q]) {
+          const double s = v0[q] + v1[q];
+          u[a0[q]] = s;
+          u[a1[q]] = s;
+        }
+    }
+  }
+  for (int t = tF + tid; t < tot; t += nth) {
     int32_t base[8];
     int nin, off;
     bool mk = false;
-    if (nf > 0 && t < tF) {
-      const int f = t / (nf > 0 ? nf : 1);
-      const int p = t - f * nf;
-      const int ax = P.f_axis[f];
-      off = (1 + p % Nm1) * f_s1(ax, n) + (1 + p / Nm1) * f_s2(ax, n);
-      nin = 2;
-      const int2 b2 = reinterpret_cast<const int2*>(P.f_base)[f];
-      base[0] = b2.x;
-      base[1] = b2.y;
-    } else if (ne > 0 && t < tF + tE) {
+    if (ne > 0 && t < tF + tE) {
       const int q = t - tF, e = q / (ne > 0 ? ne : 1);
       const int p = q - e * ne;
       off = (1 + p) * e_sd(P.e_axis[e], n);
@@ -376,11 +403,28 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
                                  const double* __restrict__ dinv, double* __restrict__ x,
                                  double* __restrict__ r, const double* __restrict__ p,
                                  const double* __restrict__ w, double* partial, PcgState* st,
-                                 double* out2) {
+                                 double* out2, const double* __restrict__ sig_part,
+                                 const int* sig_count) {
   __shared__ double scratch[32];
   __shared__ int flag;
+  __shared__ double s_sig;
   if (st->done) return;
-  const double sigma = st->sigma;
+  double sigma;
+  if (sig_part) {
+    // sigma = sum of the Ax kernel's per-CTA partials, in a fixed order
+    if (threadIdx.x < 32) {
+      const int G = *sig_count;
+      double v = 0.0;
+      for (int b = threadIdx.x; b < G; b += 32) v += sig_part[b];
+      v = warp_sum(v);
+      if (threadIdx.x == 0) s_sig = v;
+    }
+    __syncthreads();
+    sigma = s_sig;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->sigma = sigma;
+  } else {
+    sigma = st->sigma;
+  }
   const bool ok = sigma > 0.0;   // breakdown guard (also catches NaN)
   const double alpha = ok ? st->rho_old / sigma : 0.0;
   double rz = 0.0, rr = 0.0;
@@ -639,9 +683,10 @@ cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s) {
 
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
                              double* r, const double* p, const double* w, double* partial,
-                             PcgState* st, double* out2, int grid, cudaStream_t s) {
+                             PcgState* st, double* out2, const double* sig_part,
+                             const int* sig_count, int grid, cudaStream_t s) {
   dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, x, r, p, w, partial, st,
-                                                  out2);
+                                                  out2, sig_part, sig_count);
   return cudaGetLastError();
 }
 

@@ -60,9 +60,10 @@ struct AxLaunch {
   int r0lo, r0hi, r1lo, r1hi;     // element ranges (local indices)
   double* red_partial;            // PCG: per-block partials
   unsigned* red_ticket;
-  double* red_out;
+  double* red_out;                // PCG: reduced sigma (last block), or nullptr: partials only
   const int* done;
   double Dm[144];                 // D (row-major n x n), read from the constant bank
+  int* red_count;                 // PCG partials only: number of partials (written by block 0)
 };
 
 // returns max resident CTAs/SM for the Ax kernel of this N and mode
@@ -104,9 +105,12 @@ cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* 
                            const double* b, double* x, double* r, double* p, double* partial,
                            PcgState* st, double* out2, int grid, cudaStream_t s);
 cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s);
+// sig_part/sig_count: the Ax kernel's per-CTA sigma partials (P = 1; every block
+// re-sums them in a fixed order) or nullptr (P > 1: sigma is already allreduced)
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
                              double* r, const double* p, const double* w, double* partial,
-                             PcgState* st, double* out2, int grid, cudaStream_t s);
+                             PcgState* st, double* out2, const double* sig_part,
+                             const int* sig_count, int grid, cudaStream_t s);
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
                         PcgState* st, double* hist, int grid, cudaStream_t s);
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
