@@ -189,9 +189,9 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.done = &c->d_st->done;
   std::copy(c->hp.D.begin(), c->hp.D.end(), a.Dm);
   const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
-  int grid = std::min(c->ax_grid, std::max(ng, 1));
+  const int groups = std::max(ng, 1);   // the launcher caps the grid at residency
   int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
-  cudaError_t e = sem::launch_ax(c->dp, a, mode, grid, c->stream, c->fuse_gs);
+  cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream, c->fuse_gs);
   timer_end(c, tk);
   c->launches++;
   return check(e, "ax kernel");
@@ -407,8 +407,8 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   // launch geometry (persistent grids sized to the SM count x residency)
   c->ax_grid = c->num_sms * sem::ax_occupancy(h.N, sem::AX_PCG);
   c->red_grid = sem::cg_grid(c->num_sms);
-  SETUP_TRY(dalloc(&c->d_partial, (size_t)2 * std::max(c->ax_grid, c->red_grid)));
-  SETUP_TRY(dalloc(&c->d_partial_ax, (size_t)c->ax_grid + 8));
+  SETUP_TRY(dalloc(&c->d_partial, (size_t)2 * std::max(c->num_sms * 32, c->red_grid)));
+  SETUP_TRY(dalloc(&c->d_partial_ax, (size_t)c->num_sms * 32 + 8));   // >= any Ax grid
   SETUP_TRY(dalloc(&c->d_nsig, 1));
   SETUP_TRY(dalloc(&c->d_tickets, 8));
   SETUP_CUDA(cudaMemsetAsync(c->d_tickets, 0, 8 * sizeof(unsigned), s));

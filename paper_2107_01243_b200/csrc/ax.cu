@@ -34,6 +34,9 @@ template <int n>
 struct AxCfg;
 // NE: elements computed together by one CTA (64-160 compute threads)
 // NSG: depth of the G plane ring (planes in flight per CTA)
+#ifndef SEM_AX_SMEM_PAD
+#define SEM_AX_SMEM_PAD 0   // tuning experiments only: extra smem to force lower residency
+#endif
 // PPC: k-planes per bulk copy (divides n).  n=8 tuned with tools/ubench_ax.cu
 // on B200 (NSG=3, PPC=4: 6.2 TB/s on 32^3 elements); the others follow the same
 // rule of ~2 copies per element and a 2-3 slot ring within ~60 KB of smem.
@@ -60,7 +63,7 @@ template <> struct AxCfg<10> { static constexpr int NE = 1, NSG = 3, PPC = 5; };
 template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = 6, PPC = 1; };
 template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = 3, PPC = 3; };
 
-template <int n>
+template <int n, bool GS = false>
 struct AxShape {
   static constexpr int NE = AxCfg<n>::NE, NSG = AxCfg<n>::NSG, PPC = AxCfg<n>::PPC;
   static_assert(n % PPC == 0, "planes per copy must divide n");
@@ -68,7 +71,8 @@ struct AxShape {
   static constexpr int TC = NE * n2;               // computing threads
   static constexpr int TCW = (TC + 31) / 32 * 32;  // compute warps x 32
   static constexpr int NWC = TCW / 32;             // compute warps
-  static constexpr int T = TCW + 32;               // + one producer warp
+  static constexpr int T = TCW + 32 + (GS ? 32 : 0);  // + producer warp (+ gather-scatter warp)
+  static constexpr int NSD = 4;                    // element-done ring (compute -> gs warp)
   static constexpr int NSU = 2;                    // u ring depth
   static constexpr bool kBulkU = (n % 2) == 0;     // u block 16-B aligned for any element
   static constexpr int uslot = NE * n3;            // doubles per u slot
@@ -78,13 +82,16 @@ struct AxShape {
   static constexpr int wel = n * wpl;              // per element
   static constexpr int dpad = n + 1;
   static constexpr int kMaxList = NE * kRefsPerElem;
-  static constexpr int nbar = 2 * NSG + 2 * NSU;
+  static constexpr int nbar = 2 * NSG + 2 * NSU + 2 * NSD;
   static constexpr size_t smem_bytes =
       sizeof(double) * ((size_t)NSU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32) +
-      sizeof(uint64_t) * nbar + sizeof(int) * (kMaxList + 8);
+      sizeof(uint64_t) * nbar + sizeof(int) * (2 * kMaxList + 8) + SEM_AX_SMEM_PAD;
   // CTAs per SM the shared memory allows; the register budget is sized to match
+  // (with the gs warp, at most 168 registers per thread: 65536 / (T * 168) CTAs)
   static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
-  static constexpr int MINB = MINB0 < 1 ? 1 : (MINB0 > 8 ? 8 : MINB0);
+  static constexpr int MINBR = GS ? 65536 / (T * 168) : 8;
+  static constexpr int MINB1 = MINB0 < MINBR ? MINB0 : MINBR;
+  static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > 8 ? 8 : MINB1);
 };
 
 __device__ __forceinline__ int face_s1(int axis, int n) { return axis == 0 ? n : 1; }
@@ -121,15 +128,15 @@ __device__ __forceinline__ void sum_point(double* __restrict__ w, const int32_t*
 }
 
 template <int n, int MODE, bool FUSE>
-__global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
+__global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     ax_kernel(const DevPlan P, const AxLaunch a) {
-  using Sh = AxShape<n>;
+  using Sh = AxShape<n, FUSE>;
   constexpr int NE = Sh::NE, n2 = Sh::n2, n3 = Sh::n3, TCW = Sh::TCW;
-  constexpr int NSG = Sh::NSG, NSU = Sh::NSU, PPC = Sh::PPC;
+  constexpr int NSG = Sh::NSG, NSU = Sh::NSU, NSD = Sh::NSD, PPC = Sh::PPC;
   constexpr int dp = Sh::dpad, rp = Sh::rp, wpl = Sh::wpl;
   constexpr bool kBulkU = Sh::kBulkU;
   constexpr bool kMask = MODE != AX_ONLY;   // Dirichlet mask in the epilogue
-  constexpr bool kGs = kMask && FUSE;         // last-arriver gather-scatter in-kernel
+  constexpr bool kGs = kMask && FUSE;         // gather-scatter warp in-kernel
   constexpr bool kDreg = n <= 9;              // D rows in registers (else shared memory)
 #ifndef SEM_DT_REG
 #define SEM_DT_REG 1
@@ -150,11 +157,15 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
   uint64_t* emptyG = fullG + NSG;
   uint64_t* fullU = emptyG + NSG;
   uint64_t* emptyU = fullU + NSU;
-  int* s_list = reinterpret_cast<int*>(emptyU + NSU);
-  int* s_misc = s_list + Sh::kMaxList;                 // [0] list length, [1] last-block flag
+  uint64_t* doneE = emptyU + NSU;                      // compute warps -> gs warp
+  uint64_t* freeE = doneE + NSD;                       // gs warp -> compute warps
+  int* s_list = reinterpret_cast<int*>(freeE + NSD);   // gs warp: last-arrived entities
+  int* s_pref = s_list + Sh::kMaxList;                 // gs warp: point-count prefix
+  int* s_misc = s_pref + Sh::kMaxList;                 // [1] last-block flag
 
   const int tid = threadIdx.x;
-  const bool producer = tid >= TCW;
+  const bool producer = tid >= TCW && tid < TCW + 32;
+  const bool gswarp = kGs && tid >= TCW + 32;
 
   for (int q = tid; q < n2; q += Sh::T) {
     const int r = q / n, c = q % n;
@@ -170,6 +181,10 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     for (int s = 0; s < NSU; s++) {
       mbar_init(&fullU[s], kBulkU ? 1 : 32);
       mbar_init(&emptyU[s], Sh::NWC);
+    }
+    for (int s = 0; s < NSD; s++) {
+      mbar_init(&doneE[s], Sh::NWC);
+      mbar_init(&freeE[s], 1);
     }
     fence_mbar_init();
   }
@@ -226,6 +241,117 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
         if (++sg == NSG) { sg = 0; phg ^= 1u; }
       }
     }
+  } else if (gswarp) {
+    // ============ gather-scatter warp: last arriver sums shared entities ============
+    // For each group the compute warps have stored, arrive (acq_rel ticket) on
+    // every face / edge / vertex of its elements; for the entities this CTA
+    // completes, sum the incidences' slots in ascending slot order (reading
+    // Q10) while they are L2-resident and broadcast the sum (0 on Dirichlet
+    // points).  Runs concurrently with the compute warps' next elements.
+    const int lane = tid & 31;
+    constexpr int nf = (n - 2) * (n - 2), ne = n - 2;
+    constexpr int Nm1 = n > 2 ? n - 2 : 1;
+    constexpr int K = 2;   // work items per lane per round (loads issued together)
+    int sd = 0;
+    uint32_t phd = 0;
+    for (int g = blockIdx.x; g < ng; g += gridDim.x) {
+      int e0, cnt;
+      group(g, e0, cnt);
+      mbar_wait(&doneE[sd], phd);
+      int nl = 0;
+      for (int q0 = 0; q0 < cnt * kRefsPerElem; q0 += 32) {
+        const int q = q0 + lane;
+        bool last = false;
+        int ref = -1;
+        if (q < cnt * kRefsPerElem) {
+          ref = P.eref[(size_t)(e0 + q / kRefsPerElem) * kRefsPerElem + q % kRefsPerElem];
+          if (ref >= 0) {
+            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
+            const unsigned nin = cls == CLS_FACE ? 2u : (cls == CLS_EDGE ? P.e_nin[idx] : P.v_nin[idx]);
+            unsigned* tk = P.cnt + (cls == CLS_FACE ? idx : (cls == CLS_EDGE ? P.nF + idx : P.nF + P.nEd + idx));
+            // acq_rel: releases the compute warps' w stores (observed through the
+            // done barrier), acquires the other incidences' stores on the last arrival
+            if (atom_add_acq_rel_gpu(tk, 1u) == nin - 1u) {
+              *tk = 0u;
+              last = true;
+            }
+          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, last);
+        if (last) s_list[nl + __popc(m & ((1u << lane) - 1u))] = ref;
+        nl += __popc(m);
+      }
+      __syncwarp();
+      if (lane == 0) {   // point-count prefix over the list
+        int acc_p = 0;
+        for (int q = 0; q < nl; q++) {
+          s_pref[q] = acc_p;
+          const int cls = s_list[q] >> kClsShift;
+          acc_p += cls == CLS_FACE ? nf : (cls == CLS_EDGE ? ne : 1);
+        }
+        s_pref[nl] = acc_p;
+      }
+      __syncwarp();
+      const int tot = nl > 0 ? s_pref[nl] : 0;
+      for (int b = 0; b < tot; b += 32 * K) {
+        int addr[K][8], nins[K];
+        bool mk[K];
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          const int t = b + c * 32 + lane;
+          nins[c] = 0;
+          mk[c] = false;
+          if (t < tot) {
+            int lo = 0, hi = nl - 1;   // entity with s_pref[q] <= t < s_pref[q+1]
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (s_pref[mid] <= t) lo = mid; else hi = mid - 1;
+            }
+            const int ref = s_list[lo], p = t - s_pref[lo];
+            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
+            if (cls == CLS_FACE) {
+              const int ax = P.f_axis[idx];
+              const int off = (1 + p % Nm1) * face_s1(ax, n) + (1 + p / Nm1) * face_s2(ax, n);
+              nins[c] = 2;
+              addr[c][0] = P.f_base[2 * idx] + off;
+              addr[c][1] = P.f_base[2 * idx + 1] + off;
+            } else if (cls == CLS_EDGE) {
+              const int off = (1 + p) * edge_stride(P.e_axis[idx], n);
+              nins[c] = P.e_nin[idx];
+              mk[c] = P.e_mask[idx];
+#pragma unroll
+              for (int x = 0; x < 4; x++) addr[c][x] = P.e_base[4 * idx + x] + off;
+            } else {
+              nins[c] = P.v_nin[idx];
+              mk[c] = P.v_mask[idx];
+#pragma unroll
+              for (int x = 0; x < 8; x++) addr[c][x] = P.v_base[8 * idx + x];
+            }
+          }
+        }
+        double v[K][8];
+#pragma unroll
+        for (int c = 0; c < K; c++)
+#pragma unroll
+          for (int x = 0; x < 8; x++)
+            if (x < nins[c]) v[c][x] = __ldcg(&a.w[addr[c][x]]);
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          if (nins[c] == 0) continue;
+          double s = v[c][0];
+#pragma unroll
+          for (int x = 1; x < 8; x++)
+            if (x < nins[c]) s += v[c][x];
+          if (mk[c]) s = 0.0;
+#pragma unroll
+          for (int x = 0; x < 8; x++)
+            if (x < nins[c]) __stcg(&a.w[addr[c][x]], s);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&freeE[sd]);
+      if (++sd == NSD) { sd = 0; phd ^= 1u; }
+    }
   } else {
     // ======================= compute warps =======================
     const int el = tid / n2, ij = tid - (tid / n2) * n2;
@@ -241,8 +367,8 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
       Dti[m] = kDtreg ? a.Dm[m * n + i] : 0.0;
       Dtj[m] = kDtreg ? a.Dm[m * n + j] : 0.0;
     }
-    int su = 0, sg = 0;
-    uint32_t phu = 0, phg = 0;
+    int su = 0, sg = 0, sdc = 0;
+    uint32_t phu = 0, phg = 0, phdc = 0;
     for (int g = blockIdx.x; g < ng; g += gridDim.x) {
       int e0, cnt;
       group(g, e0, cnt);
@@ -318,60 +444,13 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
       }
 
       if (kGs) {
-        // ---- arrive on this group's entities; the last arriver sums them ----
-        if (tid == 0) s_misc[0] = 0;
-        compute_sync<TCW>();   // all w_e stores of the group issued; list reset visible
-        for (int q = tid; q < cnt * kRefsPerElem; q += TCW) {
-          const int e = e0 + q / kRefsPerElem;
-          const int ref = P.eref[(size_t)e * kRefsPerElem + q % kRefsPerElem];
-          if (ref >= 0) {
-            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
-            const unsigned nin = cls == CLS_FACE ? 2u : (cls == CLS_EDGE ? P.e_nin[idx] : P.v_nin[idx]);
-            unsigned* tk = P.cnt + (cls == CLS_FACE ? idx : (cls == CLS_EDGE ? P.nF + idx : P.nF + P.nEd + idx));
-            // acq_rel: releases this CTA's w stores (ordered before by the barrier),
-            // acquires the other incidences' stores when this is the last arrival
-            const unsigned old = atom_add_acq_rel_gpu(tk, 1u);
-            if (old == nin - 1u) {
-              *tk = 0u;
-              s_list[atomicAdd(&s_misc[0], 1)] = ref;
-            }
-          }
+        // hand the stored group to the gs warp (its ring slot must be free)
+        __syncwarp();   // orders this warp's w stores before lane 0's release
+        if (lane == 0) {
+          mbar_wait(&freeE[sdc], phdc ^ 1u);
+          mbar_arrive(&doneE[sdc]);
         }
-        compute_sync<TCW>();
-        const int nl = s_misc[0];
-        if (nl > 0) {
-          constexpr int NW = Sh::NWC;
-          const int wid = tid >> 5;
-          constexpr int nf = (n - 2) * (n - 2), ne = n - 2;
-          constexpr int Nm1 = n > 2 ? n - 2 : 1;
-          for (int q = wid; q < nl; q += NW) {
-            const int ref = s_list[q];
-            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
-            int32_t base[8];
-            if (n > 2 && cls == CLS_FACE) {
-              base[0] = P.f_base[2 * idx];
-              base[1] = P.f_base[2 * idx + 1];
-              const int ax = P.f_axis[idx];
-              const int s1 = face_s1(ax, n), s2 = face_s2(ax, n);
-              for (int p = lane; p < nf; p += 32) {
-                const int off = (1 + p % Nm1) * s1 + (1 + p / Nm1) * s2;
-                sum_point(a.w, base, 2, off, false);
-              }
-            } else if (n > 2 && cls == CLS_EDGE) {
-              const int nin = P.e_nin[idx];
-#pragma unroll
-              for (int t = 0; t < 4; t++) base[t] = P.e_base[4 * idx + t];
-              const int sd = edge_stride(P.e_axis[idx], n);
-              const bool mk = P.e_mask[idx];
-              for (int p = lane; p < ne; p += 32) sum_point(a.w, base, nin, (1 + p) * sd, mk);
-            } else if (cls == CLS_VERT) {
-              const int nin = P.v_nin[idx];
-#pragma unroll
-              for (int t = 0; t < 8; t++) base[t] = P.v_base[8 * idx + t];
-              if (lane == 0) sum_point(a.w, base, nin, 0, P.v_mask[idx]);
-            }
-          }
-        }
+        if (++sdc == NSD) { sdc = 0; phdc ^= 1u; }
       }
       compute_sync<TCW>();   // w_r / w_s scratch free for the next group
     }
@@ -391,24 +470,31 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
   }
 }
 
+// persistent launch: grid = min(work groups, resident CTAs x SMs) of this variant
 template <int n, int MODE, bool FUSE>
-static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
-  using Sh = AxShape<n>;
+static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cudaStream_t s) {
+  using Sh = AxShape<n, FUSE>;
   auto kern = ax_kernel<n, MODE, FUSE>;
-  static bool configured = false;
-  if (!configured) {
+  static int resident = 0;
+  if (resident == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Sh::smem_bytes);
     if (e != cudaSuccess) return e;
-    configured = true;
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Sh::T, Sh::smem_bytes) != cudaSuccess)
+      nb = 1;
+    resident = std::max(nb, 1) * sms;
   }
+  const int grid = std::max(1, std::min(groups, resident));
   kern<<<grid, Sh::T, Sh::smem_bytes, s>>>(P, a);
   return cudaGetLastError();
 }
 
 template <int n, int MODE>
 static int occupancy_n() {
-  using Sh = AxShape<n>;
+  using Sh = AxShape<n, false>;
   auto kern = ax_kernel<n, MODE, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem_bytes);
   int nb = 0;
