@@ -153,6 +153,10 @@ int sem_launch_count(const sem_ctx* c, int64_t* n);
    arriver per face/edge/vertex sums it); 0 (default) -> Ax kernel with the
    mask in its epilogue followed by one gather-scatter kernel. */
 #define SEM_OPT_FUSED_GS 1
+/* Multi-GPU transport of the hot path (nranks > 1): 1 (default) = NVLink peer
+   memory (CUDA-IPC mailboxes, see p2p.cu), 0 = NCCL send/recv + allreduce.
+   Falls back to NCCL automatically if peer memory cannot be mapped. */
+#define SEM_OPT_P2P 2
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

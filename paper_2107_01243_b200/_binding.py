@@ -245,6 +245,10 @@ class Context:
     def set_fused_gs(self, on: bool):
         _check(load().sem_set_option(self._h, 1, 1 if on else 0))
 
+    def set_p2p(self, on: bool):
+        """Multi-GPU transport: NVLink peer memory (default) or NCCL. Collective."""
+        _check(load().sem_set_option(self._h, 2, 1 if on else 0))
+
     def launch_count(self) -> int:
         n = C.c_int64()
         _check(load().sem_launch_count(self._h, C.byref(n)))

@@ -84,6 +84,7 @@ struct sem_ctx {
   unsigned* d_cnt = nullptr;
   int32_t *d_sslot = nullptr, *d_soff = nullptr;
   uint8_t *d_snloc = nullptr, *d_snr = nullptr, *d_smask = nullptr, *d_smult = nullptr;
+  int8_t* d_srank = nullptr;
   double *d_part = nullptr, *d_send = nullptr, *d_recv = nullptr;
   // work
   double *d_r = nullptr, *d_p = nullptr, *d_wv = nullptr, *d_tmp = nullptr;
@@ -106,6 +107,17 @@ struct sem_ctx {
   double t_ms[kTimerClasses] = {0, 0, 0, 0, 0};
   int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0, 0};
   bool fuse_gs = false;   // SEM_OPT_FUSED_GS
+  // NVLink peer-memory transport (nranks > 1)
+  bool p2p_ok = false, use_p2p = true;
+  sem::P2P p2p;
+  char* d_mbox = nullptr;
+  char** d_peers = nullptr;
+  int64_t* d_rdelta = nullptr;
+  int32_t* d_nbrs = nullptr;
+  unsigned* d_ptick = nullptr;
+  int* d_perr = nullptr;
+  std::vector<char*> ipc_opened;
+  uint64_t ep_gs = 0, ep_ar[sem::P2P::kSites] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -224,10 +236,50 @@ int gs_pass(sem_ctx* c, double* w) {
   return check(e, "gs kernel");
 }
 
+bool p2p(const sem_ctx* c) { return c->p2p_ok && c->use_p2p; }
+
+// global sum of K device doubles (this rank's partials at loc) into glob:
+// NVLink mailboxes (publish + rank-ordered sum) or NCCL allreduce
+int allreduce_site(sem_ctx* c, int site, const double* loc, double* glob, int K) {
+  if (c->hp.nranks == 1) return SEM_OK;
+  if (p2p(c)) {
+    const uint64_t e = ++c->ep_ar[site];
+    CUDA_TRY(sem::launch_ar_publish(c->p2p, site, e, loc, K, c->stream));
+    CUDA_TRY(sem::launch_ar_finish(c->p2p, site, e, glob, K, c->stream));
+    c->launches += 2;
+    return SEM_OK;
+  }
+  NCCL_TRY(ncclAllReduce(loc, glob, K, ncclDouble, ncclSum, c->nccl, c->stream));
+  return SEM_OK;
+}
+
 // w = mask(QQ^T A_L u) (mode AX_APPLY) or the same plus sigma (AX_PCG)
 int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   const sem::HostPlan& h = c->hp;
   sem::PcgState* st = c->d_st;
+  if (h.nranks > 1 && h.nS > 0 && p2p(c)) {
+    // Alg. 1 over NVLink: boundary elements, pack straight into the
+    // neighbours' receive buffers, interior elements meanwhile, local gs,
+    // then the rank-ordered unpack.
+    const uint64_t e = ++c->ep_gs;
+    int nparts = 1;
+    if (h.ihi > h.ilo) {
+      SEM_TRY(run_ax(c, u, w, mode, (int)h.b0lo, (int)h.b0hi, (int)h.b1lo, (int)h.b1hi,
+                     &st->sigma_part[0]));
+      CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, w, c->d_part, c->p2p, e, c->stream));
+      SEM_TRY(run_ax(c, u, w, mode, (int)h.ilo, (int)h.ihi, 0, 0, &st->sigma_part[1]));
+      nparts = 2;
+    } else {
+      SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, &st->sigma_part[0]));
+      CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, w, c->d_part, c->p2p, e, c->stream));
+    }
+    SEM_TRY(gs_pass(c, w));
+    CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
+                                       mode == sem::AX_PCG ? st : nullptr, nparts, c->stream));
+    c->launches += 2;
+    if (mode == sem::AX_PCG) SEM_TRY(allreduce_site(c, sem::AR_SIG, &st->loc[2], &st->sigma, 1));
+    return SEM_OK;
+  }
   if (h.nranks == 1 || h.nS == 0) {
     // single rank: the CG update kernel sums the per-CTA sigma partials itself
     SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0,
@@ -264,7 +316,13 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
 int gs_op(sem_ctx* c, double* u, int apply_mask) {
   CUDA_TRY(sem::launch_gs_local(c->dp, u, apply_mask, c->stream));
   c->launches++;
-  if (c->hp.nranks > 1 && c->hp.nS > 0) {
+  if (c->hp.nranks > 1 && c->hp.nS > 0 && p2p(c)) {
+    const uint64_t e = ++c->ep_gs;
+    CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, u, c->d_part, c->p2p, e, c->stream));
+    CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, u, c->d_part, c->p2p, e, apply_mask, nullptr, 1,
+                                       c->stream));
+    c->launches += 2;
+  } else if (c->hp.nranks > 1 && c->hp.nS > 0) {
     CUDA_TRY(sem::launch_gs_pack(c->dp, u, c->d_part, c->d_send, c->stream));
     c->launches++;
     SEM_TRY(exchange(c));
@@ -304,10 +362,14 @@ void free_ctx(sem_ctx* c) {
                   c->d_emask, c->d_vnin, c->d_vmask, c->d_cnt, c->d_sslot, c->d_soff,
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
-                  c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig};
+                  c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
+  for (char* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_ptick, c->d_perr};
+  for (void* p : p2ps)
+    if (p) cudaFree(p);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (c->ev_poll) cudaEventDestroy(c->ev_poll);
@@ -317,6 +379,95 @@ void free_ctx(sem_ctx* c) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Map every rank's mailbox into this process (CUDA IPC over NVLink); handles and
+// receive-buffer offsets are exchanged once with NCCL all-gathers.  Returns
+// SEM_OK with c->p2p_ok = false (NCCL transport) if peer mapping is unavailable.
+int p2p_setup(sem_ctx* c) {
+  const sem::HostPlan& h = c->hp;
+  const int P = h.nranks, me = h.rank;
+  cudaStream_t s = c->stream;
+  if (P > sem::P2P::kMaxP) return SEM_OK;
+  const size_t bytes = sem::P2P::kRecvOff + ((size_t)h.nbuf + 1) * sizeof(double);
+  SEM_TRY(dalloc(&c->d_mbox, bytes));
+  CUDA_TRY(cudaMemsetAsync(c->d_mbox, 0, bytes, s));
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, c->d_mbox) != cudaSuccess) {
+    cudaGetLastError();
+    return SEM_OK;
+  }
+  char* dh = nullptr;
+  SEM_TRY(dalloc(&dh, (size_t)64 * (P + 1)));
+  CUDA_TRY(cudaMemcpyAsync(dh, &mine, 64, cudaMemcpyHostToDevice, s));
+  NCCL_TRY(ncclAllGather(dh, dh + 64, 64, ncclChar, c->nccl, s));
+  std::vector<cudaIpcMemHandle_t> all(P);
+  CUDA_TRY(cudaMemcpyAsync(all.data(), dh + 64, (size_t)64 * P, cudaMemcpyDeviceToHost, s));
+  // receive-buffer offsets: mine[q] = where q's data lands in my buffer
+  std::vector<int64_t> myoff(P, -1);
+  for (size_t k = 0; k < h.nbr_rank.size(); k++) myoff[h.nbr_rank[k]] = h.nbr_off[k];
+  int64_t* doff = nullptr;
+  SEM_TRY(dalloc(&doff, (size_t)P * (P + 1)));
+  CUDA_TRY(cudaMemcpyAsync(doff, myoff.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, s));
+  NCCL_TRY(ncclAllGather(doff, doff + P, P, ncclInt64, c->nccl, s));
+  std::vector<int64_t> alloff((size_t)P * P);
+  CUDA_TRY(cudaMemcpyAsync(alloff.data(), doff + P, sizeof(int64_t) * P * P, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(dh);
+  cudaFree(doff);
+  std::vector<char*> peers(P, nullptr);
+  bool ok = true;
+  for (int q = 0; q < P; q++) {
+    if (q == me) { peers[q] = c->d_mbox; continue; }
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      break;
+    }
+    peers[q] = static_cast<char*>(ptr);
+    c->ipc_opened.push_back(peers[q]);
+  }
+  // every rank must agree (otherwise all fall back to NCCL)
+  {
+    double flag = ok ? 0.0 : 1.0;
+    double* df = nullptr;
+    SEM_TRY(dalloc(&df, 1));
+    CUDA_TRY(cudaMemcpyAsync(df, &flag, sizeof(double), cudaMemcpyHostToDevice, s));
+    NCCL_TRY(ncclAllReduce(df, df, 1, ncclDouble, ncclSum, c->nccl, s));
+    CUDA_TRY(cudaMemcpyAsync(&flag, df, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(df);
+    if (flag > 0.0) return SEM_OK;
+  }
+  std::vector<int64_t> rdelta(P, 0);
+  for (int q = 0; q < P; q++)
+    if (myoff[q] >= 0) rdelta[q] = alloff[(size_t)q * P + me] - myoff[q];
+  SEM_TRY(upload(reinterpret_cast<char***>(&c->d_peers), peers, s));
+  SEM_TRY(upload(&c->d_rdelta, rdelta, s));
+  SEM_TRY(upload(&c->d_nbrs, h.nbr_rank, s));
+  SEM_TRY(dalloc(&c->d_ptick, 2));
+  CUDA_TRY(cudaMemsetAsync(c->d_ptick, 0, 2 * sizeof(unsigned), s));
+  SEM_TRY(dalloc(&c->d_perr, 1));
+  CUDA_TRY(cudaMemsetAsync(c->d_perr, 0, sizeof(int), s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  sem::P2P& p = c->p2p;
+  p.P = P; p.me = me; p.nnbr = (int)h.nbr_rank.size();
+  p.local = c->d_mbox; p.peers = c->d_peers; p.rdelta = c->d_rdelta; p.nbrs = c->d_nbrs;
+  p.tick = c->d_ptick; p.err = c->d_perr;
+  c->p2p_ok = true;
+  return SEM_OK;
+}
+
+int p2p_check(sem_ctx* c) {
+  if (!c->p2p_ok) return SEM_OK;
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&err, c->d_perr, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    sem::set_error("peer-memory wait timed out (a rank did not reach the collective)");
+    return SEM_ENCCL;
+  }
+  return SEM_OK;
+}
 
 }  // namespace
 
@@ -374,6 +525,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(upload(&c->d_snr, h.s_nr, s));
   SETUP_TRY(upload(&c->d_smask, h.s_mask, s));
   SETUP_TRY(upload(&c->d_smult, h.s_mult, s));
+  SETUP_TRY(upload(&c->d_srank, h.s_rank, s));
   const size_t nent = (size_t)(h.nF + h.nEd + h.nV);
   SETUP_TRY(dalloc(&c->d_cnt, nent));
   SETUP_CUDA(cudaMemsetAsync(c->d_cnt, 0, std::max<size_t>(nent, 1) * sizeof(unsigned), s));
@@ -413,6 +565,9 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(dalloc(&c->d_tickets, 8));
   SETUP_CUDA(cudaMemsetAsync(c->d_tickets, 0, 8 * sizeof(unsigned), s));
   SETUP_TRY(dalloc(&c->d_scal, 8));
+
+  if (h.nranks > 1) SETUP_TRY(p2p_setup(c));
+  c->dp.s_rank = c->d_srank;
 
   // geometry on the device
   int* d_bad = nullptr;
@@ -531,7 +686,7 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   double* rg_out = dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, c->d_dinv, b, x, c->d_r, c->d_p, c->d_partial,
                                st, rg_out, c->red_grid, s));
-  SEM_TRY(allreduce_to(c, &st->loc[0], &st->rho_new, 2));
+  SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
   CUDA_TRY(sem::launch_cg_start(st, c->d_hist, s));
   c->launches += 2;
   int done = 0;
@@ -544,7 +699,7 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
                                      c->d_partial, st, rg_out, dist ? nullptr : c->d_partial_ax,
                                      c->d_nsig, c->red_grid, s));
       timer_end(c, tk);
-      SEM_TRY(allreduce_to(c, &st->loc[0], &st->rho_new, 2));
+      SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
       tk = timer_begin(c, 2);
       CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, st, c->d_hist, c->red_grid, s));
       timer_end(c, tk);
@@ -560,10 +715,11 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   CUDA_TRY(sem::launch_cg_residual(c->dp, c->d_mult, b, c->d_wv, c->d_partial, st,
                                    dist ? &st->loc[3] : &st->res_true, c->red_grid, s));
   c->launches++;
-  SEM_TRY(allreduce_to(c, &st->loc[3], &st->res_true, 1));
+  SEM_TRY(allreduce_site(c, sem::AR_RES, &st->loc[3], &st->res_true, 1));
   CUDA_TRY(cudaMemcpyAsync(c->h_st, st, sizeof(sem::PcgState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   timer_collect(c);
+  SEM_TRY(p2p_check(c));
   const sem::PcgState& hs = *c->h_st;
   c->last_hist = hs.iters;
   if (res) {
@@ -705,6 +861,11 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (option == SEM_OPT_FUSED_GS) {
     cudaStreamSynchronize(c->stream);
     c->fuse_gs = value != 0;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_P2P) {   // collective: every rank must set the same value
+    cudaStreamSynchronize(c->stream);
+    c->use_p2p = value != 0;
     return SEM_OK;
   }
   sem::set_error("sem_set_option: unknown option");

@@ -33,6 +33,7 @@ struct DevPlan {
   const uint8_t* s_nr = nullptr;
   const uint8_t* s_mask = nullptr;
   const uint8_t* s_mult = nullptr;
+  const int8_t* s_rank = nullptr;   // [8][nS] involved ranks (ascending)
 };
 
 // PCG scalars, resident on the device (no per-iteration host sync)
@@ -65,6 +66,35 @@ struct AxLaunch {
   double Dm[144];                 // D (row-major n x n), read from the constant bank
   int* red_count;                 // PCG partials only: number of partials (written by block 0)
 };
+
+// NVLink peer-memory collectives (p2p.cu): mailbox layout and device view
+struct P2P {
+  static constexpr int kMaxP = 64;
+  static constexpr int kSites = 4;   // allreduce call sites
+  static constexpr size_t kSlotOff = 0;
+  static constexpr size_t kArFlagOff = kSlotOff + (size_t)kSites * 2 * kMaxP * 4 * 8;
+  static constexpr size_t kGsFlagOff = kArFlagOff + (size_t)kSites * kMaxP * 8;
+  static constexpr size_t kGsAckOff = kGsFlagOff + (size_t)kMaxP * 8;
+  static constexpr size_t kRecvOff = kGsAckOff + (size_t)kMaxP * 8;
+  int P = 1, me = 0, nnbr = 0;
+  char* local = nullptr;            // this rank's mailbox
+  char* const* peers = nullptr;     // [P] mailbox of every rank (peers[me] == local)
+  const int64_t* rdelta = nullptr;  // [P] neighbour recv offset - own send offset
+  const int32_t* nbrs = nullptr;    // [nnbr] neighbour ranks
+  unsigned* tick = nullptr;         // [2] last-block tickets
+  int* err = nullptr;               // raised on a wait timeout
+};
+enum ArSite { AR_SIG = 0, AR_RG = 1, AR_RES = 2, AR_MISC = 3 };
+
+cudaError_t launch_gs_pack_p2p(const DevPlan& P, const double* u, double* part, const P2P& c,
+                               uint64_t epoch, cudaStream_t s);
+cudaError_t launch_gs_unpack_p2p(const DevPlan& P, double* u, const double* part, const P2P& c,
+                                 uint64_t epoch, int apply_mask, PcgState* st, int nparts,
+                                 cudaStream_t s);
+cudaError_t launch_ar_publish(const P2P& c, int site, uint64_t epoch, const double* v, int K,
+                              cudaStream_t s);
+cudaError_t launch_ar_finish(const P2P& c, int site, uint64_t epoch, double* out, int K,
+                             cudaStream_t s);
 
 // returns max resident CTAs/SM for the Ax kernel of this N and mode
 int ax_occupancy(int N, int mode);

@@ -433,6 +433,7 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
   p.s_mult.resize(p.nS);
   p.s_mask.resize(p.nS);
   p.s_nr.resize(p.nS);
+  p.s_rank.assign(8 * p.nS, -1);
   std::vector<int64_t> pos(m.nranks, 0);
   for (int64_t i = 0; i < p.nS; i++) {
     const SP& s = sps[i];
@@ -444,6 +445,7 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
     for (int t = 0; t < 8; t++) p.s_slot[t * p.nS + i] = s.slot[t];
     for (int q = 0; q < s.nr; q++) {
       int r = s.ranks[q];
+      p.s_rank[q * p.nS + i] = (int8_t)r;
       p.s_off[q * p.nS + i] = (r == m.rank) ? -1 : (int32_t)(off[r] + pos[r]++);
     }
   }

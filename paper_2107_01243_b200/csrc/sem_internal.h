@@ -46,6 +46,7 @@ struct HostPlan {
   std::vector<int32_t> s_slot;            // [8][nS] local slots ascending (-1 pad)
   std::vector<uint8_t> s_nloc, s_mult, s_mask, s_nr;
   std::vector<int32_t> s_off;             // [8][nS] per involved rank (ascending): -1 self, else buffer index
+  std::vector<int8_t> s_rank;             // [8][nS] the involved ranks (ascending), -1 pad
   std::vector<int32_t> nbr_rank;
   std::vector<int64_t> nbr_off, nbr_cnt;
   int64_t nbuf = 0;
