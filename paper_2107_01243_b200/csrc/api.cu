@@ -118,6 +118,7 @@ struct sem_ctx {
   int* d_perr = nullptr;
   std::vector<char*> ipc_opened;
   uint64_t ep_gs = 0, ep_ar[sem::P2P::kSites] = {0, 0, 0, 0};
+  uint64_t cur_e_sig = 0;   // sigma epoch published by the last PCG apply
 };
 
 namespace {
@@ -274,10 +275,12 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
       CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, w, c->d_part, c->p2p, e, c->stream));
     }
     SEM_TRY(gs_pass(c, w));
+    // PCG: the unpack also publishes this rank's sigma; the CG update sums it
+    c->cur_e_sig = mode == sem::AX_PCG ? ++c->ep_ar[sem::AR_SIG] : 0;
     CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
-                                       mode == sem::AX_PCG ? st : nullptr, nparts, c->stream));
+                                       mode == sem::AX_PCG ? st : nullptr, nparts, c->cur_e_sig,
+                                       c->stream));
     c->launches += 2;
-    if (mode == sem::AX_PCG) SEM_TRY(allreduce_site(c, sem::AR_SIG, &st->loc[2], &st->sigma, 1));
     return SEM_OK;
   }
   if (h.nranks == 1 || h.nS == 0) {
@@ -319,7 +322,7 @@ int gs_op(sem_ctx* c, double* u, int apply_mask) {
   if (c->hp.nranks > 1 && c->hp.nS > 0 && p2p(c)) {
     const uint64_t e = ++c->ep_gs;
     CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, u, c->d_part, c->p2p, e, c->stream));
-    CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, u, c->d_part, c->p2p, e, apply_mask, nullptr, 1,
+    CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, u, c->d_part, c->p2p, e, apply_mask, nullptr, 1, 0,
                                        c->stream));
     c->launches += 2;
   } else if (c->hp.nranks > 1 && c->hp.nS > 0) {
@@ -684,24 +687,36 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
   const bool dist = c->hp.nranks > 1;
   double* rg_out = dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
+  // peer-memory allreduces fused into the CG kernels (nranks > 1 with NVLink mailboxes)
+  const bool pp = p2p(c);
+  sem::PeerSync ps;
+  if (pp) ps.c = c->p2p;
+  ps.e_pub = ps.e_wait = pp ? ++c->ep_ar[sem::AR_RG] : 0;
   CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, c->d_dinv, b, x, c->d_r, c->d_p, c->d_partial,
-                               st, rg_out, c->red_grid, s));
-  SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
-  CUDA_TRY(sem::launch_cg_start(st, c->d_hist, s));
+                               st, rg_out, ps, c->red_grid, s));
+  if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
+  CUDA_TRY(sem::launch_cg_start(st, c->d_hist, ps, s));
   c->launches += 2;
   int done = 0;
   for (int k = 0; k < maxit && !done; k += kBatch) {
     const int nb = std::min(kBatch, maxit - k);
     for (int q = 0; q < nb; q++) {
       SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
+      sem::PeerSync psu, psp;
+      if (pp) {
+        psu.c = psp.c = c->p2p;
+        psu.e_wait = c->cur_e_sig;
+        psu.e_pub = psp.e_wait = ++c->ep_ar[sem::AR_RG];
+      }
       int tk = timer_begin(c, 1);
       CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, x, c->d_r, c->d_p, c->d_wv,
                                      c->d_partial, st, rg_out, dist ? nullptr : c->d_partial_ax,
-                                     c->d_nsig, c->red_grid, s));
+                                     c->d_nsig, psu, c->red_grid, s));
       timer_end(c, tk);
-      SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
+      if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
       tk = timer_begin(c, 2);
-      CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, st, c->d_hist, c->red_grid, s));
+      CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, st, c->d_hist, psp, c->red_grid,
+                                s));
       timer_end(c, tk);
       c->launches += 2;
     }
@@ -712,10 +727,20 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   }
   // true residual once at the end (reading Q17)
   SEM_TRY(apply_op(c, x, c->d_wv, sem::AX_APPLY));
+  sem::PeerSync psr;
+  if (pp) {
+    psr.c = c->p2p;
+    psr.e_pub = ++c->ep_ar[sem::AR_RES];
+  }
   CUDA_TRY(sem::launch_cg_residual(c->dp, c->d_mult, b, c->d_wv, c->d_partial, st,
-                                   dist ? &st->loc[3] : &st->res_true, c->red_grid, s));
+                                   dist ? &st->loc[3] : &st->res_true, psr, c->red_grid, s));
   c->launches++;
-  SEM_TRY(allreduce_site(c, sem::AR_RES, &st->loc[3], &st->res_true, 1));
+  if (pp) {
+    CUDA_TRY(sem::launch_ar_finish(c->p2p, sem::AR_RES, psr.e_pub, &st->res_true, 1, s));
+    c->launches++;
+  } else {
+    SEM_TRY(allreduce_site(c, sem::AR_RES, &st->loc[3], &st->res_true, 1));
+  }
   CUDA_TRY(cudaMemcpyAsync(c->h_st, st, sizeof(sem::PcgState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   timer_collect(c);

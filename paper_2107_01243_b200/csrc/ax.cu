@@ -359,14 +359,9 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     const int lane = tid & 31;
     // D rows/columns this thread contracts with, in registers (the uniform
     // D[k][m] operands come straight from the kernel-parameter constant bank)
+    // (loaded from shared memory per group, right before the phase that uses
+    // them, so rows and columns are never live at the same time)
     double Di[n], Dj[n], Dti[n], Dtj[n];
-#pragma unroll
-    for (int m = 0; m < n; m++) {
-      Di[m] = kDreg ? a.Dm[i * n + m] : 0.0;
-      Dj[m] = kDreg ? a.Dm[j * n + m] : 0.0;
-      Dti[m] = kDtreg ? a.Dm[m * n + i] : 0.0;
-      Dtj[m] = kDtreg ? a.Dm[m * n + j] : 0.0;
-    }
     int su = 0, sg = 0, sdc = 0;
     uint32_t phu = 0, phg = 0, phdc = 0;
     for (int g = blockIdx.x; g < ng; g += gridDim.x) {
@@ -377,6 +372,11 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       double* wr_s = sWr + el * Sh::wel;
       double* ws_s = sWs + el * Sh::wel;
       mbar_wait(&fullU[su], phu);
+#pragma unroll
+      for (int m = 0; m < n; m++) {
+        Di[m] = kDreg ? sD[i * dp + m] : 0.0;
+        Dj[m] = kDreg ? sD[j * dp + m] : 0.0;
+      }
 
       double ru[n], rw[n];
 #pragma unroll
@@ -384,7 +384,12 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
         ru[k] = active ? sUe[ij + n2 * k] : 0.0;
         rw[k] = 0.0;
       }
-#pragma unroll
+#ifndef SEM_KU
+#define SEM_KU 2
+#endif
+      // plane loop: partial unrolling keeps the live range (and registers) bounded
+      constexpr int kKU = SEM_KU;
+#pragma unroll(kKU)
       for (int k = 0; k < n; k++) {
         if (k % PPC == 0) mbar_wait(&fullG[sg], phg);
         const double* gp = sG + sg * Sh::gslot + (el * PPC + k % PPC) * 6 * n2 + ij;
@@ -418,6 +423,11 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       if (lane == 0) mbar_arrive(&emptyU[su]);   // u slot consumed
       if (++su == NSU) { su = 0; phu ^= 1u; }
       compute_sync<TCW>();                       // w_r / w_s of the group complete
+#pragma unroll
+      for (int m = 0; m < n; m++) {
+        Dti[m] = kDtreg ? sDt[i * dp + m] : 0.0;
+        Dtj[m] = kDtreg ? sDt[j * dp + m] : 0.0;
+      }
       if (active) {
         const int e = e0 + el;
         double* wg = a.w + (size_t)e * n3;

@@ -6,6 +6,7 @@
 
 #include "dev_common.cuh"
 #include "kernels.h"
+#include "p2p_dev.cuh"
 #include "sem_internal.h"
 
 namespace sem {
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint
                                const double* __restrict__ dinv, const double* __restrict__ b,
                                double* __restrict__ x, double* __restrict__ r,
                                double* __restrict__ p, double* partial, PcgState* st,
-                               double* out2) {
+                               double* out2, const PeerSync ps) {
   __shared__ double scratch[32];
   __shared__ int flag;
   double rz = 0.0, rr = 0.0;
@@ -385,10 +386,18 @@ __global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint
     rr = fma(c * bl, bl, rr);
   }
   double v[2] = {rz, rr};
-  grid_reduce<2>(v, partial, &st->tickets[1], out2, scratch, &flag);
+  if (grid_reduce<2>(v, partial, &st->tickets[1], out2, scratch, &flag) && ps.c.P > 1 &&
+      threadIdx.x == 0)
+    ar_publish(ps.c, AR_RG, ps.e_pub, out2, 2);
 }
 
-__global__ void cg_start_kernel(PcgState* st, double* hist) {
+__global__ void cg_start_kernel(PcgState* st, double* hist, const PeerSync ps) {
+  if (ps.c.P > 1) {
+    double g2[2];
+    ar_wait_sum(ps.c, AR_RG, ps.e_wait, 2, g2);
+    st->rho_new = g2[0];
+    st->gamma = g2[1];
+  }
   st->rho_old = st->rho_new;
   st->it = 0;
   const double g = sqrt(st->gamma);
@@ -404,13 +413,18 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
                                  double* __restrict__ r, const double* __restrict__ p,
                                  const double* __restrict__ w, double* partial, PcgState* st,
                                  double* out2, const double* __restrict__ sig_part,
-                                 const int* sig_count) {
+                                 const int* sig_count, const PeerSync ps) {
   __shared__ double scratch[32];
   __shared__ int flag;
   __shared__ double s_sig;
   if (st->done) return;
   double sigma;
-  if (sig_part) {
+  if (ps.c.P > 1) {   // global sigma from the peers' mailboxes (rank-ordered sum)
+    if (threadIdx.x == 0) ar_wait_sum(ps.c, AR_SIG, ps.e_wait, 1, &s_sig);
+    __syncthreads();
+    sigma = s_sig;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->sigma = sigma;
+  } else if (sig_part) {
     // sigma = sum of the Ax kernel's per-CTA partials, in a fixed order
     if (threadIdx.x < 32) {
       const int G = *sig_count;
@@ -472,20 +486,30 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
       st->done = 2;
       st->iters = st->it + 1;
     }
+    if (threadIdx.x == 0 && ps.c.P > 1) ar_publish(ps.c, AR_RG, ps.e_pub, out2, 2);
   }
 }
 
 // convergence test on sqrt(gamma); p = dinv .* r + beta p with beta = rho'/rho
 __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double* __restrict__ dinv,
                             const double* __restrict__ r, double* __restrict__ p, PcgState* st,
-                            double* hist) {
+                            double* hist, const PeerSync ps) {
   __shared__ int flag;
+  __shared__ double s_rg[2];
   if (st->done) return;
-  const double g = sqrt(st->gamma);
+  if (ps.c.P > 1) {   // global (rho', gamma) from the peers' mailboxes
+    if (threadIdx.x == 0) ar_wait_sum(ps.c, AR_RG, ps.e_wait, 2, s_rg);
+  } else if (threadIdx.x == 0) {
+    s_rg[0] = st->rho_new;
+    s_rg[1] = st->gamma;
+  }
+  __syncthreads();
+  const double rho_new = s_rg[0], gamma = s_rg[1];
+  const double g = sqrt(gamma);
   const bool conv = g <= st->tol;
-  const bool bad = !(g == g) || !(st->rho_new == st->rho_new);
+  const bool bad = !(g == g) || !(rho_new == rho_new);
   if (!conv && !bad) {
-    const double beta = st->rho_new / st->rho_old;
+    const double beta = rho_new / st->rho_old;
     const int64_t n2 = n >> 1;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     const double2* d2 = reinterpret_cast<const double2*>(dinv);
@@ -514,6 +538,8 @@ __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double*
   __syncthreads();
   if (flag && threadIdx.x == 0) {
     st->tickets[3] = 0u;
+    st->rho_new = rho_new;
+    st->gamma = gamma;
     const int it = st->it + 1;
     st->it = it;
     hist[it] = g;
@@ -524,7 +550,7 @@ __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double*
       st->done = 1;
       st->iters = it;
     } else {
-      st->rho_old = st->rho_new;
+      st->rho_old = rho_new;
       if (it >= st->maxit) {
         st->done = 4;
         st->iters = it;
@@ -536,7 +562,8 @@ __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double*
 // true residual: sqrt(sum c (b - A x)^2) -> st->res_true (after allreduce by the host)
 __global__ void cg_residual_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                    const double* __restrict__ b, const double* __restrict__ w,
-                                   double* partial, PcgState* st, double* out1) {
+                                   double* partial, PcgState* st, double* out1,
+                                   const PeerSync ps) {
   __shared__ double scratch[32];
   __shared__ int flag;
   double s = 0.0;
@@ -546,7 +573,9 @@ __global__ void cg_residual_kernel(int64_t n, const uint8_t* __restrict__ mult,
     s = fma(c_of(mult[l]) * d, d, s);
   }
   double v[1] = {s};
-  grid_reduce<1>(v, partial, &st->tickets[4], out1, scratch, &flag);
+  if (grid_reduce<1>(v, partial, &st->tickets[4], out1, scratch, &flag) && ps.c.P > 1 &&
+      threadIdx.x == 0)
+    ar_publish(ps.c, AR_RES, ps.e_pub, out1, 1);
 }
 
 inline int grid_for(int64_t work, int cap = 148 * 8) {
@@ -671,35 +700,36 @@ cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a,
 
 cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv, const double* b,
                            double* x, double* r, double* p, double* partial, PcgState* st,
-                           double* out2, int grid, cudaStream_t s) {
-  dev::cg_init_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, b, x, r, p, partial, st, out2);
+                           double* out2, const PeerSync& ps, int grid, cudaStream_t s) {
+  dev::cg_init_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, b, x, r, p, partial, st, out2,
+                                                ps);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s) {
-  dev::cg_start_kernel<<<1, 1, 0, s>>>(st, hist);
+cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cudaStream_t s) {
+  dev::cg_start_kernel<<<1, 1, 0, s>>>(st, hist, ps);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
                              double* r, const double* p, const double* w, double* partial,
                              PcgState* st, double* out2, const double* sig_part,
-                             const int* sig_count, int grid, cudaStream_t s) {
+                             const int* sig_count, const PeerSync& ps, int grid, cudaStream_t s) {
   dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, x, r, p, w, partial, st,
-                                                  out2, sig_part, sig_count);
+                                                  out2, sig_part, sig_count, ps);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
-                        PcgState* st, double* hist, int grid, cudaStream_t s) {
-  dev::cg_p_kernel<<<grid, kThreads, 0, s>>>(P.n_local, dinv, r, p, st, hist);
+                        PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s) {
+  dev::cg_p_kernel<<<grid, kThreads, 0, s>>>(P.n_local, dinv, r, p, st, hist, ps);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
                                const double* w, double* partial, PcgState* st, double* out1,
-                               int grid, cudaStream_t s) {
-  dev::cg_residual_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, b, w, partial, st, out1);
+                               const PeerSync& ps, int grid, cudaStream_t s) {
+  dev::cg_residual_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, b, w, partial, st, out1, ps);
   return cudaGetLastError();
 }
 

@@ -85,12 +85,19 @@ struct P2P {
   int* err = nullptr;               // raised on a wait timeout
 };
 enum ArSite { AR_SIG = 0, AR_RG = 1, AR_RES = 2, AR_MISC = 3 };
+// peer-memory allreduce fused into a CG kernel (c.P <= 1: unused): the kernel
+// waits for the global sums of epoch e_wait and/or publishes its partials as e_pub
+struct PeerSync {
+  P2P c;
+  uint64_t e_wait = 0, e_pub = 0;
+};
 
 cudaError_t launch_gs_pack_p2p(const DevPlan& P, const double* u, double* part, const P2P& c,
                                uint64_t epoch, cudaStream_t s);
+// st != nullptr (PCG): also combines the sigma parts and publishes them (epoch e_sig)
 cudaError_t launch_gs_unpack_p2p(const DevPlan& P, double* u, const double* part, const P2P& c,
                                  uint64_t epoch, int apply_mask, PcgState* st, int nparts,
-                                 cudaStream_t s);
+                                 uint64_t e_sig, cudaStream_t s);
 cudaError_t launch_ar_publish(const P2P& c, int site, uint64_t epoch, const double* v, int K,
                               cudaStream_t s);
 cudaError_t launch_ar_finish(const P2P& c, int site, uint64_t epoch, double* out, int K,
@@ -133,18 +140,19 @@ cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a,
 cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStream_t s);
 cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv,
                            const double* b, double* x, double* r, double* p, double* partial,
-                           PcgState* st, double* out2, int grid, cudaStream_t s);
-cudaError_t launch_cg_start(PcgState* st, double* hist, cudaStream_t s);
+                           PcgState* st, double* out2, const PeerSync& ps, int grid,
+                           cudaStream_t s);
+cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cudaStream_t s);
 // sig_part/sig_count: the Ax kernel's per-CTA sigma partials (P = 1; every block
 // re-sums them in a fixed order) or nullptr (P > 1: sigma is already allreduced)
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
                              double* r, const double* p, const double* w, double* partial,
                              PcgState* st, double* out2, const double* sig_part,
-                             const int* sig_count, int grid, cudaStream_t s);
+                             const int* sig_count, const PeerSync& ps, int grid, cudaStream_t s);
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
-                        PcgState* st, double* hist, int grid, cudaStream_t s);
+                        PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s);
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
                                const double* w, double* partial, PcgState* st, double* out1,
-                               int grid, cudaStream_t s);
+                               const PeerSync& ps, int grid, cudaStream_t s);
 
 }  // namespace sem
