@@ -142,12 +142,16 @@ int sem_nccl_comm_destroy(void* comm);
 /* ---- instrumentation ----
    sem_timing(c, 1) records CUDA events on the context stream around every
    launch of kernel class `which` (0 = Ax kernel of apply/PCG, 1 = CG
-   update, 2 = p update, 3 = Ax only, 4 = gather-scatter kernel of apply/PCG); sem_timing_read returns the summed
+   update, 2 = p update, 3 = Ax only, 4 = gather-scatter kernel of apply/PCG,
+   5 = peer-memory pack, 6 = peer-memory unpack); sem_timing_read returns the summed
    device time in ms and the number of timed launches since the last reset.
    sem_launch_count returns the number of kernels this context has launched. */
 int sem_timing(sem_ctx* c, int enable);
 int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t* count);
 int sem_launch_count(const sem_ctx* c, int64_t* n);
+/* instrumentation: which = 0 -> phase timestamps (ns, %globaltimer) of the
+   last peer-memory exchange kernels, up to 16 entries */
+int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n);
 /* Operator variants (both compute the same w; results are bit-identical):
    SEM_OPT_FUSED_GS = 1 -> gather-scatter fused into the Ax kernel (last
    arriver per face/edge/vertex sums it); 0 (default) -> Ax kernel with the
@@ -157,6 +161,9 @@ int sem_launch_count(const sem_ctx* c, int64_t* n);
    memory (CUDA-IPC mailboxes, see p2p.cu), 0 = NCCL send/recv + allreduce.
    Falls back to NCCL automatically if peer memory cannot be mapped. */
 #define SEM_OPT_P2P 2
+/* nranks > 1: 1 = Alg. 1 overlap (Ax on the boundary elements, send,
+   Ax on the interior elements while the partials travel); 0 = one Ax launch. */
+#define SEM_OPT_OVERLAP 3
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

@@ -70,6 +70,7 @@ _SIGS = {
     "sem_timing_read": [_P, C.c_int, C.POINTER(C.c_double), _I64P],
     "sem_launch_count": [_P, _I64P],
     "sem_set_option": [_P, C.c_int, C.c_int],
+    "sem_debug_read": [_P, C.c_int, _P, C.c_int],
 }
 
 
@@ -245,9 +246,18 @@ class Context:
     def set_fused_gs(self, on: bool):
         _check(load().sem_set_option(self._h, 1, 1 if on else 0))
 
+    def set_overlap(self, on: bool):
+        """Alg. 1 boundary/interior split of the operator at nranks > 1. Collective."""
+        _check(load().sem_set_option(self._h, 3, 1 if on else 0))
+
     def set_p2p(self, on: bool):
         """Multi-GPU transport: NVLink peer memory (default) or NCCL. Collective."""
         _check(load().sem_set_option(self._h, 2, 1 if on else 0))
+
+    def debug_read(self, which=0, n=16):
+        out = np.zeros(n, dtype=np.int64)
+        _check(load().sem_debug_read(self._h, which, C.c_void_p(out.ctypes.data), n))
+        return out
 
     def launch_count(self) -> int:
         n = C.c_int64()

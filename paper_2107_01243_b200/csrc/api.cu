@@ -58,7 +58,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 namespace {
 
 constexpr int kBatch = 8;            // iterations enqueued between host polls
-constexpr int kTimerClasses = 5;
+constexpr int kTimerClasses = 7;
 
 struct Timer {
   std::vector<cudaEvent_t> pool;     // pairs
@@ -104,8 +104,10 @@ struct sem_ctx {
   int64_t launches = 0;
   bool timing = false;
   Timer timer;
-  double t_ms[kTimerClasses] = {0, 0, 0, 0, 0};
-  int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0, 0};
+  double t_ms[kTimerClasses] = {0, 0, 0, 0, 0, 0, 0};
+  int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0, 0, 0, 0};
+  bool overlap = false;  // SEM_OPT_OVERLAP: Alg. 1 boundary/interior split (measured slower
+                         // on NVLink: the exchange is ~200 KB, the split costs a launch)
   bool fuse_gs = false;   // SEM_OPT_FUSED_GS
   // NVLink peer-memory transport (nranks > 1)
   bool p2p_ok = false, use_p2p = true;
@@ -258,28 +260,50 @@ int allreduce_site(sem_ctx* c, int site, const double* loc, double* glob, int K)
 int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   const sem::HostPlan& h = c->hp;
   sem::PcgState* st = c->d_st;
+  if (h.nranks > 1 && h.nS > 0 && p2p(c) && !c->fuse_gs && !c->overlap) {
+    // one Ax launch, then ONE exchange kernel: pack into the neighbours'
+    // receive buffers, rank-local gs while the partials travel, unpack
+    const uint64_t e = ++c->ep_gs;
+    // PCG: the Ax kernel leaves per-CTA sigma partials; the exchange kernel sums them
+    SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, nullptr));
+    c->cur_e_sig = mode == sem::AX_PCG ? ++c->ep_ar[sem::AR_SIG] : 0;
+    int tk = timer_begin(c, 4);
+    CUDA_TRY(sem::launch_gs_exchange_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
+                                         mode == sem::AX_PCG ? st : nullptr, 1, c->cur_e_sig,
+                                         c->d_partial_ax, c->d_nsig, c->stream));
+    timer_end(c, tk);
+    c->launches++;
+    return SEM_OK;
+  }
   if (h.nranks > 1 && h.nS > 0 && p2p(c)) {
     // Alg. 1 over NVLink: boundary elements, pack straight into the
     // neighbours' receive buffers, interior elements meanwhile, local gs,
     // then the rank-ordered unpack.
     const uint64_t e = ++c->ep_gs;
     int nparts = 1;
-    if (h.ihi > h.ilo) {
+    int tk;
+    if (c->overlap && h.ihi > h.ilo) {
       SEM_TRY(run_ax(c, u, w, mode, (int)h.b0lo, (int)h.b0hi, (int)h.b1lo, (int)h.b1hi,
                      &st->sigma_part[0]));
+      tk = timer_begin(c, 5);
       CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, w, c->d_part, c->p2p, e, c->stream));
+      timer_end(c, tk);
       SEM_TRY(run_ax(c, u, w, mode, (int)h.ilo, (int)h.ihi, 0, 0, &st->sigma_part[1]));
       nparts = 2;
     } else {
       SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, &st->sigma_part[0]));
+      tk = timer_begin(c, 5);
       CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, w, c->d_part, c->p2p, e, c->stream));
+      timer_end(c, tk);
     }
     SEM_TRY(gs_pass(c, w));
     // PCG: the unpack also publishes this rank's sigma; the CG update sums it
     c->cur_e_sig = mode == sem::AX_PCG ? ++c->ep_ar[sem::AR_SIG] : 0;
+    tk = timer_begin(c, 6);
     CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
                                        mode == sem::AX_PCG ? st : nullptr, nparts, c->cur_e_sig,
                                        c->stream));
+    timer_end(c, tk);
     c->launches += 2;
     return SEM_OK;
   }
@@ -317,15 +341,17 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
 
 // standalone gs (no mask unless asked): local entities + shared exchange
 int gs_op(sem_ctx* c, double* u, int apply_mask) {
+  const bool shared = c->hp.nranks > 1 && c->hp.nS > 0;
+  if (shared && p2p(c)) {   // one kernel: pack, local entities, unpack
+    const uint64_t e = ++c->ep_gs;
+    CUDA_TRY(sem::launch_gs_exchange_p2p(c->dp, u, c->d_part, c->p2p, e, apply_mask, nullptr, 1,
+                                         0, nullptr, nullptr, c->stream));
+    c->launches++;
+    return SEM_OK;
+  }
   CUDA_TRY(sem::launch_gs_local(c->dp, u, apply_mask, c->stream));
   c->launches++;
-  if (c->hp.nranks > 1 && c->hp.nS > 0 && p2p(c)) {
-    const uint64_t e = ++c->ep_gs;
-    CUDA_TRY(sem::launch_gs_pack_p2p(c->dp, u, c->d_part, c->p2p, e, c->stream));
-    CUDA_TRY(sem::launch_gs_unpack_p2p(c->dp, u, c->d_part, c->p2p, e, apply_mask, nullptr, 1, 0,
-                                       c->stream));
-    c->launches += 2;
-  } else if (c->hp.nranks > 1 && c->hp.nS > 0) {
+  if (shared) {
     CUDA_TRY(sem::launch_gs_pack(c->dp, u, c->d_part, c->d_send, c->stream));
     c->launches++;
     SEM_TRY(exchange(c));
@@ -888,12 +914,29 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     c->fuse_gs = value != 0;
     return SEM_OK;
   }
+  if (option == SEM_OPT_OVERLAP) {   // collective
+    cudaStreamSynchronize(c->stream);
+    c->overlap = value != 0;
+    return SEM_OK;
+  }
   if (option == SEM_OPT_P2P) {   // collective: every rank must set the same value
     cudaStreamSynchronize(c->stream);
     c->use_p2p = value != 0;
     return SEM_OK;
   }
   sem::set_error("sem_set_option: unknown option");
+  return SEM_EINVAL;
+}
+
+extern "C" int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n) {
+  if (!c || !out) return SEM_EINVAL;
+  if (which == 0) {   // peer-memory exchange phase timestamps (ns)
+    cudaStreamSynchronize(c->stream);
+    std::vector<unsigned long long> t(16, 0);
+    if (sem::p2p_debug_read(t.data(), 16) != 0) return SEM_ECUDA;
+    for (int q = 0; q < n && q < 16; q++) out[q] = (int64_t)t[q];
+    return SEM_OK;
+  }
   return SEM_EINVAL;
 }
 

@@ -94,6 +94,13 @@ struct PeerSync {
 
 cudaError_t launch_gs_pack_p2p(const DevPlan& P, const double* u, double* part, const P2P& c,
                                uint64_t epoch, cudaStream_t s);
+int p2p_debug_read(unsigned long long* out, int n);
+// pack + rank-local gs + unpack in one co-resident kernel (two-kernel operator, nranks > 1)
+// sig_part/sig_count (PCG): the Ax kernel's per-CTA sigma partials, or nullptr
+cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, const P2P& c,
+                                   uint64_t epoch, int apply_mask, PcgState* st, int nparts,
+                                   uint64_t e_sig, const double* sig_part, const int* sig_count,
+                                   cudaStream_t s);
 // st != nullptr (PCG): also combines the sigma parts and publishes them (epoch e_sig)
 cudaError_t launch_gs_unpack_p2p(const DevPlan& P, double* u, const double* part, const P2P& c,
                                  uint64_t epoch, int apply_mask, PcgState* st, int nparts,

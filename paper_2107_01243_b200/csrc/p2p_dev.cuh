@@ -23,13 +23,13 @@ __device__ __forceinline__ double ld_volatile(const double* p) {
 
 // spin until *flag >= epoch (bounded); returns false on timeout
 __device__ __forceinline__ bool wait_flag(const uint64_t* flag, uint64_t epoch, int* err) {
+  if (ld_acquire_sys(flag) >= epoch) return true;
   const long long t0 = clock64();
   while (ld_acquire_sys(flag) < epoch) {
     if (clock64() - t0 > (1ll << 33)) {   // ~4 s at 2 GHz
       atomicExch(err, 1);
       return false;
     }
-    __nanosleep(64);
   }
   return true;
 }

@@ -51,13 +51,34 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item()) * 1e3
 
-        for p2p in (True, False):
+        for p2p, ov in ((True, True), (True, False), (False, True)):
             c.set_p2p(p2p)
-            tag = "p2p" if p2p else "nccl"
+            c.set_overlap(ov)
+            tag = ("p2p" if p2p else "nccl") + ("_ov" if ov else "_noov")
             res[f"{tag}_apply_us"] = timed(lambda: c.apply(u, w), 50)
-            res[f"{tag}_ax_us"] = timed(lambda: c.ax(u, w), 50)
             res[f"{tag}_gs_us"] = timed(lambda: c.gs(w), 50)
             res[f"{tag}_pcg_iter_us"] = timed(lambda: c.pcg_solve(b, x, 0.0, 40), 3) / 40
+            c.timing(True)
+            c.pcg_solve(b, x, 0.0, 40)
+            for k, nm in ((0, "ax"), (1, "upd"), (2, "p"), (4, "gs"), (5, "pack"), (6, "unpack")):
+                ms, cnt = c.timing_read(k)
+                res[f"{tag}_k_{nm}_us"] = ms * 1e3 / 41
+            c.timing(False)
+        res["ax_only_us"] = timed(lambda: c.ax(u, w), 50)
+        c.set_p2p(True)
+        c.set_overlap(False)
+        c.pcg_solve(b, x, 0.0, 5)
+        ts = c.debug_read(0)
+        b0 = ts[0]
+        res["ts_pack_ack"] = (ts[1] - b0) / 1e3
+        res["ts_pack_stores"] = (ts[2] - b0) / 1e3
+        res["ts_pack_fence_ticket"] = (ts[3] - b0) / 1e3
+        res["ts_pack_lastblock"] = (ts[4] - b0) / 1e3 if ts[4] > b0 else -1
+        res["pack_grid"] = float(ts[5])
+        res["ts_unpack_start"] = (ts[8] - b0) / 1e3
+        res["ts_unpack_flag"] = (ts[9] - b0) / 1e3
+        res["ts_unpack_done"] = (ts[10] - b0) / 1e3
+        res["n_shared"] = float(c.n_local)
     if rank == 0:
         print(json.dumps({"P": P, "cfg": cfg, **{k: round(v, 2) for k, v in res.items()}}))
     sem.nccl_comm_destroy(comm)
