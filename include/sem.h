@@ -149,8 +149,9 @@ int sem_nccl_comm_destroy(void* comm);
 int sem_timing(sem_ctx* c, int enable);
 int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t* count);
 int sem_launch_count(const sem_ctx* c, int64_t* n);
-/* instrumentation: which = 0 -> phase timestamps (ns, %globaltimer) of the
-   last peer-memory exchange kernels, up to 16 entries */
+/* instrumentation: which = 0 -> per-block phase timestamps (ns, %globaltimer)
+   of the last peer-memory exchange kernel, [5][2048] (phases: start, packed,
+   local gs done, unpack done, end; 0 for absent blocks) */
 int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n);
 /* Operator variants (both compute the same w; results are bit-identical):
    SEM_OPT_FUSED_GS = 1 -> gather-scatter fused into the Ax kernel (last

@@ -116,7 +116,6 @@ struct sem_ctx {
   char** d_peers = nullptr;
   int64_t* d_rdelta = nullptr;
   int32_t* d_nbrs = nullptr;
-  unsigned* d_ptick = nullptr;
   int* d_perr = nullptr;
   std::vector<char*> ipc_opened;
   uint64_t ep_gs = 0, ep_ar[sem::P2P::kSites] = {0, 0, 0, 0};
@@ -396,7 +395,7 @@ void free_ctx(sem_ctx* c) {
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
   for (char* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
-  void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_ptick, c->d_perr};
+  void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_perr};
   for (void* p : p2ps)
     if (p) cudaFree(p);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
@@ -417,7 +416,8 @@ int p2p_setup(sem_ctx* c) {
   const int P = h.nranks, me = h.rank;
   cudaStream_t s = c->stream;
   if (P > sem::P2P::kMaxP) return SEM_OK;
-  const size_t bytes = sem::P2P::kRecvOff + ((size_t)h.nbuf + 1) * sizeof(double);
+  // receive entries: 16-byte records, two epoch parities each
+  const size_t bytes = sem::P2P::kRecvOff + ((size_t)h.nbuf + 1) * 2 * 16;
   SEM_TRY(dalloc(&c->d_mbox, bytes));
   CUDA_TRY(cudaMemsetAsync(c->d_mbox, 0, bytes, s));
   cudaIpcMemHandle_t mine;
@@ -474,15 +474,13 @@ int p2p_setup(sem_ctx* c) {
   SEM_TRY(upload(reinterpret_cast<char***>(&c->d_peers), peers, s));
   SEM_TRY(upload(&c->d_rdelta, rdelta, s));
   SEM_TRY(upload(&c->d_nbrs, h.nbr_rank, s));
-  SEM_TRY(dalloc(&c->d_ptick, 2));
-  CUDA_TRY(cudaMemsetAsync(c->d_ptick, 0, 2 * sizeof(unsigned), s));
   SEM_TRY(dalloc(&c->d_perr, 1));
   CUDA_TRY(cudaMemsetAsync(c->d_perr, 0, sizeof(int), s));
   CUDA_TRY(cudaStreamSynchronize(s));
   sem::P2P& p = c->p2p;
   p.P = P; p.me = me; p.nnbr = (int)h.nbr_rank.size();
   p.local = c->d_mbox; p.peers = c->d_peers; p.rdelta = c->d_rdelta; p.nbrs = c->d_nbrs;
-  p.tick = c->d_ptick; p.err = c->d_perr;
+  p.err = c->d_perr;
   c->p2p_ok = true;
   return SEM_OK;
 }
@@ -930,11 +928,11 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
 
 extern "C" int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n) {
   if (!c || !out) return SEM_EINVAL;
-  if (which == 0) {   // peer-memory exchange phase timestamps (ns)
+  if (which == 0) {   // per-block phase timestamps of the fused exchange kernel [5][2048]
     cudaStreamSynchronize(c->stream);
-    std::vector<unsigned long long> t(16, 0);
-    if (sem::p2p_debug_read(t.data(), 16) != 0) return SEM_ECUDA;
-    for (int q = 0; q < n && q < 16; q++) out[q] = (int64_t)t[q];
+    std::vector<unsigned long long> t(5 * 2048, 0);
+    if (sem::p2p_debug_read_blocks(t.data(), 5 * 2048) != 0) return SEM_ECUDA;
+    for (int q = 0; q < n && q < 5 * 2048; q++) out[q] = (int64_t)t[q];
     return SEM_OK;
   }
   return SEM_EINVAL;

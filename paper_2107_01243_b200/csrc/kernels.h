@@ -73,15 +73,14 @@ struct P2P {
   static constexpr int kSites = 4;   // allreduce call sites
   static constexpr size_t kSlotOff = 0;
   static constexpr size_t kArFlagOff = kSlotOff + (size_t)kSites * 2 * kMaxP * 4 * 8;
-  static constexpr size_t kGsFlagOff = kArFlagOff + (size_t)kSites * kMaxP * 8;
-  static constexpr size_t kGsAckOff = kGsFlagOff + (size_t)kMaxP * 8;
-  static constexpr size_t kRecvOff = kGsAckOff + (size_t)kMaxP * 8;
+  // gather-scatter receive entries: 16 B "LL" records {lo32, flag, hi32, flag},
+  // two epoch parities interleaved per entry (see p2p.cu)
+  static constexpr size_t kRecvOff = kArFlagOff + (size_t)kSites * kMaxP * 8;
   int P = 1, me = 0, nnbr = 0;
   char* local = nullptr;            // this rank's mailbox
   char* const* peers = nullptr;     // [P] mailbox of every rank (peers[me] == local)
   const int64_t* rdelta = nullptr;  // [P] neighbour recv offset - own send offset
   const int32_t* nbrs = nullptr;    // [nnbr] neighbour ranks
-  unsigned* tick = nullptr;         // [2] last-block tickets
   int* err = nullptr;               // raised on a wait timeout
 };
 enum ArSite { AR_SIG = 0, AR_RG = 1, AR_RES = 2, AR_MISC = 3 };
@@ -94,7 +93,7 @@ struct PeerSync {
 
 cudaError_t launch_gs_pack_p2p(const DevPlan& P, const double* u, double* part, const P2P& c,
                                uint64_t epoch, cudaStream_t s);
-int p2p_debug_read(unsigned long long* out, int n);
+int p2p_debug_read_blocks(unsigned long long* out, int n);   // [5][2048] exchange phases
 // pack + rank-local gs + unpack in one co-resident kernel (two-kernel operator, nranks > 1)
 // sig_part/sig_count (PCG): the Ax kernel's per-CTA sigma partials, or nullptr
 cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, const P2P& c,

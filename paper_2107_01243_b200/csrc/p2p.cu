@@ -10,13 +10,16 @@
 //     all P flags of their own mailbox and sum the partials in ascending rank
 //     order -- identical operands and order on every rank, so all ranks hold
 //     the bit-identical global value (reading Q10 applied to dot products).
-//   * gather-scatter: the pack kernel writes this rank's partial of every shared
-//     point straight into each neighbour's receive buffer (at the neighbour's
-//     offset for this rank), the last block releases one epoch flag per
-//     neighbour; the unpack kernel acquires its neighbours' flags, adds the rank
-//     partials in ascending rank order, scatters, and its last block
-//     acknowledges (the neighbours' next pack waits for that acknowledgement,
-//     so a receive buffer is never overwritten while being read).
+//   * gather-scatter receive entries, one per (shared point, sending neighbour),
+//     as 16-byte "LL" records {lo32, epoch, hi32, epoch} with the two epoch
+//     parities interleaved.  The packing thread stores its rank's partial
+//     straight into the neighbour's entry; the unpacking thread of the
+//     neighbour spins on that one entry until both halves carry the epoch.  No
+//     fence, flag or ticket sits on the path.  Parity double buffering makes an
+//     acknowledgement unnecessary: a rank writes parity e&1 again only at epoch
+//     e+2, after it received the neighbour's epoch-(e+1) entries, which the
+//     neighbour packed after it had finished reading epoch e (the neighbour
+//     relation is symmetric and kernels of one rank run in stream order).
 // Spin-waits are bounded (~4 s); on timeout an error flag is raised instead
 // of hanging the GPU.  One rank per GPU: every waiting kernel depends only on
 // kernels of other GPUs that never wait on it in the same phase.
@@ -32,120 +35,98 @@
 namespace sem {
 namespace dev {
 
-// phase timestamps (ns, %globaltimer) of the exchange kernels, block 0 thread 0;
-// read with sem_debug_read (instrumentation only)
-__device__ unsigned long long g_p2p_ts[16];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define P2P_TS(slot) \
-  do { if (blockIdx.x == 0 && threadIdx.x == 0) g_p2p_ts[slot] = gtimer(); } while (0)
+// per-block phase timestamps of the exchange kernel (instrumentation, read with
+// sem_debug_read): [phase][block], phases 0 start, 1 packed, 2 local gs done,
+// 3 unpack done, 4 end
+constexpr int kXtsBlocks = 2048;
+__device__ unsigned long long g_xts[5 * kXtsBlocks];
+#define XTS(ph) \
+  do { if (threadIdx.x == 0 && blockIdx.x < kXtsBlocks) g_xts[(ph) * kXtsBlocks + blockIdx.x] = gtimer(); } while (0)
 
 // ---------------------------------------------------------------- gather-scatter exchange
+// this rank's partial of shared point s (ascending local slots), also sent to
+// every other rank sharing s
+__device__ __forceinline__ void pack_point(const DevPlan& P, const double* u, double* part,
+                                           const P2P& c, uint64_t epoch, int s) {
+  const int nl = P.s_nloc[s];
+  double v = u[P.s_slot[s]];
+  for (int x = 1; x < nl; x++) v += u[P.s_slot[(int64_t)x * P.nS + s]];
+  part[s] = v;
+  const int nr = P.s_nr[s];
+  for (int x = 0; x < nr; x++) {
+    const int q = P.s_rank[(int64_t)x * P.nS + s];
+    if (q == c.me) continue;
+    ll_store(mb_ll(c.peers[q], P.s_off[(int64_t)x * P.nS + s] + c.rdelta[q], epoch), v,
+             (uint32_t)epoch);
+  }
+}
+
+// the rank partials of s in ascending rank order, masked, scattered to its slots
+__device__ __forceinline__ void unpack_point(const DevPlan& P, double* u, const double* part,
+                                             const P2P& c, uint64_t epoch, int apply_mask, int s) {
+  const int nr = P.s_nr[s];
+  double tot = 0.0;
+  for (int x = 0; x < nr; x++) {
+    const int o = P.s_off[(int64_t)x * P.nS + s];
+    const double v = o < 0 ? part[s] : ll_load(mb_ll(c.local, o, epoch), (uint32_t)epoch, c.err);
+    tot = x == 0 ? v : tot + v;
+  }
+  if (apply_mask && P.s_mask[s]) tot = 0.0;
+  const int nl = P.s_nloc[s];
+  for (int x = 0; x < nl; x++) u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
+}
+
+// PCG: this rank's sigma (fixed-order sum of its partials) to every rank's
+// mailbox, one warp.  The partials come from kernels earlier in the stream.
+__device__ __forceinline__ void publish_sigma(const P2P& c, PcgState* st, int nparts,
+                                              uint64_t e_sig, const double* sig_part,
+                                              const int* sig_count) {
+  double sg;
+  if (sig_part) {   // the Ax kernel's per-CTA partials
+    const int G = *sig_count;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < G; b += 32) v += sig_part[b];
+    sg = warp_sum(v);
+  } else {
+    sg = st->sigma_part[0];
+    for (int q = 1; q < nparts; q++) sg += st->sigma_part[q];
+  }
+  if (threadIdx.x == 0) {
+    st->loc[2] = sg;
+    ar_publish(c, AR_SIG, e_sig, &sg, 1);
+  }
+}
+
 __global__ void gs_pack_p2p_kernel(const DevPlan P, const double* __restrict__ u, double* part,
                                    const P2P c, uint64_t epoch) {
-  __shared__ int last;
-  P2P_TS(0);
-  if (threadIdx.x < c.nnbr)   // the neighbours finished reading the previous exchange
-    wait_flag(mb_gsack(c.local, c.nbrs[threadIdx.x]), epoch - 1, c.err);
-  __syncthreads();
-  P2P_TS(1);
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.nS;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int nl = P.s_nloc[s];
-    double v = u[P.s_slot[s]];
-    for (int x = 1; x < nl; x++) v += u[P.s_slot[(int64_t)x * P.nS + s]];
-    part[s] = v;
-    const int nr = P.s_nr[s];
-    for (int x = 0; x < nr; x++) {
-      const int q = P.s_rank[(int64_t)x * P.nS + s];
-      if (q == c.me) continue;
-      const int o = P.s_off[(int64_t)x * P.nS + s];
-      mb_recv(c.peers[q])[o + c.rdelta[q]] = v;   // NVLink store into the neighbour
-    }
-  }
-  // one system-scope fence per block, cumulative over the block's NVLink
-  // stores (ordered before it by the barrier), then the last-block ticket
-  __syncthreads();
-  P2P_TS(2);
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    last = (atomicAdd(&c.tick[0], 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  P2P_TS(3);
-  if (last) {
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      c.tick[0] = 0u;
-      g_p2p_ts[4] = gtimer();
-      g_p2p_ts[5] = gridDim.x;
-    }
-    __syncthreads();
-    if (threadIdx.x < c.nnbr) st_release_sys(mb_gsflag(c.peers[c.nbrs[threadIdx.x]], c.me), epoch);
-  }
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < P.nS; s += gridDim.x * blockDim.x)
+    pack_point(P, u, part, c, epoch, s);
 }
 
 __global__ void gs_unpack_p2p_kernel(const DevPlan P, double* __restrict__ u, const double* part,
                                      const P2P c, uint64_t epoch, int apply_mask, PcgState* st,
                                      int nparts, uint64_t e_sig) {
-  __shared__ int last;
-  P2P_TS(8);
-  if (st && blockIdx.x == 0 && threadIdx.x == 0) {
-    double sg = st->sigma_part[0];
-    for (int q = 1; q < nparts; q++) sg += st->sigma_part[q];
-    st->loc[2] = sg;
-  }
-  if (threadIdx.x < c.nnbr) wait_flag(mb_gsflag(c.local, c.nbrs[threadIdx.x]), epoch, c.err);
-  __syncthreads();
-  P2P_TS(9);
-  const double* recv = mb_recv(c.local);
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.nS;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int nr = P.s_nr[s];
-    double tot = 0.0;
-    for (int x = 0; x < nr; x++) {
-      const int o = P.s_off[(int64_t)x * P.nS + s];
-      const double v = o < 0 ? part[s] : ld_volatile(&recv[o]);
-      tot = x == 0 ? v : tot + v;
-    }
-    if (apply_mask && P.s_mask[s]) tot = 0.0;
-    const int nl = P.s_nloc[s];
-    for (int x = 0; x < nl; x++) u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
-  }
-  __syncthreads();
-  P2P_TS(10);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = (atomicAdd(&c.tick[1], 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) {   // acknowledge: the receive buffer may be overwritten
-    if (threadIdx.x < c.nnbr) st_release_sys(mb_gsack(c.peers[c.nbrs[threadIdx.x]], c.me), epoch);
-    if (threadIdx.x == 0) {
-      c.tick[1] = 0u;
-      if (st) {   // PCG: this rank's sigma to every rank's mailbox
-        __threadfence();
-        const double v = *(volatile double*)&st->loc[2];
-        ar_publish(c, AR_SIG, e_sig, &v, 1);
-      }
-    }
-  }
+  if (st && blockIdx.x == gridDim.x - 1 && threadIdx.x < 32)
+    publish_sigma(c, st, nparts, e_sig, nullptr, nullptr);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < P.nS; s += gridDim.x * blockDim.x)
+    unpack_point(P, u, part, c, epoch, apply_mask, s);
 }
 
 // One kernel per operator application for nranks > 1 (Alg. 1 over NVLink):
-//  1. pack: this rank's partial of every shared point into the neighbours'
-//     receive buffers; the last block to finish releases the neighbours' flags
-//     and this rank's own "pack done" flag;
-//  2. rank-local gather-scatter (disjoint slots) while the partials travel;
-//  3. acquire the neighbours' flags and the own pack-done flag (no block may
-//     overwrite a shared slot before every block has packed it), add the rank
-//     partials in ascending rank order, scatter; the last block acknowledges
-//     and, inside PCG, publishes this rank's sigma.
-// Every block is co-resident (grid capped at residency by the launcher), so the
-// in-kernel waits cannot starve the blocks they wait for.
+//  1. pack: the first npb blocks send this rank's partial of every shared point
+//     into the neighbours' receive entries;
+//  2. rank-local gather-scatter (slots disjoint from the shared points') while
+//     the partials travel;
+//  3. the same threads unpack the points they packed (so no block overwrites a
+//     slot another block still has to read), waiting per entry.
+// Inside PCG the last block publishes this rank's sigma first.  Every block is
+// co-resident (grid capped at residency by the launcher), so the waits cannot
+// starve a block that has yet to pack.
 template <int n>
 __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
                                                               double* __restrict__ u, double* part,
@@ -154,92 +135,22 @@ __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
                                                               int nparts, uint64_t e_sig,
                                                               const double* sig_part,
                                                               const int* sig_count) {
-  __shared__ int last;
+  XTS(0);
   const int nth = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
-  // ---- 1. pack (only the first npb blocks own shared points; the others go
-  //      straight to the local phase and skip the system-scope fence)
+  if (st && blockIdx.x == gridDim.x - 1 && threadIdx.x < 32)
+    publish_sigma(c, st, nparts, e_sig, sig_part, sig_count);
   const int npb = min((int)gridDim.x, (P.nS + (int)blockDim.x - 1) / (int)blockDim.x);
   const int nthp = npb * blockDim.x;
-  if (blockIdx.x < npb) {
-  if (threadIdx.x < c.nnbr) wait_flag(mb_gsack(c.local, c.nbrs[threadIdx.x]), epoch - 1, c.err);
-  __syncthreads();
-  for (int s = tid; s < P.nS; s += nthp) {
-    const int nl = P.s_nloc[s];
-    double v = u[P.s_slot[s]];
-    for (int x = 1; x < nl; x++) v += u[P.s_slot[(int64_t)x * P.nS + s]];
-    part[s] = v;
-    const int nr = P.s_nr[s];
-    for (int x = 0; x < nr; x++) {
-      const int q = P.s_rank[(int64_t)x * P.nS + s];
-      if (q == c.me) continue;
-      mb_recv(c.peers[q])[P.s_off[(int64_t)x * P.nS + s] + c.rdelta[q]] = v;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    last = (atomicAdd(&c.tick[0], 1u) == (unsigned)npb - 1);
-  }
-  __syncthreads();
-  if (last) {
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      c.tick[0] = 0u;
-    }
-    __syncthreads();
-    if (threadIdx.x < c.nnbr) st_release_sys(mb_gsflag(c.peers[c.nbrs[threadIdx.x]], c.me), epoch);
-    if (threadIdx.x == 32) st_release_sys(mb_gsflag(c.local, c.me), epoch);   // own pack done
-  }
-  }
-  // ---- 2. rank-local entities
+  const bool packer = blockIdx.x < npb;
+  if (packer)
+    for (int s = tid; s < P.nS; s += nthp) pack_point(P, u, part, c, epoch, s);
+  XTS(1);
   gs_local_body<n>(P, u, apply_mask, tid, nth);
-  // ---- 3. unpack
-  if (st && blockIdx.x == 0 && threadIdx.x < 32) {
-    double sg;
-    if (sig_part) {   // this rank's sigma from the Ax kernel's per-CTA partials (fixed order)
-      const int G = *sig_count;
-      double v = 0.0;
-      for (int b = threadIdx.x; b < G; b += 32) v += sig_part[b];
-      sg = warp_sum(v);
-    } else {
-      sg = st->sigma_part[0];
-      for (int q = 1; q < nparts; q++) sg += st->sigma_part[q];
-    }
-    if (threadIdx.x == 0) st->loc[2] = sg;
-  }
-  if (threadIdx.x < c.nnbr) wait_flag(mb_gsflag(c.local, c.nbrs[threadIdx.x]), epoch, c.err);
-  if (threadIdx.x == 32) wait_flag(mb_gsflag(c.local, c.me), epoch, c.err);
-  __syncthreads();
-  const double* recv = mb_recv(c.local);
-  for (int s = tid; s < P.nS; s += nth) {
-    const int nr = P.s_nr[s];
-    double tot = 0.0;
-    for (int x = 0; x < nr; x++) {
-      const int o = P.s_off[(int64_t)x * P.nS + s];
-      const double v = o < 0 ? __ldcg(&part[s]) : ld_volatile(&recv[o]);
-      tot = x == 0 ? v : tot + v;
-    }
-    if (apply_mask && P.s_mask[s]) tot = 0.0;
-    const int nl = P.s_nloc[s];
-    for (int x = 0; x < nl; x++) u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = (atomicAdd(&c.tick[1], 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) {
-    if (threadIdx.x < c.nnbr) st_release_sys(mb_gsack(c.peers[c.nbrs[threadIdx.x]], c.me), epoch);
-    if (threadIdx.x == 0) {
-      c.tick[1] = 0u;
-      if (st) {
-        __threadfence();
-        const double v = *(volatile double*)&st->loc[2];
-        ar_publish(c, AR_SIG, e_sig, &v, 1);
-      }
-    }
-  }
+  XTS(2);
+  if (packer)
+    for (int s = tid; s < P.nS; s += nthp) unpack_point(P, u, part, c, epoch, apply_mask, s);
+  XTS(3);
+  XTS(4);
 }
 
 // publish k values from device memory (one thread)
@@ -258,9 +169,9 @@ __global__ void ar_finish_kernel(const P2P c, int site, uint64_t epoch, double* 
 
 }  // namespace dev
 
-int p2p_debug_read(unsigned long long* out, int n) {
-  if (n > 16) n = 16;
-  return cudaMemcpyFromSymbol(out, dev::g_p2p_ts, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
+int p2p_debug_read_blocks(unsigned long long* out, int n) {
+  if (n > 5 * dev::kXtsBlocks) n = 5 * dev::kXtsBlocks;
+  return cudaMemcpyFromSymbol(out, dev::g_xts, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
 }
 
 cudaError_t launch_gs_pack_p2p(const DevPlan& P, const double* u, double* part, const P2P& c,

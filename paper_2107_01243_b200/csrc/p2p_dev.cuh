@@ -41,14 +41,35 @@ __device__ __forceinline__ double* mb_slot(char* mb, int site, uint64_t epoch, i
 __device__ __forceinline__ uint64_t* mb_arflag(char* mb, int site, int r) {
   return reinterpret_cast<uint64_t*>(mb + P2P::kArFlagOff) + (size_t)site * P2P::kMaxP + r;
 }
-__device__ __forceinline__ uint64_t* mb_gsflag(char* mb, int r) {
-  return reinterpret_cast<uint64_t*>(mb + P2P::kGsFlagOff) + r;
+// receive entry o of the gather-scatter exchange with the given epoch parity
+__device__ __forceinline__ uint4* mb_ll(char* mb, int64_t o, uint64_t epoch) {
+  return reinterpret_cast<uint4*>(mb + P2P::kRecvOff) + 2 * o + (epoch & 1);
 }
-__device__ __forceinline__ uint64_t* mb_gsack(char* mb, int r) {
-  return reinterpret_cast<uint64_t*>(mb + P2P::kGsAckOff) + r;
+// "LL" store: each 8-byte half {32 data bits, 32-bit epoch flag} of the 16-byte
+// record is written by one single-copy-atomic 8-byte access, so a reader that
+// sees both flags equal to the epoch holds both halves of this epoch's value --
+// no fence and no separate flag are needed
+__device__ __forceinline__ void ll_store(uint4* p, double v, uint32_t flag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+               "r"((uint32_t)b), "r"(flag), "r"((uint32_t)(b >> 32)), "r"(flag)
+               : "memory");
 }
-__device__ __forceinline__ double* mb_recv(char* mb) {
-  return reinterpret_cast<double*>(mb + P2P::kRecvOff);
+// spin until the record carries this epoch (bounded; on timeout raise err, return 0)
+__device__ __forceinline__ double ll_load(const uint4* p, uint32_t flag, int* err) {
+  uint32_t lo, f1, hi, f2;
+  long long t0 = -1;
+  for (;;) {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(lo), "=r"(f1), "=r"(hi), "=r"(f2) : "l"(p) : "memory");
+    if (f1 == flag && f2 == flag) break;
+    if (t0 < 0) t0 = clock64();
+    else if (clock64() - t0 > (1ll << 33)) {
+      atomicExch(err, 1);
+      return 0.0;
+    }
+  }
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
 }
 
 // one thread: publish K partials of this rank to every rank

@@ -9,6 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
@@ -67,20 +68,34 @@ def main():
         res["ax_only_us"] = timed(lambda: c.ax(u, w), 50)
         c.set_p2p(True)
         c.set_overlap(False)
+        def xts():
+            xt = c.debug_read(0, 5 * 2048).reshape(5, 2048)
+            nb = int((xt[0] > 0).sum())
+            xt = xt[:, :nb].astype(np.float64)
+            rel = (xt - xt[0].min()) / 1e3
+            summ = {"grid": nb}
+            for name, sl in (("pack", slice(0, 64)), ("rest", slice(nb - 256, nb))):
+                for ph, pn in enumerate(("start", "packed", "local", "unpacked", "end")):
+                    v = rel[ph, sl]
+                    summ[f"{name}_{pn}"] = [round(float(np.min(v)), 2), round(float(np.median(v)), 2),
+                                             round(float(np.max(v)), 2)]
+            summ["local_max"] = round(float(rel[2].max()), 2)
+            summ["end_max"] = round(float(rel[4].max()), 2)
+            return summ
+
         c.pcg_solve(b, x, 0.0, 5)
-        ts = c.debug_read(0)
-        b0 = ts[0]
-        res["ts_pack_ack"] = (ts[1] - b0) / 1e3
-        res["ts_pack_stores"] = (ts[2] - b0) / 1e3
-        res["ts_pack_fence_ticket"] = (ts[3] - b0) / 1e3
-        res["ts_pack_lastblock"] = (ts[4] - b0) / 1e3 if ts[4] > b0 else -1
-        res["pack_grid"] = float(ts[5])
-        res["ts_unpack_start"] = (ts[8] - b0) / 1e3
-        res["ts_unpack_flag"] = (ts[9] - b0) / 1e3
-        res["ts_unpack_done"] = (ts[10] - b0) / 1e3
+        summ = {"pcg": xts()}
+        for _ in range(10):
+            c.gs(w)
+        summ["gs"] = xts()
+        allx = [None] * P
+        dist.all_gather_object(allx, summ)
         res["n_shared"] = float(c.n_local)
     if rank == 0:
         print(json.dumps({"P": P, "cfg": cfg, **{k: round(v, 2) for k, v in res.items()}}))
+        for r, sm in enumerate(allx):
+            for k, v in sm.items():
+                print(json.dumps({"rank": r, "ctx": k, **v}))
     sem.nccl_comm_destroy(comm)
     dist.destroy_process_group()
 
