@@ -733,14 +733,14 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
         psu.e_pub = psp.e_wait = ++c->ep_ar[sem::AR_RG];
       }
       int tk = timer_begin(c, 1);
-      CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, x, c->d_r, c->d_p, c->d_wv,
+      CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, c->d_r, c->d_wv,
                                      c->d_partial, st, rg_out, dist ? nullptr : c->d_partial_ax,
                                      c->d_nsig, psu, c->red_grid, s));
       timer_end(c, tk);
       if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
       tk = timer_begin(c, 2);
-      CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, st, c->d_hist, psp, c->red_grid,
-                                s));
+      CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, x, st, c->d_hist, psp,
+                                c->red_grid, s));
       timer_end(c, tk);
       c->launches += 2;
     }

@@ -327,11 +327,11 @@ __global__ void cg_start_kernel(PcgState* st, double* hist, const PeerSync ps) {
   st->iters = 0;
 }
 
-// alpha = rho / sigma; x += alpha p; r -= alpha w; partials of
-// rho' = <r, dinv r>_c and gamma = <r, r>_c (z is never stored)
+// alpha = rho / sigma; r -= alpha w; partials of rho' = <r, dinv r>_c and
+// gamma = <r, r>_c (z is never stored).  x += alpha p is deferred to the p
+// kernel, which streams p anyway (same operation, one pass less over p and x).
 __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
-                                 const double* __restrict__ dinv, double* __restrict__ x,
-                                 double* __restrict__ r, const double* __restrict__ p,
+                                 const double* __restrict__ dinv, double* __restrict__ r,
                                  const double* __restrict__ w, double* partial, PcgState* st,
                                  double* out2, const double* __restrict__ sig_part,
                                  const int* sig_count, const PeerSync ps) {
@@ -365,25 +365,18 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
   double rz = 0.0, rr = 0.0;
   if (ok) {
     const int64_t n2 = n >> 1;
-    const double2* p2 = reinterpret_cast<const double2*>(p);
     const double2* w2 = reinterpret_cast<const double2*>(w);
     const double2* d2 = reinterpret_cast<const double2*>(dinv);
-    double2* x2 = reinterpret_cast<double2*>(x);
     double2* r2 = reinterpret_cast<double2*>(r);
     const uchar2* m2 = reinterpret_cast<const uchar2*>(mult);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
          q += (int64_t)gridDim.x * blockDim.x) {
-      const double2 pv = __ldcs(&p2[q]);
       const double2 wv = __ldcs(&w2[q]);
       const double2 dv = __ldcs(&d2[q]);
-      double2 xv = __ldcs(&x2[q]);
       double2 rv = __ldcs(&r2[q]);
       const uchar2 mv = m2[q];
-      xv.x = fma(alpha, pv.x, xv.x);
-      xv.y = fma(alpha, pv.y, xv.y);
       rv.x = fma(-alpha, wv.x, rv.x);
       rv.y = fma(-alpha, wv.y, rv.y);
-      __stcs(&x2[q], xv);
       __stcg(&r2[q], rv);
       const double c0 = c_of(mv.x), c1 = c_of(mv.y);
       rz = fma(c0 * rv.x, dv.x * rv.x, rz);
@@ -393,7 +386,6 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
       const int64_t l = n - 1;
-      x[l] = fma(alpha, p[l], x[l]);
       const double rl = fma(-alpha, w[l], r[l]);
       r[l] = rl;
       const double c = c_of(mult[l]);
@@ -411,10 +403,12 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
   }
 }
 
-// convergence test on sqrt(gamma); p = dinv .* r + beta p with beta = rho'/rho
+// x += alpha p (this iteration's alpha, always); convergence test on
+// sqrt(gamma); unless converged p = dinv .* r + beta p with beta = rho'/rho
 __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double* __restrict__ dinv,
-                            const double* __restrict__ r, double* __restrict__ p, PcgState* st,
-                            double* hist, const PeerSync ps) {
+                            const double* __restrict__ r, double* __restrict__ p,
+                            double* __restrict__ x, PcgState* st, double* hist,
+                            const PeerSync ps) {
   __shared__ int flag;
   __shared__ double s_rg[2];
   if (st->done) return;
@@ -426,28 +420,46 @@ __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double*
   }
   __syncthreads();
   const double rho_new = s_rg[0], gamma = s_rg[1];
+  const double sigma = st->sigma;
+  const double alpha = st->rho_old / sigma;   // sigma > 0 (else the update ended the solve)
   const double g = sqrt(gamma);
   const bool conv = g <= st->tol;
   const bool bad = !(g == g) || !(rho_new == rho_new);
-  if (!conv && !bad) {
-    const double beta = rho_new / st->rho_old;
-    const int64_t n2 = n >> 1;
-    const double2* r2 = reinterpret_cast<const double2*>(r);
-    const double2* d2 = reinterpret_cast<const double2*>(dinv);
-    double2* p2 = reinterpret_cast<double2*>(p);
+  const bool newp = !conv && !bad;
+  const double beta = rho_new / st->rho_old;
+  const int64_t n2 = n >> 1;
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  const double2* d2 = reinterpret_cast<const double2*>(dinv);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  if (newp) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
          q += (int64_t)gridDim.x * blockDim.x) {
       const double2 rv = __ldcg(&r2[q]);
       const double2 dv = __ldcs(&d2[q]);
       double2 pv = __ldcs(&p2[q]);
+      double2 xv = __ldcs(&x2[q]);
+      xv.x = fma(alpha, pv.x, xv.x);
+      xv.y = fma(alpha, pv.y, xv.y);
+      __stcs(&x2[q], xv);
       pv.x = fma(beta, pv.x, dv.x * rv.x);
       pv.y = fma(beta, pv.y, dv.y * rv.y);
       p2[q] = pv;
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-      const int64_t l = n - 1;
-      p[l] = fma(beta, p[l], dinv[l] * r[l]);
+  } else {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const double2 pv = __ldcs(&p2[q]);
+      double2 xv = __ldcs(&x2[q]);
+      xv.x = fma(alpha, pv.x, xv.x);
+      xv.y = fma(alpha, pv.y, xv.y);
+      __stcs(&x2[q], xv);
     }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    x[l] = fma(alpha, p[l], x[l]);
+    if (newp) p[l] = fma(beta, p[l], dinv[l] * r[l]);
   }
   // last block advances the iteration state
   __syncthreads();
@@ -573,7 +585,17 @@ cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, cudaStr
   const int64_t N = P.N;
   const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
   if (tot == 0) return cudaSuccess;
-  const int g = grid_for(tot, 148 * 16);
+  // co-resident grid: the kernel is L2-latency bound; fewer, fuller threads
+  // (several batched face groups each) beat one wave of short-lived blocks
+  static int resident = 0;
+  if (resident == 0) {
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::gs_local_kernel<8>, kThreads, 0);
+    resident = std::max(nb, 1) * sms;
+  }
+  const int g = grid_for(tot, resident);
   switch (P.n) {
     case 2: dev::gs_local_kernel<2><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
     case 3: dev::gs_local_kernel<3><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
@@ -632,18 +654,18 @@ cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
-                             double* r, const double* p, const double* w, double* partial,
-                             PcgState* st, double* out2, const double* sig_part,
-                             const int* sig_count, const PeerSync& ps, int grid, cudaStream_t s) {
-  dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, x, r, p, w, partial, st,
-                                                  out2, sig_part, sig_count, ps);
+cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* r,
+                             const double* w, double* partial, PcgState* st, double* out2,
+                             const double* sig_part, const int* sig_count, const PeerSync& ps,
+                             int grid, cudaStream_t s) {
+  dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, r, w, partial, st, out2,
+                                                  sig_part, sig_count, ps);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
+cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,
                         PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s) {
-  dev::cg_p_kernel<<<grid, kThreads, 0, s>>>(P.n_local, dinv, r, p, st, hist, ps);
+  dev::cg_p_kernel<<<grid, kThreads, 0, s>>>(P.n_local, dinv, r, p, x, st, hist, ps);
   return cudaGetLastError();
 }
 

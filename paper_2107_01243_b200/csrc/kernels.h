@@ -151,11 +151,12 @@ cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* 
 cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cudaStream_t s);
 // sig_part/sig_count: the Ax kernel's per-CTA sigma partials (P = 1; every block
 // re-sums them in a fixed order) or nullptr (P > 1: sigma is already allreduced)
-cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* x,
-                             double* r, const double* p, const double* w, double* partial,
-                             PcgState* st, double* out2, const double* sig_part,
-                             const int* sig_count, const PeerSync& ps, int grid, cudaStream_t s);
-cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p,
+cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* r,
+                             const double* w, double* partial, PcgState* st, double* out2,
+                             const double* sig_part, const int* sig_count, const PeerSync& ps,
+                             int grid, cudaStream_t s);
+// x += alpha p, then (unless the solve ended) p = dinv r + beta p
+cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,
                         PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s);
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
                                const double* w, double* partial, PcgState* st, double* out1,
