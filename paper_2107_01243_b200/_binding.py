@@ -14,7 +14,8 @@ SEM_OK, SEM_NOT_CONVERGED = 0, 1
 SEM_EINVAL, SEM_EGEOM, SEM_ECUDA, SEM_ENCCL, SEM_ENOMEM, SEM_EBREAKDOWN = -1, -2, -3, -4, -5, -6
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libsem.so")
+# SEM_LIB: a tuning build from build.py --variant (tools only); default in-tree libsem.so
+_SO = os.environ.get("SEM_LIB") or os.path.join(_HERE, "libsem.so")
 _lib = None
 
 

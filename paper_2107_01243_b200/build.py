@@ -53,20 +53,26 @@ def _check_spills(log: str, limit: int = 16):
     return bad
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _deps_mtime():
-        return SO
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str | None = None) -> str:
+    """Build libsem.so; with variant, a tuning build (extra -D defines) into
+    _var/libsem_<variant>.so, loaded only when SEM_LIB points at it."""
+    so, obj = SO, OBJ
+    if variant:
+        obj = os.path.join(HERE, "_var", variant)
+        so = os.path.join(HERE, "_var", f"libsem_{variant}.so")
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= _deps_mtime():
+        return so
+    os.makedirs(obj, exist_ok=True)
     inc, lib = _nccl_dirs()
     nvcc = _nvcc()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc,
-              "-I", os.path.join(ROOT, "include")]
+              "-I", os.path.join(ROOT, "include"), *defines]
     jobs = []
     for f in CUDA_SRCS:
-        out = os.path.join(OBJ, f + ".o")
+        out = os.path.join(obj, f + ".o")
         jobs.append([nvcc, *ARCH, *common, "-Xptxas", "-v", "-c", os.path.join(CSRC, f), "-o", out])
     for f in CXX_SRCS:
-        out = os.path.join(OBJ, f + ".o")
+        out = os.path.join(obj, f + ".o")
         jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I",
                      os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", out])
 
@@ -78,18 +84,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=4) as ex:
         logs = list(ex.map(run, jobs))
-    with open(os.path.join(OBJ, "ptxas.log"), "w") as f:
+    with open(os.path.join(obj, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     _check_spills("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    objs = [os.path.join(OBJ, f + ".o") for f in CUDA_SRCS + CXX_SRCS]
-    run([nvcc, *ARCH, "-shared", "-o", SO + ".tmp", *objs, "-L", lib, "-l:libnccl.so.2",
+    objs = [os.path.join(obj, f + ".o") for f in CUDA_SRCS + CXX_SRCS]
+    run([nvcc, *ARCH, "-shared", "-o", so + ".tmp", *objs, "-L", lib, "-l:libnccl.so.2",
          "-Xlinker", "-rpath=" + lib, "-lcudart"])
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    # python build.py [--force] [-v] [--variant NAME -DMACRO=V ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    print(build(force="--force" in args, verbose="-v" in args,
+                defines=[a for a in args if a.startswith("-D")], variant=var))

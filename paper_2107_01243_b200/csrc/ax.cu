@@ -38,8 +38,10 @@ struct AxCfg;
 #define SEM_AX_SMEM_PAD 0   // tuning experiments only: extra smem to force lower residency
 #endif
 // PPC: k-planes per bulk copy (divides n).  n=8 tuned with tools/ubench_ax.cu
-// on B200 (NSG=3, PPC=4: 6.2 TB/s on 32^3 elements); the others follow the same
-// rule of ~2 copies per element and a 2-3 slot ring within ~60 KB of smem.
+// on B200 (NSG=3, PPC=4: 6.2 TB/s on 32^3 elements); n=7, 9, 11, 12 with
+// tools/measure.py sweep over build variants (profiles/r01_measure.md); the
+// others follow the rule of ~2 copies per element and a 2-3 slot ring within
+// ~60 KB of smem.
 #ifndef SEM_AX8_NE
 #define SEM_AX8_NE 1
 #endif
@@ -54,14 +56,37 @@ template <> struct AxCfg<3> { static constexpr int NE = 8, NSG = 3, PPC = 3; };
 template <> struct AxCfg<4> { static constexpr int NE = 4, NSG = 3, PPC = 2; };
 template <> struct AxCfg<5> { static constexpr int NE = 2, NSG = 3, PPC = 5; };
 template <> struct AxCfg<6> { static constexpr int NE = 2, NSG = 3, PPC = 3; };
-template <> struct AxCfg<7> { static constexpr int NE = 1, NSG = 3, PPC = 7; };
+#ifndef SEM_AX7_NE
+#define SEM_AX7_NE 2
+#endif
+#ifndef SEM_AX7_NSG
+#define SEM_AX7_NSG 6
+#endif
+#ifndef SEM_AX7_PPC
+#define SEM_AX7_PPC 1
+#endif
+template <> struct AxCfg<7> {
+  static constexpr int NE = SEM_AX7_NE, NSG = SEM_AX7_NSG, PPC = SEM_AX7_PPC;
+};
 template <> struct AxCfg<8> {
   static constexpr int NE = SEM_AX8_NE, NSG = SEM_AX8_NSG, PPC = SEM_AX8_PPC;
 };
-template <> struct AxCfg<9> { static constexpr int NE = 1, NSG = 3, PPC = 3; };
+#ifndef SEM_AX9_NSG
+#define SEM_AX9_NSG 6
+#endif
+#ifndef SEM_AX9_PPC
+#define SEM_AX9_PPC 1
+#endif
+template <> struct AxCfg<9> { static constexpr int NE = 1, NSG = SEM_AX9_NSG, PPC = SEM_AX9_PPC; };
 template <> struct AxCfg<10> { static constexpr int NE = 1, NSG = 3, PPC = 5; };
-template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = 6, PPC = 1; };
-template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = 3, PPC = 3; };
+#ifndef SEM_AX11_NSG
+#define SEM_AX11_NSG 6
+#endif
+template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = SEM_AX11_NSG, PPC = 1; };
+#ifndef SEM_AX12_NSG
+#define SEM_AX12_NSG 2
+#endif
+template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = SEM_AX12_NSG, PPC = 3; };
 
 template <int n, bool GS = false>
 struct AxShape {
@@ -75,9 +100,14 @@ struct AxShape {
   static constexpr int NSD = 4;                    // element-done ring (compute -> gs warp)
   static constexpr int NSU = 2;                    // u ring depth
   static constexpr bool kBulkU = (n % 2) == 0;     // u block 16-B aligned for any element
-  static constexpr int uslot = NE * n3;            // doubles per u slot
+  // doubles per u slot (odd n: +2 so the 16-B aligned body can be shifted by one
+  // double, rounded to an even count so every slot starts 16-B aligned)
+  static constexpr int uslot = kBulkU ? NE * n3 : (NE * n3 + 3) / 2 * 2;
+  static_assert(uslot % 2 == 0, "u slots must stay 16-B aligned");
   static constexpr int gslot = NE * PPC * 6 * n2;  // doubles per G slot (PPC planes x NE)
-  static constexpr int rp = n + 1;                 // padded row pitch of w_r / w_s
+  // row pitch of w_r / w_s: odd, so the transposed-contraction reads
+  // w_r[k][j][m] (j across the warp) spread over distinct banks
+  static constexpr int rp = (n % 2) ? n : n + 1;
   static constexpr int wpl = n * rp;               // padded plane pitch
   static constexpr int wel = n * wpl;              // per element
   static constexpr int dpad = n + 1;
@@ -89,7 +119,9 @@ struct AxShape {
   // CTAs per SM the shared memory allows; the register budget is sized to match
   // (with the gs warp, at most 168 registers per thread: 65536 / (T * 168) CTAs)
   static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
-  static constexpr int MINBR = GS ? 65536 / (T * 168) : 8;
+  // n >= 7 (and the gs warp): keep 168 registers per thread -- the contraction
+  // state does not fit fewer without spilling, which costs far more than residency
+  static constexpr int MINBR = (GS || n >= 7) ? 65536 / (T * 168) : 8;
   static constexpr int MINB1 = MINB0 < MINBR ? MINB0 : MINBR;
   static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > 8 ? 8 : MINB1);
 };
@@ -137,7 +169,10 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
   constexpr bool kBulkU = Sh::kBulkU;
   constexpr bool kMask = MODE != AX_ONLY;   // Dirichlet mask in the epilogue
   constexpr bool kGs = kMask && FUSE;         // gather-scatter warp in-kernel
-  constexpr bool kDreg = n <= 9;              // D rows in registers (else shared memory)
+#ifndef SEM_DREG_MAX
+#define SEM_DREG_MAX 12
+#endif
+  constexpr bool kDreg = n <= SEM_DREG_MAX;   // D rows in registers (else shared memory)
 #ifndef SEM_DT_REG
 #define SEM_DT_REG 1
 #endif
@@ -179,7 +214,7 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       mbar_init(&emptyG[s], Sh::NWC);
     }
     for (int s = 0; s < NSU; s++) {
-      mbar_init(&fullU[s], kBulkU ? 1 : 32);
+      mbar_init(&fullU[s], kBulkU ? 1 : 2);
       mbar_init(&emptyU[s], Sh::NWC);
     }
     for (int s = 0; s < NSD; s++) {
@@ -222,10 +257,22 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
           bulk_g2s(sU + su * Sh::uslot, a.u + (size_t)e0 * n3, bU, &fullU[su]);
         }
       } else {
-        double* dst = sU + su * Sh::uslot;
+        // odd n: the group's u block starts 8 mod 16 for every other element.
+        // Bulk-copy its 16-B aligned body; lane 1 copies the (at most two) end
+        // doubles.  The block lands h doubles into the slot (h = source
+        // misalignment), which keeps the bulk destination 16-B aligned.
         const double* src = a.u + (size_t)e0 * n3;
-        for (int q = lane; q < cnt * n3; q += 32) dst[q] = src[q];
-        mbar_arrive(&fullU[su]);   // release: this lane's stores
+        const int h = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1u);
+        const int cntd = cnt * n3, nb = ((cntd - h) >> 1) << 1;
+        double* dst = sU + su * Sh::uslot + h;
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&fullU[su], (uint32_t)nb * 8u);
+          bulk_g2s(dst + h, src + h, (uint32_t)nb * 8u, &fullU[su]);
+        } else if (lane == 1) {
+          if (h) dst[0] = __ldg(src);
+          if (h + nb < cntd) dst[cntd - 1] = __ldg(src + cntd - 1);
+          mbar_arrive(&fullU[su]);   // release: this lane's stores
+        }
       }
       if (++su == NSU) { su = 0; phu ^= 1u; }
       // k-planes of the geometric factors
@@ -368,7 +415,8 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       int e0, cnt;
       group(g, e0, cnt);
       const bool active = el < cnt;
-      const double* sUe = sU + su * Sh::uslot + el * n3;
+      const int uoff = kBulkU ? 0 : (int)((reinterpret_cast<uintptr_t>(a.u + (size_t)e0 * n3) >> 3) & 1u);
+      const double* sUe = sU + su * Sh::uslot + uoff + el * n3;
       double* wr_s = sWr + el * Sh::wel;
       double* ws_s = sWs + el * Sh::wel;
       mbar_wait(&fullU[su], phu);

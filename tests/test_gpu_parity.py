@@ -58,6 +58,9 @@ MESHES = [
     (unit_box(2, 3, 2, periodic=(0, 1, 1)), 5),
     (tgv_box(2, 2, 3, deform=1), 11),            # maximum N
     (unit_box(3, 3, 2), 9),
+    (tgv_box(3, 2, 3, deform=1), 6),             # odd n: u blocks 8 mod 16 every other element
+    (unit_box(3, 2, 3, periodic=(0, 0, 1)), 8),
+    (tgv_box(2, 3, 2, deform=1), 10),
 ]
 IDS = [f"{s.ex}x{s.ey}x{s.ez}-p{''.join(map(str, s.periodic))}-d{s.deform}-N{N}" for s, N in MESHES]
 
@@ -118,6 +121,22 @@ def test_apply_is_deterministic_and_variants_agree_bitwise():
             outs.append(host(w))
         for o in outs[1:]:
             assert np.array_equal(outs[0], o)
+
+
+@pytest.mark.parametrize("N", [2, 4, 6, 8, 10])
+def test_odd_n_ring_wrap(N):
+    """More elements than resident CTAs, so every CTA cycles through both u
+    slots and all G slots (odd n: u blocks alternate between 0 and 8 mod 16)."""
+    spec = tgv_box(12, 10, 10, deform=1)
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=7)
+    with sem().sem_setup(spec, N) as c:
+        du = dev(u)
+        w = c.zeros()
+        c.ax(du, w)
+        assert nrel(host(w), o.ax(u)) <= 1e-12
+        c.apply(du, w)
+        assert nrel(host(w), o.apply(u)) <= 1e-12
 
 
 @pytest.mark.parametrize("cfg", ["C2", "C3"])

@@ -1,0 +1,214 @@
+"""SURVEY 8(d)/(e) measurements that bench.py (C2 PCG step) does not cover.
+
+  python tools/measure.py single            # one GPU: triad, C3, C4, N-sweep
+  torchrun --nproc-per-node P tools/measure.py strong   # C3/C4 strong scaling
+
+Each result is one JSON line on stdout (rank 0).  All timings are CUDA events
+on the context stream after warm-up, max over ranks for P > 1.  Denominators:
+nominal 8 TB/s, the measured copy peak (MEASURED_PEAKS.json) and an fp64
+STREAM triad measured in the same run (paper's convention).
+"""
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2107_01243_b200 as sem  # noqa: E402
+from sem_inputs import CONFIGS, f_tgv, p_tgv, tgv_box  # noqa: E402
+
+NOMINAL = 8000.0
+
+
+def peak_copy():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def bytes_model(N):
+    fb = 1.0 - ((N - 1) / (N + 1)) ** 3
+    return fb, 64.0, 64.0 + 20.0 * fb
+
+
+def out(d):
+    print(json.dumps(d), flush=True)
+
+
+def timed(fn, st, reps, warm=3, sync=None):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    if sync:
+        sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps   # ms
+
+
+def triad(st):
+    """a = b + s c over 2^27 fp64 (1 GiB per vector): 24 B per element."""
+    n = 1 << 27
+    b = torch.rand(n, dtype=torch.float64, device="cuda")
+    c = torch.rand(n, dtype=torch.float64, device="cuda")
+    a = torch.empty_like(b)
+    ms = timed(lambda: torch.add(b, c, alpha=3.0, out=a), st, 20)
+    return 24.0 * n / (ms * 1e-3) / 1e9
+
+
+def op_rates(c, N, st, reps, tri):
+    n = c.n_local
+    u = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+    w = c.zeros()
+    fb, bax, baxgs = bytes_model(N)
+    res = {}
+    for name, fn, bpp in (("ax", lambda: c.ax(u, w), bax), ("ax_gs", lambda: c.apply(u, w), baxgs)):
+        ms = timed(fn, st, reps)
+        gbs = bpp * n / (ms * 1e-3) / 1e9
+        res[name] = {"ms": round(ms, 4), "gdofs": round(n / (ms * 1e-3) / 1e9, 2),
+                     "useful_GBps": round(gbs, 0), "frac_nominal": round(gbs / NOMINAL, 3),
+                     "frac_copy": round(gbs / peak_copy(), 3),
+                     "frac_triad": round(gbs / tri, 3) if tri else None}
+    del u, w
+    return res
+
+
+def pcg_rate(c, st, iters):
+    """fixed-iteration PCG (tol 0) on the TGV right-hand side: iter/s, GDOF/s"""
+    X, Y, Z = c.coords()
+    b = c.zeros()
+    c.rhs(f_tgv(X, Y, Z, xp=torch), b)
+    del X, Y, Z
+    x = c.zeros()
+    c.pcg_solve(b, x, 0.0, 5)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    r = c.pcg_solve(b, x, 0.0, iters)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"iters": r["iters"], "ms": round(ms, 3), "iter_per_s": round(r["iters"] / (ms * 1e-3), 1),
+            "gdofs": round(c.n_local * r["iters"] / (ms * 1e-3) / 1e9, 2)}
+
+
+def single():
+    torch.cuda.set_device(0)
+    st = torch.cuda.current_stream()
+    tri = triad(st)
+    out({"what": "triad", "GBps": round(tri, 0), "copy_peak_GBps": peak_copy(),
+         "gpu": torch.cuda.get_device_name(0)})
+    # C3: Ax / Ax+gs rates (where the >=60% target is evaluated) and the PCG solve to tol
+    spec, N = CONFIGS["C3"]
+    with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
+        out({"what": "C3_ops", "n_p": c.n_local, **op_rates(c, N, st, 50, tri)})
+        X, Y, Z = c.coords()
+        b = c.zeros()
+        c.rhs(f_tgv(X, Y, Z, xp=torch), b)
+        x = c.zeros()
+        c.pcg_solve(b, x, 1e-10, 5000)   # warm
+        x.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        r = c.pcg_solve(b, x, 1e-10, 5000)
+        e1.record(st)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ms = e0.elapsed_time(e1)
+        B = torch.from_numpy(c.export_field("B")).cuda()
+        xm = x - (B * x).sum() / B.sum()                       # reading Q18
+        einf = float((xm - p_tgv(X, Y, Z, xp=torch)).abs().max())
+        out({"what": "C3_pcg_to_tol", "tol": 1e-10, "iters": r["iters"], "status": r["status"],
+             "res_final": r["res_final"], "res_true": r["res_true"], "ms": round(ms, 2),
+             "wall_s": round(wall, 4), "iter_per_s": round(r["iters"] / (ms * 1e-3), 1),
+             "gdofs": round(c.n_local * r["iters"] / (ms * 1e-3) / 1e9, 2), "e_inf_vs_p*": einf})
+        del X, Y, Z, b, x, B, xm
+    torch.cuda.empty_cache()
+    # C4 at P = 1: deformed 64^3, all 6 factors nonzero
+    spec, N = CONFIGS["C4"]
+    with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
+        out({"what": "C4_ops_P1", "n_p": c.n_local, **op_rates(c, N, st, 10, tri)})
+        out({"what": "C4_pcg_P1", **pcg_rate(c, st, 50)})
+    torch.cuda.empty_cache()
+    sweep(range(1, 12), st, tri)
+
+
+def sweep(Ns, st=None, tri=None):
+    """N sweep at fixed n_p ~ 1.25e8 (SURVEY C5 per-GPU size: E_axis = 500/(N+1))"""
+    if st is None:
+        torch.cuda.set_device(0)
+        st = torch.cuda.current_stream()
+        tri = triad(st)
+    for N in Ns:
+        ea = int(round(500.0 / (N + 1)))
+        ez = max(8, int(round(ea / 8.0)) * 8)
+        spec = tgv_box(ea, ea, ez)
+        t0 = time.perf_counter()
+        with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
+            setup_s = time.perf_counter() - t0
+            fb, _, baxgs = bytes_model(N)
+            out({"what": "sweep", "N": N, "mesh": [ea, ea, ez], "E": spec.E, "n_p": c.n_local,
+                 "f_b": round(fb, 3), "ax_gs_B_per_pt": round(baxgs, 1), "setup_s": round(setup_s, 1),
+                 **op_rates(c, N, st, 10, tri)})
+        torch.cuda.empty_cache()
+
+
+def strong():
+    import torch.distributed as dist
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = [sem.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = sem.nccl_comm_init(uid[0], rank, P)
+    st = torch.cuda.current_stream()
+
+    def mx(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for cfg in ("C3", "C4"):
+        spec, N = CONFIGS[cfg]
+        with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm, stream=st.cuda_stream) as c:
+            n_tot = spec.E * (N + 1) ** 3
+            u = torch.empty(c.n_local, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+            w = c.zeros()
+            ms = mx(timed(lambda: c.apply(u, w), st, 20, sync=dist.barrier))
+            p = pcg_rate(c, st, 100 if cfg == "C3" else 40)
+            pms = mx(p["ms"])
+            if rank == 0:
+                out({"what": f"{cfg}_strong", "P": P, "n_p_total": n_tot,
+                     "ax_gs_ms": round(ms, 4), "ax_gs_gdofs": round(n_tot / (ms * 1e-3) / 1e9, 2),
+                     "pcg_iters": p["iters"], "pcg_ms": round(pms, 3),
+                     "pcg_iter_per_s": round(p["iters"] / (pms * 1e-3), 1),
+                     "pcg_gdofs": round(n_tot * p["iters"] / (pms * 1e-3) / 1e9, 2)})
+            del u, w
+        torch.cuda.empty_cache()
+    sem.nccl_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1] if len(sys.argv) > 1 else "single"
+    if mode == "strong":
+        strong()
+    elif mode == "sweep":
+        sweep([int(v) for v in sys.argv[2].split(",")])
+    else:
+        single()
