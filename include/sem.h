@@ -165,6 +165,12 @@ int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n);
 /* nranks > 1: 1 = Alg. 1 overlap (Ax on the boundary elements, send,
    Ax on the interior elements while the partials travel); 0 = one Ax launch. */
 #define SEM_OPT_OVERLAP 3
+/* Rank-local gather-scatter schedule (results bit-identical in every mode):
+   0 (default) auto, 1 = flat (each entity class swept over the whole grid;
+   best while w is L2-resident), 2 = element-ordered chunks pulled dynamically
+   by the blocks (each element's w streamed from HBM about once).  Auto picks
+   2 when w exceeds 64 MB. */
+#define SEM_OPT_GS_MODE 4
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

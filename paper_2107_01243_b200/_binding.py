@@ -251,6 +251,10 @@ class Context:
         """Alg. 1 boundary/interior split of the operator at nranks > 1. Collective."""
         _check(load().sem_set_option(self._h, 3, 1 if on else 0))
 
+    def set_gs_mode(self, mode: int):
+        """Gather-scatter schedule: 0 auto, 1 flat, 2 element-ordered chunks."""
+        _check(load().sem_set_option(self._h, 4, int(mode)))
+
     def set_p2p(self, on: bool):
         """Multi-GPU transport: NVLink peer memory (default) or NCCL. Collective."""
         _check(load().sem_set_option(self._h, 2, 1 if on else 0))

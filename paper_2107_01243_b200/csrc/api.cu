@@ -82,6 +82,10 @@ struct sem_ctx {
   uint8_t *d_fax = nullptr, *d_eax = nullptr, *d_enin = nullptr, *d_emask = nullptr,
           *d_vnin = nullptr, *d_vmask = nullptr;
   unsigned* d_cnt = nullptr;
+  int32_t *d_fst = nullptr, *d_est = nullptr, *d_vst = nullptr;
+  unsigned long long* d_gsctr = nullptr;   // gs chunk counters (never reset)
+  uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
+  int gs_mode = 0;                         // SEM_OPT_GS_MODE
   int32_t *d_sslot = nullptr, *d_soff = nullptr;
   uint8_t *d_snloc = nullptr, *d_snr = nullptr, *d_smask = nullptr, *d_smult = nullptr;
   int8_t* d_srank = nullptr;
@@ -232,7 +236,7 @@ int exchange(sem_ctx* c) {
 int gs_pass(sem_ctx* c, double* w) {
   if (c->fuse_gs) return SEM_OK;
   int tk = timer_begin(c, 4);
-  cudaError_t e = sem::launch_gs_local(c->dp, w, 0, c->stream);
+  cudaError_t e = sem::launch_gs_local(c->dp, w, 0, &c->gs_base[0], c->gs_mode, c->stream);
   timer_end(c, tk);
   c->launches++;
   return check(e, "gs kernel");
@@ -269,7 +273,8 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
     int tk = timer_begin(c, 4);
     CUDA_TRY(sem::launch_gs_exchange_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
                                          mode == sem::AX_PCG ? st : nullptr, 1, c->cur_e_sig,
-                                         c->d_partial_ax, c->d_nsig, c->stream));
+                                         c->d_partial_ax, c->d_nsig, &c->gs_base[1], c->gs_mode,
+                                         c->stream));
     timer_end(c, tk);
     c->launches++;
     return SEM_OK;
@@ -344,11 +349,12 @@ int gs_op(sem_ctx* c, double* u, int apply_mask) {
   if (shared && p2p(c)) {   // one kernel: pack, local entities, unpack
     const uint64_t e = ++c->ep_gs;
     CUDA_TRY(sem::launch_gs_exchange_p2p(c->dp, u, c->d_part, c->p2p, e, apply_mask, nullptr, 1,
-                                         0, nullptr, nullptr, c->stream));
+                                         0, nullptr, nullptr, &c->gs_base[1], c->gs_mode,
+                                         c->stream));
     c->launches++;
     return SEM_OK;
   }
-  CUDA_TRY(sem::launch_gs_local(c->dp, u, apply_mask, c->stream));
+  CUDA_TRY(sem::launch_gs_local(c->dp, u, apply_mask, &c->gs_base[0], c->gs_mode, c->stream));
   c->launches++;
   if (shared) {
     CUDA_TRY(sem::launch_gs_pack(c->dp, u, c->d_part, c->d_send, c->stream));
@@ -390,7 +396,8 @@ void free_ctx(sem_ctx* c) {
                   c->d_emask, c->d_vnin, c->d_vmask, c->d_cnt, c->d_sslot, c->d_soff,
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
-                  c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank};
+                  c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank, c->d_fst, c->d_est,
+                  c->d_vst, c->d_gsctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -546,6 +553,11 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(upload(&c->d_vb, h.v_base, s));
   SETUP_TRY(upload(&c->d_vnin, h.v_nin, s));
   SETUP_TRY(upload(&c->d_vmask, h.v_mask, s));
+  SETUP_TRY(upload(&c->d_fst, h.f_start, s));
+  SETUP_TRY(upload(&c->d_est, h.e_start, s));
+  SETUP_TRY(upload(&c->d_vst, h.v_start, s));
+  SETUP_TRY(dalloc(&c->d_gsctr, 2));
+  SETUP_CUDA(cudaMemsetAsync(c->d_gsctr, 0, 2 * sizeof(unsigned long long), s));
   SETUP_TRY(upload(&c->d_sslot, h.s_slot, s));
   SETUP_TRY(upload(&c->d_soff, h.s_off, s));
   SETUP_TRY(upload(&c->d_snloc, h.s_nloc, s));
@@ -580,6 +592,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   P.e_base = c->d_eb; P.e_axis = c->d_eax; P.e_nin = c->d_enin; P.e_mask = c->d_emask;
   P.v_base = c->d_vb; P.v_nin = c->d_vnin; P.v_mask = c->d_vmask;
   P.cnt = c->d_cnt;
+  P.f_start = c->d_fst; P.e_start = c->d_est; P.v_start = c->d_vst; P.gs_ctr = c->d_gsctr;
   P.s_slot = c->d_sslot; P.s_off = c->d_soff; P.s_nloc = c->d_snloc; P.s_nr = c->d_snr;
   P.s_mask = c->d_smask; P.s_mult = c->d_smult;
 
@@ -915,6 +928,14 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (option == SEM_OPT_OVERLAP) {   // collective
     cudaStreamSynchronize(c->stream);
     c->overlap = value != 0;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_GS_MODE) {
+    if (value < 0 || value > 2) {
+      sem::set_error("sem_set_option: SEM_OPT_GS_MODE must be 0, 1 or 2");
+      return SEM_EINVAL;
+    }
+    c->gs_mode = value;
     return SEM_OK;
   }
   if (option == SEM_OPT_P2P) {   // collective: every rank must set the same value

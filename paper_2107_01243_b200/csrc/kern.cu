@@ -207,10 +207,17 @@ __global__ void mult_kernel(const DevPlan P, uint8_t* mult) {
   }
 }
 
-template <int n>
-__global__ void __launch_bounds__(256) gs_local_kernel(const DevPlan P, double* __restrict__ u,
-                                                       int apply_mask) {
-  gs_local_body<n>(P, u, apply_mask, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+#ifndef SEM_GS_MINB
+#define SEM_GS_MINB 1
+#endif
+#ifndef SEM_GS_GRIDX
+#define SEM_GS_GRIDX 1   // grid = SEM_GS_GRIDX x resident blocks
+#endif
+template <int n, bool SWEEP>
+__global__ void __launch_bounds__(256, SEM_GS_MINB) gs_local_kernel(const DevPlan P, double* __restrict__ u,
+                                                       int apply_mask, unsigned long long base,
+                                                       int ce) {
+  gs_local_body<n, SWEEP>(P, u, apply_mask, P.gs_ctr, base, ce);
 }
 
 // Alg. 1 lines 6-7: this rank's partial for every shared point (ascending local
@@ -581,35 +588,44 @@ cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, cudaStream_t s) {
+cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_t* base,
+                            int mode, cudaStream_t s) {
   const int64_t N = P.N;
   const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
   if (tot == 0) return cudaSuccess;
-  // co-resident grid: the kernel is L2-latency bound; fewer, fuller threads
-  // (several batched face groups each) beat one wave of short-lived blocks
-  static int resident = 0;
-  if (resident == 0) {
-    int dev = 0, sms = 148, nb = 1;
+  // co-resident grid (x SEM_GS_GRIDX); chunk mode: blocks pull element chunks
+  static int resident[2] = {0, 0};
+  if (resident[0] == 0) {
+    int dev = 0, sms = 148, nb0 = 1, nb1 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::gs_local_kernel<8>, kThreads, 0);
-    resident = std::max(nb, 1) * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, dev::gs_local_kernel<8, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, dev::gs_local_kernel<8, true>, kThreads, 0);
+    resident[0] = std::max(nb0, 1) * sms * SEM_GS_GRIDX;
+    resident[1] = std::max(nb1, 1) * sms * SEM_GS_GRIDX;
   }
-  const int g = grid_for(tot, resident);
+  const int ce = dev::gs_mode_ce(P, mode);
+  const int g = ce > 0 ? std::max(1, std::min(resident[1], (P.nloc + ce - 1) / ce))
+                       : grid_for(tot, resident[0]);
+  const unsigned long long b = *base;
+  *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
+#define GS_LAUNCH(k)                                                                  \
+  (ce > 0 ? dev::gs_local_kernel<k, true><<<g, kThreads, 0, s>>>(P, u, apply_mask, b, ce) \
+          : dev::gs_local_kernel<k, false><<<g, kThreads, 0, s>>>(P, u, apply_mask, b, ce))
   switch (P.n) {
-    case 2: dev::gs_local_kernel<2><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 3: dev::gs_local_kernel<3><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 4: dev::gs_local_kernel<4><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 5: dev::gs_local_kernel<5><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 6: dev::gs_local_kernel<6><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 7: dev::gs_local_kernel<7><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 8: dev::gs_local_kernel<8><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 9: dev::gs_local_kernel<9><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 10: dev::gs_local_kernel<10><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 11: dev::gs_local_kernel<11><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    case 12: dev::gs_local_kernel<12><<<g, kThreads, 0, s>>>(P, u, apply_mask); break;
-    default: return cudaErrorInvalidValue;
+    case 2: GS_LAUNCH(2); break;
+    case 3: GS_LAUNCH(3); break;
+    case 4: GS_LAUNCH(4); break;
+    case 5: GS_LAUNCH(5); break;
+    case 6: GS_LAUNCH(6); break;
+    case 7: GS_LAUNCH(7); break;
+    case 8: GS_LAUNCH(8); break;
+    case 9: GS_LAUNCH(9); break;
+    case 10: GS_LAUNCH(10); break;
+    case 11: GS_LAUNCH(11); break;
+    case 12: GS_LAUNCH(12); break;
   }
+#undef GS_LAUNCH
   return cudaGetLastError();
 }
 

@@ -26,6 +26,10 @@ struct DevPlan {
   const uint8_t* v_nin = nullptr;
   const uint8_t* v_mask = nullptr;
   unsigned* cnt = nullptr;          // [nF + nEd + nV] last-arriver tickets
+  const int32_t* f_start = nullptr; // [nloc+1] entities created by each element (gs_dev.cuh)
+  const int32_t* e_start = nullptr;
+  const int32_t* v_start = nullptr;
+  unsigned long long* gs_ctr = nullptr;   // [2] chunk counters (gs_local, exchange), never reset
   // shared points (P > 1)
   const int32_t* s_slot = nullptr;  // [8][nS]
   const int32_t* s_off = nullptr;   // [8][nS]
@@ -99,7 +103,7 @@ int p2p_debug_read_blocks(unsigned long long* out, int n);   // [5][2048] exchan
 cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, const P2P& c,
                                    uint64_t epoch, int apply_mask, PcgState* st, int nparts,
                                    uint64_t e_sig, const double* sig_part, const int* sig_count,
-                                   cudaStream_t s);
+                                   uint64_t* base, int mode, cudaStream_t s);
 // st != nullptr (PCG): also combines the sigma parts and publishes them (epoch e_sig)
 cudaError_t launch_gs_unpack_p2p(const DevPlan& P, double* u, const double* part, const P2P& c,
                                  uint64_t epoch, int apply_mask, PcgState* st, int nparts,
@@ -130,7 +134,10 @@ cudaError_t launch_mask(const DevPlan& P, double* u, cudaStream_t s);
 cudaError_t launch_export_mask(const DevPlan& P, uint8_t* m, cudaStream_t s);
 
 // gather-scatter (standalone)
-cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, cudaStream_t s);
+// *base: host copy of the chunk counter (advanced by the tickets the launch takes)
+// mode: 0 auto (flat while w fits in L2, else element-ordered chunks), 1 flat, 2 chunks
+cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_t* base,
+                            int mode, cudaStream_t s);
 cudaError_t launch_gs_pack(const DevPlan& P, const double* u, double* part, double* sendbuf,
                            cudaStream_t s);
 cudaError_t launch_gs_unpack(const DevPlan& P, double* u, const double* part,

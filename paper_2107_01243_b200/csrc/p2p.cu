@@ -127,16 +127,17 @@ __global__ void gs_unpack_p2p_kernel(const DevPlan P, double* __restrict__ u, co
 // Inside PCG the last block publishes this rank's sigma first.  Every block is
 // co-resident (grid capped at residency by the launcher), so the waits cannot
 // starve a block that has yet to pack.
-template <int n>
+template <int n, bool SWEEP>
 __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
                                                               double* __restrict__ u, double* part,
                                                               const P2P c, uint64_t epoch,
                                                               int apply_mask, PcgState* st,
                                                               int nparts, uint64_t e_sig,
                                                               const double* sig_part,
-                                                              const int* sig_count) {
+                                                              const int* sig_count,
+                                                              unsigned long long base, int ce) {
   XTS(0);
-  const int nth = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (st && blockIdx.x == gridDim.x - 1 && threadIdx.x < 32)
     publish_sigma(c, st, nparts, e_sig, sig_part, sig_count);
   const int npb = min((int)gridDim.x, (P.nS + (int)blockDim.x - 1) / (int)blockDim.x);
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
   if (packer)
     for (int s = tid; s < P.nS; s += nthp) pack_point(P, u, part, c, epoch, s);
   XTS(1);
-  gs_local_body<n>(P, u, apply_mask, tid, nth);
+  gs_local_body<n, SWEEP>(P, u, apply_mask, P.gs_ctr + 1, base, ce);
   XTS(2);
   if (packer)
     for (int s = tid; s < P.nS; s += nthp) unpack_point(P, u, part, c, epoch, apply_mask, s);
@@ -196,48 +197,58 @@ template <int n>
 static cudaError_t launch_exchange_n(const DevPlan& P, double* u, double* part, const P2P& c,
                                      uint64_t epoch, int apply_mask, PcgState* st, int nparts,
                                      uint64_t e_sig, const double* sig_part, const int* sig_count,
-                                     cudaStream_t s) {
-  static int resident = 0;
-  if (resident == 0) {
-    int dev = 0, sms = 148, nb = 1;
+                                     uint64_t* base, int mode, cudaStream_t s) {
+  static int resident[2] = {0, 0};
+  if (resident[0] == 0) {
+    int dev = 0, sms = 148, nb0 = 1, nb1 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::gs_exchange_p2p_kernel<n>, 256, 0);
-    resident = std::max(nb, 1) * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, dev::gs_exchange_p2p_kernel<n, false>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, dev::gs_exchange_p2p_kernel<n, true>, 256, 0);
+    resident[0] = std::max(nb0, 1) * sms;
+    resident[1] = std::max(nb1, 1) * sms;
   }
-  const int g = resident;   // co-resident grid (the local-gs phase is latency bound)
-  dev::gs_exchange_p2p_kernel<n><<<g, 256, 0, s>>>(P, u, part, c, epoch, apply_mask, st, nparts,
-                                                   e_sig, sig_part, sig_count);
+  const int ce = dev::gs_mode_ce(P, mode);
+  // co-resident grid (the waits must not starve unscheduled blocks)
+  const int g = resident[ce > 0 ? 1 : 0];
+  const unsigned long long b = *base;
+  *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
+  if (ce > 0)
+    dev::gs_exchange_p2p_kernel<n, true><<<g, 256, 0, s>>>(P, u, part, c, epoch, apply_mask, st,
+                                                           nparts, e_sig, sig_part, sig_count, b, ce);
+  else
+    dev::gs_exchange_p2p_kernel<n, false><<<g, 256, 0, s>>>(P, u, part, c, epoch, apply_mask, st,
+                                                            nparts, e_sig, sig_part, sig_count, b, ce);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, const P2P& c,
                                    uint64_t epoch, int apply_mask, PcgState* st, int nparts,
                                    uint64_t e_sig, const double* sig_part, const int* sig_count,
-                                   cudaStream_t s) {
+                                   uint64_t* base, int mode, cudaStream_t s) {
   switch (P.n) {
-    case 2: return launch_exchange_n<2>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 3: return launch_exchange_n<3>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 4: return launch_exchange_n<4>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 5: return launch_exchange_n<5>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 6: return launch_exchange_n<6>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 7: return launch_exchange_n<7>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 8: return launch_exchange_n<8>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 9: return launch_exchange_n<9>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 10: return launch_exchange_n<10>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 11: return launch_exchange_n<11>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
-    case 12: return launch_exchange_n<12>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig, sig_part,
-                                       sig_count, s);
+    case 2: return launch_exchange_n<2>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 3: return launch_exchange_n<3>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 4: return launch_exchange_n<4>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 5: return launch_exchange_n<5>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 6: return launch_exchange_n<6>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 7: return launch_exchange_n<7>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 8: return launch_exchange_n<8>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 9: return launch_exchange_n<9>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 10: return launch_exchange_n<10>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 11: return launch_exchange_n<11>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
+    case 12: return launch_exchange_n<12>(P, u, part, c, epoch, apply_mask, st, nparts, e_sig,
+                                        sig_part, sig_count, base, mode, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -308,8 +308,14 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
   };
   std::vector<SP> sps;
 
+  p.f_start.assign(p.nloc + 1, 0);
+  p.e_start.assign(p.nloc + 1, 0);
+  p.v_start.assign(p.nloc + 1, 0);
   for (int64_t el = 0; el < p.nloc; el++) {
     const int64_t e = p.e_lo + el;
+    p.f_start[el] = (int32_t)p.nF;
+    p.e_start[el] = (int32_t)p.nEd;
+    p.v_start[el] = (int32_t)p.nV;
     int64_t c[3];
     ecoords(m, e, c);
     uint8_t bm = 0;
@@ -408,6 +414,10 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
       }
     }
   }
+
+  p.f_start[p.nloc] = (int32_t)p.nF;
+  p.e_start[p.nloc] = (int32_t)p.nEd;
+  p.v_start[p.nloc] = (int32_t)p.nV;
 
   // shared points: ascending gid; per neighbour buffers in that order
   std::sort(sps.begin(), sps.end(), [](const SP& a, const SP& b) { return a.gid < b.gid; });

@@ -40,6 +40,9 @@ struct HostPlan {
   std::vector<uint8_t> e_axis, e_nin, e_mask;
   std::vector<int32_t> v_base;            // [8][nV]
   std::vector<uint8_t> v_nin, v_mask;
+  // entities are created by their smallest local element, in element order:
+  // element el created faces [f_start[el], f_start[el+1]) (likewise edges, vertices)
+  std::vector<int32_t> f_start, e_start, v_start;   // [nloc + 1]
   // shared points (some incidence on another rank), ascending gid
   int64_t nS = 0;
   std::vector<int64_t> s_gid;

@@ -123,6 +123,26 @@ def test_apply_is_deterministic_and_variants_agree_bitwise():
             assert np.array_equal(outs[0], o)
 
 
+@pytest.mark.parametrize("N", [1, 3, 7])
+@pytest.mark.parametrize("mode", [1, 2], ids=["flat", "chunks"])
+def test_gs_schedules_bit_exact(N, mode):
+    """Both rank-local gs schedules (SEM_OPT_GS_MODE) give the oracle's sums
+    bit for bit; the chunk counter carries across calls without a reset."""
+    spec = tgv_box(9, 7, 6, deform=1)
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=11)
+    ref_gs, ref_ap = o.gs(u), o.apply(u)
+    with sem().sem_setup(spec, N) as c:
+        c.set_gs_mode(mode)
+        w = c.zeros()
+        for _ in range(3):
+            g = dev(u)
+            c.gs(g)
+            assert np.array_equal(host(g), ref_gs)
+            c.apply(dev(u), w)
+            assert nrel(host(w), ref_ap) <= 1e-12
+
+
 @pytest.mark.parametrize("N", [2, 4, 6, 8, 10])
 def test_odd_n_ring_wrap(N):
     """More elements than resident CTAs, so every CTA cycles through both u

@@ -74,13 +74,19 @@ def op_rates(c, N, st, reps, tri):
     w = c.zeros()
     fb, bax, baxgs = bytes_model(N)
     res = {}
-    for name, fn, bpp in (("ax", lambda: c.ax(u, w), bax), ("ax_gs", lambda: c.apply(u, w), baxgs)):
+
+    cases = [("ax", lambda: c.ax(u, w), bax, 0), ("ax_gs", lambda: c.apply(u, w), baxgs, 0),
+             ("ax_gs_flat", lambda: c.apply(u, w), baxgs, 1),
+             ("ax_gs_chunks", lambda: c.apply(u, w), baxgs, 2)]
+    for name, fn, bpp, mode in cases:
+        c.set_gs_mode(mode)
         ms = timed(fn, st, reps)
         gbs = bpp * n / (ms * 1e-3) / 1e9
         res[name] = {"ms": round(ms, 4), "gdofs": round(n / (ms * 1e-3) / 1e9, 2),
                      "useful_GBps": round(gbs, 0), "frac_nominal": round(gbs / NOMINAL, 3),
                      "frac_copy": round(gbs / peak_copy(), 3),
                      "frac_triad": round(gbs / tri, 3) if tri else None}
+    c.set_gs_mode(0)
     del u, w
     return res
 
@@ -210,5 +216,14 @@ if __name__ == "__main__":
         strong()
     elif mode == "sweep":
         sweep([int(v) for v in sys.argv[2].split(",")])
+    elif mode == "ops":   # Ax / Ax+gs rates (all gs schedules) on named configs
+        torch.cuda.set_device(0)
+        st0 = torch.cuda.current_stream()
+        tri0 = triad(st0)
+        for cfg in sys.argv[2].split(","):
+            spec, N = CONFIGS[cfg]
+            with sem.sem_setup(spec, N, stream=st0.cuda_stream) as c:
+                out({"what": f"{cfg}_ops", "n_p": c.n_local, **op_rates(c, N, st0, 50, tri0)})
+            torch.cuda.empty_cache()
     else:
         single()

@@ -47,10 +47,11 @@ def main():
             o = O.Oracle(spec, N, nranks=P)
         u = random_field(E * n3, seed=100 + ci)
         ul = np.ascontiguousarray(u[lo * n3:hi * n3])
-        for fused, p2p in ((False, True), (True, True), (False, False)):
+        for fused, p2p, gsm in ((False, True, 0), (False, True, 2), (True, True, 0), (False, False, 2)):
             with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm) as c:
                 c.set_fused_gs(fused)
                 c.set_p2p(p2p)
+                c.set_gs_mode(gsm)
                 assert c.n_local == (hi - lo) * n3
                 du = torch.from_numpy(ul).cuda()
                 w = c.zeros()
@@ -73,7 +74,7 @@ def main():
                     B = np.concatenate([p[2] for p in parts])
                     Xs = np.concatenate([p[3] for p in parts])
                     ref_w = o.apply(u)
-                    tag = f"case{ci} P={P} fused={fused} p2p={p2p}"
+                    tag = f"case{ci} P={P} fused={fused} p2p={p2p} gs_mode={gsm}"
                     e = np.abs(W - ref_w).max() / np.abs(ref_w).max()
                     if not e <= 1e-12:
                         fails.append(f"{tag}: apply rel err {e:.2e}")
