@@ -66,6 +66,12 @@ def lib():
         L.oracle_pcg.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int,
                                  C.POINTER(C.c_int), C.POINTER(C.c_double),
                                  C.POINTER(C.c_double), C.c_void_p]
+        L.oracle_helm_apply.argtypes = [C.c_void_p, C.c_double, C.c_double, _D, _D]
+        L.oracle_rhs_mass.argtypes = [C.c_void_p, _D, _D]
+        L.oracle_helm_dinv.argtypes = [C.c_void_p, C.c_double, C.c_double, _D]
+        L.oracle_helm_pcg.argtypes = [C.c_void_p, C.c_double, C.c_double, _D, _D, C.c_double,
+                                      C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.c_void_p]
         L.oracle_plan.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 3 + [C.c_void_p] * 3
         L.oracle_shared.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                     C.c_void_p]
@@ -192,6 +198,33 @@ class Oracle:
                               C.byref(rt), hist.ctypes.data_as(C.c_void_p))
         if st < 0:
             raise OracleError(f"oracle_pcg failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
+                "status": st, "hist": hist[: it.value + 1]}
+
+    # ---- NEXT-2: Helmholtz h1 A + h2 B
+    def helm_apply(self, h1: float, h2: float, u):
+        w = np.zeros(self.nslots)
+        assert lib().oracle_helm_apply(self._h, h1, h2, _f64(u), w) == 0
+        return w
+
+    def rhs_mass(self, f):
+        b = np.zeros(self.nslots)
+        assert lib().oracle_rhs_mass(self._h, _f64(f), b) == 0
+        return b
+
+    def helm_dinv(self, h1: float, h2: float):
+        d = np.zeros(self.nslots)
+        assert lib().oracle_helm_dinv(self._h, h1, h2, d) == 0
+        return d
+
+    def helm_pcg(self, h1: float, h2: float, b, tol: float, maxit: int):
+        x = np.zeros(self.nslots)
+        it, rf, rt = C.c_int(), C.c_double(), C.c_double()
+        hist = np.zeros(maxit + 1)
+        st = lib().oracle_helm_pcg(self._h, h1, h2, _f64(b), x, tol, maxit, C.byref(it),
+                                   C.byref(rf), C.byref(rt), hist.ctypes.data_as(C.c_void_p))
+        if st < 0:
+            raise OracleError(f"oracle_helm_pcg failed with status {st}")
         return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
                 "status": st, "hist": hist[: it.value + 1]}
 

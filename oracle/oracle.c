@@ -531,6 +531,44 @@ int oracle_rhs(const oracle_ctx* c, const double* f, double* b) {
   return 0;
 }
 
+/* NEXT-2: the Helmholtz operator of the velocity solves (P:L257
+   "followed by a Helmholtz equation for each velocity components"; S:L294-302
+   "h1*(stiffness action) + h2*(mass action), then gather-scatter add"), with
+   the Dirichlet mask as for the Poisson operator (reading Q8):
+   w = mask(QQ^T (h1 A_L u + h2 B_L u)). */
+int oracle_helm_apply(const oracle_ctx* c, double h1, double h2, const double* u, double* w) {
+  int st = oracle_ax(c, u, w);
+  if (st) return st;
+  for (int64_t l = 0; l < c->nslots; l++) w[l] = h1 * w[l] + h2 * (c->B[l] * u[l]);
+  oracle_gs(c, w);
+  return oracle_mask_apply(c, w);
+}
+
+/* b = mask(QQ^T (B .* f)) without the periodic projection (reading Q12): the
+   right-hand side of the Helmholtz system, nonsingular for h2 > 0. */
+int oracle_rhs_mass(const oracle_ctx* c, const double* f, double* b) {
+  if (!c) return -1;
+  for (int64_t l = 0; l < c->nslots; l++) b[l] = c->B[l] * f[l];
+  oracle_gs(c, b);
+  return oracle_mask_apply(c, b);
+}
+
+/* Jacobi for the Helmholtz operator (reading Q14 applied to h1 A + h2 B):
+   d = QQ^T (h1 diag(A_L) + h2 B_L), dinv = 0 on masked slots, else 1/d. */
+int oracle_helm_dinv(const oracle_ctx* c, double h1, double h2, double* dinv) {
+  if (!c) return -1;
+  oracle_diag_raw(c->E, c->N, c->D, c->G, dinv);
+  for (int64_t l = 0; l < c->nslots; l++) dinv[l] = h1 * dinv[l] + h2 * c->B[l];
+  oracle_gs(c, dinv);
+  for (int64_t l = 0; l < c->nslots; l++) dinv[l] = c->mask[l] ? 0.0 : 1.0 / dinv[l];
+  return 0;
+}
+
+/* operator of the PCG: helm = 0 -> Poisson (oracle_apply), 1 -> Helmholtz */
+static int op_apply(const oracle_ctx* c, int helm, double h1, double h2, const double* u, double* w) {
+  return helm ? oracle_helm_apply(c, h1, h2, u, w) : oracle_apply(c, u, w);
+}
+
 /* P:L257 "preconditioned Conjugate Gradient (CG) ... with a block Jacobi
    preconditioner", written step by step (readings Q14-Q17):
    x0 = 0; r = b; z = M^-1 r; p = z; rho = <r,z>_c
@@ -538,8 +576,9 @@ int oracle_rhs(const oracle_ctx* c, const double* f, double* b) {
      x += alpha p; r -= alpha w; gamma = <r,r>_c; stop if sqrt(gamma) <= tol;
      z = M^-1 r; rho' = <r,z>_c; beta = rho'/rho; rho = rho'; p = z + beta p.
    hist[k] = sqrt(gamma) after iteration k (hist[0] = ||b||_c). */
-int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
-               int* iters, double* res_final, double* res_true, double* hist) {
+static int pcg_core(const oracle_ctx* c, int helm, double h1, double h2, const double* dinv,
+                    const double* b, double* x, double tol, int maxit, int* iters,
+                    double* res_final, double* res_true, double* hist) {
   if (!c || maxit < 0) return -1;
   int64_t ns = c->nslots;
   double* r = (double*)malloc(sizeof(double) * ns);
@@ -551,7 +590,7 @@ int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int 
   for (int64_t l = 0; l < ns; l++) {
     x[l] = 0.0;
     r[l] = b[l];
-    z[l] = c->dinv[l] * r[l];
+    z[l] = dinv[l] * r[l];
     p[l] = z[l];
   }
   double rho = oracle_dot_c(c, r, z);
@@ -560,7 +599,7 @@ int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int 
   if (sqrt(gamma) <= tol) status = 0;
   while (status == 1 && k < maxit) {
     k++;
-    oracle_apply(c, p, w);
+    op_apply(c, helm, h1, h2, p, w);
     double sigma = oracle_dot_c(c, p, w);
     if (!(sigma > 0.0)) { status = -6; break; }
     double alpha = rho / sigma;
@@ -571,7 +610,7 @@ int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int 
     gamma = oracle_dot_c(c, r, r);
     if (hist) hist[k] = sqrt(gamma);
     if (sqrt(gamma) <= tol) { status = 0; break; }
-    for (int64_t l = 0; l < ns; l++) z[l] = c->dinv[l] * r[l];
+    for (int64_t l = 0; l < ns; l++) z[l] = dinv[l] * r[l];
     double rho_new = oracle_dot_c(c, r, z);
     double beta = rho_new / rho;
     rho = rho_new;
@@ -580,12 +619,31 @@ int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int 
   if (iters) *iters = k;
   if (res_final) *res_final = sqrt(gamma);
   if (res_true) {
-    oracle_apply(c, x, w);
+    op_apply(c, helm, h1, h2, x, w);
     for (int64_t l = 0; l < ns; l++) w[l] = b[l] - w[l];
     *res_true = sqrt(oracle_dot_c(c, w, w));
   }
   free(r); free(z); free(p); free(w);
   return status;
+}
+
+int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+               int* iters, double* res_final, double* res_true, double* hist) {
+  if (!c) return -1;
+  return pcg_core(c, 0, 0.0, 0.0, c->dinv, b, x, tol, maxit, iters, res_final, res_true, hist);
+}
+
+/* the same PCG on h1 A + h2 B with its own Jacobi diagonal (oracle_helm_dinv) */
+int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, double* x,
+                    double tol, int maxit, int* iters, double* res_final, double* res_true,
+                    double* hist) {
+  if (!c) return -1;
+  double* dinv = (double*)malloc(sizeof(double) * c->nslots);
+  if (!dinv) return -5;
+  oracle_helm_dinv(c, h1, h2, dinv);
+  int st = pcg_core(c, 1, h1, h2, dinv, b, x, tol, maxit, iters, res_final, res_true, hist);
+  free(dinv);
+  return st;
 }
 
 /* ------------------------------------------------------------------ */

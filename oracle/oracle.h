@@ -69,6 +69,14 @@ int oracle_pcg(const oracle_ctx* c, const double* b, double* x, double tol, int 
 
 /* canonical gs plan (reading Q11): pairs (l_a<l_b) sorted by l_a, segments
    (>=3 slots, ascending) sorted by first slot. Call with NULL arrays to size. */
+/* NEXT-2 Helmholtz h1 A + h2 B: operator, mass RHS without
+   the periodic projection, Jacobi inverse diagonal, and the same PCG on it. */
+int oracle_helm_apply(const oracle_ctx* c, double h1, double h2, const double* u, double* w);
+int oracle_rhs_mass(const oracle_ctx* c, const double* f, double* b);
+int oracle_helm_dinv(const oracle_ctx* c, double h1, double h2, double* dinv);
+int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, double* x,
+                    double tol, int maxit, int* iters, double* res_final, double* res_true,
+                    double* hist);
 int oracle_plan(const oracle_ctx* c, int64_t* npairs, int64_t* nseg, int64_t* nsegslots,
                 int64_t* pairs, int64_t* seg_off, int64_t* seg_slot);
 /* gids shared between ranks r and q (r != q), ascending; NULL list to size. */
