@@ -2,9 +2,10 @@
 """Benchmark of the B200-native SEM pressure-Poisson hot path.
 
 A "step" is one Jacobi-PCG iteration over the whole hot path:
-fused Ax+gs+mask with <p,Ap>, the NCCL exchange of shared
-entities (Alg. 1) and allreduce (N > 1), the x/r update with <r,z>_c and
-<r,r>_c, the convergence test and the p update.
+Ax+mask with <p,Ap> fused, the gather-scatter (with, for N > 1,
+the NVLink peer-memory exchange of shared entities, Alg. 1, and the allreduce),
+the r update with <r,z>_c and <r,r>_c, the convergence test and the x and p
+updates.
 
 Workload (BASELINE.json configs[1]): the 8192-element Cartesian box (32x16x16
 elements, N=7, all 6 geometric factors stored and streamed, BP5 convention)
@@ -270,7 +271,7 @@ def main():
     assert res["iters"] == args.steps, res
     value = n_p_total * args.steps / (t_ms / 1e3) / 1e9
 
-    # ---- dominant kernel (fused Ax+gs), CUDA events on the context stream
+    # ---- dominant kernel (Ax + mask + sigma), CUDA events on the context stream
     ctx.timing(True)
     ctx.pcg_solve(b, x, 0.0, args.steps)
     k_ms, k_cnt = ctx.timing_read(0)
@@ -362,9 +363,11 @@ def main():
                 "workload": (f"{args.config}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU "
                              f"(box stacked x{P} along z), N={N}, periodic, all 6 G stored"),
                 "N": N, "elements": spec.E, "n_p": n_p_total, "n_glob": ctx.n_glob,
-                "step": "one Jacobi-PCG iteration (fused Ax+gs+mask+<p,Ap>, update+dots, p)",
+                "step": "one Jacobi-PCG iteration (Ax+mask+<p,Ap>, gs [+ NVLink exchange], "
+                        "r update+dots, x/p update)",
                 "l2": "no flush: per-iteration working set ~370 MB/GPU > 126 MB L2",
-                "parallelism": f"element z-slabs x{P}, NCCL gs exchange + allreduce",
+                "parallelism": (f"element z-slabs x{P}, NVLink peer-memory gs exchange + "
+                                "allreduce (CUDA IPC)") if P > 1 else "single GPU",
             },
             "pcg_iter_per_s": args.steps / (t_ms / 1e3),
             "ax_gs": {

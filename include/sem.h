@@ -104,6 +104,19 @@ typedef struct {
 } sem_pcg_result;
 int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                   sem_pcg_result* res);
+/* NEXT-2: the Helmholtz operator of the velocity solves, h1 A + h2 B (P:L257
+   "followed by a Helmholtz equation for each velocity component").
+   sem_helm_apply: w = mask(QQ^T (h1 A_L u + h2 B_L u)) for any local u (B_L the
+   diagonal GLL mass); asynchronous, like sem_apply.  sem_rhs_mass: b =
+   mask(QQ^T (B .* f)) WITHOUT the periodic mean projection of sem_rhs (the
+   Helmholtz system is nonsingular for h2 > 0).  sem_helm_pcg_solve: Jacobi-PCG
+   on h1 A + h2 B (h1, h2 >= 0, not both 0) with the exact assembled diagonal
+   QQ^T(h1 diag(A_L) + h2 B_L) (cached per (h1, h2)); same contract, status
+   codes and result as sem_pcg_solve.  Always the two-kernel operator. */
+int sem_helm_apply(sem_ctx* c, double h1, double h2, const double* u, double* w);
+int sem_rhs_mass(sem_ctx* c, const double* f, double* b);
+int sem_helm_pcg_solve(sem_ctx* c, double h1, double h2, const double* b, double* x,
+                       double tol, int32_t maxit, sem_pcg_result* r);
 int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_host, double tol,
                        int32_t maxit, sem_pcg_result* res);
 /* recursive residual history of the last solve: hist[k] after k iterations */
@@ -153,6 +166,15 @@ int sem_launch_count(const sem_ctx* c, int64_t* n);
    of the last peer-memory exchange kernel, [5][2048] (phases: start, packed,
    local gs done, unpack done, end; 0 for absent blocks) */
 int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n);
+/* Interconnect probes for the performance model (nranks > 1 with
+   peer-memory mailboxes).  sem_p2p_pingpong: collective between this rank and
+   `peer` (both call it with the same iters); the lower rank writes `iters`
+   round-trip times (ns, one flag each way through the mailboxes) into host
+   rtt_ns.  sem_p2p_write_bw: one-sided, writes `bytes` of zeros into the peer's
+   receive area `reps` times with 16-B stores and returns GB/s; do not call
+   while an exchange with that peer is in flight.  Both block. */
+int sem_p2p_pingpong(sem_ctx* c, int peer, int iters, int64_t* rtt_ns);
+int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps);
 /* Operator variants (both compute the same w; results are bit-identical):
    SEM_OPT_FUSED_GS = 1 -> gather-scatter fused into the Ax kernel (last
    arriver per face/edge/vertex sums it); 0 (default) -> Ax kernel with the

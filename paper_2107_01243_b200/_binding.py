@@ -53,6 +53,10 @@ _SIGS = {
     "sem_coords": [_P, _P, _P, _P],
     "sem_pcg_solve": [_P, _P, _P, C.c_double, C.c_int32, C.POINTER(PcgResult)],
     "sem_pcg_solve_host": [_P, _P, _P, C.c_double, C.c_int32, C.POINTER(PcgResult)],
+    "sem_helm_apply": [_P, C.c_double, C.c_double, _P, _P],
+    "sem_rhs_mass": [_P, _P, _P],
+    "sem_helm_pcg_solve": [_P, C.c_double, C.c_double, _P, _P, C.c_double, C.c_int32,
+                           C.POINTER(PcgResult)],
     "sem_pcg_history": [_P, _P, C.c_int32, C.POINTER(C.c_int32)],
     "sem_export_field": [_P, C.c_int, _P],
     "sem_export_int": [_P, C.c_int, _P],
@@ -72,6 +76,8 @@ _SIGS = {
     "sem_launch_count": [_P, _I64P],
     "sem_set_option": [_P, C.c_int, C.c_int],
     "sem_debug_read": [_P, C.c_int, _P, C.c_int],
+    "sem_p2p_pingpong": [_P, C.c_int, C.c_int, _P],
+    "sem_p2p_write_bw": [_P, C.c_int, C.c_int64, C.c_int, _P],
 }
 
 
@@ -201,6 +207,21 @@ class Context:
         return {"iters": r.iters, "status": r.status, "res_final": r.res_final,
                 "res_true": r.res_true}
 
+    # ---- NEXT-2: Helmholtz h1 A + h2 B
+    def helm_apply(self, h1, h2, u, w):
+        _check(load().sem_helm_apply(self._h, float(h1), float(h2), self._f64(u), self._f64(w)))
+
+    def rhs_mass(self, f, b):
+        _check(load().sem_rhs_mass(self._h, self._f64(f), self._f64(b)))
+
+    def helm_pcg_solve(self, h1, h2, b, x, tol, maxit):
+        r = PcgResult()
+        _check(load().sem_helm_pcg_solve(self._h, float(h1), float(h2), self._f64(b), self._f64(x),
+                                         float(tol), int(maxit), C.byref(r)),
+               allow=(SEM_OK, SEM_NOT_CONVERGED))
+        return {"iters": r.iters, "status": r.status, "res_final": r.res_final,
+                "res_true": r.res_true}
+
     def pcg_solve_host(self, b_host: np.ndarray, x_host: np.ndarray, tol, maxit):
         """End-to-end entry point: HOST b in, HOST x out (copies inside libsem)."""
         assert b_host.dtype == np.float64 and x_host.dtype == np.float64
@@ -263,6 +284,17 @@ class Context:
         out = np.zeros(n, dtype=np.int64)
         _check(load().sem_debug_read(self._h, which, C.c_void_p(out.ctypes.data), n))
         return out
+
+    def p2p_pingpong(self, peer: int, iters: int) -> np.ndarray:
+        """Collective with `peer`: round-trip ns samples (returned on the lower rank)."""
+        out = np.zeros(iters, dtype=np.int64)
+        _check(load().sem_p2p_pingpong(self._h, peer, iters, C.c_void_p(out.ctypes.data)))
+        return out
+
+    def p2p_write_bw(self, peer: int, nbytes: int, reps: int = 20) -> float:
+        g = C.c_double()
+        _check(load().sem_p2p_write_bw(self._h, peer, int(nbytes), reps, C.byref(g)))
+        return g.value
 
     def launch_count(self) -> int:
         n = C.c_int64()

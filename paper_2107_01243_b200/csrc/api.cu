@@ -86,6 +86,11 @@ struct sem_ctx {
   unsigned long long* d_gsctr = nullptr;   // gs chunk counters (never reset)
   uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
   int gs_mode = 0;                         // SEM_OPT_GS_MODE
+  // Helmholtz (NEXT-2): operator in use by apply_op / pcg_run, and its Jacobi cache
+  bool helm = false;
+  double h1 = 1.0, h2 = 0.0;
+  double* d_dinv_helm = nullptr;
+  double helm_key[2] = {0.0, -1.0};
   int32_t *d_sslot = nullptr, *d_soff = nullptr;
   uint8_t *d_snloc = nullptr, *d_snr = nullptr, *d_smask = nullptr, *d_smult = nullptr;
   int8_t* d_srank = nullptr;
@@ -123,6 +128,7 @@ struct sem_ctx {
   int* d_perr = nullptr;
   std::vector<char*> ipc_opened;
   uint64_t ep_gs = 0, ep_ar[sem::P2P::kSites] = {0, 0, 0, 0};
+  std::vector<uint64_t> ep_ping;   // per peer: ping-pong flag epochs
   uint64_t cur_e_sig = 0;   // sigma epoch published by the last PCG apply
 };
 
@@ -193,6 +199,9 @@ int check(cudaError_t e, const char* what) {
 }
 
 // ---- the operator ----------------------------------------------------------
+// the fused Ax+gs operator is in use (the Helmholtz variant is two-kernel only)
+bool fused(const sem_ctx* c) { return c->fuse_gs && !c->helm; }
+
 int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi, int r1lo,
            int r1hi, double* red_out) {
   sem::AxLaunch a{};
@@ -206,10 +215,14 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.red_out = red_out;
   a.done = &c->d_st->done;
   std::copy(c->hp.D.begin(), c->hp.D.end(), a.Dm);
+  a.B = c->d_B;
+  a.h1 = c->h1;
+  a.h2 = c->h2;
   const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
   const int groups = std::max(ng, 1);   // the launcher caps the grid at residency
   int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
-  cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream, c->fuse_gs);
+  cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream, fused(c),
+                                 c->helm && mode != sem::AX_ONLY);
   timer_end(c, tk);
   c->launches++;
   return check(e, "ax kernel");
@@ -234,7 +247,7 @@ int exchange(sem_ctx* c) {
 // rank-local gather-scatter pass of the two-kernel operator (masked slots are
 // already zero, so every masked entity point sums to zero)
 int gs_pass(sem_ctx* c, double* w) {
-  if (c->fuse_gs) return SEM_OK;
+  if (fused(c)) return SEM_OK;
   int tk = timer_begin(c, 4);
   cudaError_t e = sem::launch_gs_local(c->dp, w, 0, &c->gs_base[0], c->gs_mode, c->stream);
   timer_end(c, tk);
@@ -243,6 +256,7 @@ int gs_pass(sem_ctx* c, double* w) {
 }
 
 bool p2p(const sem_ctx* c) { return c->p2p_ok && c->use_p2p; }
+
 
 // global sum of K device doubles (this rank's partials at loc) into glob:
 // NVLink mailboxes (publish + rank-ordered sum) or NCCL allreduce
@@ -263,7 +277,7 @@ int allreduce_site(sem_ctx* c, int site, const double* loc, double* glob, int K)
 int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   const sem::HostPlan& h = c->hp;
   sem::PcgState* st = c->d_st;
-  if (h.nranks > 1 && h.nS > 0 && p2p(c) && !c->fuse_gs && !c->overlap) {
+  if (h.nranks > 1 && h.nS > 0 && p2p(c) && !fused(c) && !c->overlap) {
     // one Ax launch, then ONE exchange kernel: pack into the neighbours'
     // receive buffers, rank-local gs while the partials travel, unpack
     const uint64_t e = ++c->ep_gs;
@@ -397,7 +411,7 @@ void free_ctx(sem_ctx* c) {
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
                   c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank, c->d_fst, c->d_est,
-                  c->d_vst, c->d_gsctr};
+                  c->d_vst, c->d_gsctr, c->d_dinv_helm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -424,7 +438,8 @@ int p2p_setup(sem_ctx* c) {
   cudaStream_t s = c->stream;
   if (P > sem::P2P::kMaxP) return SEM_OK;
   // receive entries: 16-byte records, two epoch parities each
-  const size_t bytes = sem::P2P::kRecvOff + ((size_t)h.nbuf + 1) * 2 * 16;
+  const size_t bytes =
+      sem::P2P::kRecvOff + (size_t)std::max<int64_t>(h.nbuf + 1, sem::P2P::kMinRecv) * 2 * 16;
   SEM_TRY(dalloc(&c->d_mbox, bytes));
   CUDA_TRY(cudaMemsetAsync(c->d_mbox, 0, bytes, s));
   cudaIpcMemHandle_t mine;
@@ -488,6 +503,7 @@ int p2p_setup(sem_ctx* c) {
   p.P = P; p.me = me; p.nnbr = (int)h.nbr_rank.size();
   p.local = c->d_mbox; p.peers = c->d_peers; p.rdelta = c->d_rdelta; p.nbrs = c->d_nbrs;
   p.err = c->d_perr;
+  c->ep_ping.assign(P, 0);
   c->p2p_ok = true;
   return SEM_OK;
 }
@@ -697,7 +713,7 @@ extern "C" int sem_coords(sem_ctx* c, double* X, double* Y, double* Z) {
 
 extern "C" int sem_rhs(sem_ctx* c, const double* f, double* b) {
   if (!c || !f || !b) { sem::set_error("sem_rhs: NULL argument"); return SEM_EINVAL; }
-  CUDA_TRY(sem::launch_scale(c->d_B, f, b, c->hp.n_local, c->stream));
+  CUDA_TRY(sem::launch_scale_mask(c->dp, c->d_B, f, b, c->stream));
   c->launches++;
   SEM_TRY(gs_op(c, b, 1));
   if (c->hp.fully_periodic) {
@@ -723,13 +739,14 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   std::memcpy(c->h_st, &init, sizeof(init));   // h_st is idle: every solve ends synchronised
   CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
   const bool dist = c->hp.nranks > 1;
+  const double* dinv = c->helm ? c->d_dinv_helm : c->d_dinv;   // Jacobi of the operator in use
   double* rg_out = dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   // peer-memory allreduces fused into the CG kernels (nranks > 1 with NVLink mailboxes)
   const bool pp = p2p(c);
   sem::PeerSync ps;
   if (pp) ps.c = c->p2p;
   ps.e_pub = ps.e_wait = pp ? ++c->ep_ar[sem::AR_RG] : 0;
-  CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, c->d_dinv, b, x, c->d_r, c->d_p, c->d_partial,
+  CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, dinv, b, x, c->d_r, c->d_p, c->d_partial,
                                st, rg_out, ps, c->red_grid, s));
   if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
   CUDA_TRY(sem::launch_cg_start(st, c->d_hist, ps, s));
@@ -746,13 +763,13 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
         psu.e_pub = psp.e_wait = ++c->ep_ar[sem::AR_RG];
       }
       int tk = timer_begin(c, 1);
-      CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, c->d_dinv, c->d_r, c->d_wv,
+      CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv,
                                      c->d_partial, st, rg_out, dist ? nullptr : c->d_partial_ax,
                                      c->d_nsig, psu, c->red_grid, s));
       timer_end(c, tk);
       if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
       tk = timer_begin(c, 2);
-      CUDA_TRY(sem::launch_cg_p(c->dp, c->d_dinv, c->d_r, c->d_p, x, st, c->d_hist, psp,
+      CUDA_TRY(sem::launch_cg_p(c->dp, dinv, c->d_r, c->d_p, x, st, c->d_hist, psp,
                                 c->red_grid, s));
       timer_end(c, tk);
       c->launches += 2;
@@ -805,6 +822,68 @@ extern "C" int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol,
     sem::set_error("sem_pcg_solve: bad arguments");
     return SEM_EINVAL;
   }
+  return pcg_run(c, b, x, tol, maxit, res);
+}
+
+// ---------------------------------------------------------------- NEXT-2: Helmholtz
+// h1 A + h2 B (P:L257 velocity solves); the context switches to
+// the Helmholtz operator for the duration of one call
+struct HelmScope {
+  sem_ctx* c;
+  HelmScope(sem_ctx* ctx, double h1, double h2) : c(ctx) {
+    c->helm = true;
+    c->h1 = h1;
+    c->h2 = h2;
+  }
+  ~HelmScope() {
+    c->helm = false;
+    c->h1 = 1.0;
+    c->h2 = 0.0;
+  }
+};
+
+extern "C" int sem_helm_apply(sem_ctx* c, double h1, double h2, const double* u, double* w) {
+  if (!c || !u || !w || !aligned16(u) || !aligned16(w) || u == w) {
+    sem::set_error("sem_helm_apply: bad arguments (NULL, misaligned or aliased pointers)");
+    return SEM_EINVAL;
+  }
+  HelmScope hs(c, h1, h2);
+  return apply_op(c, u, w, sem::AX_APPLY);
+}
+
+extern "C" int sem_rhs_mass(sem_ctx* c, const double* f, double* b) {
+  if (!c || !f || !b) { sem::set_error("sem_rhs_mass: NULL argument"); return SEM_EINVAL; }
+  CUDA_TRY(sem::launch_scale_mask(c->dp, c->d_B, f, b, c->stream));
+  c->launches++;
+  return gs_op(c, b, 1);
+}
+
+// Jacobi of h1 A + h2 B: dinv = mask ? 0 : 1 / QQ^T(h1 diag(A_L) + h2 B_L), cached per (h1, h2)
+static int helm_jacobi(sem_ctx* c, double h1, double h2) {
+  if (c->d_dinv_helm && c->helm_key[0] == h1 && c->helm_key[1] == h2) return SEM_OK;
+  if (!c->d_dinv_helm) SEM_TRY(dalloc(&c->d_dinv_helm, (size_t)c->hp.n_local));
+  CUDA_TRY(sem::launch_diag(c->dp, c->d_G, c->d_dinv_helm, c->stream));
+  CUDA_TRY(sem::launch_helm_diag(c->d_dinv_helm, c->d_B, h1, h2, c->hp.n_local, c->stream));
+  SEM_TRY(gs_op(c, c->d_dinv_helm, 0));
+  CUDA_TRY(sem::launch_invert_mask(c->dp, c->d_dinv_helm, c->stream));
+  c->launches += 3;
+  c->helm_key[0] = h1;
+  c->helm_key[1] = h2;
+  return SEM_OK;
+}
+
+extern "C" int sem_helm_pcg_solve(sem_ctx* c, double h1, double h2, const double* b, double* x,
+                                  double tol, int32_t maxit, sem_pcg_result* res) {
+  if (!c || !b || !x || !aligned16(b) || !aligned16(x) || b == x) {
+    sem::set_error("sem_helm_pcg_solve: bad arguments");
+    return SEM_EINVAL;
+  }
+  if (!(h1 >= 0.0) || !(h2 >= 0.0) || (h1 == 0.0 && h2 == 0.0)) {
+    sem::set_error("sem_helm_pcg_solve: need h1 >= 0, h2 >= 0, not both 0");
+    return SEM_EINVAL;
+  }
+  SEM_TRY(helm_jacobi(c, h1, h2));
+  HelmScope hs(c, h1, h2);
   return pcg_run(c, b, x, tol, maxit, res);
 }
 
@@ -945,6 +1024,53 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   }
   sem::set_error("sem_set_option: unknown option");
   return SEM_EINVAL;
+}
+
+extern "C" int sem_p2p_pingpong(sem_ctx* c, int peer, int iters, int64_t* rtt_ns) {
+  if (!c || !rtt_ns || iters < 1) return SEM_EINVAL;
+  if (!c->p2p_ok || peer < 0 || peer >= c->hp.nranks || peer == c->hp.rank) {
+    sem::set_error("sem_p2p_pingpong: needs peer-memory mailboxes and a peer rank != self");
+    return SEM_EINVAL;
+  }
+  long long* d = nullptr;
+  SEM_TRY(dalloc(&d, (size_t)iters));
+  cudaError_t e = sem::launch_p2p_pingpong(c->p2p, peer, iters, c->ep_ping[peer], d, c->stream);
+  c->ep_ping[peer] += (uint64_t)iters;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && c->hp.rank < peer)
+    e = cudaMemcpy(rtt_ns, d, sizeof(long long) * iters, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  CUDA_TRY(e);
+  return p2p_check(c);
+}
+
+extern "C" int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps) {
+  if (!c || !gbps || bytes < 16 || reps < 1) return SEM_EINVAL;
+  if (!c->p2p_ok || peer < 0 || peer >= c->hp.nranks) {
+    sem::set_error("sem_p2p_write_bw: needs peer-memory mailboxes");
+    return SEM_EINVAL;
+  }
+  const int64_t n = bytes / 16 * 2;   // doubles (even)
+  double* src = nullptr;
+  SEM_TRY(dalloc(&src, (size_t)n));
+  // zeros: the receive entries stay in their initial (flag 0) state
+  CUDA_TRY(cudaMemsetAsync(src, 0, sizeof(double) * n, c->stream));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  CUDA_TRY(sem::launch_p2p_write(c->p2p, peer, src, n, sem::P2P::kMinRecv * 4, 1, c->stream));
+  cudaEventRecord(e0, c->stream);
+  cudaError_t e = sem::launch_p2p_write(c->p2p, peer, src, n, sem::P2P::kMinRecv * 4, reps, c->stream);
+  cudaEventRecord(e1, c->stream);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(src);
+  CUDA_TRY(e);
+  *gbps = (double)n * 8.0 * reps / (ms * 1e-3) / 1e9;
+  return SEM_OK;
 }
 
 extern "C" int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n) {

@@ -159,7 +159,7 @@ __device__ __forceinline__ void sum_point(double* __restrict__ w, const int32_t*
     if (t < nin) __stcg(&w[base[t] + off], s);
 }
 
-template <int n, int MODE, bool FUSE>
+template <int n, int MODE, bool FUSE, bool HELM = false>
 __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     ax_kernel(const DevPlan P, const AxLaunch a) {
   using Sh = AxShape<n, FUSE>;
@@ -426,7 +426,15 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
         Dj[m] = kDreg ? sD[j * dp + m] : 0.0;
       }
 
-      double ru[n], rw[n];
+      // Helmholtz: this thread's mass column (coalesced per plane), prefetched into
+      // registers where they are free (else loaded by the epilogue; no spills either way)
+      constexpr bool kBpre = HELM && (n <= 3 || (n >= 5 && n <= 9));
+      double ru[n], rw[n], rb[kBpre ? n : 1];
+      const double* Bc = HELM ? a.B + (size_t)(e0 + el) * n3 + ij : nullptr;
+      if (kBpre) {
+#pragma unroll
+        for (int k = 0; k < n; k++) rb[kBpre ? k : 0] = active ? __ldg(Bc + n2 * k) : 0.0;
+      }
 #pragma unroll
       for (int k = 0; k < n; k++) {
         ru[k] = active ? sUe[ij + n2 * k] : 0.0;
@@ -495,6 +503,8 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
             v = fma(kDtreg ? Dti[m] : sDt[i * dp + m], wr_s[m + rp * j + wpl * k], v);
             v = fma(kDtreg ? Dtj[m] : sDt[j * dp + m], ws_s[i + rp * m + wpl * k], v);
           }
+          if (HELM)   // h1 A_L u + h2 B_L u
+            v = a.h1 * v + a.h2 * ((kBpre ? rb[kBpre ? k : 0] : __ldg(Bc + n2 * k)) * ru[k]);
           if (kMask && ((kmask >> k) & 1u)) v = 0.0;
           if (MODE == AX_PCG) acc = fma(ru[k], v, acc);
           wg[ij + n2 * k] = v;
@@ -529,10 +539,10 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
 }
 
 // persistent launch: grid = min(work groups, resident CTAs x SMs) of this variant
-template <int n, int MODE, bool FUSE>
+template <int n, int MODE, bool FUSE, bool HELM>
 static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cudaStream_t s) {
   using Sh = AxShape<n, FUSE>;
-  auto kern = ax_kernel<n, MODE, FUSE>;
+  auto kern = ax_kernel<n, MODE, FUSE, HELM>;
   static int resident = 0;
   if (resident == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -561,24 +571,24 @@ static int occupancy_n() {
   return std::max(nb, 1);
 }
 
-template <int MODE, bool FUSE>
+template <int MODE, bool FUSE, bool HELM = false>
 static cudaError_t dispatch(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
 #ifdef SEM_AX_ONLY_N8
-  if (P.n == 8) return launch_n<8, MODE, FUSE>(P, a, grid, s);
+  if (P.n == 8) return launch_n<8, MODE, FUSE, HELM>(P, a, grid, s);
   return cudaErrorInvalidValue;
 #endif
   switch (P.n) {
-    case 2: return launch_n<2, MODE, FUSE>(P, a, grid, s);
-    case 3: return launch_n<3, MODE, FUSE>(P, a, grid, s);
-    case 4: return launch_n<4, MODE, FUSE>(P, a, grid, s);
-    case 5: return launch_n<5, MODE, FUSE>(P, a, grid, s);
-    case 6: return launch_n<6, MODE, FUSE>(P, a, grid, s);
-    case 7: return launch_n<7, MODE, FUSE>(P, a, grid, s);
-    case 8: return launch_n<8, MODE, FUSE>(P, a, grid, s);
-    case 9: return launch_n<9, MODE, FUSE>(P, a, grid, s);
-    case 10: return launch_n<10, MODE, FUSE>(P, a, grid, s);
-    case 11: return launch_n<11, MODE, FUSE>(P, a, grid, s);
-    case 12: return launch_n<12, MODE, FUSE>(P, a, grid, s);
+    case 2: return launch_n<2, MODE, FUSE, HELM>(P, a, grid, s);
+    case 3: return launch_n<3, MODE, FUSE, HELM>(P, a, grid, s);
+    case 4: return launch_n<4, MODE, FUSE, HELM>(P, a, grid, s);
+    case 5: return launch_n<5, MODE, FUSE, HELM>(P, a, grid, s);
+    case 6: return launch_n<6, MODE, FUSE, HELM>(P, a, grid, s);
+    case 7: return launch_n<7, MODE, FUSE, HELM>(P, a, grid, s);
+    case 8: return launch_n<8, MODE, FUSE, HELM>(P, a, grid, s);
+    case 9: return launch_n<9, MODE, FUSE, HELM>(P, a, grid, s);
+    case 10: return launch_n<10, MODE, FUSE, HELM>(P, a, grid, s);
+    case 11: return launch_n<11, MODE, FUSE, HELM>(P, a, grid, s);
+    case 12: return launch_n<12, MODE, FUSE, HELM>(P, a, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -613,6 +623,12 @@ static int ne_of(int n) {
     case 4: return dev::AxCfg<4>::NE;
     case 5: return dev::AxCfg<5>::NE;
     case 6: return dev::AxCfg<6>::NE;
+    case 7: return dev::AxCfg<7>::NE;
+    case 8: return dev::AxCfg<8>::NE;
+    case 9: return dev::AxCfg<9>::NE;
+    case 10: return dev::AxCfg<10>::NE;
+    case 11: return dev::AxCfg<11>::NE;
+    case 12: return dev::AxCfg<12>::NE;
     default: return 1;
   }
 }
@@ -630,8 +646,13 @@ int ax_occupancy(int N, int mode) {
 }
 
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
-                      bool fuse_gs) {
+                      bool fuse_gs, bool helm) {
   if (grid < 1) grid = 1;
+  if (helm) {   // Helmholtz: two-kernel operator only
+    if (mode == AX_APPLY) return dev::dispatch<AX_APPLY, false, true>(P, a, grid, s);
+    if (mode == AX_PCG) return dev::dispatch<AX_PCG, false, true>(P, a, grid, s);
+    return cudaErrorInvalidValue;
+  }
   if (mode == AX_ONLY) return dev::dispatch<AX_ONLY, false>(P, a, grid, s);
   if (mode == AX_APPLY)
     return fuse_gs ? dev::dispatch<AX_APPLY, true>(P, a, grid, s)

@@ -160,11 +160,29 @@ __global__ void export_mask_kernel(const DevPlan P, uint8_t* m) {
     m[l] = slot_mask(P, l) ? 1 : 0;
 }
 
+// Helmholtz Jacobi (NEXT-2): d = h1 d + h2 B on the element diagonals before gs
+__global__ void helm_diag_kernel(double* __restrict__ d, const double* __restrict__ B, double h1,
+                                 double h2, int64_t n) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x)
+    d[l] = h1 * d[l] + h2 * B[l];
+}
+
 __global__ void scale_kernel(const double* __restrict__ B, const double* __restrict__ f,
                              double* __restrict__ b, int64_t n) {
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
        l += (int64_t)gridDim.x * blockDim.x)
     b[l] = B[l] * f[l];
+}
+
+// b = mask ? 0 : B f.  Masking before the gather-scatter equals masking after it
+// (every copy of a Dirichlet global point is a Dirichlet slot), and reaches the
+// boundary slots no gs entity touches (points of a single element).
+__global__ void scale_mask_kernel(const DevPlan P, const double* __restrict__ B,
+                                  const double* __restrict__ f, double* __restrict__ b) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < P.n_local;
+       l += (int64_t)gridDim.x * blockDim.x)
+    b[l] = slot_mask(P, l) ? 0.0 : B[l] * f[l];
 }
 
 __global__ void sub_scalar_kernel(double* a, const double* scal, int64_t n) {
@@ -575,6 +593,18 @@ cudaError_t launch_mask(const DevPlan& P, double* u, cudaStream_t s) {
 
 cudaError_t launch_export_mask(const DevPlan& P, uint8_t* m, cudaStream_t s) {
   dev::export_mask_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_helm_diag(double* d, const double* B, double h1, double h2, int64_t n,
+                             cudaStream_t s) {
+  dev::helm_diag_kernel<<<grid_for(n), kThreads, 0, s>>>(d, B, h1, h2, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_mask(const DevPlan& P, const double* B, const double* f, double* b,
+                              cudaStream_t s) {
+  dev::scale_mask_kernel<<<grid_for(P.n_local), kThreads, 0, s>>>(P, B, f, b);
   return cudaGetLastError();
 }
 

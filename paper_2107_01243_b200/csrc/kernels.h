@@ -69,6 +69,9 @@ struct AxLaunch {
   const int* done;
   double Dm[144];                 // D (row-major n x n), read from the constant bank
   int* red_count;                 // PCG partials only: number of partials (written by block 0)
+  // Helmholtz variant (NEXT-2): w = h1 A_L u + h2 B_L u before gs and mask
+  const double* B;
+  double h1, h2;
 };
 
 // NVLink peer-memory collectives (p2p.cu): mailbox layout and device view
@@ -79,7 +82,9 @@ struct P2P {
   static constexpr size_t kArFlagOff = kSlotOff + (size_t)kSites * 2 * kMaxP * 4 * 8;
   // gather-scatter receive entries: 16 B "LL" records {lo32, flag, hi32, flag},
   // two epoch parities interleaved per entry (see p2p.cu)
-  static constexpr size_t kRecvOff = kArFlagOff + (size_t)kSites * kMaxP * 8;
+  static constexpr size_t kPingOff = kArFlagOff + (size_t)kSites * kMaxP * 8;   // [kMaxP] ping-pong flags
+  static constexpr size_t kRecvOff = kPingOff + (size_t)kMaxP * 8;
+  static constexpr int64_t kMinRecv = 1 << 18;   // receive entries allocated at least (probes)
   int P = 1, me = 0, nnbr = 0;
   char* local = nullptr;            // this rank's mailbox
   char* const* peers = nullptr;     // [P] mailbox of every rank (peers[me] == local)
@@ -108,6 +113,12 @@ cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, co
 cudaError_t launch_gs_unpack_p2p(const DevPlan& P, double* u, const double* part, const P2P& c,
                                  uint64_t epoch, int apply_mask, PcgState* st, int nparts,
                                  uint64_t e_sig, cudaStream_t s);
+// interconnect probes for the performance model: one-thread ping-pong
+// with `peer` (round-trip ns per sample), and one-sided peer writes (bandwidth)
+cudaError_t launch_p2p_pingpong(const P2P& c, int peer, int iters, uint64_t e0, long long* out,
+                                cudaStream_t s);
+cudaError_t launch_p2p_write(const P2P& c, int peer, const double* src, int64_t n, int64_t cap,
+                             int reps, cudaStream_t s);
 cudaError_t launch_ar_publish(const P2P& c, int site, uint64_t epoch, const double* v, int K,
                               cudaStream_t s);
 cudaError_t launch_ar_finish(const P2P& c, int site, uint64_t epoch, double* out, int K,
@@ -115,8 +126,9 @@ cudaError_t launch_ar_finish(const P2P& c, int site, uint64_t epoch, double* out
 
 // returns max resident CTAs/SM for the Ax kernel of this N and mode
 int ax_occupancy(int N, int mode);
+// helm: the Helmholtz variant (a.B, a.h1, a.h2), AX_APPLY / AX_PCG, two-kernel operator
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
-                      bool fuse_gs);
+                      bool fuse_gs, bool helm = false);
 int ax_groups(int N, int nelem);   // element groups processed per launch
 
 // setup
@@ -130,6 +142,10 @@ cudaError_t launch_diag(const DevPlan& P, const double* G, double* d, cudaStream
 cudaError_t launch_mult(const DevPlan& P, uint8_t* mult, cudaStream_t s);
 cudaError_t launch_invert_mask(const DevPlan& P, double* d, cudaStream_t s);
 cudaError_t launch_scale(const double* B, const double* f, double* b, int64_t n, cudaStream_t s);
+cudaError_t launch_scale_mask(const DevPlan& P, const double* B, const double* f, double* b,
+                              cudaStream_t s);
+cudaError_t launch_helm_diag(double* d, const double* B, double h1, double h2, int64_t n,
+                             cudaStream_t s);
 cudaError_t launch_mask(const DevPlan& P, double* u, cudaStream_t s);
 cudaError_t launch_export_mask(const DevPlan& P, uint8_t* m, cudaStream_t s);
 

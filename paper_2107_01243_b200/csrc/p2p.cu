@@ -154,6 +154,41 @@ __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
   XTS(4);
 }
 
+// ---------------------------------------------------------------- interconnect probes
+// Ping-pong between this rank and `peer` through their mailboxes: the lower rank
+// releases a flag in the peer's mailbox and waits for the answer in its own; the
+// other rank answers.  Round-trip time per sample from %globaltimer (P:L373 samples
+// 10,000 ping-pongs for alpha*).
+__global__ void p2p_pingpong_kernel(const P2P c, int peer, int iters, uint64_t e0, long long* out) {
+  uint64_t* mine = mb_ping(c.local, peer);
+  uint64_t* theirs = mb_ping(c.peers[peer], c.me);
+  const bool ping = c.me < peer;
+  for (int it = 0; it < iters; it++) {
+    const uint64_t e = e0 + it + 1;
+    if (ping) {
+      const unsigned long long t0 = gtimer();
+      st_release_sys(theirs, e);
+      wait_flag(mine, e, c.err);
+      out[it] = (long long)(gtimer() - t0);
+    } else {
+      wait_flag(mine, e, c.err);
+      st_release_sys(theirs, e);
+    }
+  }
+}
+
+// one-sided bandwidth probe: n doubles written into the peer's receive area
+// (wrapping at cap doubles), reps times, 16-B vector stores
+__global__ void p2p_write_kernel(const P2P c, int peer, const double2* __restrict__ src, int64_t n2,
+                                 int64_t cap2, int reps) {
+  double2* dst = reinterpret_cast<double2*>(c.peers[peer] + P2P::kRecvOff);
+  for (int r = 0; r < reps; r++)
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
+         q += (int64_t)gridDim.x * blockDim.x)
+      dst[q % cap2] = src[q];
+  __threadfence_system();
+}
+
 // publish k values from device memory (one thread)
 __global__ void ar_publish_kernel(const P2P c, int site, uint64_t epoch, const double* v, int K) {
   double t[4];
@@ -251,6 +286,19 @@ cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, co
                                         sig_part, sig_count, base, mode, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_p2p_pingpong(const P2P& c, int peer, int iters, uint64_t e0, long long* out,
+                                cudaStream_t s) {
+  dev::p2p_pingpong_kernel<<<1, 1, 0, s>>>(c, peer, iters, e0, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_write(const P2P& c, int peer, const double* src, int64_t n, int64_t cap,
+                             int reps, cudaStream_t s) {
+  dev::p2p_write_kernel<<<148 * 4, 256, 0, s>>>(c, peer, reinterpret_cast<const double2*>(src),
+                                                 n / 2, cap / 2, reps);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ar_publish(const P2P& c, int site, uint64_t epoch, const double* v, int K,

@@ -41,6 +41,9 @@ __device__ __forceinline__ double* mb_slot(char* mb, int site, uint64_t epoch, i
 __device__ __forceinline__ uint64_t* mb_arflag(char* mb, int site, int r) {
   return reinterpret_cast<uint64_t*>(mb + P2P::kArFlagOff) + (size_t)site * P2P::kMaxP + r;
 }
+__device__ __forceinline__ uint64_t* mb_ping(char* mb, int r) {
+  return reinterpret_cast<uint64_t*>(mb + P2P::kPingOff) + r;
+}
 // receive entry o of the gather-scatter exchange with the given epoch parity
 __device__ __forceinline__ uint4* mb_ll(char* mb, int64_t o, uint64_t epoch) {
   return reinterpret_cast<uint4*>(mb + P2P::kRecvOff) + 2 * o + (epoch & 1);

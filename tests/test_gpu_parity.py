@@ -177,12 +177,42 @@ def test_full_size_apply(cfg):
             assert nrel(host(dw), ref) <= 1e-12
 
 
+def test_full_size_c4():
+    """BASELINE configs[3] at full size on one GPU (64^3 deformed elements, N=7,
+    134M slots, all six factors nonzero): every slot of Ax and of the operator
+    within 1e-12 and gs bit-exact, in both gs schedules (the chunk schedule is
+    the one auto picks at this size).  The oracle needs ~20 GB of host RAM."""
+    import os
+    if os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") < 48e9:
+        pytest.skip("host RAM < 48 GB for the full-size oracle")
+    spec, N = CONFIGS["C4"]
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=21)
+    with sem().sem_setup(spec, N) as c:
+        du, dw = dev(u), c.zeros()
+        c.ax(du, dw)
+        assert nrel(host(dw), o.ax(u)) <= 1e-12
+        ref_ap, ref_gs = o.apply(u), o.gs(u)
+        for mode in (0, 1):
+            c.set_gs_mode(mode)
+            c.apply(du, dw)
+            assert nrel(host(dw), ref_ap) <= 1e-12
+            g = dev(u)
+            c.gs(g)
+            assert np.array_equal(host(g), ref_gs)
+            del g
+
+
 @pytest.mark.parametrize("spec,N,fun", [(CONFIGS["C1"][0], 3, f_sin), (tgv_box(4, 4, 3), 5, f_tgv),
                                         (tgv_box(3, 4, 3, deform=1), 6, f_tgv),
-                                        (unit_box(2, 3, 2, periodic=(0, 1, 1)), 5, f_sin)])
+                                        (unit_box(2, 3, 2, periodic=(0, 1, 1)), 5, f_sin),
+                                        (CONFIGS["C1"][0], 3, None),
+                                        (unit_box(3, 2, 2, periodic=(0, 1, 0)), 4, None)])
 def test_rhs_parity(spec, N, fun):
+    """fun None: a random f, nonzero on the Dirichlet boundary (every masked slot,
+    including the ones no gather-scatter entity touches, must come out 0)."""
     o = O.Oracle(spec, N)
-    f = fun(o.get("X"), o.get("Y"), o.get("Z"))
+    f = fun(o.get("X"), o.get("Y"), o.get("Z")) if fun else random_field(o.nslots, seed=41)
     with sem().sem_setup(spec, N) as c:
         b = c.zeros()
         c.rhs(dev(f), b)
@@ -277,3 +307,47 @@ def test_launch_counts_and_native_library_loaded():
             assert c.launch_count() == n0 + k
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libsem.so" in maps
+
+
+# ---------------------------------------------------------------- NEXT-2: Helmholtz h1 A + h2 B
+HELM_MESHES = [(CONFIGS["C1"][0], 3), (tgv_box(4, 3, 5, deform=1), 7), (unit_box(3, 2, 3), 4),
+               (tgv_box(3, 3, 2, deform=1), 11), (tgv_box(12, 10, 10, deform=1), 6)]
+
+
+@pytest.mark.parametrize("spec,N", HELM_MESHES,
+                         ids=[f"{s.ex}x{s.ey}x{s.ez}-d{s.deform}-N{N}" for s, N in HELM_MESHES])
+@pytest.mark.parametrize("h1,h2", [(1.0, 0.0), (0.3, 2.5), (1.0 / 1600.0, 2000.0)])
+def test_helm_apply_parity(spec, N, h1, h2):
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=31)          # discontinuous: exercises the element-level B term
+    with sem().sem_setup(spec, N) as c:
+        w = c.zeros()
+        c.helm_apply(h1, h2, dev(u), w)
+        assert nrel(host(w), o.helm_apply(h1, h2, u)) <= 1e-12
+        f = random_field(o.nslots, seed=32)
+        b = c.zeros()
+        c.rhs_mass(dev(f), b)
+        assert nrel(host(b), o.rhs_mass(f)) <= 1e-12
+
+
+@pytest.mark.parametrize("spec,N,h1,h2", [(CONFIGS["C1"][0], 3, 1.0, 10.0),
+                                          (tgv_box(6, 6, 6, deform=1), 5, 0.5, 3.0),
+                                          (tgv_box(8, 8, 8), 7, 1.0 / 1600.0, 2000.0)])
+def test_helm_pcg_parity(spec, N, h1, h2):
+    """Helmholtz Jacobi-PCG: iterations +-1 and x within 1e-10 of the oracle's
+    (fully periodic boxes included: h2 > 0 makes the system nonsingular)."""
+    o = O.Oracle(spec, N)
+    X, Y, Z = o.get("X"), o.get("Y"), o.get("Z")
+    fun = f_sin if not all(spec.periodic) else f_tgv
+    b = o.rhs_mass(fun(X, Y, Z))
+    ref = o.helm_pcg(h1, h2, b, 1e-10, 3000)
+    with sem().sem_setup(spec, N) as c:
+        x = c.zeros()
+        r = c.helm_pcg_solve(h1, h2, dev(b), x, 1e-10, 3000)
+        assert r["status"] == 0 and abs(r["iters"] - ref["iters"]) <= 1
+        assert np.abs(host(x) - ref["x"]).max() <= 1e-10
+        assert abs(r["res_final"] - ref["res_final"]) <= 1e-10
+        assert abs(r["res_true"] - ref["res_true"]) <= 1e-10
+        # the Poisson solve on the same context is unaffected afterwards
+        c.apply(dev(b), x)
+        assert nrel(host(x), o.apply(b)) <= 1e-12
