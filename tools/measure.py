@@ -91,6 +91,42 @@ def op_rates(c, N, st, reps, tri):
     return res
 
 
+def helm(cfg="C3", h1=1.0 / 1600.0, h2=2000.0):
+    """NEXT-2 Helmholtz on a BASELINE config: h1 A + h2 B apply rate (72 + 20 f_b
+    B/pt: the Ax kernel also streams B) and Jacobi-PCG to 1e-10 at the velocity-
+    solve coefficients of S:L302 (Re = 1600, dt = 5e-4)."""
+    torch.cuda.set_device(0)
+    st = torch.cuda.current_stream()
+    spec, N = CONFIGS[cfg]
+    fb = bytes_model(N)[0]
+    with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
+        n = c.n_local
+        u = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        w = c.zeros()
+        ms = timed(lambda: c.helm_apply(h1, h2, u, w), st, 50)
+        bpp = 72.0 + 20.0 * fb
+        gbs = bpp * n / (ms * 1e-3) / 1e9
+        X, Y, Z = c.coords()
+        f = h1 * f_tgv(X, Y, Z, xp=torch) + h2 * p_tgv(X, Y, Z, xp=torch)   # (-h1 lap + h2) p*
+        b = c.zeros()
+        c.rhs_mass(f, b)
+        x = c.zeros()
+        c.helm_pcg_solve(h1, h2, b, x, 1e-10, 2000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        r = c.helm_pcg_solve(h1, h2, b, x, 1e-10, 2000)
+        e1.record(st)
+        torch.cuda.synchronize()
+        pms = e0.elapsed_time(e1)
+        einf = float((x - p_tgv(X, Y, Z, xp=torch)).abs().max())
+        out({"what": f"{cfg}_helm", "h1": h1, "h2": h2, "apply_ms": round(ms, 4),
+             "apply_gdofs": round(n / (ms * 1e-3) / 1e9, 2), "apply_B_per_pt": round(bpp, 1),
+             "apply_frac_nominal": round(gbs / NOMINAL, 3), "apply_frac_copy": round(gbs / peak_copy(), 3),
+             "pcg_iters": r["iters"], "pcg_status": r["status"], "pcg_ms": round(pms, 3),
+             "pcg_iter_per_s": round(r["iters"] / (pms * 1e-3), 1),
+             "pcg_gdofs": round(n * r["iters"] / (pms * 1e-3) / 1e9, 2), "e_inf_vs_p*": einf})
+
+
 def pcg_rate(c, st, iters):
     """fixed-iteration PCG (tol 0) on the TGV right-hand side: iter/s, GDOF/s"""
     X, Y, Z = c.coords()
@@ -216,6 +252,8 @@ if __name__ == "__main__":
         strong()
     elif mode == "sweep":
         sweep([int(v) for v in sys.argv[2].split(",")])
+    elif mode == "helm":
+        helm(sys.argv[2] if len(sys.argv) > 2 else "C3")
     elif mode == "ops":   # Ax / Ax+gs rates (all gs schedules) on named configs
         torch.cuda.set_device(0)
         st0 = torch.cuda.current_stream()
