@@ -193,6 +193,10 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    by the blocks (each element's w streamed from HBM about once).  Auto picks
    2 when w exceeds 64 MB. */
 #define SEM_OPT_GS_MODE 4
+/* 1 (default) = the PCG iteration kernels are launched with programmatic
+   dependent launch (each kernel's launch and prologue overlap the previous
+   kernel's tail); 0 = plain stream order.  Results are identical. */
+#define SEM_OPT_PDL 5
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

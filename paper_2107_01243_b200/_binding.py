@@ -276,6 +276,10 @@ class Context:
         """Gather-scatter schedule: 0 auto, 1 flat, 2 element-ordered chunks."""
         _check(load().sem_set_option(self._h, 4, int(mode)))
 
+    def set_pdl(self, on: bool):
+        """Programmatic dependent launch of the PCG iteration kernels (default on)."""
+        _check(load().sem_set_option(self._h, 5, 1 if on else 0))
+
     def set_p2p(self, on: bool):
         """Multi-GPU transport: NVLink peer memory (default) or NCCL. Collective."""
         _check(load().sem_set_option(self._h, 2, 1 if on else 0))

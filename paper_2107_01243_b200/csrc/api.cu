@@ -86,6 +86,7 @@ struct sem_ctx {
   unsigned long long* d_gsctr = nullptr;   // gs chunk counters (never reset)
   uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
   int gs_mode = 0;                         // SEM_OPT_GS_MODE
+  bool use_pdl = false;                    // SEM_OPT_PDL (measured slower)
   // Helmholtz (NEXT-2): operator in use by apply_op / pcg_run, and its Jacobi cache
   bool helm = false;
   double h1 = 1.0, h2 = 0.0;
@@ -752,6 +753,10 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   CUDA_TRY(sem::launch_cg_start(st, c->d_hist, ps, s));
   c->launches += 2;
   int done = 0;
+  struct PdlScope {   // programmatic dependent launch for the iteration kernels
+    explicit PdlScope(bool on) { sem::set_pdl(on); }
+    ~PdlScope() { sem::set_pdl(false); }
+  } pdl_scope(c->use_pdl && !c->timing);   // per-kernel event timers need plain order
   for (int k = 0; k < maxit && !done; k += kBatch) {
     const int nb = std::min(kBatch, maxit - k);
     for (int q = 0; q < nb; q++) {
@@ -779,6 +784,7 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
     CUDA_TRY(cudaEventSynchronize(c->ev_poll));
     done = c->h_st->done;
   }
+  sem::set_pdl(false);
   // true residual once at the end (reading Q17)
   SEM_TRY(apply_op(c, x, c->d_wv, sem::AX_APPLY));
   sem::PeerSync psr;
@@ -1007,6 +1013,10 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (option == SEM_OPT_OVERLAP) {   // collective
     cudaStreamSynchronize(c->stream);
     c->overlap = value != 0;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_PDL) {
+    c->use_pdl = value != 0;
     return SEM_OK;
   }
   if (option == SEM_OPT_GS_MODE) {

@@ -178,8 +178,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
 #endif
   constexpr bool kDtreg = kDreg && SEM_DT_REG; // transposed-contraction D columns in registers
 
-  if (MODE == AX_PCG && *a.done) return;
-
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;                                   // [NSU][NE*n3]
   double* sG = sU + NSU * Sh::uslot;                   // [NSG][NE][6][n2]
@@ -224,6 +222,9 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();   // u (= p) and the done flag come from the preceding kernel
+  pdl_trigger();
+  if (MODE == AX_PCG && *a.done) return;
 
   const int r0lo = a.r0lo, r0hi = a.r0hi, r1lo = a.r1lo, r1hi = a.r1hi;
   const int ng0 = (r0hi - r0lo + NE - 1) / NE, ng1 = (r1hi - r1lo + NE - 1) / NE, ng = ng0 + ng1;
@@ -415,6 +416,8 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       int e0, cnt;
       group(g, e0, cnt);
       const bool active = el < cnt;
+      // the element's Dirichlet face bits, fetched now, used by the epilogue
+      const unsigned bm = (kMask && active) ? (unsigned)__ldg(P.bmask + e0 + el) : 0u;
       const int uoff = kBulkU ? 0 : (int)((reinterpret_cast<uintptr_t>(a.u + (size_t)e0 * n3) >> 3) & 1u);
       const double* sUe = sU + su * Sh::uslot + uoff + el * n3;
       double* wr_s = sWr + el * Sh::wel;
@@ -428,7 +431,10 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
 
       // Helmholtz: this thread's mass column (coalesced per plane), prefetched into
       // registers where they are free (else loaded by the epilogue; no spills either way)
-      constexpr bool kBpre = HELM && (n <= 3 || (n >= 5 && n <= 9));
+#ifndef SEM_HELM_PRE
+#define SEM_HELM_PRE 1
+#endif
+      constexpr bool kBpre = SEM_HELM_PRE && HELM && (n <= 3 || (n >= 5 && n <= 9));
       double ru[n], rw[n], rb[kBpre ? n : 1];
       const double* Bc = HELM ? a.B + (size_t)(e0 + el) * n3 + ij : nullptr;
       if (kBpre) {
@@ -452,11 +458,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
         double gk[6];
 #pragma unroll
         for (int f = 0; f < 6; f++) gk[f] = active ? gp[f * n2] : 0.0;
-        if (k % PPC == PPC - 1) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&emptyG[sg]);
-          if (++sg == NSG) { sg = 0; phg ^= 1u; }
-        }
         if (active) {
           double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
@@ -474,6 +475,15 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
 #pragma unroll
           for (int m = 0; m < n; m++) rw[m] = fma(a.Dm[k * n + m], wt, rw[m]);
         }
+        // release the G slot only after its last plane was consumed: the w_r / w_s
+        // shared stores above depend on the loaded factors and the arrive's memory
+        // clobber keeps them before it, so no shared-memory read of the slot is
+        // still in flight when the producer's TMA may overwrite it (WAR hazard)
+        if (k % PPC == PPC - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&emptyG[sg]);
+          if (++sg == NSG) { sg = 0; phg ^= 1u; }
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyU[su]);   // u slot consumed
@@ -489,7 +499,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
         double* wg = a.w + (size_t)e * n3;
         uint32_t kmask = 0u;   // bit k set: slot (i,j,k) is a Dirichlet slot
         if (kMask) {
-          const unsigned bm = P.bmask[e];
           const bool mij = ((i == 0) && (bm & 1u)) || ((i == n - 1) && (bm & 2u)) ||
                            ((j == 0) && (bm & 4u)) || ((j == n - 1) && (bm & 8u));
           kmask = mij ? 0xffffffffu
@@ -556,8 +565,7 @@ static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cud
     resident = std::max(nb, 1) * sms;
   }
   const int grid = std::max(1, std::min(groups, resident));
-  kern<<<grid, Sh::T, Sh::smem_bytes, s>>>(P, a);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(grid), dim3(Sh::T), Sh::smem_bytes, s, P, a);
 }
 
 template <int n, int MODE>

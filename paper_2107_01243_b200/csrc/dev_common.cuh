@@ -6,6 +6,15 @@
 namespace sem {
 namespace dev {
 
+// Programmatic dependent launch (PCG loop kernels): wait until the preceding
+// grid has completed and its writes are visible, then let the next grid's CTAs
+// be scheduled (they run their prologue and wait in turn).  Both are no-ops
+// when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- PTX: mbarrier + bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

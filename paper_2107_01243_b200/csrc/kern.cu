@@ -11,6 +11,11 @@
 #include "sem_internal.h"
 
 namespace sem {
+
+static thread_local bool t_pdl = false;
+void set_pdl(bool on) { t_pdl = on; }
+bool pdl_on() { return t_pdl; }
+
 namespace dev {
 
 constexpr int kThreads = 256;
@@ -235,6 +240,8 @@ template <int n, bool SWEEP>
 __global__ void __launch_bounds__(256, SEM_GS_MINB) gs_local_kernel(const DevPlan P, double* __restrict__ u,
                                                        int apply_mask, unsigned long long base,
                                                        int ce) {
+  pdl_wait();
+  pdl_trigger();
   gs_local_body<n, SWEEP>(P, u, apply_mask, P.gs_ctr, base, ce);
 }
 
@@ -363,6 +370,8 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
   __shared__ double scratch[32];
   __shared__ int flag;
   __shared__ double s_sig;
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   double sigma;
   if (ps.c.P > 1) {   // global sigma from the peers' mailboxes (rank-ordered sum)
@@ -436,6 +445,8 @@ __global__ void __launch_bounds__(kThreads) cg_p_kernel(int64_t n, const double*
                             const PeerSync ps) {
   __shared__ int flag;
   __shared__ double s_rg[2];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   if (ps.c.P > 1) {   // global (rho', gamma) from the peers' mailboxes
     if (threadIdx.x == 0) ar_wait_sum(ps.c, AR_RG, ps.e_wait, 2, s_rg);
@@ -639,21 +650,23 @@ cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_
                        : grid_for(tot, resident[0]);
   const unsigned long long b = *base;
   *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
-#define GS_LAUNCH(k)                                                                  \
-  (ce > 0 ? dev::gs_local_kernel<k, true><<<g, kThreads, 0, s>>>(P, u, apply_mask, b, ce) \
-          : dev::gs_local_kernel<k, false><<<g, kThreads, 0, s>>>(P, u, apply_mask, b, ce))
+#define GS_LAUNCH(k)                                                                        \
+  return ce > 0 ? launch_k(dev::gs_local_kernel<k, true>, dim3(g), dim3(kThreads), 0, s, P, u, \
+                           apply_mask, b, ce)                                                  \
+                : launch_k(dev::gs_local_kernel<k, false>, dim3(g), dim3(kThreads), 0, s, P, u, \
+                           apply_mask, b, ce)
   switch (P.n) {
-    case 2: GS_LAUNCH(2); break;
-    case 3: GS_LAUNCH(3); break;
-    case 4: GS_LAUNCH(4); break;
-    case 5: GS_LAUNCH(5); break;
-    case 6: GS_LAUNCH(6); break;
-    case 7: GS_LAUNCH(7); break;
-    case 8: GS_LAUNCH(8); break;
-    case 9: GS_LAUNCH(9); break;
-    case 10: GS_LAUNCH(10); break;
-    case 11: GS_LAUNCH(11); break;
-    case 12: GS_LAUNCH(12); break;
+    case 2: GS_LAUNCH(2);
+    case 3: GS_LAUNCH(3);
+    case 4: GS_LAUNCH(4);
+    case 5: GS_LAUNCH(5);
+    case 6: GS_LAUNCH(6);
+    case 7: GS_LAUNCH(7);
+    case 8: GS_LAUNCH(8);
+    case 9: GS_LAUNCH(9);
+    case 10: GS_LAUNCH(10);
+    case 11: GS_LAUNCH(11);
+    case 12: GS_LAUNCH(12);
   }
 #undef GS_LAUNCH
   return cudaGetLastError();
@@ -704,15 +717,14 @@ cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
                              int grid, cudaStream_t s) {
-  dev::cg_update_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, r, w, partial, st, out2,
-                                                  sig_part, sig_count, ps);
-  return cudaGetLastError();
+  return launch_k(dev::cg_update_kernel, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult, dinv, r,
+                  w, partial, st, out2, sig_part, sig_count, ps);
 }
 
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,
                         PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s) {
-  dev::cg_p_kernel<<<grid, kThreads, 0, s>>>(P.n_local, dinv, r, p, x, st, hist, ps);
-  return cudaGetLastError();
+  return launch_k(dev::cg_p_kernel, dim3(grid), dim3(kThreads), 0, s, P.n_local, dinv, r, p, x, st,
+                  hist, ps);
 }
 
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,

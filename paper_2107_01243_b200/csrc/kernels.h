@@ -1,5 +1,6 @@
 // Launchers for the libsem CUDA kernels (called from api.cu).
 #pragma once
+#include <utility>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -9,6 +10,26 @@ namespace sem {
 enum AxMode { AX_ONLY = 0, AX_APPLY = 1, AX_PCG = 2 };
 
 // device view of the gather-scatter plan
+// PCG loop launches with programmatic dependent launch (thread-local switch set
+// by pcg_run; kernels call pdl_wait / pdl_trigger, see dev_common.cuh)
+void set_pdl(bool on);
+bool pdl_on();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 struct DevPlan {
   int N = 0, n = 0, nloc = 0;
   int64_t n_local = 0;

@@ -136,6 +136,8 @@ __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
                                                               const double* sig_part,
                                                               const int* sig_count,
                                                               unsigned long long base, int ce) {
+  pdl_wait();
+  pdl_trigger();
   XTS(0);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (st && blockIdx.x == gridDim.x - 1 && threadIdx.x < 32)
@@ -249,12 +251,10 @@ static cudaError_t launch_exchange_n(const DevPlan& P, double* u, double* part, 
   const unsigned long long b = *base;
   *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
   if (ce > 0)
-    dev::gs_exchange_p2p_kernel<n, true><<<g, 256, 0, s>>>(P, u, part, c, epoch, apply_mask, st,
-                                                           nparts, e_sig, sig_part, sig_count, b, ce);
-  else
-    dev::gs_exchange_p2p_kernel<n, false><<<g, 256, 0, s>>>(P, u, part, c, epoch, apply_mask, st,
-                                                            nparts, e_sig, sig_part, sig_count, b, ce);
-  return cudaGetLastError();
+    return launch_k(dev::gs_exchange_p2p_kernel<n, true>, dim3(g), dim3(256), 0, s, P, u, part, c,
+                    epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
+  return launch_k(dev::gs_exchange_p2p_kernel<n, false>, dim3(g), dim3(256), 0, s, P, u, part, c,
+                  epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
 }
 
 cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, const P2P& c,

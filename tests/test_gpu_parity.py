@@ -351,3 +351,39 @@ def test_helm_pcg_parity(spec, N, h1, h2):
         # the Poisson solve on the same context is unaffected afterwards
         c.apply(dev(b), x)
         assert nrel(host(x), o.apply(b)) <= 1e-12
+
+
+def test_ring_release_stress():
+    """Regression for the G-ring write-after-read hazard: a CTA released a G
+    slot right after issuing its shared-memory reads, so the producer's TMA
+    could overwrite factors still being read (showed as ~6 % wrong Helmholtz
+    applications at n=7 with NE=2, PPC=1).  Repeated applies must all match."""
+    spec, N = tgv_box(12, 10, 10, deform=1), 6
+    o = O.Oracle(spec, N)
+    u = random_field(o.nslots, seed=31)
+    ref_h, ref_p = o.helm_apply(0.3, 2.5, u), o.apply(u)
+    with sem().sem_setup(spec, N) as c:
+        w = c.zeros()
+        du = dev(u)
+        for _ in range(60):
+            c.helm_apply(0.3, 2.5, du, w)
+            assert nrel(host(w), ref_h) <= 1e-12
+            c.apply(du, w)
+            assert nrel(host(w), ref_p) <= 1e-12
+
+
+def test_pdl_option_identical():
+    """SEM_OPT_PDL (programmatic dependent launch of the iteration kernels, off
+    by default) changes scheduling only: bit-identical PCG iterates."""
+    spec, N = tgv_box(8, 8, 8), 7
+    o = O.Oracle(spec, N)
+    X, Y, Z = o.get("X"), o.get("Y"), o.get("Z")
+    b = dev(o.rhs(f_tgv(X, Y, Z)))
+    with sem().sem_setup(spec, N) as c:
+        xs = []
+        for on in (False, True):
+            c.set_pdl(on)
+            x = c.zeros()
+            r = c.pcg_solve(b, x, 1e-10, 500)
+            xs.append((host(x), r["iters"]))
+        assert xs[0][1] == xs[1][1] and np.array_equal(xs[0][0], xs[1][0])
