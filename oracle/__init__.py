@@ -72,6 +72,18 @@ def lib():
         L.oracle_helm_pcg.argtypes = [C.c_void_p, C.c_double, C.c_double, _D, _D, C.c_double,
                                       C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.c_void_p]
+        L.oracle_gmres.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int,
+                                   C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.c_void_p]
+        L.oracle_proj_create.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_proj_free.argtypes = [C.c_void_p]
+        L.oracle_proj_free.restype = None
+        L.oracle_proj_size.argtypes = [C.c_void_p]
+        L.oracle_proj_project.argtypes = [C.c_void_p, _D, _D, _D]
+        L.oracle_proj_update.argtypes = [C.c_void_p, _D]
+        L.oracle_proj_solve.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int,
+                                        C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.oracle_proj_gram.argtypes = [C.c_void_p, _D]
         L.oracle_plan.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 3 + [C.c_void_p] * 3
         L.oracle_shared.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                     C.c_void_p]
@@ -228,6 +240,21 @@ class Oracle:
         return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
                 "status": st, "hist": hist[: it.value + 1]}
 
+    # ---- NEXT-3: restarted GMRES and the solution projection
+    def gmres(self, b, tol: float, maxit: int, restart: int = 30, x0=None):
+        x = np.zeros(self.nslots) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+        it, rf, rt = C.c_int(), C.c_double(), C.c_double()
+        hist = np.zeros(maxit + 1)
+        st = lib().oracle_gmres(self._h, _f64(b), x, tol, maxit, restart, C.byref(it),
+                                C.byref(rf), C.byref(rt), hist.ctypes.data_as(C.c_void_p))
+        if st < 0:
+            raise OracleError(f"oracle_gmres failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
+                "status": st, "hist": hist[: it.value + 1]}
+
+    def proj(self, m: int = 20):
+        return Proj(self, m)
+
     def plan(self):
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
         lib().oracle_plan(self._h, C.byref(a), C.byref(b), C.byref(c), None, None, None)
@@ -247,3 +274,46 @@ class Oracle:
         assert lib().oracle_shared(self._h, r, q, C.byref(cnt),
                                    g.ctypes.data_as(C.c_void_p)) == 0
         return g
+
+
+class Proj:
+    """Solution-projection space of the oracle (Fischer 1998)."""
+
+    def __init__(self, o: "Oracle", m: int):
+        self.o = o
+        h = C.c_void_p()
+        assert lib().oracle_proj_create(o._h, m, C.byref(h)) == 0
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().oracle_proj_free(self._h)
+            self._h = None
+
+    @property
+    def size(self) -> int:
+        return lib().oracle_proj_size(self._h)
+
+    def project(self, b):
+        xb, bd = np.zeros(self.o.nslots), np.zeros(self.o.nslots)
+        assert lib().oracle_proj_project(self._h, _f64(b), xb, bd) == 0
+        return xb, bd
+
+    def update(self, x) -> bool:
+        """True if x was appended, False if skipped (negligible new direction)."""
+        return lib().oracle_proj_update(self._h, _f64(x)) == 0
+
+    def solve(self, b, tol: float, maxit: int, restart: int = 30):
+        x = np.zeros(self.o.nslots)
+        it, rf = C.c_int(), C.c_double()
+        st = lib().oracle_proj_solve(self._h, _f64(b), x, tol, maxit, restart, C.byref(it),
+                                     C.byref(rf))
+        if st < 0:
+            raise OracleError(f"oracle_proj_solve failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "status": st}
+
+    def gram(self):
+        k = self.size
+        G = np.zeros(k * k)
+        assert lib().oracle_proj_gram(self._h, G) == 0
+        return G.reshape(k, k)

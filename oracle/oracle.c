@@ -647,6 +647,209 @@ int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, 
 }
 
 /* ------------------------------------------------------------------ */
+/* NEXT-3: restarted GMRES and solution projection (Table 2) */
+
+/* Restarted GMRES(m) with right Jacobi preconditioning (readings Q25, Q26),
+   Saad's algorithm step by step: x0 given; per cycle r = b - A x, beta = ||r||_c,
+   v1 = r / beta; for j = 1..m: w = A M^-1 v_j (one iteration); modified Gram-
+   Schmidt h_ij = <w, v_i>_c, w -= h_ij v_i; h_{j+1,j} = ||w||_c; v_{j+1} = w/h;
+   previous Givens rotations applied to column j, a new one zeroes h_{j+1,j};
+   |g_{j+1}| is the residual norm; stop when it is <= tol or at maxit; then
+   y = H^-1 g (upper triangular), x += M^-1 V y.  hist[k] = |g| after iteration
+   k (hist[0] = ||b - A x0||_c).  Returns 0 converged, 1 not converged. */
+int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+                 int restart, int* iters, double* res_final, double* res_true, double* hist) {
+  if (!c || maxit < 0 || restart < 1) return -1;
+  const int64_t ns = c->nslots;
+  const int m = restart;
+  double* V = (double*)malloc(sizeof(double) * ns * (m + 1));
+  double* w = (double*)malloc(sizeof(double) * ns);
+  double* t = (double*)malloc(sizeof(double) * ns);
+  double* H = (double*)calloc((size_t)(m + 1) * m, sizeof(double));   /* H[i*m + j] */
+  double* cs = (double*)malloc(sizeof(double) * m);
+  double* sn = (double*)malloc(sizeof(double) * m);
+  double* g = (double*)malloc(sizeof(double) * (m + 1));
+  double* y = (double*)malloc(sizeof(double) * m);
+  if (!V || !w || !t || !H || !cs || !sn || !g || !y) {
+    free(V); free(w); free(t); free(H); free(cs); free(sn); free(g); free(y);
+    return -5;
+  }
+  int k = 0, status = 1;
+  double res = 0.0;
+  for (int cycle = 0;; cycle++) {
+    /* r = b - A x */
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) V[l] = b[l] - w[l];
+    const double beta = sqrt(oracle_dot_c(c, V, V));
+    res = beta;
+    if (cycle == 0 && hist) hist[0] = beta;
+    if (beta <= tol) { status = 0; break; }
+    if (k >= maxit) break;
+    for (int64_t l = 0; l < ns; l++) V[l] /= beta;
+    for (int i = 0; i <= m; i++) g[i] = 0.0;
+    g[0] = beta;
+    int j = 0;
+    for (; j < m && k < maxit; j++) {
+      double* vj = V + (int64_t)j * ns;
+      for (int64_t l = 0; l < ns; l++) t[l] = c->dinv[l] * vj[l];
+      oracle_apply(c, t, w);
+      k++;
+      for (int i = 0; i <= j; i++) {
+        const double* vi = V + (int64_t)i * ns;
+        const double h = oracle_dot_c(c, w, vi);
+        H[i * m + j] = h;
+        for (int64_t l = 0; l < ns; l++) w[l] -= h * vi[l];
+      }
+      const double hn = sqrt(oracle_dot_c(c, w, w));
+      H[(j + 1) * m + j] = hn;
+      double* vn = V + (int64_t)(j + 1) * ns;
+      for (int64_t l = 0; l < ns; l++) vn[l] = hn > 0.0 ? w[l] / hn : 0.0;
+      for (int i = 0; i < j; i++) {   /* previous rotations */
+        const double a = H[i * m + j], bb = H[(i + 1) * m + j];
+        H[i * m + j] = cs[i] * a + sn[i] * bb;
+        H[(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      }
+      const double a = H[j * m + j], bb = H[(j + 1) * m + j];
+      const double r = sqrt(a * a + bb * bb);
+      cs[j] = r > 0.0 ? a / r : 1.0;
+      sn[j] = r > 0.0 ? bb / r : 0.0;
+      H[j * m + j] = r;
+      H[(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      res = fabs(g[j + 1]);
+      if (hist) hist[k] = res;
+      if (res <= tol || hn == 0.0) { j++; break; }
+    }
+    /* y = H(0:j,0:j)^-1 g(0:j), x += M^-1 V y */
+    for (int i = j - 1; i >= 0; i--) {
+      double sacc = g[i];
+      for (int q = i + 1; q < j; q++) sacc -= H[i * m + q] * y[q];
+      y[i] = sacc / H[i * m + i];
+    }
+    for (int64_t l = 0; l < ns; l++) {
+      double vy = 0.0;
+      for (int i = 0; i < j; i++) vy += V[(int64_t)i * ns + l] * y[i];
+      x[l] += c->dinv[l] * vy;
+    }
+    if (res <= tol) { status = 0; break; }
+    if (k >= maxit) break;
+  }
+  if (iters) *iters = k;
+  if (res_final) *res_final = res;
+  if (res_true) {
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) w[l] = b[l] - w[l];
+    *res_true = sqrt(oracle_dot_c(c, w, w));
+  }
+  free(V); free(w); free(t); free(H); free(cs); free(sn); free(g); free(y);
+  return status;
+}
+
+/* Solution projection ("projections techniques as in Nek5000 [20] ...
+   storing a set of previous solutions"; Fischer 1998, ref. [20]; readings Q26):
+   up to m A-orthonormal directions z_i (with A z_i stored), <z_i, A z_j>_c = d_ij. */
+struct oracle_proj {
+  const oracle_ctx* c;
+  int m, k;
+  double *Z, *AZ;   /* [m][nslots] */
+};
+
+int oracle_proj_create(const oracle_ctx* c, int m, oracle_proj** out) {
+  if (!c || m < 1 || !out) return -1;
+  oracle_proj* p = (oracle_proj*)calloc(1, sizeof(oracle_proj));
+  if (!p) return -5;
+  p->c = c;
+  p->m = m;
+  p->Z = (double*)malloc(sizeof(double) * c->nslots * m);
+  p->AZ = (double*)malloc(sizeof(double) * c->nslots * m);
+  if (!p->Z || !p->AZ) { free(p->Z); free(p->AZ); free(p); return -5; }
+  *out = p;
+  return 0;
+}
+
+void oracle_proj_free(oracle_proj* p) {
+  if (!p) return;
+  free(p->Z); free(p->AZ); free(p);
+}
+
+int oracle_proj_size(const oracle_proj* p) { return p ? p->k : -1; }
+
+/* x_bar = sum_i <z_i, b>_c z_i, b_defl = b - sum_i <z_i, b>_c A z_i (= b - A x_bar) */
+int oracle_proj_project(const oracle_proj* p, const double* b, double* xbar, double* bdefl) {
+  const int64_t ns = p->c->nslots;
+  for (int64_t l = 0; l < ns; l++) { xbar[l] = 0.0; bdefl[l] = b[l]; }
+  for (int i = 0; i < p->k; i++) {
+    const double* zi = p->Z + (int64_t)i * ns;
+    const double* azi = p->AZ + (int64_t)i * ns;
+    const double a = oracle_dot_c(p->c, zi, b);
+    for (int64_t l = 0; l < ns; l++) {
+      xbar[l] += a * zi[l];
+      bdefl[l] -= a * azi[l];
+    }
+  }
+  return 0;
+}
+
+/* append x: A-orthonormalise against the stored directions (modified Gram-
+   Schmidt, two passes), skip if ||z||_A < 1e-12 ||x||_A; when the space is
+   full it is reset to the single most recent solution.  Returns 1 if skipped. */
+int oracle_proj_update(oracle_proj* p, const double* x) {
+  const oracle_ctx* c = p->c;
+  const int64_t ns = c->nslots;
+  if (p->k == p->m) p->k = 0;   /* reset, keep the latest */
+  double* z = p->Z + (int64_t)p->k * ns;
+  double* az = p->AZ + (int64_t)p->k * ns;
+  for (int64_t l = 0; l < ns; l++) z[l] = x[l];
+  oracle_apply(c, z, az);
+  const double nx = sqrt(fabs(oracle_dot_c(c, z, az)));
+  for (int pass = 0; pass < 2; pass++)
+    for (int i = 0; i < p->k; i++) {
+      const double* zi = p->Z + (int64_t)i * ns;
+      const double* azi = p->AZ + (int64_t)i * ns;
+      const double a = oracle_dot_c(c, zi, az);   /* <z_i, z>_A */
+      for (int64_t l = 0; l < ns; l++) {
+        z[l] -= a * zi[l];
+        az[l] -= a * azi[l];
+      }
+    }
+  const double nz = sqrt(fabs(oracle_dot_c(c, z, az)));
+  if (!(nz > 1e-12 * nx)) return 1;
+  for (int64_t l = 0; l < ns; l++) {
+    z[l] /= nz;
+    az[l] /= nz;
+  }
+  p->k++;
+  return 0;
+}
+
+/* the pressure-solve pipeline: project, GMRES(restart) on the deflated right-
+   hand side from x = 0, x = x_bar + delta, append x to the space */
+int oracle_proj_solve(oracle_proj* p, const double* b, double* x, double tol, int maxit,
+                      int restart, int* iters, double* res_final) {
+  const int64_t ns = p->c->nslots;
+  double* xb = (double*)malloc(sizeof(double) * ns);
+  double* bd = (double*)malloc(sizeof(double) * ns);
+  if (!xb || !bd) { free(xb); free(bd); return -5; }
+  oracle_proj_project(p, b, xb, bd);
+  for (int64_t l = 0; l < ns; l++) x[l] = 0.0;
+  int st = oracle_gmres(p->c, bd, x, tol, maxit, restart, iters, res_final, NULL, NULL);
+  for (int64_t l = 0; l < ns; l++) x[l] += xb[l];
+  if (st >= 0) oracle_proj_update(p, x);
+  free(xb); free(bd);
+  return st;
+}
+
+/* test access: A-inner products of the stored directions (k x k, row-major) */
+int oracle_proj_gram(const oracle_proj* p, double* G) {
+  const int64_t ns = p->c->nslots;
+  for (int i = 0; i < p->k; i++)
+    for (int j = 0; j < p->k; j++)
+      G[i * p->k + j] = oracle_dot_c(p->c, p->Z + (int64_t)i * ns, p->AZ + (int64_t)j * ns);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
 /* canonical plan export (P:L231 sorted tuples + variable blocks)       */
 static int cmp_first(const void* a, const void* b) {
   int64_t x = ((const int64_t*)a)[0], y = ((const int64_t*)b)[0];

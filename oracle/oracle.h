@@ -77,6 +77,19 @@ int oracle_helm_dinv(const oracle_ctx* c, double h1, double h2, double* dinv);
 int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, double* x,
                     double tol, int maxit, int* iters, double* res_final, double* res_true,
                     double* hist);
+/* NEXT-3 (Table 2): restarted GMRES with right Jacobi
+   preconditioning, and the solution-projection space (Fischer 1998). */
+int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+                 int restart, int* iters, double* res_final, double* res_true, double* hist);
+typedef struct oracle_proj oracle_proj;
+int oracle_proj_create(const oracle_ctx* c, int m, oracle_proj** out);
+void oracle_proj_free(oracle_proj* p);
+int oracle_proj_size(const oracle_proj* p);
+int oracle_proj_project(const oracle_proj* p, const double* b, double* xbar, double* bdefl);
+int oracle_proj_update(oracle_proj* p, const double* x);
+int oracle_proj_solve(oracle_proj* p, const double* b, double* x, double tol, int maxit,
+                      int restart, int* iters, double* res_final);
+int oracle_proj_gram(const oracle_proj* p, double* G);
 int oracle_plan(const oracle_ctx* c, int64_t* npairs, int64_t* nseg, int64_t* nsegslots,
                 int64_t* pairs, int64_t* seg_off, int64_t* seg_slot);
 /* gids shared between ranks r and q (r != q), ascending; NULL list to size. */
