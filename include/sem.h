@@ -117,6 +117,23 @@ int sem_helm_apply(sem_ctx* c, double h1, double h2, const double* u, double* w)
 int sem_rhs_mass(sem_ctx* c, const double* f, double* b);
 int sem_helm_pcg_solve(sem_ctx* c, double h1, double h2, const double* b, double* x,
                        double tol, int32_t maxit, sem_pcg_result* r);
+/* NEXT-3 (Table 2 "GMRES ... Projections 20"): the pressure
+   solver pipeline.  sem_gmres_solve: restarted GMRES(restart), restart in
+   [1, 31], right Jacobi preconditioning, x0 = 0, same tolerance / iteration /
+   result conventions as sem_pcg_solve (an iteration = one operator application
+   in the Arnoldi process; res_final = the Arnoldi residual estimate, res_true =
+   ||b - A x||_c).  sem_proj_solve: Fischer's solution projection with a space
+   of m <= 32 A-orthonormal previous solutions kept in the context: x_bar =
+   sum <z_i, b>_c z_i, GMRES on b - A x_bar, x = x_bar + delta, then x is
+   A-orthonormalised into the space (reset to the latest solution when full;
+   skipped if negligible).  Changing m resets the space; sem_proj_reset empties
+   it.  Collective for nranks > 1; blocking. */
+int sem_gmres_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                    int32_t restart, sem_pcg_result* r);
+int sem_proj_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                   int32_t restart, int32_t m, sem_pcg_result* r);
+int sem_proj_reset(sem_ctx* c);
+int sem_proj_size(const sem_ctx* c, int32_t* k);
 int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_host, double tol,
                        int32_t maxit, sem_pcg_result* res);
 /* recursive residual history of the last solve: hist[k] after k iterations */

@@ -652,7 +652,8 @@ int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, 
 /* Restarted GMRES(m) with right Jacobi preconditioning (readings Q25, Q26),
    Saad's algorithm step by step: x0 given; per cycle r = b - A x, beta = ||r||_c,
    v1 = r / beta; for j = 1..m: w = A M^-1 v_j (one iteration); modified Gram-
-   Schmidt h_ij = <w, v_i>_c, w -= h_ij v_i; h_{j+1,j} = ||w||_c; v_{j+1} = w/h;
+   Schmidt h_ij = <w, v_i>_c, w -= h_ij v_i, done twice (reorthogonalisation,
+   h_ij summed over both passes); h_{j+1,j} = ||w||_c; v_{j+1} = w/h;
    previous Givens rotations applied to column j, a new one zeroes h_{j+1,j};
    |g_{j+1}| is the residual norm; stop when it is <= tol or at maxit; then
    y = H^-1 g (upper triangular), x += M^-1 V y.  hist[k] = |g| after iteration
@@ -694,12 +695,16 @@ int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, in
       for (int64_t l = 0; l < ns; l++) t[l] = c->dinv[l] * vj[l];
       oracle_apply(c, t, w);
       k++;
-      for (int i = 0; i <= j; i++) {
-        const double* vi = V + (int64_t)i * ns;
-        const double h = oracle_dot_c(c, w, vi);
-        H[i * m + j] = h;
-        for (int64_t l = 0; l < ns; l++) w[l] -= h * vi[l];
-      }
+      /* modified Gram-Schmidt, applied twice (one reorthogonalisation pass,
+         reading Q25): keeps the basis orthogonal over long cycles */
+      for (int i = 0; i <= j; i++) H[i * m + j] = 0.0;
+      for (int pass = 0; pass < 2; pass++)
+        for (int i = 0; i <= j; i++) {
+          const double* vi = V + (int64_t)i * ns;
+          const double h = oracle_dot_c(c, w, vi);
+          H[i * m + j] += h;
+          for (int64_t l = 0; l < ns; l++) w[l] -= h * vi[l];
+        }
       const double hn = sqrt(oracle_dot_c(c, w, w));
       H[(j + 1) * m + j] = hn;
       double* vn = V + (int64_t)(j + 1) * ns;

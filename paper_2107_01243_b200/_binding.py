@@ -54,6 +54,11 @@ _SIGS = {
     "sem_pcg_solve": [_P, _P, _P, C.c_double, C.c_int32, C.POINTER(PcgResult)],
     "sem_pcg_solve_host": [_P, _P, _P, C.c_double, C.c_int32, C.POINTER(PcgResult)],
     "sem_helm_apply": [_P, C.c_double, C.c_double, _P, _P],
+    "sem_gmres_solve": [_P, _P, _P, C.c_double, C.c_int32, C.c_int32, C.POINTER(PcgResult)],
+    "sem_proj_solve": [_P, _P, _P, C.c_double, C.c_int32, C.c_int32, C.c_int32,
+                       C.POINTER(PcgResult)],
+    "sem_proj_reset": [_P],
+    "sem_proj_size": [_P, C.POINTER(C.c_int32)],
     "sem_rhs_mass": [_P, _P, _P],
     "sem_helm_pcg_solve": [_P, C.c_double, C.c_double, _P, _P, C.c_double, C.c_int32,
                            C.POINTER(PcgResult)],
@@ -221,6 +226,30 @@ class Context:
                allow=(SEM_OK, SEM_NOT_CONVERGED))
         return {"iters": r.iters, "status": r.status, "res_final": r.res_final,
                 "res_true": r.res_true}
+
+    # ---- NEXT-3: GMRES and the solution projection
+    def gmres_solve(self, b, x, tol, maxit, restart=30):
+        r = PcgResult()
+        _check(load().sem_gmres_solve(self._h, self._f64(b), self._f64(x), float(tol), int(maxit),
+                                      int(restart), C.byref(r)), allow=(SEM_OK, SEM_NOT_CONVERGED))
+        return {"iters": r.iters, "status": r.status, "res_final": r.res_final,
+                "res_true": r.res_true}
+
+    def proj_solve(self, b, x, tol, maxit, restart=30, m=20):
+        r = PcgResult()
+        _check(load().sem_proj_solve(self._h, self._f64(b), self._f64(x), float(tol), int(maxit),
+                                     int(restart), int(m), C.byref(r)),
+               allow=(SEM_OK, SEM_NOT_CONVERGED))
+        return {"iters": r.iters, "status": r.status, "res_final": r.res_final,
+                "res_true": r.res_true}
+
+    def proj_reset(self):
+        _check(load().sem_proj_reset(self._h))
+
+    def proj_size(self) -> int:
+        k = C.c_int32()
+        _check(load().sem_proj_size(self._h, C.byref(k)))
+        return k.value
 
     def pcg_solve_host(self, b_host: np.ndarray, x_host: np.ndarray, tol, maxit):
         """End-to-end entry point: HOST b in, HOST x out (copies inside libsem)."""

@@ -87,6 +87,14 @@ struct sem_ctx {
   uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
   int gs_mode = 0;                         // SEM_OPT_GS_MODE
   bool use_pdl = false;                    // SEM_OPT_PDL (measured slower)
+  // NEXT-3: GMRES work space, projection space
+  const int* ax_gate = nullptr;            // Ax early-exit flag of GMRES Arnoldi steps
+  double *d_V = nullptr, *d_gt = nullptr, *d_kpart = nullptr;
+  sem::GmresState* d_gs = nullptr;
+  unsigned* d_ktick = nullptr;
+  int gm_cap = 0;
+  double *d_Z = nullptr, *d_AZ = nullptr, *d_pdelta = nullptr, *d_pbd = nullptr;
+  int proj_m = 0, proj_k = 0;
   // Helmholtz (NEXT-2): operator in use by apply_op / pcg_run, and its Jacobi cache
   bool helm = false;
   double h1 = 1.0, h2 = 0.0;
@@ -214,7 +222,8 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.red_count = c->d_nsig;
   a.red_ticket = &c->d_st->tickets[0];
   a.red_out = red_out;
-  a.done = &c->d_st->done;
+  a.done = c->ax_gate ? c->ax_gate : &c->d_st->done;
+  a.gate = c->ax_gate ? 1 : 0;
   std::copy(c->hp.D.begin(), c->hp.D.end(), a.Dm);
   a.B = c->d_B;
   a.h1 = c->h1;
@@ -412,9 +421,12 @@ void free_ctx(sem_ctx* c) {
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
                   c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank, c->d_fst, c->d_est,
-                  c->d_vst, c->d_gsctr, c->d_dinv_helm};
+                  c->d_vst, c->d_gsctr, c->d_dinv_helm,
+                  c->d_V, c->d_gt, c->d_kpart, c->d_Z, c->d_AZ, c->d_pdelta, c->d_pbd};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (c->d_gs) cudaFree(c->d_gs);
+  if (c->d_ktick) cudaFree(c->d_ktick);
   if (c->h_st) cudaFreeHost(c->h_st);
   for (char* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_perr};
@@ -891,6 +903,269 @@ extern "C" int sem_helm_pcg_solve(sem_ctx* c, double h1, double h2, const double
   SEM_TRY(helm_jacobi(c, h1, h2));
   HelmScope hs(c, h1, h2);
   return pcg_run(c, b, x, tol, maxit, res);
+}
+
+// ---------------------------------------------------------------- NEXT-3: GMRES, projection
+// restarted GMRES(m) with right Jacobi preconditioning (readings Q25, Q26);
+// device-resident: the host enqueues 8 Arnoldi steps per poll
+static int gm_alloc(sem_ctx* c, int m) {
+  if (m < 1 || m >= sem::kGmMax) {
+    sem::set_error("restart must be in [1, 31]");
+    return SEM_EINVAL;
+  }
+  const size_t n = (size_t)c->hp.n_local;
+  if (!c->d_gs) {
+    SEM_TRY(dalloc(&c->d_gs, 1));
+    SEM_TRY(dalloc(&c->d_ktick, 4));
+    CUDA_TRY(cudaMemsetAsync(c->d_ktick, 0, 4 * sizeof(unsigned), c->stream));
+    SEM_TRY(dalloc(&c->d_kpart, (size_t)4 * c->num_sms * sem::kGmMax));
+    SEM_TRY(dalloc(&c->d_gt, n));
+    sem::GmresState init{};
+    init.one = 1.0;
+    CUDA_TRY(cudaMemcpyAsync(c->d_gs, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  if (m + 1 > c->gm_cap) {
+    if (c->d_V) cudaFree(c->d_V);
+    c->d_V = nullptr;
+    SEM_TRY(dalloc(&c->d_V, (m + 1) * n));
+    // finite contents: unused basis vectors are multiplied by zero coefficients
+    CUDA_TRY(cudaMemsetAsync(c->d_V, 0, (m + 1) * n * sizeof(double), c->stream));
+    c->gm_cap = m + 1;
+  }
+  return SEM_OK;
+}
+
+struct GateScope {
+  sem_ctx* c;
+  GateScope(sem_ctx* ctx, const int* g) : c(ctx) { c->ax_gate = g; }
+  ~GateScope() { c->ax_gate = nullptr; }
+};
+
+static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit, int m,
+                     sem_pcg_result* res) {
+  if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
+  SEM_TRY(gm_alloc(c, m));
+  SEM_TRY(ensure_hist(c, maxit));
+  cudaStream_t s = c->stream;
+  const int64_t n = c->hp.n_local;
+  const int sms = c->num_sms;
+  sem::PcgState* st = c->d_st;
+  sem::GmresState* gs = c->d_gs;
+  double* part = c->d_kpart;
+  unsigned* tk = c->d_ktick;
+  double* w = c->d_wv;
+  const double* dinv = c->d_dinv;
+  const uint8_t* mult = c->d_mult;
+  const bool dist = c->hp.nranks > 1;
+  sem::PcgState init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  std::memcpy(c->h_st, &init, sizeof(init));
+  CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  const int* done = &st->done;
+  const int* cyc = &gs->cycle_done;
+  int status_done = 0;
+  while (!status_done) {
+    // restart: V0 = (b - A x) / ||b - A x||_c, t = dinv V0
+    {
+      GateScope g(c, done);
+      SEM_TRY(apply_op(c, x, w, sem::AX_APPLY));
+    }
+    CUDA_TRY(sem::launch_resid(n, b, w, c->d_V, mult, part, tk, &gs->norm2[0], done, sms, s));
+    if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
+    CUDA_TRY(sem::launch_gm_start(gs, st, c->d_hist, s));
+    CUDA_TRY(sem::launch_vnorm(n, c->d_V, c->d_V, c->d_gt, dinv, gs, cyc, sms, s));
+    c->launches += 4;
+    for (int j = 0; j < m; j++) {
+      double* Vn = c->d_V + (size_t)(j + 1) * n;
+      {
+        GateScope g(c, cyc);
+        SEM_TRY(apply_op(c, c->d_gt, w, sem::AX_APPLY));   // w = A M^-1 v_j
+      }
+      // two classical Gram-Schmidt passes against v_0..v_j, then ||w||_c
+      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, n, j + 1, part, tk, gs->h1, cyc, sms, s));
+      if (dist) SEM_TRY(allreduce(c, gs->h1, j + 1));
+      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, n, j + 1, gs->h1, -1.0, nullptr, mult, part, tk,
+                                 nullptr, cyc, sms, s));
+      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, n, j + 1, part, tk, gs->h2, cyc, sms, s));
+      if (dist) SEM_TRY(allreduce(c, gs->h2, j + 1));
+      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, n, j + 1, gs->h2, -1.0, nullptr, mult, part, tk,
+                                 &gs->norm2[0], cyc, sms, s));
+      if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
+      CUDA_TRY(sem::launch_gm_arnoldi(gs, st, c->d_hist, m, s));
+      CUDA_TRY(sem::launch_vnorm(n, w, Vn, c->d_gt, dinv, gs, cyc, sms, s));
+      c->launches += 6;
+      if ((j + 1) % kBatch == 0 && j + 1 < m) {   // poll: stop enqueuing a finished cycle
+        int cd = 0;
+        CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &gs->cycle_done, sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        cd = c->h_st->done;
+        if (cd) break;
+      }
+    }
+    // y = H^-1 g; x += M^-1 V y; converged / maxit -> done
+    CUDA_TRY(sem::launch_gm_solve(gs, st, m, s));
+    CUDA_TRY(sem::launch_maxpy(n, x, c->d_V, n, m, gs->y, 1.0, dinv, mult, part, tk, nullptr, done,
+                               sms, s));
+    CUDA_TRY(sem::launch_gm_end_cycle(gs, st, s));
+    c->launches += 3;
+    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    status_done = c->h_st->done;
+  }
+  // true residual once at the end (reading Q17)
+  SEM_TRY(apply_op(c, x, w, sem::AX_APPLY));
+  CUDA_TRY(sem::launch_resid(n, b, w, c->d_gt, mult, part, tk, &gs->norm2[1], nullptr, sms, s));
+  if (dist) SEM_TRY(allreduce(c, &gs->norm2[1], 1));
+  c->launches++;
+  sem::GmresState hg;
+  CUDA_TRY(cudaMemcpyAsync(&hg, gs, sizeof(hg), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(c->h_st, st, sizeof(sem::PcgState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  SEM_TRY(p2p_check(c));
+  const sem::PcgState& hs = *c->h_st;
+  c->last_hist = hs.iters;
+  if (res) {
+    res->iters = hs.iters;
+    res->res_final = hg.res;
+    res->res_true = std::sqrt(hg.norm2[1]);
+  }
+  int status = hs.done == 1 ? SEM_OK : SEM_NOT_CONVERGED;
+  if (res) res->status = status;
+  return status;
+}
+
+extern "C" int sem_gmres_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                               int32_t restart, sem_pcg_result* r) {
+  if (!c || !b || !x || !aligned16(b) || !aligned16(x) || b == x) {
+    sem::set_error("sem_gmres_solve: bad arguments");
+    return SEM_EINVAL;
+  }
+  return gmres_run(c, b, x, tol, maxit, restart, r);
+}
+
+// ---- solution projection (Fischer 1998): Z, AZ [m][n], A-orthonormal
+static int proj_alloc(sem_ctx* c, int m) {
+  if (m < 1 || m > sem::kGmMax) {
+    sem::set_error("projection dimension must be in [1, 32]");
+    return SEM_EINVAL;
+  }
+  SEM_TRY(gm_alloc(c, 1));
+  if (m == c->proj_m) return SEM_OK;
+  const size_t n = (size_t)c->hp.n_local;
+  double* bufs[4] = {c->d_Z, c->d_AZ, c->d_pdelta, c->d_pbd};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  c->d_Z = c->d_AZ = c->d_pdelta = c->d_pbd = nullptr;
+  SEM_TRY(dalloc(&c->d_Z, m * n));
+  SEM_TRY(dalloc(&c->d_AZ, m * n));
+  SEM_TRY(dalloc(&c->d_pdelta, n));
+  SEM_TRY(dalloc(&c->d_pbd, n));
+  c->proj_m = m;
+  c->proj_k = 0;
+  return SEM_OK;
+}
+
+// append x to the space (two CGS passes in the A inner product); returns 1 if skipped
+static int proj_update(sem_ctx* c, const double* x, int* skipped) {
+  cudaStream_t s = c->stream;
+  const int64_t n = c->hp.n_local;
+  const int sms = c->num_sms;
+  const bool dist = c->hp.nranks > 1;
+  sem::GmresState* gs = c->d_gs;
+  if (c->proj_k == c->proj_m) c->proj_k = 0;   // full: reset, keep the latest
+  const int k = c->proj_k;
+  double* z = c->d_Z + (size_t)k * n;
+  double* az = c->d_AZ + (size_t)k * n;
+  CUDA_TRY(cudaMemcpyAsync(z, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  SEM_TRY(apply_op(c, z, az, sem::AX_APPLY));
+  CUDA_TRY(sem::launch_mdot(n, c->d_mult, z, az, n, 1, c->d_kpart, c->d_ktick, &gs->norm2[0],
+                            nullptr, sms, s));
+  if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
+  for (int pass = 0; pass < 2 && k > 0; pass++) {
+    double* coef = pass == 0 ? gs->h1 : gs->h2;
+    CUDA_TRY(sem::launch_mdot(n, c->d_mult, az, c->d_Z, n, k, c->d_kpart, c->d_ktick, coef,
+                              nullptr, sms, s));
+    if (dist) SEM_TRY(allreduce(c, coef, k));
+    CUDA_TRY(sem::launch_maxpy(n, z, c->d_Z, n, k, coef, -1.0, nullptr, c->d_mult, c->d_kpart,
+                               c->d_ktick, nullptr, nullptr, sms, s));
+    CUDA_TRY(sem::launch_maxpy(n, az, c->d_AZ, n, k, coef, -1.0, nullptr, c->d_mult, c->d_kpart,
+                               c->d_ktick, nullptr, nullptr, sms, s));
+    c->launches += 3;
+  }
+  CUDA_TRY(sem::launch_mdot(n, c->d_mult, z, az, n, 1, c->d_kpart, c->d_ktick, &gs->norm2[1],
+                            nullptr, sms, s));
+  if (dist) SEM_TRY(allreduce(c, &gs->norm2[1], 1));
+  double nrm[2];
+  CUDA_TRY(cudaMemcpyAsync(nrm, &gs->norm2[0], sizeof(nrm), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  c->launches += 2;
+  const double nx = std::sqrt(std::fabs(nrm[0])), nz = std::sqrt(std::fabs(nrm[1]));
+  if (!(nz > 1e-12 * nx)) {
+    *skipped = 1;
+    return SEM_OK;
+  }
+  // z, az /= ||z||_A  (scale: y += (1/nz - 1) y via maxpy on itself would alias; use vnorm)
+  sem::GmresState* g = c->d_gs;
+  const double inv = 1.0 / nz;
+  CUDA_TRY(cudaMemcpyAsync(&g->inv_norm, &inv, sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(sem::launch_vnorm(n, z, z, nullptr, nullptr, g, nullptr, sms, s));
+  CUDA_TRY(sem::launch_vnorm(n, az, az, nullptr, nullptr, g, nullptr, sms, s));
+  c->launches += 2;
+  c->proj_k = k + 1;
+  *skipped = 0;
+  return SEM_OK;
+}
+
+extern "C" int sem_proj_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                              int32_t restart, int32_t m, sem_pcg_result* r) {
+  if (!c || !b || !x || !aligned16(b) || !aligned16(x) || b == x) {
+    sem::set_error("sem_proj_solve: bad arguments");
+    return SEM_EINVAL;
+  }
+  SEM_TRY(proj_alloc(c, m));
+  cudaStream_t s = c->stream;
+  const int64_t n = c->hp.n_local;
+  const int sms = c->num_sms;
+  sem::GmresState* gs = c->d_gs;
+  const int k = c->proj_k;
+  // x_bar = sum <z_i, b>_c z_i ; b_defl = b - sum <z_i, b>_c A z_i
+  CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  CUDA_TRY(cudaMemcpyAsync(c->d_pbd, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (k > 0) {
+    CUDA_TRY(sem::launch_mdot(n, c->d_mult, b, c->d_Z, n, k, c->d_kpart, c->d_ktick, gs->y,
+                              nullptr, sms, s));
+    if (c->hp.nranks > 1) SEM_TRY(allreduce(c, gs->y, k));
+    CUDA_TRY(sem::launch_maxpy(n, x, c->d_Z, n, k, gs->y, 1.0, nullptr, c->d_mult, c->d_kpart,
+                               c->d_ktick, nullptr, nullptr, sms, s));
+    CUDA_TRY(sem::launch_maxpy(n, c->d_pbd, c->d_AZ, n, k, gs->y, -1.0, nullptr, c->d_mult,
+                               c->d_kpart, c->d_ktick, nullptr, nullptr, sms, s));
+    c->launches += 3;
+  }
+  // delta: GMRES on the deflated right-hand side from 0; x = x_bar + delta
+  const int st = gmres_run(c, c->d_pbd, c->d_pdelta, tol, maxit, restart, r);
+  if (st < 0) return st;
+  CUDA_TRY(sem::launch_maxpy(n, x, c->d_pdelta, n, 1, &gs->one, 1.0, nullptr, c->d_mult,
+                             c->d_kpart, c->d_ktick, nullptr, nullptr, sms, s));
+  c->launches++;
+  int skipped = 0;
+  SEM_TRY(proj_update(c, x, &skipped));
+  return st;
+}
+
+extern "C" int sem_proj_reset(sem_ctx* c) {
+  if (!c) return SEM_EINVAL;
+  c->proj_k = 0;
+  return SEM_OK;
+}
+
+extern "C" int sem_proj_size(const sem_ctx* c, int32_t* k) {
+  if (!c || !k) return SEM_EINVAL;
+  *k = c->proj_k;
+  return SEM_OK;
 }
 
 extern "C" int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_host, double tol,

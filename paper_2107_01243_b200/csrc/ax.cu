@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
   __syncthreads();
   pdl_wait();   // u (= p) and the done flag come from the preceding kernel
   pdl_trigger();
-  if (MODE == AX_PCG && *a.done) return;
+  if ((MODE == AX_PCG || a.gate) && *a.done) return;
 
   const int r0lo = a.r0lo, r0hi = a.r0hi, r1lo = a.r1lo, r1hi = a.r1hi;
   const int ng0 = (r0hi - r0lo + NE - 1) / NE, ng1 = (r1hi - r1lo + NE - 1) / NE, ng = ng0 + ng1;

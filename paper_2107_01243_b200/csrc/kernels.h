@@ -79,6 +79,18 @@ struct PcgState {
   unsigned tickets[8];   // last-block tickets
 };
 
+// restarted GMRES state (krylov.cu), device-resident; restart <= kGmMax - 1
+constexpr int kGmMax = 32;
+struct GmresState {
+  double H[(kGmMax + 1) * kGmMax];   // Hessenberg, row stride kGmMax (rotated in place)
+  double cs[kGmMax], sn[kGmMax];     // Givens rotations
+  double g[kGmMax + 1], y[kGmMax];   // rotated residual vector, solution coefficients
+  double h1[kGmMax], h2[kGmMax];     // the two CGS passes' projections
+  double norm2[2];                   // c-weighted squared norms (reduction outputs)
+  double inv_norm, res, one;         // 1/||.|| for the next basis vector; |g_{j+1}|; 1.0
+  int j, jy, cycle_done, converged;  // Arnoldi step, back-substituted size, gates
+};
+
 struct AxLaunch {
   const double* u;
   double* w;
@@ -93,6 +105,7 @@ struct AxLaunch {
   // Helmholtz variant (NEXT-2): w = h1 A_L u + h2 B_L u before gs and mask
   const double* B;
   double h1, h2;
+  int gate;                       // 1: any mode returns early when *done (GMRES cycle gate)
 };
 
 // NVLink peer-memory collectives (p2p.cu): mailbox layout and device view
@@ -134,6 +147,24 @@ cudaError_t launch_gs_exchange_p2p(const DevPlan& P, double* u, double* part, co
 cudaError_t launch_gs_unpack_p2p(const DevPlan& P, double* u, const double* part, const P2P& c,
                                  uint64_t epoch, int apply_mask, PcgState* st, int nparts,
                                  uint64_t e_sig, cudaStream_t s);
+// Krylov BLAS-1 (krylov.cu); every kernel is skipped when *done (nullptr: never)
+cudaError_t launch_mdot(int64_t n, const uint8_t* mult, const double* a, const double* V,
+                        int64_t ldv, int K, double* part, unsigned* ticket, double* out,
+                        const int* done, int num_sms, cudaStream_t s);
+cudaError_t launch_maxpy(int64_t n, double* y, const double* V, int64_t ldv, int K,
+                         const double* coef, double alpha, const double* dinv, const uint8_t* mult,
+                         double* part, unsigned* ticket, double* out_norm, const int* done,
+                         int num_sms, cudaStream_t s);
+cudaError_t launch_resid(int64_t n, const double* b, const double* w, double* v,
+                         const uint8_t* mult, double* part, unsigned* ticket, double* out,
+                         const int* done, int num_sms, cudaStream_t s);
+cudaError_t launch_vnorm(int64_t n, const double* w, double* v, double* t, const double* dinv,
+                         const GmresState* gs, const int* done, int num_sms, cudaStream_t s);
+cudaError_t launch_gm_start(GmresState* gs, PcgState* st, double* hist, cudaStream_t s);
+cudaError_t launch_gm_arnoldi(GmresState* gs, PcgState* st, double* hist, int m, cudaStream_t s);
+cudaError_t launch_gm_solve(GmresState* gs, PcgState* st, int m, cudaStream_t s);
+cudaError_t launch_gm_end_cycle(GmresState* gs, PcgState* st, cudaStream_t s);
+
 // interconnect probes for the performance model: one-thread ping-pong
 // with `peer` (round-trip ns per sample), and one-sided peer writes (bandwidth)
 cudaError_t launch_p2p_pingpong(const P2P& c, int peer, int iters, uint64_t e0, long long* out,

@@ -1,0 +1,309 @@
+// Restarted GMRES and the solution-projection space on the device (SURVEY
+// 8(f) NEXT-3; Table 2 "GMRES ... Projections 20"; Fischer
+// 1998).  HBM-bound BLAS-1 work fused per pass:
+//   * mdot: k c-weighted dots <a, V_i>_c of one vector against k basis vectors
+//     in one read of a and the k vectors ((k+1)*8 B/pt), per-block partials
+//     summed in a fixed order by the last block (deterministic);
+//   * maxpy: y += alpha * D * sum_i coef_i V_i (D = dinv or 1), optionally with
+//     the c-weighted squared norm of the result in the same pass;
+//   * the Hessenberg / Givens bookkeeping runs in one device thread on a
+//     device-resident state, so an Arnoldi step needs no host round trip.
+// Arnoldi orthogonalisation is classical Gram-Schmidt applied twice (CGS2):
+// two fused passes instead of the oracle's j+1 sequential MGS updates; equal
+// in exact arithmetic, and as stable as MGS with the second pass.
+#include <cmath>
+#include <cstdint>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace sem {
+namespace dev {
+
+constexpr int kKT = 256;   // threads per block of the vector kernels
+
+__device__ __forceinline__ double c_of_k(uint8_t m) { return __drcp_rn((double)m); }
+
+// fixed-order reduction of K per-block partials (part[b*K + i]) by the last
+// block to arrive; returns true in that block (after out[] is written)
+template <int KMAX>
+__device__ __forceinline__ void reduce_cols(const double* acc, int K, double* part, unsigned* ticket,
+                                            double* out, double* s_w) {
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < KMAX; i++) {   // compile-time indices keep acc[] in registers
+    if (i < K) {
+      double v = warp_sum(acc[i]);
+      if (lane == 0) s_w[warp * KMAX + i] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double v = s_w[threadIdx.x];
+    for (int q = 1; q < nw; q++) v += s_w[q * KMAX + threadIdx.x];
+    part[(size_t)blockIdx.x * K + threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < K) {
+    double v = 0.0;
+    for (unsigned b = 0; b < gridDim.x; b++) v += __ldcg(&part[(size_t)b * K + threadIdx.x]);
+    out[threadIdx.x] = v;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// out[i] = <a, V_i>_c, i < K (V_i = V + i*ldv); skipped when *done
+template <int KMAX>
+__global__ void __launch_bounds__(kKT) mdot_kernel(int64_t n, const uint8_t* __restrict__ mult,
+                                                   const double* __restrict__ a,
+                                                   const double* __restrict__ V, int64_t ldv, int K,
+                                                   double* part, unsigned* ticket, double* out,
+                                                   const int* done) {
+  __shared__ double s_w[(kKT / 32) * KMAX];
+  if (done && *done) return;
+  double acc[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; i++) acc[i] = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double ca = c_of_k(mult[l]) * a[l];
+#pragma unroll
+    for (int i = 0; i < KMAX; i++)
+      if (i < K) acc[i] = fma(ca, __ldcs(&V[i * ldv + l]), acc[i]);
+  }
+  reduce_cols<KMAX>(acc, K, part, ticket, out, s_w);
+}
+
+// y += alpha * (dinv ? dinv : 1) * sum_{i<K} coef[i] V_i ; NORM: out_norm = <y, y>_c
+template <int KMAX, bool NORM>
+__global__ void __launch_bounds__(kKT) maxpy_kernel(int64_t n, double* __restrict__ y,
+                                                    const double* __restrict__ V, int64_t ldv, int K,
+                                                    const double* __restrict__ coef, double alpha,
+                                                    const double* __restrict__ dinv,
+                                                    const uint8_t* __restrict__ mult, double* part,
+                                                    unsigned* ticket, double* out_norm,
+                                                    const int* done) {
+  __shared__ double s_w[(kKT / 32) * 1];
+  __shared__ double s_c[KMAX];
+  if (done && *done) return;
+  if (threadIdx.x < K) s_c[threadIdx.x] = alpha * coef[threadIdx.x];
+  __syncthreads();
+  double nrm[1] = {0.0};
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++)
+      if (i < K) s = fma(s_c[i], __ldcs(&V[i * ldv + l]), s);
+    const double v = y[l] + (dinv ? dinv[l] * s : s);
+    y[l] = v;
+    if (NORM) nrm[0] = fma(c_of_k(mult[l]) * v, v, nrm[0]);
+  }
+  if (NORM) reduce_cols<1>(nrm, 1, part, ticket, out_norm, s_w);
+}
+
+// v = (b - w) (restart residual) with its c-norm^2, or v = w with its c-norm^2
+__global__ void __launch_bounds__(kKT) resid_kernel(int64_t n, const double* __restrict__ b,
+                                                    const double* __restrict__ w,
+                                                    double* __restrict__ v,
+                                                    const uint8_t* __restrict__ mult, double* part,
+                                                    unsigned* ticket, double* out, const int* done) {
+  __shared__ double s_w[kKT / 32];
+  if (done && *done) return;
+  double acc[1] = {0.0};
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double r = b ? b[l] - w[l] : w[l];
+    v[l] = r;
+    acc[0] = fma(c_of_k(mult[l]) * r, r, acc[0]);
+  }
+  reduce_cols<1>(acc, 1, part, ticket, out, s_w);
+}
+
+// v = w / norm, t = dinv v (the next Arnoldi direction, preconditioned)
+__global__ void __launch_bounds__(kKT) vnorm_kernel(int64_t n, const double* __restrict__ w,
+                                                    double* __restrict__ v, double* __restrict__ t,
+                                                    const double* __restrict__ dinv,
+                                                    const GmresState* gs, const int* done) {
+  if (done && *done) return;
+  const double s = gs->inv_norm;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double x = w[l] * s;
+    v[l] = x;
+    if (t) t[l] = dinv[l] * x;
+  }
+}
+
+// start of a cycle: beta = sqrt(norm2); converged if beta <= tol
+__global__ void gm_start_kernel(GmresState* gs, PcgState* st, double* hist) {
+  if (st->done) return;
+  if (st->it == 0) gs->converged = 0;   // a new solve
+  const double beta = sqrt(gs->norm2[0]);
+  gs->j = 0;
+  gs->g[0] = beta;
+  for (int i = 1; i <= kGmMax; i++) gs->g[i] = 0.0;
+  gs->res = beta;
+  if (st->it == 0) hist[0] = beta;
+  if (beta <= st->tol) {
+    st->done = 1;
+    st->iters = st->it;
+    gs->cycle_done = 1;
+    return;
+  }
+  if (st->it >= st->maxit) {
+    st->done = 4;
+    st->iters = st->it;
+    gs->cycle_done = 1;
+    return;
+  }
+  gs->inv_norm = 1.0 / beta;
+  gs->cycle_done = 0;
+}
+
+// Arnoldi step j: H[0..j][j] = h1 + h2 (two CGS passes), H[j+1][j] = ||w||_c;
+// Givens rotations; |g_{j+1}| = residual; cycle end at convergence, maxit or
+// the restart length (the outer loop then solves H y = g and updates x)
+__global__ void gm_arnoldi_kernel(GmresState* gs, PcgState* st, double* hist, int m) {
+  if (st->done || gs->cycle_done) return;
+  const int j = gs->j;
+  double* H = gs->H;
+  for (int i = 0; i <= j; i++) H[i * kGmMax + j] = gs->h1[i] + gs->h2[i];
+  const double hn = sqrt(gs->norm2[0]);
+  H[(j + 1) * kGmMax + j] = hn;
+  for (int i = 0; i < j; i++) {
+    const double a = H[i * kGmMax + j], b = H[(i + 1) * kGmMax + j];
+    H[i * kGmMax + j] = gs->cs[i] * a + gs->sn[i] * b;
+    H[(i + 1) * kGmMax + j] = -gs->sn[i] * a + gs->cs[i] * b;
+  }
+  const double a = H[j * kGmMax + j], b = H[(j + 1) * kGmMax + j];
+  const double r = sqrt(a * a + b * b);
+  gs->cs[j] = r > 0.0 ? a / r : 1.0;
+  gs->sn[j] = r > 0.0 ? b / r : 0.0;
+  H[j * kGmMax + j] = r;
+  H[(j + 1) * kGmMax + j] = 0.0;
+  gs->g[j + 1] = -gs->sn[j] * gs->g[j];
+  gs->g[j] = gs->cs[j] * gs->g[j];
+  const double res = fabs(gs->g[j + 1]);
+  gs->res = res;
+  const int it = st->it + 1;
+  st->it = it;
+  hist[it] = res;
+  gs->j = j + 1;
+  gs->inv_norm = hn > 0.0 ? 1.0 / hn : 0.0;
+  const bool conv = res <= st->tol || hn == 0.0;
+  if (conv || it >= st->maxit || j + 1 == m) gs->cycle_done = 1;
+  if (conv) gs->converged = 1;
+}
+
+// y = H(0:j,0:j)^-1 g(0:j) (back substitution), jy = j; y beyond j zeroed
+__global__ void gm_solve_kernel(GmresState* gs, PcgState* st, int m) {
+  if (st->done) return;
+  const int j = gs->j;
+  for (int i = j; i < m; i++) gs->y[i] = 0.0;
+  for (int i = j - 1; i >= 0; i--) {
+    double s = gs->g[i];
+    for (int q = i + 1; q < j; q++) s -= gs->H[i * kGmMax + q] * gs->y[q];
+    gs->y[i] = s / gs->H[i * kGmMax + i];
+  }
+  gs->jy = j;
+}
+
+// after the x update: converged or out of iterations -> done
+__global__ void gm_end_cycle_kernel(GmresState* gs, PcgState* st) {
+  if (st->done) return;
+  if (gs->converged) {
+    st->done = 1;
+    st->iters = st->it;
+  } else if (st->it >= st->maxit) {
+    st->done = 4;
+    st->iters = st->it;
+  }
+}
+
+}  // namespace dev
+
+static int kgrid(int64_t n, int num_sms) {
+  int64_t g = (n + dev::kKT - 1) / dev::kKT;
+  const int cap = num_sms * 4;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+cudaError_t launch_mdot(int64_t n, const uint8_t* mult, const double* a, const double* V,
+                        int64_t ldv, int K, double* part, unsigned* ticket, double* out,
+                        const int* done, int num_sms, cudaStream_t s) {
+  const int g = kgrid(n, num_sms);
+  if (K <= 8)
+    dev::mdot_kernel<8><<<g, dev::kKT, 0, s>>>(n, mult, a, V, ldv, K, part, ticket, out, done);
+  else
+    dev::mdot_kernel<32><<<g, dev::kKT, 0, s>>>(n, mult, a, V, ldv, K, part, ticket, out, done);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpy(int64_t n, double* y, const double* V, int64_t ldv, int K,
+                         const double* coef, double alpha, const double* dinv, const uint8_t* mult,
+                         double* part, unsigned* ticket, double* out_norm, const int* done,
+                         int num_sms, cudaStream_t s) {
+  const int g = kgrid(n, num_sms);
+  const bool nrm = out_norm != nullptr;
+  if (K <= 8) {
+    if (nrm)
+      dev::maxpy_kernel<8, true><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv, mult,
+                                                        part, ticket, out_norm, done);
+    else
+      dev::maxpy_kernel<8, false><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv, mult,
+                                                         part, ticket, out_norm, done);
+  } else {
+    if (nrm)
+      dev::maxpy_kernel<32, true><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv, mult,
+                                                         part, ticket, out_norm, done);
+    else
+      dev::maxpy_kernel<32, false><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv,
+                                                          mult, part, ticket, out_norm, done);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resid(int64_t n, const double* b, const double* w, double* v,
+                         const uint8_t* mult, double* part, unsigned* ticket, double* out,
+                         const int* done, int num_sms, cudaStream_t s) {
+  dev::resid_kernel<<<kgrid(n, num_sms), dev::kKT, 0, s>>>(n, b, w, v, mult, part, ticket, out,
+                                                          done);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vnorm(int64_t n, const double* w, double* v, double* t, const double* dinv,
+                         const GmresState* gs, const int* done, int num_sms, cudaStream_t s) {
+  dev::vnorm_kernel<<<kgrid(n, num_sms), dev::kKT, 0, s>>>(n, w, v, t, dinv, gs, done);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gm_start(GmresState* gs, PcgState* st, double* hist, cudaStream_t s) {
+  dev::gm_start_kernel<<<1, 1, 0, s>>>(gs, st, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gm_arnoldi(GmresState* gs, PcgState* st, double* hist, int m, cudaStream_t s) {
+  dev::gm_arnoldi_kernel<<<1, 1, 0, s>>>(gs, st, hist, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gm_solve(GmresState* gs, PcgState* st, int m, cudaStream_t s) {
+  dev::gm_solve_kernel<<<1, 1, 0, s>>>(gs, st, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gm_end_cycle(GmresState* gs, PcgState* st, cudaStream_t s) {
+  dev::gm_end_cycle_kernel<<<1, 1, 0, s>>>(gs, st);
+  return cudaGetLastError();
+}
+
+}  // namespace sem
