@@ -84,6 +84,18 @@ def lib():
         L.oracle_proj_solve.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int,
                                         C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.oracle_proj_gram.argtypes = [C.c_void_p, _D]
+        L.oracle_proj_set_schwarz.argtypes = [C.c_void_p, C.c_void_p]
+        L.oracle_schwarz_create.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_schwarz_free.argtypes = [C.c_void_p]
+        L.oracle_schwarz_free.restype = None
+        L.oracle_schwarz_local_matrix.argtypes = [C.c_void_p, C.c_int64, _D]
+        L.oracle_schwarz_apply.argtypes = [C.c_void_p, _D, _D, C.c_int]
+        L.oracle_schwarz_pcg.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int,
+                                         C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double), C.c_void_p]
+        L.oracle_schwarz_gmres.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int,
+                                           C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.c_void_p]
         L.oracle_plan.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 3 + [C.c_void_p] * 3
         L.oracle_shared.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                     C.c_void_p]
@@ -255,6 +267,9 @@ class Oracle:
     def proj(self, m: int = 20):
         return Proj(self, m)
 
+    def schwarz(self, coarse_iters: int = 10):
+        return Schwarz(self, coarse_iters)
+
     def plan(self):
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
         lib().oracle_plan(self._h, C.byref(a), C.byref(b), C.byref(c), None, None, None)
@@ -303,6 +318,11 @@ class Proj:
         """True if x was appended, False if skipped (negligible new direction)."""
         return lib().oracle_proj_update(self._h, _f64(x)) == 0
 
+    def set_schwarz(self, s: "Schwarz | None"):
+        """NEXT-1 pipeline: projection + flexible GMRES + Schwarz (None: Jacobi)."""
+        self._schw = s   # keep it alive
+        assert lib().oracle_proj_set_schwarz(self._h, s._h if s is not None else None) == 0
+
     def solve(self, b, tol: float, maxit: int, restart: int = 30):
         x = np.zeros(self.o.nslots)
         it, rf = C.c_int(), C.c_double()
@@ -317,3 +337,55 @@ class Proj:
         G = np.zeros(k * k)
         assert lib().oracle_proj_gram(self._h, G) == 0
         return G.reshape(k, k)
+
+
+class Schwarz:
+    """Two-level additive overlapping Schwarz of the oracle (NEXT-1; P:L257-261;
+    readings Q28-Q32 in DESIGN.md)."""
+
+    def __init__(self, o: "Oracle", coarse_iters: int = 10):
+        self.o = o
+        h = C.c_void_p()
+        st = lib().oracle_schwarz_create(o._h, coarse_iters, C.byref(h))
+        if st != 0:
+            raise OracleError(f"oracle_schwarz_create failed with status {st}")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value and _lib is not None:
+            _lib.oracle_schwarz_free(self._h)
+            self._h = None
+
+    def local_matrix(self, e: int):
+        n3 = self.o.n ** 3
+        A = np.zeros(n3 * n3)
+        assert lib().oracle_schwarz_local_matrix(self._h, e, A) == 0
+        return A.reshape(n3, n3)
+
+    def apply(self, r, which: int = 3):
+        z = np.zeros(self.o.nslots)
+        assert lib().oracle_schwarz_apply(self._h, _f64(r), z, which) == 0
+        return z
+
+    def pcg(self, b, tol: float, maxit: int):
+        x = np.zeros(self.o.nslots)
+        it, rf, rt = C.c_int(), C.c_double(), C.c_double()
+        hist = np.zeros(maxit + 1)
+        st = lib().oracle_schwarz_pcg(self._h, _f64(b), x, tol, maxit, C.byref(it), C.byref(rf),
+                                      C.byref(rt), hist.ctypes.data_as(C.c_void_p))
+        if st < 0:
+            raise OracleError(f"oracle_schwarz_pcg failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
+                "status": st, "hist": hist[: it.value + 1]}
+
+    def gmres(self, b, tol: float, maxit: int, restart: int = 30):
+        x = np.zeros(self.o.nslots)
+        it, rf, rt = C.c_int(), C.c_double(), C.c_double()
+        hist = np.zeros(maxit + 1)
+        st = lib().oracle_schwarz_gmres(self._h, _f64(b), x, tol, maxit, restart, C.byref(it),
+                                        C.byref(rf), C.byref(rt),
+                                        hist.ctypes.data_as(C.c_void_p))
+        if st < 0:
+            raise OracleError(f"oracle_schwarz_gmres failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
+                "status": st, "hist": hist[: it.value + 1]}

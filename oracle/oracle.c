@@ -756,6 +756,7 @@ int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, in
    up to m A-orthonormal directions z_i (with A z_i stored), <z_i, A z_j>_c = d_ij. */
 struct oracle_proj {
   const oracle_ctx* c;
+  const oracle_schwarz* schw;   /* NULL: Jacobi GMRES; else flexible GMRES + Schwarz */
   int m, k;
   double *Z, *AZ;   /* [m][nslots] */
 };
@@ -779,6 +780,7 @@ void oracle_proj_free(oracle_proj* p) {
 }
 
 int oracle_proj_size(const oracle_proj* p) { return p ? p->k : -1; }
+
 
 /* x_bar = sum_i <z_i, b>_c z_i, b_defl = b - sum_i <z_i, b>_c A z_i (= b - A x_bar) */
 int oracle_proj_project(const oracle_proj* p, const double* b, double* xbar, double* bdefl) {
@@ -838,7 +840,9 @@ int oracle_proj_solve(oracle_proj* p, const double* b, double* x, double tol, in
   if (!xb || !bd) { free(xb); free(bd); return -5; }
   oracle_proj_project(p, b, xb, bd);
   for (int64_t l = 0; l < ns; l++) x[l] = 0.0;
-  int st = oracle_gmres(p->c, bd, x, tol, maxit, restart, iters, res_final, NULL, NULL);
+  int st = p->schw ? oracle_schwarz_gmres(p->schw, bd, x, tol, maxit, restart, iters,
+                                          res_final, NULL, NULL)
+                  : oracle_gmres(p->c, bd, x, tol, maxit, restart, iters, res_final, NULL, NULL);
   for (int64_t l = 0; l < ns; l++) x[l] += xb[l];
   if (st >= 0) oracle_proj_update(p, x);
   free(xb); free(bd);
@@ -851,6 +855,456 @@ int oracle_proj_gram(const oracle_proj* p, double* G) {
   for (int i = 0; i < p->k; i++)
     for (int j = 0; j < p->k; j++)
       G[i * p->k + j] = oracle_dot_c(p->c, p->Z + (int64_t)i * ns, p->AZ + (int64_t)j * ns);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* NEXT-1: two-level additive overlapping Schwarz preconditioner        */
+/* (M0^-1 = R0^T A0^-1 R0 + sum_k R_k^T A~_k^-1 R_k; "the   */
+/* coarse grid (on linear elements) is solved for using an approximate  */
+/* Krylov solver, in essence performing few (~10) CG iterations").      */
+/* Readings Q28-Q31:                                         */
+/*  Q28 subdomain k = the closed node set of element k (overlap of one   */
+/*      node layer into every neighbour, homogeneous Dirichlet on the    */
+/*      next layer); A~_k = the separable operator                       */
+/*      Bz (x) By (x) Ax + Bz (x) Ay (x) Bx + Az (x) By (x) Bx with the   */
+/*      1-D SEM stiffness/mass of the element extended by the            */
+/*      neighbours' end entries (element lengths = mean edge length).   */
+/*      On Cartesian meshes this is exactly the principal submatrix of   */
+/*      the assembled A on the element's unmasked nodes.                 */
+/*  Q29 weights: c^(1/2) on input and output of the local sum, so M      */
+/*      stays symmetric: z_loc = c^1/2 QQ^T (A~^-1 (c^1/2 r))_L          */
+/*  Q30 coarse space: the N = 1 discretisation on the same mesh; R0^T    */
+/*      interpolates vertex values trilinearly (J_ia = (1 -+ xi_i)/2),   */
+/*      R0 is its transpose (c-weighted, then summed); periodic: the     */
+/*      coarse right-hand side loses its unique-DOF mean.               */
+/*  Q31 coarse solve: plain CG from 0, at most K0 iterations, stopped    */
+/*      early when ||r||_c <= 1e-12 ||b0||_c or p^T A0 p <= 0.           */
+/* The local inverse is computed from its definition: the dense          */
+/* n^3 x n^3 matrix A~_k is assembled and Cholesky-factored.            */
+struct oracle_schwarz {
+  const oracle_ctx* c;
+  oracle_ctx* c0;        /* the N = 1 coarse space on the same mesh */
+  int K0;
+  double* L;             /* [E][n3*n3] Cholesky factors (masked rows: identity) */
+  double* sqc;           /* c^1/2 per slot */
+};
+
+/* 1-D reference stiffness Ah_ij = sum_q w_q D_qi D_qj (exact for degree 2N-2) */
+static void ref_stiff_1d(const oracle_ctx* c, double* Ah) {
+  const int n = c->n;
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < n; j++) {
+      double s = 0.0;
+      for (int q = 0; q < n; q++) s += c->w[q] * c->D[q * n + i] * c->D[q * n + j];
+      Ah[i * n + j] = s;
+    }
+}
+
+/* mean length of element e along axis a: the four element edges parallel to
+   a, straight vertex-to-vertex distances (reading Q28) */
+static double elem_len(const oracle_ctx* c, int64_t e, int a) {
+  const int n = c->n, N = c->N;
+  double s = 0.0;
+  for (int u = 0; u < 2; u++)
+    for (int v = 0; v < 2; v++) {
+      int i0[3], i1[3];
+      int o1 = u * N, o2 = v * N;
+      if (a == 0) { i0[0] = 0; i1[0] = N; i0[1] = i1[1] = o1; i0[2] = i1[2] = o2; }
+      else if (a == 1) { i0[1] = 0; i1[1] = N; i0[0] = i1[0] = o1; i0[2] = i1[2] = o2; }
+      else { i0[2] = 0; i1[2] = N; i0[0] = i1[0] = o1; i0[1] = i1[1] = o2; }
+      int64_t l0 = e * c->n3 + i0[0] + n * i0[1] + (int64_t)n * n * i0[2];
+      int64_t l1 = e * c->n3 + i1[0] + n * i1[1] + (int64_t)n * n * i1[2];
+      double dx = c->X[l1] - c->X[l0], dy = c->Y[l1] - c->Y[l0], dz = c->Z[l1] - c->Z[l0];
+      s += sqrt(dx * dx + dy * dy + dz * dz);
+    }
+  return 0.25 * s;
+}
+
+/* the extended 1-D operators of element e along axis a (n x n, mass diagonal) */
+static void ext_1d(const oracle_ctx* c, const double* Ah, int64_t e, int a, double* A1,
+                   double* B1) {
+  const int n = c->n, N = c->N;
+  const oracle_mesh* m = &c->m;
+  const int64_t Ea[3] = {m->ex, m->ey, m->ez};
+  int64_t idx[3] = {e % m->ex, (e / m->ex) % m->ey, e / ((int64_t)m->ex * m->ey)};
+  const double h = elem_len(c, e, a);
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < n; j++) A1[i * n + j] = (2.0 / h) * Ah[i * n + j];
+  for (int i = 0; i < n; i++) B1[i] = 0.5 * h * c->w[i];
+  for (int side = 0; side < 2; side++) {
+    int64_t q = idx[a] + (side ? 1 : -1);
+    if (q < 0 || q >= Ea[a]) {
+      if (!m->periodic[a]) continue;      /* Dirichlet face: no neighbour */
+      q = (q + Ea[a]) % Ea[a];
+    }
+    int64_t nb[3] = {idx[0], idx[1], idx[2]};
+    nb[a] = q;
+    const int64_t en = nb[0] + m->ex * (nb[1] + (int64_t)m->ey * nb[2]);
+    const double hn = elem_len(c, en, a);
+    if (side == 0) {   /* left neighbour: its node N coincides with our node 0 */
+      A1[0] += (2.0 / hn) * Ah[N * n + N];
+      B1[0] += 0.5 * hn * c->w[N];
+    } else {
+      A1[N * n + N] += (2.0 / hn) * Ah[0];
+      B1[N] += 0.5 * hn * c->w[0];
+    }
+  }
+}
+
+/* dense A~_e (n3 x n3, row-major, p = i + n j + n^2 k); masked rows and
+   columns are zero */
+static void local_matrix(const oracle_ctx* c, const double* Ah, int64_t e, double* A) {
+  const int n = c->n;
+  const int64_t n3 = c->n3;
+  double* A1 = (double*)malloc(sizeof(double) * 3 * n * n);
+  double* B1 = (double*)malloc(sizeof(double) * 3 * n);
+  for (int a = 0; a < 3; a++) ext_1d(c, Ah, e, a, A1 + a * n * n, B1 + a * n);
+  const double *Ax = A1, *Ay = A1 + n * n, *Az = A1 + 2 * n * n;
+  const double *Bx = B1, *By = B1 + n, *Bz = B1 + 2 * n;
+  for (int64_t p = 0; p < n3; p++) {
+    const int i = (int)(p % n), j = (int)((p / n) % n), k = (int)(p / ((int64_t)n * n));
+    for (int64_t q = 0; q < n3; q++) {
+      const int i2 = (int)(q % n), j2 = (int)((q / n) % n), k2 = (int)(q / ((int64_t)n * n));
+      double v = 0.0;
+      if (k == k2 && j == j2) v += Bz[k] * By[j] * Ax[i * n + i2];
+      if (k == k2 && i == i2) v += Bz[k] * Ay[j * n + j2] * Bx[i];
+      if (j == j2 && i == i2) v += Az[k * n + k2] * By[j] * Bx[i];
+      const int mp = c->mask[e * n3 + p], mq = c->mask[e * n3 + q];
+      A[p * n3 + q] = (mp || mq) ? 0.0 : v;
+    }
+  }
+  free(A1);
+  free(B1);
+}
+
+/* in-place Cholesky A = L L^T (lower triangle); returns -6 if not SPD */
+static int cholesky(double* A, int64_t m) {
+  for (int64_t j = 0; j < m; j++) {
+    double d = A[j * m + j];
+    for (int64_t k = 0; k < j; k++) d -= A[j * m + k] * A[j * m + k];
+    if (!(d > 0.0)) return -6;
+    const double ljj = sqrt(d);
+    A[j * m + j] = ljj;
+    for (int64_t i = j + 1; i < m; i++) {
+      double s = A[i * m + j];
+      for (int64_t k = 0; k < j; k++) s -= A[i * m + k] * A[j * m + k];
+      A[i * m + j] = s / ljj;
+    }
+  }
+  return 0;
+}
+
+int oracle_schwarz_create(const oracle_ctx* c, int coarse_iters, oracle_schwarz** out) {
+  if (!c || !out || coarse_iters < 0) return -1;
+  *out = NULL;
+  oracle_schwarz* s = (oracle_schwarz*)calloc(1, sizeof(oracle_schwarz));
+  if (!s) return -5;
+  s->c = c;
+  s->K0 = coarse_iters;
+  const int64_t n3 = c->n3, E = c->E;
+  s->L = (double*)malloc(sizeof(double) * E * n3 * n3);
+  s->sqc = (double*)malloc(sizeof(double) * c->nslots);
+  double* Ah = (double*)malloc(sizeof(double) * c->n * c->n);
+  if (!s->L || !s->sqc || !Ah) { free(Ah); oracle_schwarz_free(s); return -5; }
+  for (int64_t l = 0; l < c->nslots; l++) s->sqc[l] = sqrt(c->c[l]);
+  ref_stiff_1d(c, Ah);
+  int st = 0;
+  for (int64_t e = 0; e < E && !st; e++) {
+    double* A = s->L + e * n3 * n3;
+    local_matrix(c, Ah, e, A);
+    for (int64_t p = 0; p < n3; p++)
+      if (c->mask[e * n3 + p]) A[p * n3 + p] = 1.0;
+    st = cholesky(A, n3);
+  }
+  free(Ah);
+  if (!st) st = oracle_setup(&c->m, 1, 1, &s->c0);
+  if (st) { oracle_schwarz_free(s); return st; }
+  *out = s;
+  return 0;
+}
+
+void oracle_schwarz_free(oracle_schwarz* s) {
+  if (!s) return;
+  if (s->c0) oracle_free(s->c0);
+  free(s->L); free(s->sqc); free(s);
+}
+
+int oracle_schwarz_local_matrix(const oracle_schwarz* s, int64_t e, double* A) {
+  if (!s || e < 0 || e >= s->c->E) return -1;
+  double* Ah = (double*)malloc(sizeof(double) * s->c->n * s->c->n);
+  if (!Ah) return -5;
+  ref_stiff_1d(s->c, Ah);
+  local_matrix(s->c, Ah, e, A);
+  free(Ah);
+  return 0;
+}
+
+/* the coarse correction z_c = R0^T A0^-1 R0 r (readings Q30, Q31) */
+static int coarse_correction(const oracle_schwarz* s, const double* r, double* zc) {
+  const oracle_ctx* c = s->c;
+  const oracle_ctx* c0 = s->c0;
+  const int n = c->n;
+  const int64_t n3 = c->n3, ns0 = c0->nslots;
+  double J[2 * 12];   /* J[i*2 + a]: vertex a's linear basis at xi_i */
+  for (int i = 0; i < n; i++) {
+    J[i * 2 + 0] = 0.5 * (1.0 - c->xi[i]);
+    J[i * 2 + 1] = 0.5 * (1.0 + c->xi[i]);
+  }
+  double* b0 = (double*)calloc(ns0, sizeof(double));
+  double* x0 = (double*)calloc(ns0, sizeof(double));
+  double* r0 = (double*)malloc(sizeof(double) * ns0);
+  double* p0 = (double*)malloc(sizeof(double) * ns0);
+  double* w0 = (double*)malloc(sizeof(double) * ns0);
+  if (!b0 || !x0 || !r0 || !p0 || !w0) { free(b0); free(x0); free(r0); free(p0); free(w0); return -5; }
+  /* R0 r: per element (J^T (x) J^T (x) J^T)(c r_e), then QQ^T on the coarse space, mask */
+  for (int64_t e = 0; e < c->E; e++)
+    for (int v = 0; v < 8; v++) {
+      const int a = v & 1, b = (v >> 1) & 1, cc = v >> 2;
+      double sacc = 0.0;
+      for (int k = 0; k < n; k++)
+        for (int j = 0; j < n; j++)
+          for (int i = 0; i < n; i++) {
+            const int64_t l = e * n3 + i + n * j + (int64_t)n * n * k;
+            sacc += J[i * 2 + a] * J[j * 2 + b] * J[k * 2 + cc] * (c->c[l] * r[l]);
+          }
+      b0[e * 8 + v] = sacc;
+    }
+  oracle_gs(c0, b0);
+  oracle_mask_apply(c0, b0);
+  if (c0->fully_periodic) {   /* remove the unique-DOF mean (b0 in range(A0)) */
+    double sb = 0.0, sc = 0.0;
+    for (int64_t l = 0; l < ns0; l++) { sb += c0->c[l] * b0[l]; sc += c0->c[l]; }
+    const double mean = sb / sc;
+    for (int64_t l = 0; l < ns0; l++) b0[l] -= mean;
+  }
+  /* plain CG, x0 = 0, at most K0 iterations */
+  for (int64_t l = 0; l < ns0; l++) { r0[l] = b0[l]; p0[l] = b0[l]; }
+  double rho = oracle_dot_c(c0, r0, r0);
+  const double stop = 1e-12 * sqrt(rho);
+  for (int k = 0; k < s->K0 && rho > 0.0; k++) {
+    oracle_apply(c0, p0, w0);
+    const double sigma = oracle_dot_c(c0, p0, w0);
+    if (!(sigma > 0.0)) break;
+    const double alpha = rho / sigma;
+    for (int64_t l = 0; l < ns0; l++) {
+      x0[l] += alpha * p0[l];
+      r0[l] -= alpha * w0[l];
+    }
+    const double gamma = oracle_dot_c(c0, r0, r0);
+    if (sqrt(gamma) <= stop) break;
+    const double beta = gamma / rho;
+    rho = gamma;
+    for (int64_t l = 0; l < ns0; l++) p0[l] = r0[l] + beta * p0[l];
+  }
+  /* R0^T x0: trilinear interpolation of the element's vertex values */
+  for (int64_t e = 0; e < c->E; e++)
+    for (int k = 0; k < n; k++)
+      for (int j = 0; j < n; j++)
+        for (int i = 0; i < n; i++) {
+          double sacc = 0.0;
+          for (int v = 0; v < 8; v++) {
+            const int a = v & 1, b = (v >> 1) & 1, cc = v >> 2;
+            sacc += J[i * 2 + a] * J[j * 2 + b] * J[k * 2 + cc] * x0[e * 8 + v];
+          }
+          zc[e * n3 + i + n * j + (int64_t)n * n * k] = sacc;
+        }
+  free(b0); free(x0); free(r0); free(p0); free(w0);
+  return 0;
+}
+
+/* z = mask(c^1/2 QQ^T (A~^-1 c^1/2 r)_L + R0^T A0^-1 R0 r).  which: 1 local
+   part only, 2 coarse part only, 3 both */
+int oracle_schwarz_apply(const oracle_schwarz* s, const double* r, double* z, int which) {
+  if (!s || which < 1 || which > 3) return -1;
+  const oracle_ctx* c = s->c;
+  const int64_t n3 = c->n3, ns = c->nslots;
+  for (int64_t l = 0; l < ns; l++) z[l] = 0.0;
+  if (which & 1) {
+    double* y = (double*)malloc(sizeof(double) * n3);
+    if (!y) return -5;
+    for (int64_t e = 0; e < c->E; e++) {
+      const double* L = s->L + e * n3 * n3;
+      for (int64_t p = 0; p < n3; p++) {   /* forward: L y = c^1/2 r (0 on masked) */
+        const int64_t l = e * n3 + p;
+        double v = c->mask[l] ? 0.0 : s->sqc[l] * r[l];
+        for (int64_t q = 0; q < p; q++) v -= L[p * n3 + q] * y[q];
+        y[p] = v / L[p * n3 + p];
+      }
+      for (int64_t p = n3 - 1; p >= 0; p--) {   /* backward: L^T x = y */
+        double v = y[p];
+        for (int64_t q = p + 1; q < n3; q++) v -= L[q * n3 + p] * y[q];
+        y[p] = v / L[p * n3 + p];
+      }
+      for (int64_t p = 0; p < n3; p++) z[e * n3 + p] = c->mask[e * n3 + p] ? 0.0 : y[p];
+    }
+    free(y);
+    oracle_gs(c, z);
+    for (int64_t l = 0; l < ns; l++) z[l] *= s->sqc[l];
+  }
+  if (which & 2) {
+    double* zc = (double*)malloc(sizeof(double) * ns);
+    if (!zc) return -5;
+    int st = coarse_correction(s, r, zc);
+    if (st) { free(zc); return st; }
+    for (int64_t l = 0; l < ns; l++) z[l] += zc[l];
+    free(zc);
+  }
+  oracle_mask_apply(c, z);
+  return 0;
+}
+
+/* PCG with the Schwarz preconditioner.  The coarse solve is a fixed number of
+   CG iterations, a nonlinear operator, so beta takes the flexible (Polak-
+   Ribiere) form beta = <z', r' - r>_c / <z, r>_c = -alpha <z', w>_c / rho
+   (reading Q32); otherwise the loop is pcg_core's. */
+int oracle_schwarz_pcg(const oracle_schwarz* s, const double* b, double* x, double tol,
+                       int maxit, int* iters, double* res_final, double* res_true, double* hist) {
+  if (!s || maxit < 0) return -1;
+  const oracle_ctx* c = s->c;
+  const int64_t ns = c->nslots;
+  double* r = (double*)malloc(sizeof(double) * ns);
+  double* z = (double*)malloc(sizeof(double) * ns);
+  double* p = (double*)malloc(sizeof(double) * ns);
+  double* w = (double*)malloc(sizeof(double) * ns);
+  if (!r || !z || !p || !w) { free(r); free(z); free(p); free(w); return -5; }
+  int status = 1, k = 0;
+  for (int64_t l = 0; l < ns; l++) { x[l] = 0.0; r[l] = b[l]; }
+  oracle_schwarz_apply(s, r, z, 3);
+  for (int64_t l = 0; l < ns; l++) p[l] = z[l];
+  double rho = oracle_dot_c(c, r, z);
+  double gamma = oracle_dot_c(c, r, r);
+  if (hist) hist[0] = sqrt(gamma);
+  if (sqrt(gamma) <= tol) status = 0;
+  while (status == 1 && k < maxit) {
+    k++;
+    oracle_apply(c, p, w);
+    const double sigma = oracle_dot_c(c, p, w);
+    if (!(sigma > 0.0)) { status = -6; break; }
+    const double alpha = rho / sigma;
+    for (int64_t l = 0; l < ns; l++) {
+      x[l] += alpha * p[l];
+      r[l] -= alpha * w[l];
+    }
+    gamma = oracle_dot_c(c, r, r);
+    if (hist) hist[k] = sqrt(gamma);
+    if (sqrt(gamma) <= tol) { status = 0; break; }
+    oracle_schwarz_apply(s, r, z, 3);
+    const double rho_new = oracle_dot_c(c, r, z);
+    const double beta = -alpha * oracle_dot_c(c, w, z) / rho;
+    rho = rho_new;
+    for (int64_t l = 0; l < ns; l++) p[l] = z[l] + beta * p[l];
+  }
+  if (iters) *iters = k;
+  if (res_final) *res_final = sqrt(gamma);
+  if (res_true) {
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) w[l] = b[l] - w[l];
+    *res_true = sqrt(oracle_dot_c(c, w, w));
+  }
+  free(r); free(z); free(p); free(w);
+  return status;
+}
+
+/* flexible restarted GMRES with the Schwarz preconditioner (right, variable:
+   z_j = M v_j is stored and x += Z y, Saad's FGMRES); otherwise as oracle_gmres
+   (two MGS passes, Givens rotations, the same stopping rule). */
+int oracle_schwarz_gmres(const oracle_schwarz* s, const double* b, double* x, double tol,
+                         int maxit, int restart, int* iters, double* res_final, double* res_true,
+                         double* hist) {
+  if (!s || maxit < 0 || restart < 1) return -1;
+  const oracle_ctx* c = s->c;
+  const int64_t ns = c->nslots;
+  const int m = restart;
+  double* V = (double*)malloc(sizeof(double) * ns * (m + 1));
+  double* Zs = (double*)malloc(sizeof(double) * ns * m);
+  double* w = (double*)malloc(sizeof(double) * ns);
+  double* H = (double*)calloc((size_t)(m + 1) * m, sizeof(double));
+  double* cs = (double*)malloc(sizeof(double) * m);
+  double* sn = (double*)malloc(sizeof(double) * m);
+  double* g = (double*)malloc(sizeof(double) * (m + 1));
+  double* y = (double*)malloc(sizeof(double) * m);
+  if (!V || !Zs || !w || !H || !cs || !sn || !g || !y) {
+    free(V); free(Zs); free(w); free(H); free(cs); free(sn); free(g); free(y);
+    return -5;
+  }
+  int k = 0, status = 1;
+  double res = 0.0;
+  for (int cycle = 0;; cycle++) {
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) V[l] = b[l] - w[l];
+    const double beta = sqrt(oracle_dot_c(c, V, V));
+    res = beta;
+    if (cycle == 0 && hist) hist[0] = beta;
+    if (beta <= tol) { status = 0; break; }
+    if (k >= maxit) break;
+    for (int64_t l = 0; l < ns; l++) V[l] /= beta;
+    for (int i = 0; i <= m; i++) g[i] = 0.0;
+    g[0] = beta;
+    int j = 0;
+    for (; j < m && k < maxit; j++) {
+      double* vj = V + (int64_t)j * ns;
+      double* zj = Zs + (int64_t)j * ns;
+      oracle_schwarz_apply(s, vj, zj, 3);
+      oracle_apply(c, zj, w);
+      k++;
+      for (int i = 0; i <= j; i++) H[i * m + j] = 0.0;
+      for (int pass = 0; pass < 2; pass++)
+        for (int i = 0; i <= j; i++) {
+          const double* vi = V + (int64_t)i * ns;
+          const double h = oracle_dot_c(c, w, vi);
+          H[i * m + j] += h;
+          for (int64_t l = 0; l < ns; l++) w[l] -= h * vi[l];
+        }
+      const double hn = sqrt(oracle_dot_c(c, w, w));
+      H[(j + 1) * m + j] = hn;
+      double* vn = V + (int64_t)(j + 1) * ns;
+      for (int64_t l = 0; l < ns; l++) vn[l] = hn > 0.0 ? w[l] / hn : 0.0;
+      for (int i = 0; i < j; i++) {
+        const double a = H[i * m + j], bb = H[(i + 1) * m + j];
+        H[i * m + j] = cs[i] * a + sn[i] * bb;
+        H[(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      }
+      const double a = H[j * m + j], bb = H[(j + 1) * m + j];
+      const double rr = sqrt(a * a + bb * bb);
+      cs[j] = rr > 0.0 ? a / rr : 1.0;
+      sn[j] = rr > 0.0 ? bb / rr : 0.0;
+      H[j * m + j] = rr;
+      H[(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      res = fabs(g[j + 1]);
+      if (hist) hist[k] = res;
+      if (res <= tol || hn == 0.0) { j++; break; }
+    }
+    for (int i = j - 1; i >= 0; i--) {
+      double sacc = g[i];
+      for (int q = i + 1; q < j; q++) sacc -= H[i * m + q] * y[q];
+      y[i] = sacc / H[i * m + i];
+    }
+    for (int64_t l = 0; l < ns; l++) {
+      double zy = 0.0;
+      for (int i = 0; i < j; i++) zy += Zs[(int64_t)i * ns + l] * y[i];
+      x[l] += zy;
+    }
+    if (res <= tol) { status = 0; break; }
+    if (k >= maxit) break;
+  }
+  if (iters) *iters = k;
+  if (res_final) *res_final = res;
+  if (res_true) {
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) w[l] = b[l] - w[l];
+    *res_true = sqrt(oracle_dot_c(c, w, w));
+  }
+  free(V); free(Zs); free(w); free(H); free(cs); free(sn); free(g); free(y);
+  return status;
+}
+
+/* NEXT-1 pressure pipeline: projection + GMRES + Schwarz; NULL restores Jacobi */
+int oracle_proj_set_schwarz(oracle_proj* p, const oracle_schwarz* s) {
+  if (!p || (s && s->c != p->c)) return -1;
+  p->schw = s;
   return 0;
 }
 

@@ -90,6 +90,20 @@ int oracle_proj_update(oracle_proj* p, const double* x);
 int oracle_proj_solve(oracle_proj* p, const double* b, double* x, double tol, int maxit,
                       int restart, int* iters, double* res_final);
 int oracle_proj_gram(const oracle_proj* p, double* G);
+/* NEXT-1: two-level additive overlapping Schwarz, readings Q28-Q32:
+   element subdomains with one node of overlap (separable local operator, dense
+   Cholesky here), N = 1 coarse space solved by <= coarse_iters plain CG steps. */
+typedef struct oracle_schwarz oracle_schwarz;
+int oracle_schwarz_create(const oracle_ctx* c, int coarse_iters, oracle_schwarz** out);
+void oracle_schwarz_free(oracle_schwarz* s);
+int oracle_schwarz_local_matrix(const oracle_schwarz* s, int64_t e, double* A);  /* n3 x n3 */
+int oracle_schwarz_apply(const oracle_schwarz* s, const double* r, double* z, int which);
+int oracle_schwarz_pcg(const oracle_schwarz* s, const double* b, double* x, double tol,
+                       int maxit, int* iters, double* res_final, double* res_true, double* hist);
+int oracle_schwarz_gmres(const oracle_schwarz* s, const double* b, double* x, double tol,
+                         int maxit, int restart, int* iters, double* res_final, double* res_true,
+                         double* hist);
+int oracle_proj_set_schwarz(oracle_proj* p, const oracle_schwarz* s);
 int oracle_plan(const oracle_ctx* c, int64_t* npairs, int64_t* nseg, int64_t* nsegslots,
                 int64_t* pairs, int64_t* seg_off, int64_t* seg_slot);
 /* gids shared between ranks r and q (r != q), ascending; NULL list to size. */
