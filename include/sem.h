@@ -134,6 +134,23 @@ int sem_proj_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t m
                    int32_t restart, int32_t m, sem_pcg_result* r);
 int sem_proj_reset(sem_ctx* c);
 int sem_proj_size(const sem_ctx* c, int32_t* k);
+/* NEXT-1 ("two-level additive overlapping Schwarz method ...
+   M0^-1 = R0^T A0^-1 R0 + sum_k R_k^T A~_k^-1 R_k"; the coarse grid on linear
+   elements solved by "few (~10) CG iterations"; readings Q28-Q32 in DESIGN.md).
+   sem_schwarz_apply: z = M r for an assembled residual r (device, n_local,
+   slot order; r and z must not alias):
+     z = mask( c^1/2 QQ^T (A~^-1 (c^1/2 r))_L + R0^T A0^-1 R0 r )
+   A~_e = the separable operator of element e with one node of overlap
+   (applied by fast diagonalisation), A0 = the N = 1 operator on the same mesh
+   (an internal second context), A0^-1 = at most SEM_OPT_COARSE_ITERS plain CG
+   steps from 0 (stopped at ||r0||_c <= 1e-12 ||b0||_c).  which: 1 = local
+   part, 2 = coarse part, 3 = both.  The first call builds the preconditioner
+   (collective for nranks > 1, blocking); later calls are asynchronous on the
+   stream.  With SEM_OPT_PRECOND = SEM_PRECOND_SCHWARZ, sem_pcg_solve runs
+   flexible PCG (beta = -alpha <z', w>_c / rho) and sem_gmres_solve /
+   sem_proj_solve run flexible GMRES (the preconditioned basis is stored) with
+   M; sem_helm_pcg_solve keeps Jacobi (the paper's velocity solver). */
+int sem_schwarz_apply(sem_ctx* c, const double* r, double* z, int32_t which);
 int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_host, double tol,
                        int32_t maxit, sem_pcg_result* res);
 /* recursive residual history of the last solve: hist[k] after k iterations */
@@ -214,6 +231,14 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    dependent launch (each kernel's launch and prologue overlap the previous
    kernel's tail); 0 = plain stream order.  Results are identical. */
 #define SEM_OPT_PDL 5
+/* Preconditioner of sem_pcg_solve / sem_gmres_solve / sem_proj_solve:
+   SEM_PRECOND_JACOBI (default) or SEM_PRECOND_SCHWARZ (NEXT-1; setting it
+   builds the Schwarz preconditioner: collective, blocking). */
+#define SEM_OPT_PRECOND 6
+#define SEM_PRECOND_JACOBI 0
+#define SEM_PRECOND_SCHWARZ 1
+/* maximum CG iterations of the Schwarz coarse solve (default 10) */
+#define SEM_OPT_COARSE_ITERS 7
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

@@ -58,6 +58,7 @@ _SIGS = {
     "sem_proj_solve": [_P, _P, _P, C.c_double, C.c_int32, C.c_int32, C.c_int32,
                        C.POINTER(PcgResult)],
     "sem_proj_reset": [_P],
+    "sem_schwarz_apply": [_P, _P, _P, C.c_int32],
     "sem_proj_size": [_P, C.POINTER(C.c_int32)],
     "sem_rhs_mass": [_P, _P, _P],
     "sem_helm_pcg_solve": [_P, C.c_double, C.c_double, _P, _P, C.c_double, C.c_int32,
@@ -242,6 +243,20 @@ class Context:
                allow=(SEM_OK, SEM_NOT_CONVERGED))
         return {"iters": r.iters, "status": r.status, "res_final": r.res_final,
                 "res_true": r.res_true}
+
+    # ---- NEXT-1: two-level additive Schwarz
+    def schwarz_apply(self, r, z, which=3):
+        """z = M r (which: 1 local part, 2 coarse part, 3 both); builds M on first use."""
+        _check(load().sem_schwarz_apply(self._h, self._f64(r), self._f64(z), int(which)))
+
+    def set_precond(self, kind: str):
+        """Preconditioner of pcg_solve / gmres_solve / proj_solve: 'jacobi' or
+        'schwarz' (flexible PCG / flexible GMRES).  Collective (builds Schwarz)."""
+        _check(load().sem_set_option(self._h, 6, {"jacobi": 0, "schwarz": 1}[kind]))
+
+    def set_coarse_iters(self, k: int):
+        """Maximum CG iterations of the Schwarz coarse solve (default 10)."""
+        _check(load().sem_set_option(self._h, 7, int(k)))
 
     def proj_reset(self):
         _check(load().sem_proj_reset(self._h))

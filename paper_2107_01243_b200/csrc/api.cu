@@ -58,7 +58,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 namespace {
 
 constexpr int kBatch = 8;            // iterations enqueued between host polls
-constexpr int kTimerClasses = 7;
+constexpr int kTimerClasses = 9;
 
 struct Timer {
   std::vector<cudaEvent_t> pool;     // pairs
@@ -95,6 +95,18 @@ struct sem_ctx {
   int gm_cap = 0;
   double *d_Z = nullptr, *d_AZ = nullptr, *d_pdelta = nullptr, *d_pbd = nullptr;
   int proj_m = 0, proj_k = 0;
+  // NEXT-1: two-level Schwarz (schwarz.cu); the coarse space is a second
+  // context at N = 1 on the same mesh and partition
+  int precond = SEM_PRECOND_JACOBI;
+  int coarse_iters = 10;
+  sem_ctx* c0 = nullptr;
+  double *d_fS = nullptr, *d_flam = nullptr;     // [nloc][3][n*n], [nloc][3][n]
+  double *d_sy = nullptr;                        // local solves (then assembled)
+  double *d_b0 = nullptr, *d_x0 = nullptr, *d_dinv0 = nullptr;   // coarse vectors
+  sem::PcgState* d_st0 = nullptr;                // coarse CG start state
+  double *d_rw = nullptr, *d_z = nullptr;        // flexible PCG: [r | w], z
+  double* d_Zs = nullptr;                        // flexible GMRES: M v_j
+  int zs_cap = 0;
   // Helmholtz (NEXT-2): operator in use by apply_op / pcg_run, and its Jacobi cache
   bool helm = false;
   double h1 = 1.0, h2 = 0.0;
@@ -122,8 +134,8 @@ struct sem_ctx {
   int64_t launches = 0;
   bool timing = false;
   Timer timer;
-  double t_ms[kTimerClasses] = {0, 0, 0, 0, 0, 0, 0};
-  int64_t t_cnt[kTimerClasses] = {0, 0, 0, 0, 0, 0, 0};
+  double t_ms[kTimerClasses] = {};
+  int64_t t_cnt[kTimerClasses] = {};
   bool overlap = false;  // SEM_OPT_OVERLAP: Alg. 1 boundary/interior split (measured slower
                          // on NVLink: the exchange is ~200 KB, the split costs a launch)
   bool fuse_gs = false;   // SEM_OPT_FUSED_GS
@@ -422,11 +434,14 @@ void free_ctx(sem_ctx* c) {
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
                   c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank, c->d_fst, c->d_est,
                   c->d_vst, c->d_gsctr, c->d_dinv_helm,
-                  c->d_V, c->d_gt, c->d_kpart, c->d_Z, c->d_AZ, c->d_pdelta, c->d_pbd};
+                  c->d_V, c->d_gt, c->d_kpart, c->d_Z, c->d_AZ, c->d_pdelta, c->d_pbd,
+                  c->d_fS, c->d_flam, c->d_sy, c->d_b0, c->d_x0, c->d_dinv0, c->d_st0,
+                  c->d_rw, c->d_z, c->d_Zs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->d_gs) cudaFree(c->d_gs);
   if (c->d_ktick) cudaFree(c->d_ktick);
+  if (c->c0) free_ctx(c->c0);
   if (c->h_st) cudaFreeHost(c->h_st);
   for (char* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_perr};
@@ -739,65 +754,62 @@ extern "C" int sem_rhs(sem_ctx* c, const double* f, double* b) {
   return SEM_OK;
 }
 
-static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
-                   sem_pcg_result* res) {
-  if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
-  SEM_TRY(ensure_hist(c, maxit));
+// ---- PCG building blocks (pcg_run and the Schwarz coarse solve)
+struct PcgCtl {
+  bool dist = false, pp = false;
+  double* rg_out = nullptr;
+};
+
+// x = 0, r = b, p = dinv b, (rho, gamma), start state; the host wrote tol/maxit
+static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, double* x,
+                            PcgCtl* k) {
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
-  // scalars: tol, maxit
-  sem::PcgState init{};
-  init.tol = tol;
-  init.maxit = maxit;
-  std::memcpy(c->h_st, &init, sizeof(init));   // h_st is idle: every solve ends synchronised
-  CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
-  const bool dist = c->hp.nranks > 1;
-  const double* dinv = c->helm ? c->d_dinv_helm : c->d_dinv;   // Jacobi of the operator in use
-  double* rg_out = dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
+  k->dist = c->hp.nranks > 1;
+  k->rg_out = k->dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   // peer-memory allreduces fused into the CG kernels (nranks > 1 with NVLink mailboxes)
-  const bool pp = p2p(c);
+  k->pp = p2p(c);
   sem::PeerSync ps;
-  if (pp) ps.c = c->p2p;
-  ps.e_pub = ps.e_wait = pp ? ++c->ep_ar[sem::AR_RG] : 0;
+  if (k->pp) ps.c = c->p2p;
+  ps.e_pub = ps.e_wait = k->pp ? ++c->ep_ar[sem::AR_RG] : 0;
   CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, dinv, b, x, c->d_r, c->d_p, c->d_partial,
-                               st, rg_out, ps, c->red_grid, s));
-  if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
+                               st, k->rg_out, ps, c->red_grid, s));
+  if (!k->pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
   CUDA_TRY(sem::launch_cg_start(st, c->d_hist, ps, s));
   c->launches += 2;
-  int done = 0;
-  struct PdlScope {   // programmatic dependent launch for the iteration kernels
-    explicit PdlScope(bool on) { sem::set_pdl(on); }
-    ~PdlScope() { sem::set_pdl(false); }
-  } pdl_scope(c->use_pdl && !c->timing);   // per-kernel event timers need plain order
-  for (int k = 0; k < maxit && !done; k += kBatch) {
-    const int nb = std::min(kBatch, maxit - k);
-    for (int q = 0; q < nb; q++) {
-      SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
-      sem::PeerSync psu, psp;
-      if (pp) {
-        psu.c = psp.c = c->p2p;
-        psu.e_wait = c->cur_e_sig;
-        psu.e_pub = psp.e_wait = ++c->ep_ar[sem::AR_RG];
-      }
-      int tk = timer_begin(c, 1);
-      CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv,
-                                     c->d_partial, st, rg_out, dist ? nullptr : c->d_partial_ax,
-                                     c->d_nsig, psu, c->red_grid, s));
-      timer_end(c, tk);
-      if (!pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
-      tk = timer_begin(c, 2);
-      CUDA_TRY(sem::launch_cg_p(c->dp, dinv, c->d_r, c->d_p, x, st, c->d_hist, psp,
-                                c->red_grid, s));
-      timer_end(c, tk);
-      c->launches += 2;
-    }
-    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaEventRecord(c->ev_poll, s));
-    CUDA_TRY(cudaEventSynchronize(c->ev_poll));
-    done = c->h_st->done;
+  return SEM_OK;
+}
+
+// one PCG iteration: w = A p (+ sigma), update (r, rho', gamma), x and p
+static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const PcgCtl& k) {
+  cudaStream_t s = c->stream;
+  sem::PcgState* st = c->d_st;
+  SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
+  sem::PeerSync psu, psp;
+  if (k.pp) {
+    psu.c = psp.c = c->p2p;
+    psu.e_wait = c->cur_e_sig;
+    psu.e_pub = psp.e_wait = ++c->ep_ar[sem::AR_RG];
   }
-  sem::set_pdl(false);
-  // true residual once at the end (reading Q17)
+  int tk = timer_begin(c, 1);
+  CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv, c->d_partial, st,
+                                 k.rg_out, k.dist ? nullptr : c->d_partial_ax, c->d_nsig, psu,
+                                 c->red_grid, s));
+  timer_end(c, tk);
+  if (!k.pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
+  tk = timer_begin(c, 2);
+  CUDA_TRY(sem::launch_cg_p(c->dp, dinv, c->d_r, c->d_p, x, st, c->d_hist, psp, c->red_grid, s));
+  timer_end(c, tk);
+  c->launches += 2;
+  return SEM_OK;
+}
+
+// true residual once at the end (reading Q17), status and result of a PCG solve
+static int pcg_finish(sem_ctx* c, const double* b, const double* x, sem_pcg_result* res) {
+  cudaStream_t s = c->stream;
+  sem::PcgState* st = c->d_st;
+  const bool dist = c->hp.nranks > 1;
+  const bool pp = p2p(c);
   SEM_TRY(apply_op(c, x, c->d_wv, sem::AX_APPLY));
   sem::PeerSync psr;
   if (pp) {
@@ -834,11 +846,225 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   return status;
 }
 
+
+static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                   sem_pcg_result* res) {
+  if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
+  SEM_TRY(ensure_hist(c, maxit));
+  cudaStream_t s = c->stream;
+  sem::PcgState* st = c->d_st;
+  // scalars: tol, maxit
+  sem::PcgState init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  std::memcpy(c->h_st, &init, sizeof(init));   // h_st is idle: every solve ends synchronised
+  CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
+  const double* dinv = c->helm ? c->d_dinv_helm : c->d_dinv;   // Jacobi of the operator in use
+  PcgCtl k;
+  SEM_TRY(pcg_enqueue_init(c, dinv, b, x, &k));
+  int done = 0;
+  struct PdlScope {   // programmatic dependent launch for the iteration kernels
+    explicit PdlScope(bool on) { sem::set_pdl(on); }
+    ~PdlScope() { sem::set_pdl(false); }
+  } pdl_scope(c->use_pdl && !c->timing);   // per-kernel event timers need plain order
+  for (int it = 0; it < maxit && !done; it += kBatch) {
+    const int nb = std::min(kBatch, maxit - it);
+    for (int q = 0; q < nb; q++) SEM_TRY(pcg_enqueue_iter(c, dinv, x, k));
+    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(c->ev_poll, s));
+    CUDA_TRY(cudaEventSynchronize(c->ev_poll));
+    done = c->h_st->done;
+  }
+  sem::set_pdl(false);
+  return pcg_finish(c, b, x, res);
+}
+
+// gate of the operator's Ax kernel (any mode returns early when *g)
+struct GateScope {
+  sem_ctx* c;
+  GateScope(sem_ctx* ctx, const int* g) : c(ctx) { c->ax_gate = g; }
+  ~GateScope() { c->ax_gate = nullptr; }
+};
+
+// ---------------------------------------------------------------- NEXT-1: Schwarz
+// two-level additive overlapping Schwarz (readings Q28-Q32;
+// kernels in schwarz.cu).  The coarse space is a second context at N = 1 on
+// the same mesh and element partition (its operator, gather-scatter, PCG
+// kernels and multi-GPU transports are the fine level's, at n = 2).
+static int schwarz_setup(sem_ctx* c) {
+  if (c->c0) return SEM_OK;
+  const sem::HostPlan& h = c->hp;
+  cudaStream_t s = c->stream;
+  sem_ctx* c0 = nullptr;
+  SEM_TRY(sem_setup(&h.m, 1, &c0));   // collective for nranks > 1
+  c->c0 = c0;
+  const size_t nloc = (size_t)h.nloc, n = (size_t)h.n;
+  SEM_TRY(dalloc(&c->d_fS, nloc * 3 * n * n));
+  SEM_TRY(dalloc(&c->d_flam, nloc * 3 * n));
+  SEM_TRY(dalloc(&c->d_sy, (size_t)h.n_local));
+  const size_t n0 = (size_t)c0->hp.n_local;
+  SEM_TRY(dalloc(&c->d_b0, n0));
+  SEM_TRY(dalloc(&c->d_x0, n0));
+  SEM_TRY(dalloc(&c->d_st0, 1));
+  // plain CG on the coarse level: the "Jacobi" vector is 1 on unmasked slots
+  std::vector<double> ones(n0, 1.0);
+  SEM_TRY(upload(&c->d_dinv0, ones, s));
+  CUDA_TRY(sem::launch_invert_mask(c0->dp, c->d_dinv0, s));
+  const sem_mesh& m = h.m;
+  const double box[6] = {m.x0, m.x1, m.y0, m.y1, m.z0, m.z1};
+  CUDA_TRY(sem::launch_fdm_setup(h.n, (int)h.nloc, h.e_lo, m.ex, m.ey, m.ez, box, m.deform,
+                                 m.deform_amp, m.periodic, c->d_xi, c->d_w, c->d_D, c->d_fS,
+                                 c->d_flam, s));
+  c->launches += 2;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return SEM_OK;
+}
+
+// coarse start state: tol set from ||b0|| on the device, at most K0 iterations
+static int coarse_state(sem_ctx* c) {
+  sem::PcgState init{};
+  init.maxit = c->coarse_iters;
+  CUDA_TRY(cudaMemcpyAsync(c->d_st0, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  SEM_TRY(ensure_hist(c->c0, c->coarse_iters));
+  return SEM_OK;
+}
+
+// x0 = A0^-1 b0 by <= K0 plain CG steps (reading Q31); no-op when *gate
+static int coarse_solve(sem_ctx* c, const int* gate) {
+  sem_ctx* c0 = c->c0;
+  cudaStream_t s = c0->stream;
+  SEM_TRY(gs_op(c0, c->d_b0, 1));
+  if (c0->hp.fully_periodic) {   // b0 in range(A0): remove the unique-DOF mean
+    CUDA_TRY(sem::launch_sum_c(c0->dp, c0->d_mult, c->d_b0, c0->d_partial, &c0->d_tickets[0],
+                               c0->d_scal, c0->red_grid, s));
+    SEM_TRY(allreduce(c0, c0->d_scal, 2));
+    CUDA_TRY(sem::launch_sub_scalar(c->d_b0, c0->d_scal, c0->hp.n_local, s));
+    c0->launches += 2;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c0->d_st, c->d_st0, sizeof(sem::PcgState), cudaMemcpyDeviceToDevice, s));
+  PcgCtl k;
+  SEM_TRY(pcg_enqueue_init(c0, c->d_dinv0, c->d_b0, c->d_x0, &k));
+  CUDA_TRY(sem::launch_rel_tol(c0->d_st, 1e-12, s));
+  CUDA_TRY(sem::launch_gate_state(c0->d_st, gate, s));
+  c0->launches += 2;
+  for (int q = 0; q < c->coarse_iters; q++) SEM_TRY(pcg_enqueue_iter(c0, c->d_dinv0, c->d_x0, k));
+  return SEM_OK;
+}
+
+// z = M r (which: 1 local, 2 coarse, 3 both); dots (flexible PCG): <z, r>_c and
+// <z, w>_c into st->dz; every kernel is a no-op when *gate
+static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, const int* gate,
+                         const double* w_dot) {
+  const sem::HostPlan& h = c->hp;
+  cudaStream_t s = c->stream;
+  double* y = (which & 1) ? c->d_sy : nullptr;
+  double* b0 = (which & 2) ? c->d_b0 : nullptr;
+  int tk = timer_begin(c, 7);
+  CUDA_TRY(sem::launch_fdm(h.n, (int)h.nloc, r, c->d_mult, c->d_fS, c->d_flam, c->d_xi, y, b0,
+                           gate, c->num_sms, s));
+  timer_end(c, tk);
+  c->launches++;
+  if (y) SEM_TRY(gs_op(c, y, 0));
+  if (b0) SEM_TRY(coarse_solve(c, gate));
+  sem::PcgState* st = c->d_st;
+  const bool dist = h.nranks > 1;
+  double* dots = w_dot ? (dist ? st->loc_dz : st->dz) : nullptr;
+  tk = timer_begin(c, 8);
+  CUDA_TRY(sem::launch_schwarz_combine(h.n, h.n_local, y, b0 ? c->d_x0 : nullptr, c->d_mult,
+                                       c->d_xi, z, r, w_dot, c->d_partial, &c->d_tickets[5], dots,
+                                       gate, c->num_sms, s));
+  timer_end(c, tk);
+  c->launches++;
+  if (dots && dist) SEM_TRY(allreduce_to(c, st->loc_dz, st->dz, 2));
+  return SEM_OK;
+}
+
+// flexible PCG with the Schwarz preconditioner (reading Q32); scalars stay on
+// the device, the host polls every kBatch iterations
+static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                           sem_pcg_result* res) {
+  if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
+  SEM_TRY(ensure_hist(c, maxit));
+  const sem::HostPlan& h = c->hp;
+  const int64_t n = h.n_local;
+  cudaStream_t s = c->stream;
+  const int sms = c->num_sms;
+  if (!c->d_rw) SEM_TRY(dalloc(&c->d_rw, 2 * (size_t)n));
+  if (!c->d_z) SEM_TRY(dalloc(&c->d_z, (size_t)n));
+  double *r = c->d_rw, *w = c->d_rw + n, *z = c->d_z, *p = c->d_p;
+  sem::PcgState* st = c->d_st;
+  const int* done = &st->done;
+  const bool dist = h.nranks > 1;
+  double* part = c->d_partial;
+  unsigned* tk = &c->d_tickets[6];
+  sem::PcgState init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  std::memcpy(c->h_st, &init, sizeof(init));
+  CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
+  SEM_TRY(coarse_state(c));
+  CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(w, 0, sizeof(double) * n, s));
+  // z = M r, p = z, rho = <r, z>_c, gamma = <r, r>_c
+  SEM_TRY(schwarz_apply(c, r, z, 3, nullptr, w));
+  CUDA_TRY(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(sem::launch_mdot(n, c->d_mult, r, r, n, 1, part, tk, dist ? &st->loc[1] : &st->gamma,
+                            nullptr, sms, s));
+  if (dist) SEM_TRY(allreduce_to(c, &st->loc[1], &st->gamma, 1));
+  CUDA_TRY(cudaMemcpyAsync(&st->rho_new, &st->dz[0], sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(sem::launch_fcg_scalar(0, st, c->d_hist, s));
+  c->launches += 2;
+  int hd = 0;
+  for (int it = 0; it < maxit && !hd; it += kBatch) {
+    const int nb = std::min(kBatch, maxit - it);
+    for (int q = 0; q < nb; q++) {
+      {
+        GateScope g(c, done);
+        SEM_TRY(apply_op(c, p, w, sem::AX_APPLY));   // w = A p
+      }
+      CUDA_TRY(sem::launch_mdot(n, c->d_mult, p, w, n, 1, part, tk,
+                                dist ? &st->loc[2] : &st->sigma, done, sms, s));
+      if (dist) SEM_TRY(allreduce_to(c, &st->loc[2], &st->sigma, 1));
+      CUDA_TRY(sem::launch_fcg_scalar(1, st, c->d_hist, s));       // alpha
+      CUDA_TRY(sem::launch_maxpy(n, x, p, n, 1, &st->alpha, 1.0, nullptr, c->d_mult, part, tk,
+                                 nullptr, done, sms, s));           // x += alpha p
+      CUDA_TRY(sem::launch_maxpy(n, r, w, n, 1, &st->alpha, -1.0, nullptr, c->d_mult, part, tk,
+                                 dist ? &st->loc[1] : &st->gamma, done, sms, s));   // r -= alpha w
+      if (dist) SEM_TRY(allreduce_to(c, &st->loc[1], &st->gamma, 1));
+      CUDA_TRY(sem::launch_fcg_scalar(2, st, c->d_hist, s));       // convergence
+      SEM_TRY(schwarz_apply(c, r, z, 3, done, w));                  // z = M r, dots
+      CUDA_TRY(sem::launch_fcg_scalar(3, st, c->d_hist, s));       // beta
+      CUDA_TRY(sem::launch_xpay(n, p, z, st, sms, s));              // p = z + beta p
+      c->launches += 7;
+    }
+    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    hd = c->h_st->done;
+  }
+  return pcg_finish(c, b, x, res);
+}
+
+extern "C" int sem_schwarz_apply(sem_ctx* c, const double* r, double* z, int32_t which) {
+  if (!c || !r || !z || r == z || which < 1 || which > 3) {
+    sem::set_error("sem_schwarz_apply: bad arguments");
+    return SEM_EINVAL;
+  }
+  SEM_TRY(schwarz_setup(c));
+  SEM_TRY(coarse_state(c));
+  return schwarz_apply(c, r, z, which, nullptr, nullptr);
+}
+
 extern "C" int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                              sem_pcg_result* res) {
   if (!c || !b || !x || !aligned16(b) || !aligned16(x) || b == x) {
     sem::set_error("sem_pcg_solve: bad arguments");
     return SEM_EINVAL;
+  }
+  if (c->precond == SEM_PRECOND_SCHWARZ) {
+    SEM_TRY(schwarz_setup(c));
+    return schwarz_pcg_run(c, b, x, tol, maxit, res);
   }
   return pcg_run(c, b, x, tol, maxit, res);
 }
@@ -936,17 +1162,25 @@ static int gm_alloc(sem_ctx* c, int m) {
   return SEM_OK;
 }
 
-struct GateScope {
-  sem_ctx* c;
-  GateScope(sem_ctx* ctx, const int* g) : c(ctx) { c->ax_gate = g; }
-  ~GateScope() { c->ax_gate = nullptr; }
-};
 
 static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit, int m,
                      sem_pcg_result* res) {
   if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
   SEM_TRY(gm_alloc(c, m));
   SEM_TRY(ensure_hist(c, maxit));
+  // flexible GMRES with the Schwarz preconditioner (NEXT-1): z_j = M v_j stored
+  const bool schw = c->precond == SEM_PRECOND_SCHWARZ && !c->helm;
+  if (schw) {
+    SEM_TRY(schwarz_setup(c));
+    SEM_TRY(coarse_state(c));
+    if (m > c->zs_cap) {
+      if (c->d_Zs) cudaFree(c->d_Zs);
+      c->d_Zs = nullptr;
+      SEM_TRY(dalloc(&c->d_Zs, (size_t)m * c->hp.n_local));
+      CUDA_TRY(cudaMemsetAsync(c->d_Zs, 0, (size_t)m * c->hp.n_local * sizeof(double), c->stream));
+      c->zs_cap = m;
+    }
+  }
   cudaStream_t s = c->stream;
   const int64_t n = c->hp.n_local;
   const int sms = c->num_sms;
@@ -976,13 +1210,15 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
     CUDA_TRY(sem::launch_resid(n, b, w, c->d_V, mult, part, tk, &gs->norm2[0], done, sms, s));
     if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
     CUDA_TRY(sem::launch_gm_start(gs, st, c->d_hist, s));
-    CUDA_TRY(sem::launch_vnorm(n, c->d_V, c->d_V, c->d_gt, dinv, gs, cyc, sms, s));
+    CUDA_TRY(sem::launch_vnorm(n, c->d_V, c->d_V, schw ? nullptr : c->d_gt, dinv, gs, cyc, sms, s));
     c->launches += 4;
+    if (schw) SEM_TRY(schwarz_apply(c, c->d_V, c->d_Zs, 3, cyc, nullptr));
     for (int j = 0; j < m; j++) {
       double* Vn = c->d_V + (size_t)(j + 1) * n;
       {
         GateScope g(c, cyc);
-        SEM_TRY(apply_op(c, c->d_gt, w, sem::AX_APPLY));   // w = A M^-1 v_j
+        SEM_TRY(apply_op(c, schw ? c->d_Zs + (size_t)j * n : c->d_gt, w,
+                         sem::AX_APPLY));   // w = A M^-1 v_j
       }
       // two classical Gram-Schmidt passes against v_0..v_j, then ||w||_c
       CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, n, j + 1, part, tk, gs->h1, cyc, sms, s));
@@ -995,8 +1231,9 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
                                  &gs->norm2[0], cyc, sms, s));
       if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
       CUDA_TRY(sem::launch_gm_arnoldi(gs, st, c->d_hist, m, s));
-      CUDA_TRY(sem::launch_vnorm(n, w, Vn, c->d_gt, dinv, gs, cyc, sms, s));
+      CUDA_TRY(sem::launch_vnorm(n, w, Vn, schw ? nullptr : c->d_gt, dinv, gs, cyc, sms, s));
       c->launches += 6;
+      if (schw && j + 1 < m) SEM_TRY(schwarz_apply(c, Vn, c->d_Zs + (size_t)(j + 1) * n, 3, cyc, nullptr));
       if ((j + 1) % kBatch == 0 && j + 1 < m) {   // poll: stop enqueuing a finished cycle
         int cd = 0;
         CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &gs->cycle_done, sizeof(int),
@@ -1008,8 +1245,12 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
     }
     // y = H^-1 g; x += M^-1 V y; converged / maxit -> done
     CUDA_TRY(sem::launch_gm_solve(gs, st, m, s));
-    CUDA_TRY(sem::launch_maxpy(n, x, c->d_V, n, m, gs->y, 1.0, dinv, mult, part, tk, nullptr, done,
-                               sms, s));
+    if (schw)   // x += Z y
+      CUDA_TRY(sem::launch_maxpy(n, x, c->d_Zs, n, m, gs->y, 1.0, nullptr, mult, part, tk, nullptr,
+                                 done, sms, s));
+    else        // x += M^-1 V y
+      CUDA_TRY(sem::launch_maxpy(n, x, c->d_V, n, m, gs->y, 1.0, dinv, mult, part, tk, nullptr,
+                                 done, sms, s));
     CUDA_TRY(sem::launch_gm_end_cycle(gs, st, s));
     c->launches += 3;
     CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1305,6 +1546,25 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (option == SEM_OPT_P2P) {   // collective: every rank must set the same value
     cudaStreamSynchronize(c->stream);
     c->use_p2p = value != 0;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_PRECOND) {   // collective for nranks > 1 (builds Schwarz)
+    if (value != SEM_PRECOND_JACOBI && value != SEM_PRECOND_SCHWARZ) {
+      sem::set_error("sem_set_option: SEM_OPT_PRECOND must be 0 (Jacobi) or 1 (Schwarz)");
+      return SEM_EINVAL;
+    }
+    cudaStreamSynchronize(c->stream);
+    if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
+    c->precond = value;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_COARSE_ITERS) {
+    if (value < 0 || value > 10000) {
+      sem::set_error("sem_set_option: SEM_OPT_COARSE_ITERS must be in [0, 10000]");
+      return SEM_EINVAL;
+    }
+    cudaStreamSynchronize(c->stream);
+    c->coarse_iters = value;
     return SEM_OK;
   }
   sem::set_error("sem_set_option: unknown option");

@@ -148,6 +148,31 @@ __host__ __device__ __forceinline__ int64_t g_index(int64_t el, int f, int p, in
   return el * 6 * n2 * n + (int64_t)(k * 6 + f) * n2 + ij;
 }
 
+// ---------------------------------------------------------------- geometry
+struct Box {
+  double x0, x1, y0, y1, z0, z1;
+};
+
+// node coordinates (reading Q4)
+__device__ __forceinline__ void node_xyz(const double* xi, int ex, int ey, int ez, int64_t e,
+                                         int i, int j, int k, const Box& b, int deform,
+                                         double amp, double* x) {
+  const int64_t cx = e % ex, cy = (e / ex) % ey, cz = e / ((int64_t)ex * ey);
+  const double hx = (b.x1 - b.x0) / ex, hy = (b.y1 - b.y0) / ey, hz = (b.z1 - b.z0) / ez;
+  double X = b.x0 + hx * ((double)cx + 0.5 * (xi[i] + 1.0));
+  double Y = b.y0 + hy * ((double)cy + 0.5 * (xi[j] + 1.0));
+  double Z = b.z0 + hz * ((double)cz + 0.5 * (xi[k] + 1.0));
+  if (deform) {
+    const double tp = 6.283185307179586476925286766559;
+    const double s = amp * sin(tp * (X - b.x0) / (b.x1 - b.x0)) *
+                     sin(tp * (Y - b.y0) / (b.y1 - b.y0)) * sin(tp * (Z - b.z0) / (b.z1 - b.z0));
+    X += s * (b.x1 - b.x0) / tp;
+    Y += s * (b.y1 - b.y0) / tp;
+    Z += s * (b.z1 - b.z0) / tp;
+  }
+  x[0] = X; x[1] = Y; x[2] = Z;
+}
+
 // slot-mask from the element's 6-bit Dirichlet face code (reading Q8)
 __device__ __forceinline__ bool face_masked(unsigned bm, int i, int j, int k, int nm1) {
   return ((i == 0) && (bm & 1u)) || ((i == nm1) && (bm & 2u)) || ((j == 0) && (bm & 4u)) ||

@@ -23,29 +23,7 @@ constexpr int kThreads = 256;
 __device__ __forceinline__ double c_of(unsigned m) { return __drcp_rn((double)m); }
 
 // ---------------------------------------------------------------- geometry
-struct Box {
-  double x0, x1, y0, y1, z0, z1;
-};
-
-// node coordinates (reading Q4)
-__device__ __forceinline__ void node_xyz(const double* xi, int ex, int ey, int ez, int64_t e,
-                                         int i, int j, int k, const Box& b, int deform,
-                                         double amp, double* x) {
-  const int64_t cx = e % ex, cy = (e / ex) % ey, cz = e / ((int64_t)ex * ey);
-  const double hx = (b.x1 - b.x0) / ex, hy = (b.y1 - b.y0) / ey, hz = (b.z1 - b.z0) / ez;
-  double X = b.x0 + hx * ((double)cx + 0.5 * (xi[i] + 1.0));
-  double Y = b.y0 + hy * ((double)cy + 0.5 * (xi[j] + 1.0));
-  double Z = b.z0 + hz * ((double)cz + 0.5 * (xi[k] + 1.0));
-  if (deform) {
-    const double tp = 6.283185307179586476925286766559;
-    const double s = amp * sin(tp * (X - b.x0) / (b.x1 - b.x0)) *
-                     sin(tp * (Y - b.y0) / (b.y1 - b.y0)) * sin(tp * (Z - b.z0) / (b.z1 - b.z0));
-    X += s * (b.x1 - b.x0) / tp;
-    Y += s * (b.y1 - b.y0) / tp;
-    Z += s * (b.z1 - b.z0) / tp;
-  }
-  x[0] = X; x[1] = Y; x[2] = Z;
-}
+// Box and node_xyz (reading Q4) live in dev_common.cuh
 
 // one thread per slot: dx_a/dr_b through D on the isoparametric coordinates,
 // J = det, dr/dx by cofactors, G_ab = J w w w (dr_a/dx . dr_b/dx), B = J w w w

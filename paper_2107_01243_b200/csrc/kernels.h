@@ -72,6 +72,9 @@ struct PcgState {
   double sigma_part[2];  // per Ax launch when the operator is split (Alg. 1 overlap)
   double loc[4];         // P > 1: this rank's rho_new, gamma, sigma, res_true partial sums;
                          // the allreduce is out-of-place loc -> global, hence idempotent
+  double alpha, beta;    // flexible PCG (Schwarz) scalars
+  double dz[2];          // flexible PCG: <z', r'>_c, <z', w>_c
+  double loc_dz[2];      // P > 1: this rank's partials of dz
   int it;                // completed iterations
   int done;              // 0 running, 1 converged, 2 breakdown, 3 NaN, 4 maxit
   int iters;
@@ -164,6 +167,25 @@ cudaError_t launch_gm_start(GmresState* gs, PcgState* st, double* hist, cudaStre
 cudaError_t launch_gm_arnoldi(GmresState* gs, PcgState* st, double* hist, int m, cudaStream_t s);
 cudaError_t launch_gm_solve(GmresState* gs, PcgState* st, int m, cudaStream_t s);
 cudaError_t launch_gm_end_cycle(GmresState* gs, PcgState* st, cudaStream_t s);
+
+// NEXT-1 two-level Schwarz (schwarz.cu)
+cudaError_t launch_fdm_setup(int n, int nloc, int64_t e_lo, int ex, int ey, int ez,
+                             const double* box, int deform, double amp, const int* per,
+                             const double* xi, const double* wq, const double* D, double* S,
+                             double* lam, cudaStream_t s);
+cudaError_t launch_fdm(int n, int nloc, const double* r, const uint8_t* mult, const double* S,
+                       const double* lam, const double* xi, double* y, double* b0,
+                       const int* gate, int num_sms, cudaStream_t s);
+cudaError_t launch_schwarz_combine(int n, int64_t nslots, const double* y, const double* x0,
+                                   const uint8_t* mult, const double* xi, double* z,
+                                   const double* r, const double* w, double* partial,
+                                   unsigned* ticket, double* dots, const int* gate, int num_sms,
+                                   cudaStream_t s);
+cudaError_t launch_fcg_scalar(int stage, PcgState* st, double* hist, cudaStream_t s);
+cudaError_t launch_xpay(int64_t n, double* p, const double* z, const PcgState* st, int num_sms,
+                        cudaStream_t s);
+cudaError_t launch_gate_state(PcgState* st, const int* gate, cudaStream_t s);
+cudaError_t launch_rel_tol(PcgState* st, double rtol, cudaStream_t s);
 
 // interconnect probes for the performance model: one-thread ping-pong
 // with `peer` (round-trip ns per sample), and one-sided peer writes (bandwidth)

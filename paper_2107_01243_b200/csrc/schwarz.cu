@@ -1,0 +1,464 @@
+// Two-level additive overlapping Schwarz preconditioner on the device (SURVEY
+// 8(f) NEXT-1; "M0^-1 = R0^T A0^-1 R0 + sum_k R_k^T A~_k^-1 R_k",
+// "the coarse grid (on linear elements) is solved for using an approximate
+// Krylov solver, in essence performing few (~10) CG iterations"; readings
+// Q28-Q32 in DESIGN.md).
+//
+// Local solves by fast diagonalisation (Lynch-Rice-Thomas; Fischer 1997,
+// ref. [19]): the subdomain operator of element e is separable,
+//   A~ = Bz (x) By (x) Ax + Bz (x) Ay (x) Bx + Az (x) By (x) Bx,
+// with the element's 1-D SEM stiffness/mass extended by the neighbours' end
+// entries (one node of overlap, Dirichlet beyond).  With the generalised
+// eigenvectors S_d (S^T B S = I, S^T A S = Lambda) its inverse is
+//   A~^-1 = (Sz (x) Sy (x) Sx) diag(1 / (lx_a + ly_b + lz_c)) (Sz (x) Sy (x) Sx)^T,
+// six n x n contractions per element instead of an n^3 x n^3 solve.  The
+// 1-D eigenproblems are solved once at setup on the device (cyclic Jacobi on
+// B^-1/2 A B^-1/2, one thread per element and axis).  A node on a Dirichlet
+// face is dropped from its 1-D problem (zero row and column of S), so the
+// local solve ignores and returns zero on masked slots without a mask test.
+//
+// The same pass over r also forms the element's coarse restriction
+// (J^T (x) J^T (x) J^T)(c r_e), J_ia = (1 -+ xi_i)/2 (8 values per element):
+// r is read once for both levels.  The combine kernel scales the assembled
+// local part by c^1/2 (reading Q29), adds the trilinear prolongation of the
+// coarse solution and optionally forms the flexible-CG dots <z,r>_c, <z,w>_c.
+//
+// Roofline: HBM.  fdm_kernel moves 8 (r) + 1 (mult) + 8 (y) B/pt plus
+// 24 (n^2 + n) B per element of factors; combine 8 + 8 + 1 (+16) B/pt.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace sem {
+namespace dev {
+
+constexpr int kFT = 256;   // threads per block of the Schwarz kernels
+
+// mean length of global element eg along axis a: the four element edges
+// parallel to a, straight vertex-to-vertex distances (reading Q28)
+__device__ double elem_len(const double* xi, int N, int ex, int ey, int ez, int64_t eg, int a,
+                           const Box& b, int deform, double amp) {
+  double s = 0.0;
+  for (int u = 0; u < 2; u++)
+    for (int v = 0; v < 2; v++) {
+      int i0[3], i1[3];
+      const int o1 = u * N, o2 = v * N;
+      for (int d = 0; d < 3; d++) i0[d] = i1[d] = 0;
+      i0[a] = 0;
+      i1[a] = N;
+      const int d1 = a == 0 ? 1 : 0, d2 = a == 2 ? 1 : 2;
+      i0[d1] = i1[d1] = o1;
+      i0[d2] = i1[d2] = o2;
+      double p0[3], p1[3];
+      node_xyz(xi, ex, ey, ez, eg, i0[0], i0[1], i0[2], b, deform, amp, p0);
+      node_xyz(xi, ex, ey, ez, eg, i1[0], i1[1], i1[2], b, deform, amp, p1);
+      const double dx = p1[0] - p0[0], dy = p1[1] - p0[1], dz = p1[2] - p0[2];
+      s += sqrt(dx * dx + dy * dy + dz * dz);
+    }
+  return 0.25 * s;
+}
+
+// one thread per (local element, axis): extended 1-D operators, generalised
+// eigenvectors S[el][a][i*n + mode] and eigenvalues lam[el][a][mode]
+__global__ void fdm_setup_kernel(int n, int nloc, int64_t e_lo, int ex, int ey, int ez, Box b,
+                                 int deform, double amp, int per0, int per1, int per2,
+                                 const double* __restrict__ xi, const double* __restrict__ wq,
+                                 const double* __restrict__ D, double* __restrict__ Sg,
+                                 double* __restrict__ lamg) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * nloc) return;
+  const int el = t / 3, a = t - 3 * el;
+  const int N = n - 1;
+  const int64_t eg = e_lo + el;
+  const int64_t idx[3] = {eg % ex, (eg / ex) % ey, eg / ((int64_t)ex * ey)};
+  const int64_t Ea[3] = {ex, ey, ez};
+  const int per[3] = {per0, per1, per2};
+  double M[144], V[144], Bd[12];
+  const double h = elem_len(xi, N, ex, ey, ez, eg, a, b, deform, amp);
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < n; j++) {
+      double s = 0.0;
+      for (int q = 0; q < n; q++) s += wq[q] * D[q * n + i] * D[q * n + j];
+      M[i * n + j] = (2.0 / h) * s;
+    }
+  for (int i = 0; i < n; i++) Bd[i] = 0.5 * h * wq[i];
+  bool keep[2] = {false, false};
+  for (int side = 0; side < 2; side++) {
+    int64_t q = idx[a] + (side ? 1 : -1);
+    if (q < 0 || q >= Ea[a]) {
+      if (!per[a]) continue;   // Dirichlet face: the end node is dropped
+      q = (q + Ea[a]) % Ea[a];
+    }
+    keep[side] = true;
+    int64_t nb[3] = {idx[0], idx[1], idx[2]};
+    nb[a] = q;
+    const int64_t en = nb[0] + ex * (nb[1] + (int64_t)ey * nb[2]);
+    const double hn = elem_len(xi, N, ex, ey, ez, en, a, b, deform, amp);
+    double s = 0.0;   // the neighbour's stiffness entry at its shared end node
+    const int m = side ? 0 : N;
+    for (int q2 = 0; q2 < n; q2++) s += wq[q2] * D[q2 * n + m] * D[q2 * n + m];
+    const int e = side ? N : 0;
+    M[e * n + e] += (2.0 / hn) * s;
+    Bd[e] += 0.5 * hn * wq[m];
+  }
+  // B^-1/2 A B^-1/2 with the dropped nodes decoupled (zero rows and columns)
+  for (int i = 0; i < n; i++) {
+    const bool di = (i == 0 && !keep[0]) || (i == N && !keep[1]);
+    for (int j = 0; j < n; j++) {
+      const bool dj = (j == 0 && !keep[0]) || (j == N && !keep[1]);
+      M[i * n + j] = (di || dj) ? 0.0 : M[i * n + j] / sqrt(Bd[i] * Bd[j]);
+      V[i * n + j] = i == j ? 1.0 : 0.0;
+    }
+  }
+  // cyclic Jacobi (Golub-Van Loan 8.5.3)
+  for (int sweep = 0; sweep < 30; sweep++) {
+    double off = 0.0, dia = 0.0;
+    for (int i = 0; i < n; i++)
+      for (int j = 0; j < n; j++)
+        if (i != j) off += M[i * n + j] * M[i * n + j];
+        else dia += M[i * n + j] * M[i * n + j];
+    if (off <= 1e-34 * dia) break;
+    for (int p = 0; p < n - 1; p++)
+      for (int q = p + 1; q < n; q++) {
+        const double apq = M[p * n + q];
+        if (fabs(apq) < 1e-300) continue;
+        const double tau = (M[q * n + q] - M[p * n + p]) / (2.0 * apq);
+        const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = tt * c;
+        for (int k = 0; k < n; k++) {
+          const double mkp = M[k * n + p], mkq = M[k * n + q];
+          M[k * n + p] = c * mkp - s * mkq;
+          M[k * n + q] = s * mkp + c * mkq;
+        }
+        for (int k = 0; k < n; k++) {
+          const double mpk = M[p * n + k], mqk = M[q * n + k];
+          M[p * n + k] = c * mpk - s * mqk;
+          M[q * n + k] = s * mpk + c * mqk;
+        }
+        for (int k = 0; k < n; k++) {
+          const double vkp = V[k * n + p], vkq = V[k * n + q];
+          V[k * n + p] = c * vkp - s * vkq;
+          V[k * n + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  double* S = Sg + ((size_t)el * 3 + a) * n * n;
+  double* lam = lamg + ((size_t)el * 3 + a) * n;
+  for (int mode = 0; mode < n; mode++) {
+    // a dropped node keeps its own (never rotated) mode: zero column, lambda 1
+    const bool dm = (mode == 0 && !keep[0]) || (mode == N && !keep[1]);
+    lam[mode] = dm ? 1.0 : M[mode * n + mode];
+    for (int i = 0; i < n; i++) {
+      const bool di = (i == 0 && !keep[0]) || (i == N && !keep[1]);
+      S[i * n + mode] = (dm || di) ? 0.0 : V[i * n + mode] / sqrt(Bd[i]);
+    }
+  }
+}
+
+// y_e = A~_e^-1 (c^1/2 r)_e (fast diagonalisation) and b0_e = (J^T)^3 (c r)_e;
+// either output may be null.  Skipped when *gate.
+template <int n>
+__global__ void __launch_bounds__(kFT) fdm_kernel(int nloc, const double* __restrict__ r,
+                                                  const uint8_t* __restrict__ mult,
+                                                  const double* __restrict__ Sg,
+                                                  const double* __restrict__ lamg,
+                                                  const double* __restrict__ xi,
+                                                  double* __restrict__ y, double* __restrict__ b0,
+                                                  const int* gate) {
+  constexpr int n2 = n * n, n3 = n2 * n;
+  __shared__ double u[n3], t[n3];
+  __shared__ double S[3][n2], lam[3][n], J[n][2];
+  __shared__ double red[kFT / 32][8];
+  if (gate && *gate) return;
+  const int tid = threadIdx.x;
+  if (tid < n) {
+    J[tid][0] = 0.5 * (1.0 - xi[tid]);
+    J[tid][1] = 0.5 * (1.0 + xi[tid]);
+  }
+  for (int el = blockIdx.x; el < nloc; el += gridDim.x) {
+    const double* re = r + (int64_t)el * n3;
+    const uint8_t* me = mult + (int64_t)el * n3;
+    __syncthreads();   // J ready; the previous element is done with u, t, S
+    double acc[8];
+#pragma unroll
+    for (int v = 0; v < 8; v++) acc[v] = 0.0;
+    for (int p = tid; p < n3; p += kFT) {
+      const double rv = __ldcs(&re[p]);
+      const double c = __drcp_rn((double)me[p]);
+      u[p] = sqrt(c) * rv;
+      if (b0) {
+        const int i = p % n, j = (p / n) % n, k = p / n2;
+        const double cr = c * rv;
+#pragma unroll
+        for (int v = 0; v < 8; v++)
+          acc[v] = fma(J[i][v & 1] * J[j][(v >> 1) & 1] * J[k][v >> 2], cr, acc[v]);
+      }
+    }
+    if (y) {
+      const double* Se = Sg + (size_t)el * 3 * n2;
+      const double* le = lamg + (size_t)el * 3 * n;
+      for (int q = tid; q < 3 * n2; q += kFT) (&S[0][0])[q] = __ldcs(&Se[q]);
+      for (int q = tid; q < 3 * n; q += kFT) (&lam[0][0])[q] = __ldcs(&le[q]);
+    }
+    if (b0) {
+      const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+      for (int v = 0; v < 8; v++) {
+        const double s = warp_sum(acc[v]);
+        if (lane == 0) red[wid][v] = s;
+      }
+    }
+    __syncthreads();
+    if (b0 && tid < 8) {
+      double s = 0.0;
+      for (int w = 0; w < kFT / 32; w++) s += red[w][tid];
+      b0[(int64_t)el * 8 + tid] = s;
+    }
+    if (!y) continue;
+    // forward transform: t = (Sx^T) u along i, u = (Sy^T) t along j, t = (Sz^T) u / Lambda
+    for (int p = tid; p < n3; p += kFT) {
+      const int a = p % n, jk = p / n;
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; i++) s = fma(S[0][i * n + a], u[i + n * jk], s);
+      t[p] = s;
+    }
+    __syncthreads();
+    for (int p = tid; p < n3; p += kFT) {
+      const int a = p % n, b = (p / n) % n, k = p / n2;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < n; j++) s = fma(S[1][j * n + b], t[a + n * j + n2 * k], s);
+      u[p] = s;
+    }
+    __syncthreads();
+    for (int p = tid; p < n3; p += kFT) {
+      const int a = p % n, b = (p / n) % n, c = p / n2;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < n; k++) s = fma(S[2][k * n + c], u[a + n * b + n2 * k], s);
+      t[p] = s / (lam[0][a] + lam[1][b] + lam[2][c]);
+    }
+    __syncthreads();
+    // backward: u = Sz t along c, t = Sy u along b, y = Sx t along a
+    for (int p = tid; p < n3; p += kFT) {
+      const int ab = p % n2, k = p / n2;
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < n; c++) s = fma(S[2][k * n + c], t[ab + n2 * c], s);
+      u[p] = s;
+    }
+    __syncthreads();
+    for (int p = tid; p < n3; p += kFT) {
+      const int a = p % n, j = (p / n) % n, k = p / n2;
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < n; b++) s = fma(S[1][j * n + b], u[a + n * b + n2 * k], s);
+      t[p] = s;
+    }
+    __syncthreads();
+    double* ye = y + (int64_t)el * n3;
+    for (int p = tid; p < n3; p += kFT) {
+      const int i = p % n, jk = p / n;
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < n; a++) s = fma(S[0][i * n + a], t[a + n * jk], s);
+      __stcs(&ye[p], s);
+    }
+  }
+}
+
+// z = c^1/2 y + (J (x) J (x) J) x0_e (either part may be null).  DOTS: the
+// flexible-CG dots <z, r>_c and <z, w>_c into dots[0..1] (deterministic grid
+// reduction).  Skipped when *gate.
+template <bool DOTS>
+__global__ void __launch_bounds__(kFT) schwarz_combine_kernel(
+    int n, int64_t nslots, const double* __restrict__ y, const double* __restrict__ x0,
+    const uint8_t* __restrict__ mult, const double* __restrict__ xi, double* __restrict__ z,
+    const double* __restrict__ r, const double* __restrict__ w, double* partial,
+    unsigned* ticket, double* dots, const int* gate) {
+  __shared__ double J[12][2];
+  __shared__ double scratch[32];
+  __shared__ int flag;
+  if (gate && *gate) return;
+  if (threadIdx.x < n) {
+    J[threadIdx.x][0] = 0.5 * (1.0 - xi[threadIdx.x]);
+    J[threadIdx.x][1] = 0.5 * (1.0 + xi[threadIdx.x]);
+  }
+  __syncthreads();
+  const int n2 = n * n, n3 = n2 * n;
+  double zr = 0.0, zw = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nslots;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double c = __drcp_rn((double)mult[l]);
+    double v = y ? sqrt(c) * __ldcs(&y[l]) : 0.0;
+    if (x0) {
+      const int64_t el = l / n3;
+      const int p = (int)(l - el * n3);
+      const int i = p % n, j = (p / n) % n, k = p / n2;
+      const double* xe = x0 + el * 8;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) s = fma(J[i][q & 1] * J[j][(q >> 1) & 1] * J[k][q >> 2], xe[q], s);
+      v += s;
+    }
+    z[l] = v;
+    if (DOTS) {
+      const double cv = c * v;
+      zr = fma(cv, r[l], zr);
+      zw = fma(cv, w[l], zw);
+    }
+  }
+  if (DOTS) {
+    double vv[2] = {zr, zw};
+    grid_reduce<2>(vv, partial, ticket, dots, scratch, &flag);
+  }
+}
+
+// ---- flexible PCG scalars (device-resident, one thread)
+// stage 0: start (rho = <r,z>, gamma = <r,r> reduced into st->rho_new, st->gamma)
+// stage 1: alpha = rho / sigma (breakdown if sigma <= 0)
+// stage 2: iteration count, history, convergence on sqrt(gamma)
+// stage 3: beta = -alpha <z', w>_c / rho, rho = <z', r'>_c; maxit
+__global__ void fcg_scalar_kernel(int stage, PcgState* st, double* hist) {
+  if (stage == 0) {
+    st->rho_old = st->rho_new;
+    st->it = 0;
+    st->iters = 0;
+    const double g = sqrt(st->gamma);
+    hist[0] = g;
+    st->done = (g <= st->tol) ? 1 : (st->maxit == 0 ? 4 : 0);
+    return;
+  }
+  if (st->done) return;
+  if (stage == 1) {
+    const double sigma = st->sigma;
+    if (!(sigma > 0.0)) {
+      st->done = 2;
+      st->iters = st->it + 1;
+      return;
+    }
+    st->alpha = st->rho_old / sigma;
+  } else if (stage == 2) {
+    const int it = st->it + 1;
+    st->it = it;
+    const double g = sqrt(st->gamma);
+    hist[it] = g;
+    if (!(g == g)) {
+      st->done = 3;
+      st->iters = it;
+    } else if (g <= st->tol) {
+      st->done = 1;
+      st->iters = it;
+    }
+  } else {
+    st->beta = -st->alpha * st->dz[1] / st->rho_old;
+    st->rho_old = st->dz[0];
+    if (!(st->beta == st->beta)) {
+      st->done = 3;
+      st->iters = st->it;
+    } else if (st->it >= st->maxit) {
+      st->done = 4;
+      st->iters = st->it;
+    }
+  }
+}
+
+// p = z + beta p (skipped when *done)
+__global__ void __launch_bounds__(kFT) xpay_kernel(int64_t n, double* __restrict__ p,
+                                                   const double* __restrict__ z,
+                                                   const PcgState* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x)
+    p[l] = fma(beta, p[l], z[l]);
+}
+
+// coarse solve gate: a finished outer iteration makes the coarse CG a no-op
+__global__ void gate_state_kernel(PcgState* st, const int* gate) {
+  if (gate && *gate) st->done = 5;
+}
+
+// relative stopping rule of the coarse CG (reading Q31): tol = rtol ||b0||_c
+__global__ void rel_tol_kernel(PcgState* st, double rtol) {
+  const double g = sqrt(st->gamma);
+  st->tol = rtol * g;
+  st->done = (g <= st->tol) ? 1 : (st->maxit == 0 ? 4 : 0);
+}
+
+}  // namespace dev
+
+cudaError_t launch_fdm_setup(int n, int nloc, int64_t e_lo, int ex, int ey, int ez,
+                             const double* box, int deform, double amp, const int* per,
+                             const double* xi, const double* wq, const double* D, double* S,
+                             double* lam, cudaStream_t s) {
+  dev::Box b{box[0], box[1], box[2], box[3], box[4], box[5]};
+  const int nt = 3 * nloc;
+  if (nt == 0) return cudaSuccess;
+  dev::fdm_setup_kernel<<<(nt + 63) / 64, 64, 0, s>>>(n, nloc, e_lo, ex, ey, ez, b, deform, amp,
+                                                      per[0], per[1], per[2], xi, wq, D, S, lam);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fdm(int n, int nloc, const double* r, const uint8_t* mult, const double* S,
+                       const double* lam, const double* xi, double* y, double* b0,
+                       const int* gate, int num_sms, cudaStream_t s) {
+  if (nloc == 0) return cudaSuccess;
+  const int grid = std::min(nloc, num_sms * 8);
+#define FDM_CASE(NN)                                                                        \
+  case NN:                                                                                  \
+    dev::fdm_kernel<NN><<<grid, dev::kFT, 0, s>>>(nloc, r, mult, S, lam, xi, y, b0, gate); \
+    break;
+  switch (n) {
+    FDM_CASE(2) FDM_CASE(3) FDM_CASE(4) FDM_CASE(5) FDM_CASE(6) FDM_CASE(7) FDM_CASE(8)
+    FDM_CASE(9) FDM_CASE(10) FDM_CASE(11) FDM_CASE(12)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FDM_CASE
+  return cudaGetLastError();
+}
+
+cudaError_t launch_schwarz_combine(int n, int64_t nslots, const double* y, const double* x0,
+                                   const uint8_t* mult, const double* xi, double* z,
+                                   const double* r, const double* w, double* partial,
+                                   unsigned* ticket, double* dots, const int* gate, int num_sms,
+                                   cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + dev::kFT - 1) / dev::kFT,
+                                                                (int64_t)num_sms * 8));
+  if (dots)
+    dev::schwarz_combine_kernel<true><<<grid, dev::kFT, 0, s>>>(
+        n, nslots, y, x0, mult, xi, z, r, w, partial, ticket, dots, gate);
+  else
+    dev::schwarz_combine_kernel<false><<<grid, dev::kFT, 0, s>>>(
+        n, nslots, y, x0, mult, xi, z, r, w, partial, ticket, dots, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fcg_scalar(int stage, PcgState* st, double* hist, cudaStream_t s) {
+  dev::fcg_scalar_kernel<<<1, 1, 0, s>>>(stage, st, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xpay(int64_t n, double* p, const double* z, const PcgState* st, int num_sms,
+                        cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + dev::kFT - 1) / dev::kFT,
+                                                                (int64_t)num_sms * 8));
+  dev::xpay_kernel<<<grid, dev::kFT, 0, s>>>(n, p, z, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_state(PcgState* st, const int* gate, cudaStream_t s) {
+  dev::gate_state_kernel<<<1, 1, 0, s>>>(st, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rel_tol(PcgState* st, double rtol, cudaStream_t s) {
+  dev::rel_tol_kernel<<<1, 1, 0, s>>>(st, rtol);
+  return cudaGetLastError();
+}
+
+}  // namespace sem

@@ -127,6 +127,63 @@ def helm(cfg="C3", h1=1.0 / 1600.0, h2=2000.0):
              "pcg_gdofs": round(n * r["iters"] / (pms * 1e-3) / 1e9, 2), "e_inf_vs_p*": einf})
 
 
+def schwarz(cfgs=("C3", "C4")):
+    """NEXT-1: the two-level Schwarz preconditioner on BASELINE
+    configs: time of one application (local FDM part, coarse part, both), the
+    FDM kernel against HBM (8 r + 1 mult + 8 y B/pt + 24 (n^2 + n) B of
+    factors per element), and time-to-solution to 1e-10 on the TGV pressure
+    right-hand side: Jacobi-PCG, Schwarz flexible PCG, Jacobi GMRES(30),
+    Schwarz flexible GMRES(30)."""
+    torch.cuda.set_device(0)
+    st = torch.cuda.current_stream()
+    for cfg in cfgs:
+        spec, N = CONFIGS[cfg]
+        n1 = N + 1
+        with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
+            n = c.n_local
+            X, Y, Z = c.coords()
+            b = c.zeros()
+            c.rhs(f_tgv(X, Y, Z, xp=torch), b)
+            del X, Y, Z
+            z = c.zeros()
+            c.schwarz_apply(b, z, 3)
+            res = {"what": f"{cfg}_schwarz", "n_local": n}
+            for which, name in ((1, "local"), (2, "coarse"), (3, "both")):
+                c.timing(True)
+                ms = timed(lambda: c.schwarz_apply(b, z, which), st, 20)
+                t_fdm, k_fdm = c.timing_read(7)
+                t_cmb, k_cmb = c.timing_read(8)
+                c.timing(False)
+                res[f"apply_{name}_ms"] = round(ms, 4)
+                if which == 1 and k_fdm:
+                    fdm_ms = t_fdm / k_fdm
+                    bpp = 17.0 + 24.0 * (n1 * n1 + n1) / n1 ** 3
+                    res["fdm_kernel_ms"] = round(fdm_ms, 4)
+                    res["fdm_B_per_pt"] = round(bpp, 2)
+                    res["fdm_GBps"] = round(bpp * n / (fdm_ms * 1e-3) / 1e9, 0)
+                    res["fdm_frac_copy"] = round(bpp * n / (fdm_ms * 1e-3) / 1e9 / peak_copy(), 3)
+                    res["combine_kernel_ms"] = round(t_cmb / max(k_cmb, 1), 4)
+            for pc in ("jacobi", "schwarz"):
+                c.set_precond(pc)
+                for solver in ("pcg", "gmres"):
+                    x = c.zeros()
+                    fn = (lambda: c.pcg_solve(b, x, 1e-10, 3000)) if solver == "pcg" else \
+                        (lambda: c.gmres_solve(b, x, 1e-10, 3000, 30))
+                    fn()
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    r = fn()
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    ms = e0.elapsed_time(e1)
+                    res[f"{solver}_{pc}"] = {"iters": r["iters"], "status": r["status"],
+                                             "ms": round(ms, 3), "res_true": r["res_true"],
+                                             "ms_per_iter": round(ms / max(r["iters"], 1), 4)}
+            c.set_precond("jacobi")
+            out(res)
+
+
 def pcg_rate(c, st, iters):
     """fixed-iteration PCG (tol 0) on the TGV right-hand side: iter/s, GDOF/s"""
     X, Y, Z = c.coords()
@@ -252,6 +309,8 @@ if __name__ == "__main__":
         strong()
     elif mode == "sweep":
         sweep([int(v) for v in sys.argv[2].split(",")])
+    elif mode == "schwarz":
+        schwarz(tuple(sys.argv[2].split(",")) if len(sys.argv) > 2 else ("C3", "C4"))
     elif mode == "helm":
         helm(sys.argv[2] if len(sys.argv) > 2 else "C3")
     elif mode == "ops":   # Ax / Ax+gs rates (all gs schedules) on named configs
