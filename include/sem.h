@@ -190,7 +190,8 @@ int sem_nccl_comm_destroy(void* comm);
    sem_timing(c, 1) records CUDA events on the context stream around every
    launch of kernel class `which` (0 = Ax kernel of apply/PCG, 1 = CG
    update, 2 = p update, 3 = Ax only, 4 = gather-scatter kernel of apply/PCG,
-   5 = peer-memory pack, 6 = peer-memory unpack); sem_timing_read returns the summed
+   5 = peer-memory pack, 6 = peer-memory unpack, 7 = Schwarz local-solve kernel,
+   8 = Schwarz combine kernel); sem_timing_read returns the summed
    device time in ms and the number of timed launches since the last reset.
    sem_launch_count returns the number of kernels this context has launched. */
 int sem_timing(sem_ctx* c, int enable);
@@ -239,6 +240,12 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
 #define SEM_PRECOND_SCHWARZ 1
 /* maximum CG iterations of the Schwarz coarse solve (default 10) */
 #define SEM_OPT_COARSE_ITERS 7
+/* 1 (default) = on one rank the Schwarz coarse solve is captured once and
+   replayed as a CUDA graph (identical results); 0 = stream launches */
+#define SEM_OPT_COARSE_GRAPH 8
+/* 1 (default) = at N = 7 the Schwarz local solves run their six 8x8
+   contractions on the fp64 tensor cores (DMMA m8n8k4); 0 = CUDA-core kernel */
+#define SEM_OPT_FDM_TC 9
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

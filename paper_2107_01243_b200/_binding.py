@@ -254,6 +254,14 @@ class Context:
         'schwarz' (flexible PCG / flexible GMRES).  Collective (builds Schwarz)."""
         _check(load().sem_set_option(self._h, 6, {"jacobi": 0, "schwarz": 1}[kind]))
 
+    def set_coarse_graph(self, on: bool):
+        """Replay the one-rank Schwarz coarse solve as a CUDA graph (default on)."""
+        _check(load().sem_set_option(self._h, 8, 1 if on else 0))
+
+    def set_fdm_tc(self, on: bool):
+        """N = 7 Schwarz local solves on the fp64 tensor cores (default) or CUDA cores."""
+        _check(load().sem_set_option(self._h, 9, 1 if on else 0))
+
     def set_coarse_iters(self, k: int):
         """Maximum CG iterations of the Schwarz coarse solve (default 10)."""
         _check(load().sem_set_option(self._h, 7, int(k)))

@@ -93,6 +93,10 @@ struct sem_ctx {
   sem::GmresState* d_gs = nullptr;
   unsigned* d_ktick = nullptr;
   int gm_cap = 0;
+  // leading dimension of the multi-vector blocks (V, Z, projection space):
+  // n rounded up plus an odd multiple of 128 B, so the k streams a multi-dot
+  // reads concurrently do not start at the same power-of-two offset
+  int64_t ldv = 0;
   double *d_Z = nullptr, *d_AZ = nullptr, *d_pdelta = nullptr, *d_pbd = nullptr;
   int proj_m = 0, proj_k = 0;
   // NEXT-1: two-level Schwarz (schwarz.cu); the coarse space is a second
@@ -107,6 +111,15 @@ struct sem_ctx {
   double *d_rw = nullptr, *d_z = nullptr;        // flexible PCG: [r | w], z
   double* d_Zs = nullptr;                        // flexible GMRES: M v_j
   int zs_cap = 0;
+  // single rank: the coarse solve replayed as one CUDA graph (its launches are
+  // argument-stable: flat gs schedule, no peer epochs); gate copied to d_gate
+  bool coarse_graph = true;
+  bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
+  cudaGraphExec_t g0exec = nullptr;
+  int g0_iters = -1;
+  int64_t g0_launches = 0;
+  int* d_gate = nullptr;
+  cudaStream_t cap_stream = nullptr;   // capture stream (the legacy stream cannot capture)
   // Helmholtz (NEXT-2): operator in use by apply_op / pcg_run, and its Jacobi cache
   bool helm = false;
   double h1 = 1.0, h2 = 0.0;
@@ -442,6 +455,9 @@ void free_ctx(sem_ctx* c) {
   if (c->d_gs) cudaFree(c->d_gs);
   if (c->d_ktick) cudaFree(c->d_ktick);
   if (c->c0) free_ctx(c->c0);
+  if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
+  if (c->d_gate) cudaFree(c->d_gate);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->h_st) cudaFreeHost(c->h_st);
   for (char* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_perr};
@@ -616,6 +632,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(dalloc(&c->d_send, (size_t)h.nbuf));
   SETUP_TRY(dalloc(&c->d_recv, (size_t)h.nbuf));
   const size_t nl = (size_t)h.n_local;
+  c->ldv = ((h.n_local + 255) / 256) * 256 + 304;   // + 2432 B = 19 x 128 B
   SETUP_TRY(dalloc(&c->d_G, 6 * nl));
   SETUP_TRY(dalloc(&c->d_B, nl));
   SETUP_TRY(dalloc(&c->d_dinv, nl));
@@ -898,6 +915,7 @@ static int schwarz_setup(sem_ctx* c) {
   sem_ctx* c0 = nullptr;
   SEM_TRY(sem_setup(&h.m, 1, &c0));   // collective for nranks > 1
   c->c0 = c0;
+  if (h.nranks == 1) c0->gs_mode = 1;   // flat schedule: graph-stable launches (bit-identical)
   const size_t nloc = (size_t)h.nloc, n = (size_t)h.n;
   SEM_TRY(dalloc(&c->d_fS, nloc * 3 * n * n));
   SEM_TRY(dalloc(&c->d_flam, nloc * 3 * n));
@@ -931,7 +949,7 @@ static int coarse_state(sem_ctx* c) {
 }
 
 // x0 = A0^-1 b0 by <= K0 plain CG steps (reading Q31); no-op when *gate
-static int coarse_solve(sem_ctx* c, const int* gate) {
+static int coarse_body(sem_ctx* c, const int* gate) {
   sem_ctx* c0 = c->c0;
   cudaStream_t s = c0->stream;
   SEM_TRY(gs_op(c0, c->d_b0, 1));
@@ -952,6 +970,54 @@ static int coarse_solve(sem_ctx* c, const int* gate) {
   return SEM_OK;
 }
 
+static int coarse_solve(sem_ctx* c, const int* gate) {
+  if (c->hp.nranks > 1 || !c->coarse_graph || c->timing) return coarse_body(c, gate);
+  cudaStream_t s = c->stream;
+  if (!c->g0exec || c->g0_iters != c->coarse_iters) {
+    if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
+    c->g0exec = nullptr;
+    if (!c->d_gate) SEM_TRY(dalloc(&c->d_gate, 1));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (!c->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    const int64_t l0 = c->launches + c->c0->launches;
+    cudaGraph_t graph = nullptr;
+    // capture on a private stream (the context stream may be the legacy one)
+    cudaStream_t s_save = c->stream, s0_save = c->c0->stream;
+    c->stream = c->c0->stream = c->cap_stream;
+    if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      c->stream = s_save;
+      c->c0->stream = s0_save;
+      c->coarse_graph = false;
+      return coarse_body(c, gate);
+    }
+    const int st = coarse_body(c, c->d_gate);
+    const cudaError_t ec = cudaStreamEndCapture(c->cap_stream, &graph);
+    c->stream = s_save;
+    c->c0->stream = s0_save;
+    if (st != SEM_OK || ec != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      c->coarse_graph = false;   // fall back to stream launches
+      return coarse_body(c, gate);
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&c->g0exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      cudaGetLastError();
+      c->g0exec = nullptr;
+      c->coarse_graph = false;
+      return coarse_body(c, gate);
+    }
+    c->g0_launches = c->launches + c->c0->launches - l0;
+    c->g0_iters = c->coarse_iters;
+  }
+  CUDA_TRY(sem::launch_copy_gate(c->d_gate, gate, s));
+  CUDA_TRY(cudaGraphLaunch(c->g0exec, s));
+  c->launches += 1 + c->g0_launches;
+  return SEM_OK;
+}
+
 // z = M r (which: 1 local, 2 coarse, 3 both); dots (flexible PCG): <z, r>_c and
 // <z, w>_c into st->dz; every kernel is a no-op when *gate
 static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, const int* gate,
@@ -962,7 +1028,7 @@ static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, cons
   double* b0 = (which & 2) ? c->d_b0 : nullptr;
   int tk = timer_begin(c, 7);
   CUDA_TRY(sem::launch_fdm(h.n, (int)h.nloc, r, c->d_mult, c->d_fS, c->d_flam, c->d_xi, y, b0,
-                           gate, c->num_sms, s));
+                           gate, c->num_sms, c->fdm_tc, s));
   timer_end(c, tk);
   c->launches++;
   if (y) SEM_TRY(gs_op(c, y, 0));
@@ -971,7 +1037,7 @@ static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, cons
   const bool dist = h.nranks > 1;
   double* dots = w_dot ? (dist ? st->loc_dz : st->dz) : nullptr;
   tk = timer_begin(c, 8);
-  CUDA_TRY(sem::launch_schwarz_combine(h.n, h.n_local, y, b0 ? c->d_x0 : nullptr, c->d_mult,
+  CUDA_TRY(sem::launch_schwarz_combine(h.n, (int)h.nloc, y, b0 ? c->d_x0 : nullptr, c->d_mult,
                                        c->d_xi, z, r, w_dot, c->d_partial, &c->d_tickets[5], dots,
                                        gate, c->num_sms, s));
   timer_end(c, tk);
@@ -1154,9 +1220,9 @@ static int gm_alloc(sem_ctx* c, int m) {
   if (m + 1 > c->gm_cap) {
     if (c->d_V) cudaFree(c->d_V);
     c->d_V = nullptr;
-    SEM_TRY(dalloc(&c->d_V, (m + 1) * n));
+    SEM_TRY(dalloc(&c->d_V, (m + 1) * (size_t)c->ldv));
     // finite contents: unused basis vectors are multiplied by zero coefficients
-    CUDA_TRY(cudaMemsetAsync(c->d_V, 0, (m + 1) * n * sizeof(double), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->d_V, 0, (m + 1) * (size_t)c->ldv * sizeof(double), c->stream));
     c->gm_cap = m + 1;
   }
   return SEM_OK;
@@ -1170,14 +1236,15 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
   SEM_TRY(ensure_hist(c, maxit));
   // flexible GMRES with the Schwarz preconditioner (NEXT-1): z_j = M v_j stored
   const bool schw = c->precond == SEM_PRECOND_SCHWARZ && !c->helm;
+  const int64_t ld = c->ldv;
   if (schw) {
     SEM_TRY(schwarz_setup(c));
     SEM_TRY(coarse_state(c));
     if (m > c->zs_cap) {
       if (c->d_Zs) cudaFree(c->d_Zs);
       c->d_Zs = nullptr;
-      SEM_TRY(dalloc(&c->d_Zs, (size_t)m * c->hp.n_local));
-      CUDA_TRY(cudaMemsetAsync(c->d_Zs, 0, (size_t)m * c->hp.n_local * sizeof(double), c->stream));
+      SEM_TRY(dalloc(&c->d_Zs, (size_t)m * c->ldv));
+      CUDA_TRY(cudaMemsetAsync(c->d_Zs, 0, (size_t)m * c->ldv * sizeof(double), c->stream));
       c->zs_cap = m;
     }
   }
@@ -1214,26 +1281,26 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
     c->launches += 4;
     if (schw) SEM_TRY(schwarz_apply(c, c->d_V, c->d_Zs, 3, cyc, nullptr));
     for (int j = 0; j < m; j++) {
-      double* Vn = c->d_V + (size_t)(j + 1) * n;
+      double* Vn = c->d_V + (size_t)(j + 1) * ld;
       {
         GateScope g(c, cyc);
-        SEM_TRY(apply_op(c, schw ? c->d_Zs + (size_t)j * n : c->d_gt, w,
+        SEM_TRY(apply_op(c, schw ? c->d_Zs + (size_t)j * ld : c->d_gt, w,
                          sem::AX_APPLY));   // w = A M^-1 v_j
       }
       // two classical Gram-Schmidt passes against v_0..v_j, then ||w||_c
-      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, n, j + 1, part, tk, gs->h1, cyc, sms, s));
+      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, ld, j + 1, part, tk, gs->h1, cyc, sms, s));
       if (dist) SEM_TRY(allreduce(c, gs->h1, j + 1));
-      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, n, j + 1, gs->h1, -1.0, nullptr, mult, part, tk,
+      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, ld, j + 1, gs->h1, -1.0, nullptr, mult, part, tk,
                                  nullptr, cyc, sms, s));
-      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, n, j + 1, part, tk, gs->h2, cyc, sms, s));
+      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, ld, j + 1, part, tk, gs->h2, cyc, sms, s));
       if (dist) SEM_TRY(allreduce(c, gs->h2, j + 1));
-      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, n, j + 1, gs->h2, -1.0, nullptr, mult, part, tk,
+      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, ld, j + 1, gs->h2, -1.0, nullptr, mult, part, tk,
                                  &gs->norm2[0], cyc, sms, s));
       if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
       CUDA_TRY(sem::launch_gm_arnoldi(gs, st, c->d_hist, m, s));
       CUDA_TRY(sem::launch_vnorm(n, w, Vn, schw ? nullptr : c->d_gt, dinv, gs, cyc, sms, s));
       c->launches += 6;
-      if (schw && j + 1 < m) SEM_TRY(schwarz_apply(c, Vn, c->d_Zs + (size_t)(j + 1) * n, 3, cyc, nullptr));
+      if (schw && j + 1 < m) SEM_TRY(schwarz_apply(c, Vn, c->d_Zs + (size_t)(j + 1) * ld, 3, cyc, nullptr));
       if ((j + 1) % kBatch == 0 && j + 1 < m) {   // poll: stop enqueuing a finished cycle
         int cd = 0;
         CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &gs->cycle_done, sizeof(int),
@@ -1246,10 +1313,10 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
     // y = H^-1 g; x += M^-1 V y; converged / maxit -> done
     CUDA_TRY(sem::launch_gm_solve(gs, st, m, s));
     if (schw)   // x += Z y
-      CUDA_TRY(sem::launch_maxpy(n, x, c->d_Zs, n, m, gs->y, 1.0, nullptr, mult, part, tk, nullptr,
+      CUDA_TRY(sem::launch_maxpy(n, x, c->d_Zs, ld, m, gs->y, 1.0, nullptr, mult, part, tk, nullptr,
                                  done, sms, s));
     else        // x += M^-1 V y
-      CUDA_TRY(sem::launch_maxpy(n, x, c->d_V, n, m, gs->y, 1.0, dinv, mult, part, tk, nullptr,
+      CUDA_TRY(sem::launch_maxpy(n, x, c->d_V, ld, m, gs->y, 1.0, dinv, mult, part, tk, nullptr,
                                  done, sms, s));
     CUDA_TRY(sem::launch_gm_end_cycle(gs, st, s));
     c->launches += 3;
@@ -1301,8 +1368,8 @@ static int proj_alloc(sem_ctx* c, int m) {
   for (double* p : bufs)
     if (p) cudaFree(p);
   c->d_Z = c->d_AZ = c->d_pdelta = c->d_pbd = nullptr;
-  SEM_TRY(dalloc(&c->d_Z, m * n));
-  SEM_TRY(dalloc(&c->d_AZ, m * n));
+  SEM_TRY(dalloc(&c->d_Z, m * (size_t)c->ldv));
+  SEM_TRY(dalloc(&c->d_AZ, m * (size_t)c->ldv));
   SEM_TRY(dalloc(&c->d_pdelta, n));
   SEM_TRY(dalloc(&c->d_pbd, n));
   c->proj_m = m;
@@ -1319,8 +1386,8 @@ static int proj_update(sem_ctx* c, const double* x, int* skipped) {
   sem::GmresState* gs = c->d_gs;
   if (c->proj_k == c->proj_m) c->proj_k = 0;   // full: reset, keep the latest
   const int k = c->proj_k;
-  double* z = c->d_Z + (size_t)k * n;
-  double* az = c->d_AZ + (size_t)k * n;
+  double* z = c->d_Z + (size_t)k * c->ldv;
+  double* az = c->d_AZ + (size_t)k * c->ldv;
   CUDA_TRY(cudaMemcpyAsync(z, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   SEM_TRY(apply_op(c, z, az, sem::AX_APPLY));
   CUDA_TRY(sem::launch_mdot(n, c->d_mult, z, az, n, 1, c->d_kpart, c->d_ktick, &gs->norm2[0],
@@ -1328,12 +1395,12 @@ static int proj_update(sem_ctx* c, const double* x, int* skipped) {
   if (dist) SEM_TRY(allreduce(c, &gs->norm2[0], 1));
   for (int pass = 0; pass < 2 && k > 0; pass++) {
     double* coef = pass == 0 ? gs->h1 : gs->h2;
-    CUDA_TRY(sem::launch_mdot(n, c->d_mult, az, c->d_Z, n, k, c->d_kpart, c->d_ktick, coef,
+    CUDA_TRY(sem::launch_mdot(n, c->d_mult, az, c->d_Z, c->ldv, k, c->d_kpart, c->d_ktick, coef,
                               nullptr, sms, s));
     if (dist) SEM_TRY(allreduce(c, coef, k));
-    CUDA_TRY(sem::launch_maxpy(n, z, c->d_Z, n, k, coef, -1.0, nullptr, c->d_mult, c->d_kpart,
+    CUDA_TRY(sem::launch_maxpy(n, z, c->d_Z, c->ldv, k, coef, -1.0, nullptr, c->d_mult, c->d_kpart,
                                c->d_ktick, nullptr, nullptr, sms, s));
-    CUDA_TRY(sem::launch_maxpy(n, az, c->d_AZ, n, k, coef, -1.0, nullptr, c->d_mult, c->d_kpart,
+    CUDA_TRY(sem::launch_maxpy(n, az, c->d_AZ, c->ldv, k, coef, -1.0, nullptr, c->d_mult, c->d_kpart,
                                c->d_ktick, nullptr, nullptr, sms, s));
     c->launches += 3;
   }
@@ -1377,12 +1444,12 @@ extern "C" int sem_proj_solve(sem_ctx* c, const double* b, double* x, double tol
   CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
   CUDA_TRY(cudaMemcpyAsync(c->d_pbd, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   if (k > 0) {
-    CUDA_TRY(sem::launch_mdot(n, c->d_mult, b, c->d_Z, n, k, c->d_kpart, c->d_ktick, gs->y,
+    CUDA_TRY(sem::launch_mdot(n, c->d_mult, b, c->d_Z, c->ldv, k, c->d_kpart, c->d_ktick, gs->y,
                               nullptr, sms, s));
     if (c->hp.nranks > 1) SEM_TRY(allreduce(c, gs->y, k));
-    CUDA_TRY(sem::launch_maxpy(n, x, c->d_Z, n, k, gs->y, 1.0, nullptr, c->d_mult, c->d_kpart,
+    CUDA_TRY(sem::launch_maxpy(n, x, c->d_Z, c->ldv, k, gs->y, 1.0, nullptr, c->d_mult, c->d_kpart,
                                c->d_ktick, nullptr, nullptr, sms, s));
-    CUDA_TRY(sem::launch_maxpy(n, c->d_pbd, c->d_AZ, n, k, gs->y, -1.0, nullptr, c->d_mult,
+    CUDA_TRY(sem::launch_maxpy(n, c->d_pbd, c->d_AZ, c->ldv, k, gs->y, -1.0, nullptr, c->d_mult,
                                c->d_kpart, c->d_ktick, nullptr, nullptr, sms, s));
     c->launches += 3;
   }
@@ -1556,6 +1623,16 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     cudaStreamSynchronize(c->stream);
     if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
     c->precond = value;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_FDM_TC) {
+    cudaStreamSynchronize(c->stream);
+    c->fdm_tc = value != 0;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_COARSE_GRAPH) {
+    cudaStreamSynchronize(c->stream);
+    c->coarse_graph = value != 0;
     return SEM_OK;
   }
   if (option == SEM_OPT_COARSE_ITERS) {

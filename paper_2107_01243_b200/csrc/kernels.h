@@ -175,8 +175,8 @@ cudaError_t launch_fdm_setup(int n, int nloc, int64_t e_lo, int ex, int ey, int 
                              double* lam, cudaStream_t s);
 cudaError_t launch_fdm(int n, int nloc, const double* r, const uint8_t* mult, const double* S,
                        const double* lam, const double* xi, double* y, double* b0,
-                       const int* gate, int num_sms, cudaStream_t s);
-cudaError_t launch_schwarz_combine(int n, int64_t nslots, const double* y, const double* x0,
+                       const int* gate, int num_sms, bool tensor_cores, cudaStream_t s);
+cudaError_t launch_schwarz_combine(int n, int nloc, const double* y, const double* x0,
                                    const uint8_t* mult, const double* xi, double* z,
                                    const double* r, const double* w, double* partial,
                                    unsigned* ticket, double* dots, const int* gate, int num_sms,
@@ -186,6 +186,7 @@ cudaError_t launch_xpay(int64_t n, double* p, const double* z, const PcgState* s
                         cudaStream_t s);
 cudaError_t launch_gate_state(PcgState* st, const int* gate, cudaStream_t s);
 cudaError_t launch_rel_tol(PcgState* st, double rtol, cudaStream_t s);
+cudaError_t launch_copy_gate(int* dst, const int* gate, cudaStream_t s);
 
 // interconnect probes for the performance model: one-thread ping-pong
 // with `peer` (round-trip ns per sample), and one-sided peer writes (bandwidth)

@@ -11,6 +11,7 @@
 // Arnoldi orthogonalisation is classical Gram-Schmidt applied twice (CGS2):
 // two fused passes instead of the oracle's j+1 sequential MGS updates; equal
 // in exact arithmetic, and as stable as MGS with the second pass.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -60,9 +61,19 @@ __device__ __forceinline__ void reduce_cols(const double* acc, int K, double* pa
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// All vector kernels work on point PAIRS (16-byte loads and stores; ldv is
+// even, see api.cu) and unroll the grid-stride loop UN times with every load
+// of the unrolled body issued first: with one double per thread and
+// iteration, a small K left only K+2 loads in flight per thread and the
+// kernels ran at 1.1-2.4 TB/s (ncu, C3).  An odd n has its last point done by
+// block 0 / thread 0.
+__device__ __forceinline__ double2 ld2cs(const double* p, int64_t q) {
+  return __ldcs(reinterpret_cast<const double2*>(p) + q);
+}
+
 // out[i] = <a, V_i>_c, i < K (V_i = V + i*ldv); skipped when *done
-template <int KMAX>
-__global__ void __launch_bounds__(kKT) mdot_kernel(int64_t n, const uint8_t* __restrict__ mult,
+template <int KMAX, int UN>
+__global__ void __launch_bounds__(kKT, 2) mdot_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                                    const double* __restrict__ a,
                                                    const double* __restrict__ V, int64_t ldv, int K,
                                                    double* part, unsigned* ticket, double* out,
@@ -72,19 +83,44 @@ __global__ void __launch_bounds__(kKT) mdot_kernel(int64_t n, const uint8_t* __r
   double acc[KMAX];
 #pragma unroll
   for (int i = 0; i < KMAX; i++) acc[i] = 0.0;
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
-       l += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t np = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q0 < np; q0 += UN * stride) {
+    double2 av[UN], vv[UN][KMAX];
+    uchar2 mv[UN];
+#pragma unroll
+    for (int u = 0; u < UN; u++) {
+      const int64_t q = q0 + u * stride;
+      if (q < np) {
+        av[u] = ld2cs(a, q);
+        mv[u] = reinterpret_cast<const uchar2*>(mult)[q];
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if (i < K) vv[u][i] = ld2cs(V + i * ldv, q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UN; u++) {
+      if (q0 + u * stride < np) {
+        const double ca0 = c_of_k(mv[u].x) * av[u].x, ca1 = c_of_k(mv[u].y) * av[u].y;
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if (i < K) acc[i] = fma(ca1, vv[u][i].y, fma(ca0, vv[u][i].x, acc[i]));
+      }
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
     const double ca = c_of_k(mult[l]) * a[l];
 #pragma unroll
     for (int i = 0; i < KMAX; i++)
-      if (i < K) acc[i] = fma(ca, __ldcs(&V[i * ldv + l]), acc[i]);
+      if (i < K) acc[i] = fma(ca, V[i * ldv + l], acc[i]);
   }
   reduce_cols<KMAX>(acc, K, part, ticket, out, s_w);
 }
 
 // y += alpha * (dinv ? dinv : 1) * sum_{i<K} coef[i] V_i ; NORM: out_norm = <y, y>_c
-template <int KMAX, bool NORM>
-__global__ void __launch_bounds__(kKT) maxpy_kernel(int64_t n, double* __restrict__ y,
+template <int KMAX, bool NORM, int UN>
+__global__ void __launch_bounds__(kKT, 2) maxpy_kernel(int64_t n, double* __restrict__ y,
                                                     const double* __restrict__ V, int64_t ldv, int K,
                                                     const double* __restrict__ coef, double alpha,
                                                     const double* __restrict__ dinv,
@@ -97,13 +133,50 @@ __global__ void __launch_bounds__(kKT) maxpy_kernel(int64_t n, double* __restric
   if (threadIdx.x < K) s_c[threadIdx.x] = alpha * coef[threadIdx.x];
   __syncthreads();
   double nrm[1] = {0.0};
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
-       l += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
+  const int64_t np = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+  double2* y2 = reinterpret_cast<double2*>(y);
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q0 < np; q0 += UN * stride) {
+    double2 yv[UN], dv[UN], vv[UN][KMAX];
+    uchar2 mv[UN];
 #pragma unroll
-    for (int i = 0; i < KMAX; i++)
-      if (i < K) s = fma(s_c[i], __ldcs(&V[i * ldv + l]), s);
-    const double v = y[l] + (dinv ? dinv[l] * s : s);
+    for (int u = 0; u < UN; u++) {
+      const int64_t q = q0 + u * stride;
+      if (q < np) {
+        yv[u] = y2[q];
+        if (dinv) dv[u] = ld2cs(dinv, q);
+        if (NORM) mv[u] = reinterpret_cast<const uchar2*>(mult)[q];
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if (i < K) vv[u][i] = ld2cs(V + i * ldv, q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UN; u++) {
+      const int64_t q = q0 + u * stride;
+      if (q < np) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if (i < K) {
+            s0 = fma(s_c[i], vv[u][i].x, s0);
+            s1 = fma(s_c[i], vv[u][i].y, s1);
+          }
+        double2 v;
+        v.x = yv[u].x + (dinv ? dv[u].x * s0 : s0);
+        v.y = yv[u].y + (dinv ? dv[u].y * s1 : s1);
+        y2[q] = v;
+        if (NORM) {
+          nrm[0] = fma(c_of_k(mv[u].x) * v.x, v.x, nrm[0]);
+          nrm[0] = fma(c_of_k(mv[u].y) * v.y, v.y, nrm[0]);
+        }
+      }
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    double sacc = 0.0;
+    for (int i = 0; i < K; i++) sacc = fma(s_c[i], V[i * ldv + l], sacc);
+    const double v = y[l] + (dinv ? dinv[l] * sacc : sacc);
     y[l] = v;
     if (NORM) nrm[0] = fma(c_of_k(mult[l]) * v, v, nrm[0]);
   }
@@ -119,8 +192,23 @@ __global__ void __launch_bounds__(kKT) resid_kernel(int64_t n, const double* __r
   __shared__ double s_w[kKT / 32];
   if (done && *done) return;
   double acc[1] = {0.0};
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
-       l += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t np = n >> 1;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < np;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 wv = ld2cs(w, q);
+    double2 rv = wv;
+    if (b) {
+      const double2 bv = ld2cs(b, q);
+      rv.x = bv.x - wv.x;
+      rv.y = bv.y - wv.y;
+    }
+    const uchar2 mv = reinterpret_cast<const uchar2*>(mult)[q];
+    reinterpret_cast<double2*>(v)[q] = rv;
+    acc[0] = fma(c_of_k(mv.x) * rv.x, rv.x, acc[0]);
+    acc[0] = fma(c_of_k(mv.y) * rv.y, rv.y, acc[0]);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
     const double r = b ? b[l] - w[l] : w[l];
     v[l] = r;
     acc[0] = fma(c_of_k(mult[l]) * r, r, acc[0]);
@@ -128,15 +216,26 @@ __global__ void __launch_bounds__(kKT) resid_kernel(int64_t n, const double* __r
   reduce_cols<1>(acc, 1, part, ticket, out, s_w);
 }
 
-// v = w / norm, t = dinv v (the next Arnoldi direction, preconditioned)
-__global__ void __launch_bounds__(kKT) vnorm_kernel(int64_t n, const double* __restrict__ w,
-                                                    double* __restrict__ v, double* __restrict__ t,
+// v = w / norm, t = dinv v (the next Arnoldi direction, preconditioned); v may be w
+__global__ void __launch_bounds__(kKT) vnorm_kernel(int64_t n, const double* w, double* v,
+                                                    double* __restrict__ t,
                                                     const double* __restrict__ dinv,
                                                     const GmresState* gs, const int* done) {
   if (done && *done) return;
   const double s = gs->inv_norm;
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
-       l += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t np = n >> 1;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < np;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 wv = reinterpret_cast<const double2*>(w)[q];
+    const double2 x = make_double2(wv.x * s, wv.y * s);
+    reinterpret_cast<double2*>(v)[q] = x;
+    if (t) {
+      const double2 dv = ld2cs(dinv, q);
+      reinterpret_cast<double2*>(t)[q] = make_double2(dv.x * x.x, dv.y * x.y);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
     const double x = w[l] * s;
     v[l] = x;
     if (t) t[l] = dinv[l] * x;
@@ -240,11 +339,21 @@ static int kgrid(int64_t n, int num_sms) {
 cudaError_t launch_mdot(int64_t n, const uint8_t* mult, const double* a, const double* V,
                         int64_t ldv, int K, double* part, unsigned* ticket, double* out,
                         const int* done, int num_sms, cudaStream_t s) {
-  const int g = kgrid(n, num_sms);
-  if (K <= 8)
-    dev::mdot_kernel<8><<<g, dev::kKT, 0, s>>>(n, mult, a, V, ldv, K, part, ticket, out, done);
-  else
-    dev::mdot_kernel<32><<<g, dev::kKT, 0, s>>>(n, mult, a, V, ldv, K, part, ticket, out, done);
+  if (K > 1 && (ldv & 1)) return cudaErrorInvalidValue;   // pair accesses need an even ldv
+  const int g = kgrid(n / 2 + 1, num_sms);
+  for (int k0 = 0; k0 < K; k0 += 16) {   // > 16 vectors: slices of 16 (a is re-read)
+    const int kk = std::min(16, K - k0);
+    const double* Vk = V + k0 * ldv;
+    if (kk <= 2)
+      dev::mdot_kernel<2, 4><<<g, dev::kKT, 0, s>>>(n, mult, a, Vk, ldv, kk, part, ticket, out + k0,
+                                                    done);
+    else if (kk <= 8)
+      dev::mdot_kernel<8, 2><<<g, dev::kKT, 0, s>>>(n, mult, a, Vk, ldv, kk, part, ticket, out + k0,
+                                                    done);
+    else
+      dev::mdot_kernel<16, 1><<<g, dev::kKT, 0, s>>>(n, mult, a, Vk, ldv, kk, part, ticket,
+                                                     out + k0, done);
+  }
   return cudaGetLastError();
 }
 
@@ -252,22 +361,25 @@ cudaError_t launch_maxpy(int64_t n, double* y, const double* V, int64_t ldv, int
                          const double* coef, double alpha, const double* dinv, const uint8_t* mult,
                          double* part, unsigned* ticket, double* out_norm, const int* done,
                          int num_sms, cudaStream_t s) {
-  const int g = kgrid(n, num_sms);
-  const bool nrm = out_norm != nullptr;
-  if (K <= 8) {
-    if (nrm)
-      dev::maxpy_kernel<8, true><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv, mult,
-                                                        part, ticket, out_norm, done);
-    else
-      dev::maxpy_kernel<8, false><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv, mult,
-                                                         part, ticket, out_norm, done);
-  } else {
-    if (nrm)
-      dev::maxpy_kernel<32, true><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv, mult,
-                                                         part, ticket, out_norm, done);
-    else
-      dev::maxpy_kernel<32, false><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, alpha, dinv,
-                                                          mult, part, ticket, out_norm, done);
+  if (K > 1 && (ldv & 1)) return cudaErrorInvalidValue;
+  const int g = kgrid(n / 2 + 1, num_sms);
+  for (int k0 = 0; k0 < K; k0 += 16) {   // > 16 vectors: slices of 16 (y is re-read)
+    const int kk = std::min(16, K - k0);
+    const double* Vk = V + k0 * ldv;
+    const double* ck = coef + k0;
+    const bool nrm = out_norm != nullptr && k0 + 16 >= K;   // norm of the final y
+    double* on = nrm ? out_norm : nullptr;
+#define MAXPY(KM, UN)                                                                        \
+  (nrm ? (dev::maxpy_kernel<KM, true, UN><<<g, dev::kKT, 0, s>>>(                             \
+              n, y, Vk, ldv, kk, ck, alpha, dinv, mult, part, ticket, on, done),              \
+          0)                                                                                 \
+       : (dev::maxpy_kernel<KM, false, UN><<<g, dev::kKT, 0, s>>>(                            \
+              n, y, Vk, ldv, kk, ck, alpha, dinv, mult, part, ticket, on, done),              \
+          0))
+    if (kk <= 2) MAXPY(2, 4);
+    else if (kk <= 8) MAXPY(8, 2);
+    else MAXPY(16, 1);
+#undef MAXPY
   }
   return cudaGetLastError();
 }
@@ -275,14 +387,14 @@ cudaError_t launch_maxpy(int64_t n, double* y, const double* V, int64_t ldv, int
 cudaError_t launch_resid(int64_t n, const double* b, const double* w, double* v,
                          const uint8_t* mult, double* part, unsigned* ticket, double* out,
                          const int* done, int num_sms, cudaStream_t s) {
-  dev::resid_kernel<<<kgrid(n, num_sms), dev::kKT, 0, s>>>(n, b, w, v, mult, part, ticket, out,
+  dev::resid_kernel<<<kgrid(n / 2 + 1, num_sms), dev::kKT, 0, s>>>(n, b, w, v, mult, part, ticket, out,
                                                           done);
   return cudaGetLastError();
 }
 
 cudaError_t launch_vnorm(int64_t n, const double* w, double* v, double* t, const double* dinv,
                          const GmresState* gs, const int* done, int num_sms, cudaStream_t s) {
-  dev::vnorm_kernel<<<kgrid(n, num_sms), dev::kKT, 0, s>>>(n, w, v, t, dinv, gs, done);
+  dev::vnorm_kernel<<<kgrid(n / 2 + 1, num_sms), dev::kKT, 0, s>>>(n, w, v, t, dinv, gs, done);
   return cudaGetLastError();
 }
 

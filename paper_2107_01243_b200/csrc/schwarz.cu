@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "dev_common.cuh"
 #include "kernels.h"
@@ -271,45 +272,267 @@ __global__ void __launch_bounds__(kFT) fdm_kernel(int nloc, const double* __rest
   }
 }
 
+// ---- n = 8 (N = 7): the six contractions on the fp64 tensor cores.
+// One warp per element; every stage is 8 tiles x 2 k-steps of DMMA m8n8k4
+// (D[8x8] += A[8x4] B[4x8]).  The S factors are operands held in registers
+// (2 per stage per lane, read once from global/L2); the element's data moves
+// between two shared-memory buffers with the padded layout
+// a(i,j,k) = i + 12 j + 100 k, which makes every fragment load and store of
+// the six stages (strides 1/12/100 against the lane fields g = lane/4,
+// q = lane%4 and the accumulator columns 2q+e) hit each bank pair exactly
+// twice: conflict-free.  The same smem traffic as one CUDA-core stage moves
+// 8x the arithmetic, which is what takes the kernel from shared-memory bound
+// (15 % of HBM bandwidth) towards the HBM roofline.
+constexpr int kF8W = 4;          // warps (elements in flight) per CTA
+constexpr int kF8Buf = 800;      // doubles per padded buffer (max index 791)
+constexpr int kF8Smem = kF8W * 2 * kF8Buf + 2 * 256;   // + 1/m and (1/m)^1/2 tables
+
+__device__ __forceinline__ int pad8(int i, int j, int k) { return i + 12 * j + 100 * k; }
+
+// not volatile: the tiles of a stage are independent and the scheduler may
+// interleave their DMMAs (a volatile asm keeps program order)
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
+    int nloc, const double* __restrict__ r, const uint8_t* __restrict__ mult,
+    const double* __restrict__ Sg, const double* __restrict__ lamg, const double* __restrict__ xi,
+    double* __restrict__ y, double* __restrict__ b0, const int* gate) {
+  extern __shared__ double f8smem[];
+  if (gate && *gate) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double* U = f8smem + warp * 2 * kF8Buf;
+  double* T = U + kF8Buf;
+  double* cinv = f8smem + kF8W * 2 * kF8Buf;   // [256]: 1/m (as __drcp_rn), then its sqrt
+  double* csq = cinv + 256;
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) {
+    const double c = __drcp_rn((double)(m > 0 ? m : 1));
+    cinv[m] = c;
+    csq[m] = sqrt(c);
+  }
+  // this lane's points in the load phase: p = 2 (lane + 32 m) -> i = 2 lane % 8,
+  // j = lane / 4, k = m: the restriction weights J_ia J_jb J_kc factor per lane
+  const int i0 = (2 * lane) & 7, j0 = lane >> 2;
+  const double xa = __ldg(&xi[i0]), xb = __ldg(&xi[i0 + 1]), xj = __ldg(&xi[j0]);
+  const double ja[2] = {0.5 * (1.0 - xa), 0.5 * (1.0 + xa)};
+  const double jb[2] = {0.5 * (1.0 - xb), 0.5 * (1.0 + xb)};
+  const double jj[2] = {0.5 * (1.0 - xj), 0.5 * (1.0 + xj)};
+  __syncthreads();
+  for (int el = blockIdx.x * kF8W + warp; el < nloc; el += gridDim.x * kF8W) {
+    // every global load of the element first: r, mult, the S fragments, lambda
+    const double2* r2 = reinterpret_cast<const double2*>(r + (int64_t)el * 512);
+    const uchar2* m2 = reinterpret_cast<const uchar2*>(mult + (int64_t)el * 512);
+    double2 rv[8];
+    uchar2 mv[8];
+#pragma unroll
+    for (int m = 0; m < 8; m++) {
+      rv[m] = __ldcs(&r2[lane + 32 * m]);
+      mv[m] = m2[lane + 32 * m];
+    }
+    const double* Sx = Sg + (size_t)el * 192;
+    const double* Sy = Sx + 64;
+    const double* Sz = Sx + 128;
+    const double* lx = lamg + (size_t)el * 24;
+    const double AX0 = __ldcs(&Sx[q * 8 + g]), AX1 = __ldcs(&Sx[(4 + q) * 8 + g]);
+    const double BY0 = __ldcs(&Sy[q * 8 + g]), BY1 = __ldcs(&Sy[(4 + q) * 8 + g]);
+    const double BZ0 = __ldcs(&Sz[q * 8 + g]), BZ1 = __ldcs(&Sz[(4 + q) * 8 + g]);
+    const double CZ0 = __ldcs(&Sz[g * 8 + q]), CZ1 = __ldcs(&Sz[g * 8 + 4 + q]);
+    const double CY0 = __ldcs(&Sy[g * 8 + q]), CY1 = __ldcs(&Sy[g * 8 + 4 + q]);
+    const double CX0 = __ldcs(&Sx[g * 8 + q]), CX1 = __ldcs(&Sx[g * 8 + 4 + q]);
+    const double lxg = __ldcs(&lx[g]);
+    const double lz0 = __ldcs(&lx[16 + 2 * q]), lz1 = __ldcs(&lx[17 + 2 * q]);
+    // c^1/2 r into U (padded), restriction partials of (J^T)^3 (c r)
+    double acc[8];
+#pragma unroll
+    for (int v = 0; v < 8; v++) acc[v] = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; m++) {
+      U[pad8(i0, j0, m)] = csq[mv[m].x] * rv[m].x;
+      U[pad8(i0 + 1, j0, m)] = csq[mv[m].y] * rv[m].y;
+      if (b0) {
+        const double xk = __ldg(&xi[m]);
+        const double jk[2] = {0.5 * (1.0 - xk), 0.5 * (1.0 + xk)};
+        const double cr0 = cinv[mv[m].x] * rv[m].x, cr1 = cinv[mv[m].y] * rv[m].y;
+#pragma unroll
+        for (int v = 0; v < 8; v++) {
+          const double wjk = jj[(v >> 1) & 1] * jk[v >> 2];
+          acc[v] = fma(ja[v & 1] * wjk, cr0, acc[v]);
+          acc[v] = fma(jb[v & 1] * wjk, cr1, acc[v]);
+        }
+      }
+    }
+    if (b0) {
+#pragma unroll
+      for (int v = 0; v < 8; v++) acc[v] = warp_sum(acc[v]);
+      if (lane < 8) {
+        double o = acc[0];
+#pragma unroll
+        for (int v = 1; v < 8; v++) o = lane == v ? acc[v] : o;
+        b0[(int64_t)el * 8 + lane] = o;
+      }
+    }
+    __syncwarp();
+    // 1. T[a][j][k] = sum_i Sx[i][a] U[i][j][k]
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma884(d0, d1, AX0, U[pad8(q, g, t)]);
+      dmma884(d0, d1, AX1, U[pad8(4 + q, g, t)]);
+      T[pad8(g, 2 * q, t)] = d0;
+      T[pad8(g, 2 * q + 1, t)] = d1;
+    }
+    __syncwarp();
+    // 2. U[a][b][k] = sum_j T[a][j][k] Sy[j][b]
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma884(d0, d1, T[pad8(g, q, t)], BY0);
+      dmma884(d0, d1, T[pad8(g, 4 + q, t)], BY1);
+      U[pad8(g, 2 * q, t)] = d0;
+      U[pad8(g, 2 * q + 1, t)] = d1;
+    }
+    __syncwarp();
+    // 3. T[a][b][c] = sum_k U[a][b][k] Sz[k][c] / (lx_a + ly_b + lz_c)
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma884(d0, d1, U[pad8(g, t, q)], BZ0);
+      dmma884(d0, d1, U[pad8(g, t, 4 + q)], BZ1);
+      const double lyt = __ldg(&lx[8 + t]);
+      T[pad8(g, t, 2 * q)] = d0 / (lxg + lyt + lz0);
+      T[pad8(g, t, 2 * q + 1)] = d1 / (lxg + lyt + lz1);
+    }
+    __syncwarp();
+    // 4. U[a][b][k] = sum_c T[a][b][c] Sz[k][c]
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma884(d0, d1, T[pad8(g, t, q)], CZ0);
+      dmma884(d0, d1, T[pad8(g, t, 4 + q)], CZ1);
+      U[pad8(g, t, 2 * q)] = d0;
+      U[pad8(g, t, 2 * q + 1)] = d1;
+    }
+    __syncwarp();
+    // 5. T[a][j][k] = sum_b U[a][b][k] Sy[j][b]
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma884(d0, d1, U[pad8(g, q, t)], CY0);
+      dmma884(d0, d1, U[pad8(g, 4 + q, t)], CY1);
+      T[pad8(g, 2 * q, t)] = d0;
+      T[pad8(g, 2 * q + 1, t)] = d1;
+    }
+    __syncwarp();
+    // 6. U[i][j][k] = sum_a Sx[i][a] T[a][j][k]
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma884(d0, d1, CX0, T[pad8(q, g, t)]);
+      dmma884(d0, d1, CX1, T[pad8(4 + q, g, t)]);
+      U[pad8(g, 2 * q, t)] = d0;
+      U[pad8(g, 2 * q + 1, t)] = d1;
+    }
+    __syncwarp();
+    double2* y2 = reinterpret_cast<double2*>(y + (int64_t)el * 512);
+#pragma unroll
+    for (int m = 0; m < 8; m++)
+      __stcs(&y2[lane + 32 * m], make_double2(U[pad8(i0, j0, m)], U[pad8(i0 + 1, j0, m)]));
+    __syncwarp();   // U is refilled by the next element
+  }
+}
+
 // z = c^1/2 y + (J (x) J (x) J) x0_e (either part may be null).  DOTS: the
 // flexible-CG dots <z, r>_c and <z, w>_c into dots[0..1] (deterministic grid
-// reduction).  Skipped when *gate.
+// reduction).  Flat over point pairs (16-byte accesses); a shared table maps
+// the in-element index p to its (i, j, k) and holds the J factors, so a point
+// costs no integer division beyond one per pair.  Skipped when *gate.
 template <bool DOTS>
 __global__ void __launch_bounds__(kFT) schwarz_combine_kernel(
-    int n, int64_t nslots, const double* __restrict__ y, const double* __restrict__ x0,
+    int n, int nloc, const double* __restrict__ y, const double* __restrict__ x0,
     const uint8_t* __restrict__ mult, const double* __restrict__ xi, double* __restrict__ z,
     const double* __restrict__ r, const double* __restrict__ w, double* partial,
     unsigned* ticket, double* dots, const int* gate) {
-  __shared__ double J[12][2];
   __shared__ double scratch[32];
   __shared__ int flag;
+  __shared__ uint32_t ijk[1728];
+  __shared__ double Js[12][2];
   if (gate && *gate) return;
+  const int n3 = n * n * n;
+  for (int p = threadIdx.x; p < n3; p += blockDim.x)
+    ijk[p] = (uint32_t)(p % n) | ((uint32_t)((p / n) % n) << 8) | ((uint32_t)(p / (n * n)) << 16);
   if (threadIdx.x < n) {
-    J[threadIdx.x][0] = 0.5 * (1.0 - xi[threadIdx.x]);
-    J[threadIdx.x][1] = 0.5 * (1.0 + xi[threadIdx.x]);
+    Js[threadIdx.x][0] = 0.5 * (1.0 - xi[threadIdx.x]);
+    Js[threadIdx.x][1] = 0.5 * (1.0 + xi[threadIdx.x]);
   }
   __syncthreads();
-  const int n2 = n * n, n3 = n2 * n;
+  const int64_t nslots = (int64_t)nloc * n3;
+  const int64_t npair = nslots >> 1;
   double zr = 0.0, zw = 0.0;
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nslots;
-       l += (int64_t)gridDim.x * blockDim.x) {
-    const double c = __drcp_rn((double)mult[l]);
-    double v = y ? sqrt(c) * __ldcs(&y[l]) : 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npair;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = 2 * q;
+    int64_t el = l / n3;
+    int p = (int)(l - el * n3);
+    const uchar2 mv = *reinterpret_cast<const uchar2*>(mult + l);
+    const double c0 = __drcp_rn((double)mv.x), c1 = __drcp_rn((double)mv.y);
+    double v0 = 0.0, v1 = 0.0;
+    if (y) {
+      const double2 yv = __ldcs(reinterpret_cast<const double2*>(y) + q);
+      v0 = sqrt(c0) * yv.x;
+      v1 = sqrt(c1) * yv.y;
+    }
     if (x0) {
-      const int64_t el = l / n3;
-      const int p = (int)(l - el * n3);
-      const int i = p % n, j = (p / n) % n, k = p / n2;
-      const double* xe = x0 + el * 8;
-      double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; q++) s = fma(J[i][q & 1] * J[j][(q >> 1) & 1] * J[k][q >> 2], xe[q], s);
+      for (int h = 0; h < 2; h++) {
+        if (h == 1 && ++p == n3) {   // the pair straddles two elements (odd n)
+          p = 0;
+          el++;
+        }
+        const uint32_t t = ijk[p];
+        const int i = t & 255, j = (t >> 8) & 255, k = t >> 16;
+        const double2* xe = reinterpret_cast<const double2*>(x0 + el * 8);
+        const double2 a01 = __ldg(xe), a23 = __ldg(xe + 1), a45 = __ldg(xe + 2), a67 = __ldg(xe + 3);
+        const double xv[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; v++)
+          s = fma(Js[i][v & 1] * Js[j][(v >> 1) & 1] * Js[k][v >> 2], xv[v], s);
+        if (h == 0) v0 += s;
+        else v1 += s;
+      }
+    }
+    reinterpret_cast<double2*>(z)[q] = make_double2(v0, v1);
+    if (DOTS) {
+      const double2 rv = __ldcs(reinterpret_cast<const double2*>(r) + q);
+      const double2 wv = __ldcs(reinterpret_cast<const double2*>(w) + q);
+      zr = fma(c0 * v0, rv.x, zr);
+      zr = fma(c1 * v1, rv.y, zr);
+      zw = fma(c0 * v0, wv.x, zw);
+      zw = fma(c1 * v1, wv.y, zw);
+    }
+  }
+  if ((nslots & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // odd tail point
+    const int64_t l = nslots - 1;
+    const int64_t el = l / n3;
+    const int p = (int)(l - el * n3);
+    const double c = __drcp_rn((double)mult[l]);
+    double v = y ? sqrt(c) * y[l] : 0.0;
+    if (x0) {
+      const uint32_t t = ijk[p];
+      const int i = t & 255, j = (t >> 8) & 255, k = t >> 16;
+      double s = 0.0;
+      for (int vv = 0; vv < 8; vv++)
+        s = fma(Js[i][vv & 1] * Js[j][(vv >> 1) & 1] * Js[k][vv >> 2], x0[el * 8 + vv], s);
       v += s;
     }
     z[l] = v;
     if (DOTS) {
-      const double cv = c * v;
-      zr = fma(cv, r[l], zr);
-      zw = fma(cv, w[l], zw);
+      zr = fma(c * v, r[l], zr);
+      zw = fma(c * v, w[l], zw);
     }
   }
   if (DOTS) {
@@ -390,7 +613,15 @@ __global__ void rel_tol_kernel(PcgState* st, double rtol) {
   st->done = (g <= st->tol) ? 1 : (st->maxit == 0 ? 4 : 0);
 }
 
+// the coarse-graph gate slot: *dst = gate ? *gate : 0
+__global__ void copy_gate_kernel(int* dst, const int* gate) { *dst = gate ? *gate : 0; }
+
 }  // namespace dev
+
+cudaError_t launch_copy_gate(int* dst, const int* gate, cudaStream_t s) {
+  dev::copy_gate_kernel<<<1, 1, 0, s>>>(dst, gate);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fdm_setup(int n, int nloc, int64_t e_lo, int ex, int ey, int ez,
                              const double* box, int deform, double amp, const int* per,
@@ -406,8 +637,19 @@ cudaError_t launch_fdm_setup(int n, int nloc, int64_t e_lo, int ex, int ey, int 
 
 cudaError_t launch_fdm(int n, int nloc, const double* r, const uint8_t* mult, const double* S,
                        const double* lam, const double* xi, double* y, double* b0,
-                       const int* gate, int num_sms, cudaStream_t s) {
+                       const int* gate, int num_sms, bool tensor_cores, cudaStream_t s) {
   if (nloc == 0) return cudaSuccess;
+  if (n == 8 && y && tensor_cores) {   // fp64 tensor-core path (N = 7)
+    const size_t smem = (size_t)dev::kF8Smem * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dev::fdm8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int grid8 = std::min((nloc + dev::kF8W - 1) / dev::kF8W, num_sms * 4);
+    dev::fdm8_kernel<<<grid8, dev::kF8W * 32, smem, s>>>(nloc, r, mult, S, lam, xi, y, b0, gate);
+    return cudaGetLastError();
+  }
   const int grid = std::min(nloc, num_sms * 8);
 #define FDM_CASE(NN)                                                                        \
   case NN:                                                                                  \
@@ -422,19 +664,20 @@ cudaError_t launch_fdm(int n, int nloc, const double* r, const uint8_t* mult, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_schwarz_combine(int n, int64_t nslots, const double* y, const double* x0,
+cudaError_t launch_schwarz_combine(int n, int nloc, const double* y, const double* x0,
                                    const uint8_t* mult, const double* xi, double* z,
                                    const double* r, const double* w, double* partial,
                                    unsigned* ticket, double* dots, const int* gate, int num_sms,
                                    cudaStream_t s) {
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nslots + dev::kFT - 1) / dev::kFT,
-                                                                (int64_t)num_sms * 8));
+  const int64_t npair = ((int64_t)nloc * n * n * n) / 2;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((npair + dev::kFT - 1) / dev::kFT, (int64_t)num_sms * 8));
   if (dots)
-    dev::schwarz_combine_kernel<true><<<grid, dev::kFT, 0, s>>>(
-        n, nslots, y, x0, mult, xi, z, r, w, partial, ticket, dots, gate);
+    dev::schwarz_combine_kernel<true><<<grid, dev::kFT, 0, s>>>(n, nloc, y, x0, mult, xi, z, r, w,
+                                                                partial, ticket, dots, gate);
   else
-    dev::schwarz_combine_kernel<false><<<grid, dev::kFT, 0, s>>>(
-        n, nslots, y, x0, mult, xi, z, r, w, partial, ticket, dots, gate);
+    dev::schwarz_combine_kernel<false><<<grid, dev::kFT, 0, s>>>(n, nloc, y, x0, mult, xi, z, r, w,
+                                                                 partial, ticket, dots, gate);
   return cudaGetLastError();
 }
 

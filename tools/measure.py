@@ -149,8 +149,9 @@ def schwarz(cfgs=("C3", "C4")):
             c.schwarz_apply(b, z, 3)
             res = {"what": f"{cfg}_schwarz", "n_local": n}
             for which, name in ((1, "local"), (2, "coarse"), (3, "both")):
+                ms = timed(lambda: c.schwarz_apply(b, z, which), st, 20)   # graph on
                 c.timing(True)
-                ms = timed(lambda: c.schwarz_apply(b, z, which), st, 20)
+                timed(lambda: c.schwarz_apply(b, z, which), st, 5)
                 t_fdm, k_fdm = c.timing_read(7)
                 t_cmb, k_cmb = c.timing_read(8)
                 c.timing(False)
@@ -163,12 +164,23 @@ def schwarz(cfgs=("C3", "C4")):
                     res["fdm_GBps"] = round(bpp * n / (fdm_ms * 1e-3) / 1e9, 0)
                     res["fdm_frac_copy"] = round(bpp * n / (fdm_ms * 1e-3) / 1e9 / peak_copy(), 3)
                     res["combine_kernel_ms"] = round(t_cmb / max(k_cmb, 1), 4)
+                    if n1 == 8:   # the CUDA-core kernel for comparison
+                        c.set_fdm_tc(False)
+                        c.timing(True)
+                        timed(lambda: c.schwarz_apply(b, z, 1), st, 5)
+                        t2, k2 = c.timing_read(7)
+                        c.timing(False)
+                        c.set_fdm_tc(True)
+                        res["fdm_cuda_core_kernel_ms"] = round(t2 / max(k2, 1), 4)
             for pc in ("jacobi", "schwarz"):
                 c.set_precond(pc)
                 for solver in ("pcg", "gmres"):
                     x = c.zeros()
-                    fn = (lambda: c.pcg_solve(b, x, 1e-10, 3000)) if solver == "pcg" else \
-                        (lambda: c.gmres_solve(b, x, 1e-10, 3000, 30))
+                    # Jacobi GMRES needs thousands of iterations on C3/C4: capped at
+                    # 300 (ms_per_iter is the comparable number there)
+                    mi = 300 if (solver == "gmres" and pc == "jacobi") else 3000
+                    fn = (lambda: c.pcg_solve(b, x, 1e-10, mi)) if solver == "pcg" else \
+                        (lambda: c.gmres_solve(b, x, 1e-10, mi, 30))
                     fn()
                     torch.cuda.synchronize()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -303,12 +315,65 @@ def strong():
     dist.destroy_process_group()
 
 
+def schwarz_strong(cfgs=("C3", "C4")):
+    """NEXT-1 at P ranks: time-to-solution (tol 1e-10, TGV pressure RHS) of
+    Jacobi-PCG, Schwarz flexible PCG and Schwarz flexible GMRES(30); the
+    coarse N=1 solve runs distributed over the same ranks (its ten CG steps
+    each carry a gather-scatter exchange and two allreduces)."""
+    import torch.distributed as dist
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = [sem.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = sem.nccl_comm_init(uid[0], rank, P)
+    st = torch.cuda.current_stream()
+
+    def mx(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for cfg in cfgs:
+        spec, N = CONFIGS[cfg]
+        with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm, stream=st.cuda_stream) as c:
+            X, Y, Z = c.coords()
+            b = c.zeros()
+            c.rhs(f_tgv(X, Y, Z, xp=torch), b)
+            del X, Y, Z
+            res = {"what": f"{cfg}_schwarz_strong", "P": P}
+            for pc, solver in (("jacobi", "pcg"), ("schwarz", "pcg"), ("schwarz", "gmres")):
+                c.set_precond(pc)
+                x = c.zeros()
+                fn = (lambda: c.pcg_solve(b, x, 1e-10, 3000)) if solver == "pcg" else \
+                    (lambda: c.gmres_solve(b, x, 1e-10, 3000, 30))
+                fn()
+                torch.cuda.synchronize()
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                r = fn()
+                e1.record(st)
+                torch.cuda.synchronize()
+                ms = mx(e0.elapsed_time(e1))
+                res[f"{solver}_{pc}"] = {"iters": r["iters"], "status": r["status"], "ms": round(ms, 3)}
+            c.set_precond("jacobi")
+            if rank == 0:
+                out(res)
+        torch.cuda.empty_cache()
+    sem.nccl_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     mode = sys.argv[1] if len(sys.argv) > 1 else "single"
     if mode == "strong":
         strong()
     elif mode == "sweep":
         sweep([int(v) for v in sys.argv[2].split(",")])
+    elif mode == "schwarz_strong":
+        schwarz_strong(tuple(sys.argv[2].split(",")) if len(sys.argv) > 2 else ("C3", "C4"))
     elif mode == "schwarz":
         schwarz(tuple(sys.argv[2].split(",")) if len(sys.argv) > 2 else ("C3", "C4"))
     elif mode == "helm":
