@@ -363,8 +363,10 @@ def main():
                 "workload": (f"{args.config}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU "
                              f"(box stacked x{P} along z), N={N}, periodic, all 6 G stored"),
                 "N": N, "elements": spec.E, "n_p": n_p_total, "n_glob": ctx.n_glob,
-                "step": "one Jacobi-PCG iteration (Ax+mask+<p,Ap>, gs [+ NVLink exchange], "
-                        "r update+dots, x/p update)",
+                "step": ("one Jacobi-PCG iteration (Ax+mask+<p,Ap>, gs [+ NVLink exchange], "
+                         "r update+dots, x/p update)") if P > 1 else
+                        ("one Jacobi-PCG iteration (Ax+mask+<p,Ap>; gs fused with the r update "
+                         "and dots; x/p update)"),
                 "l2": "no flush: per-iteration working set ~370 MB/GPU > 126 MB L2",
                 "parallelism": (f"element z-slabs x{P}, NVLink peer-memory gs exchange + "
                                 "allreduce (CUDA IPC)") if P > 1 else "single GPU",
@@ -387,7 +389,8 @@ def main():
                 "peak_source": peak_src,
                 "step_share": k_ms / max(k_ms + u_ms + p_ms + g_ms, 1e-9),
                 "other_kernels_ms_per_step": {"gs": g_ms / n_apply,
-                                              "cg_update": u_ms / max(u_cnt, 1),
+                                              ("gs_update" if g_cnt == 0 else "cg_update"):
+                                                  u_ms / max(u_cnt, 1),
                                               "cg_p": p_ms / max(p_cnt, 1)},
             },
             "cpu_baseline": cpu,

@@ -246,6 +246,12 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
 /* 1 (default) = at N = 7 the Schwarz local solves run their six 8x8
    contractions on the fp64 tensor cores (DMMA m8n8k4); 0 = CUDA-core kernel */
 #define SEM_OPT_FDM_TC 9
+/* 1 = on one rank, when the gather-scatter runs the flat schedule (w
+   L2-resident), each PCG iteration fuses the gather-scatter of A p with the
+   r update and the two dots (one pass; dots per unique point); 0 (default) =
+   separate gather-scatter and update kernels (measured faster on C2: 123 vs
+   133 us per iteration).  Same iterates up to summation order. */
+#define SEM_OPT_GS_UPDATE 10
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

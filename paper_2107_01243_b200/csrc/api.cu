@@ -114,6 +114,8 @@ struct sem_ctx {
   // single rank: the coarse solve replayed as one CUDA graph (its launches are
   // argument-stable: flat gs schedule, no peer epochs); gate copied to d_gate
   bool coarse_graph = true;
+  bool gs_update = false;  // SEM_OPT_GS_UPDATE: one rank, flat gs -> gs + CG update fused
+                           // (measured slower on C2: 133 vs 123 us per iteration)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
   cudaGraphExec_t g0exec = nullptr;
   int g0_iters = -1;
@@ -801,6 +803,20 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
 static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const PcgCtl& k) {
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
+  if (c->gs_update && c->hp.nranks == 1 && !fused(c) && sem::gs_flat(c->dp, c->gs_mode)) {
+    // Ax (+ sigma partials), then gather-scatter and update fused in one pass
+    SEM_TRY(run_ax(c, c->d_p, c->d_wv, sem::AX_PCG, 0, (int)c->hp.nloc, 0, 0, nullptr));
+    int tk = timer_begin(c, 1);
+    CUDA_TRY(sem::launch_gs_update(c->dp, dinv, c->d_r, c->d_wv, c->d_partial, st, k.rg_out,
+                                   c->d_partial_ax, c->d_nsig, s));
+    timer_end(c, tk);
+    tk = timer_begin(c, 2);
+    CUDA_TRY(sem::launch_cg_p(c->dp, dinv, c->d_r, c->d_p, x, st, c->d_hist, sem::PeerSync{},
+                              c->red_grid, s));
+    timer_end(c, tk);
+    c->launches += 2;
+    return SEM_OK;
+  }
   SEM_TRY(apply_op(c, c->d_p, c->d_wv, sem::AX_PCG));
   sem::PeerSync psu, psp;
   if (k.pp) {
@@ -1056,9 +1072,10 @@ static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, i
   const int64_t n = h.n_local;
   cudaStream_t s = c->stream;
   const int sms = c->num_sms;
-  if (!c->d_rw) SEM_TRY(dalloc(&c->d_rw, 2 * (size_t)n));
+  // r and w 16-byte aligned (the vector kernels move point pairs)
+  if (!c->d_rw) SEM_TRY(dalloc(&c->d_rw, 2 * (size_t)c->ldv));
   if (!c->d_z) SEM_TRY(dalloc(&c->d_z, (size_t)n));
-  double *r = c->d_rw, *w = c->d_rw + n, *z = c->d_z, *p = c->d_p;
+  double *r = c->d_rw, *w = c->d_rw + c->ldv, *z = c->d_z, *p = c->d_p;
   sem::PcgState* st = c->d_st;
   const int* done = &st->done;
   const bool dist = h.nranks > 1;
@@ -1480,9 +1497,9 @@ extern "C" int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_ho
                                   int32_t maxit, sem_pcg_result* res) {
   if (!c || !b_host || !x_host) { sem::set_error("sem_pcg_solve_host: NULL argument"); return SEM_EINVAL; }
   const size_t bytes = (size_t)c->hp.n_local * sizeof(double);
-  if (!c->d_tmp) SEM_TRY(dalloc(&c->d_tmp, 2 * (size_t)c->hp.n_local));
+  if (!c->d_tmp) SEM_TRY(dalloc(&c->d_tmp, 2 * (size_t)c->ldv));
   double* db = c->d_tmp;
-  double* dx = c->d_tmp + c->hp.n_local;
+  double* dx = c->d_tmp + c->ldv;   // 16-byte aligned
   CUDA_TRY(cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, c->stream));
   int st = pcg_run(c, db, dx, tol, maxit, res);
   if (st < 0) return st;
@@ -1623,6 +1640,11 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     cudaStreamSynchronize(c->stream);
     if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
     c->precond = value;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_GS_UPDATE) {
+    cudaStreamSynchronize(c->stream);
+    c->gs_update = value != 0;
     return SEM_OK;
   }
   if (option == SEM_OPT_FDM_TC) {

@@ -253,6 +253,12 @@ cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
                              int grid, cudaStream_t s);
+bool gs_flat(const DevPlan& P, int mode);   // the gs schedule `mode` resolves to the flat sweep
+// one rank, flat gs schedule: gather-scatter of w and the CG update in one pass
+// (sigma from the Ax kernel's partials; rho', gamma into out2)
+cudaError_t launch_gs_update(const DevPlan& P, const double* dinv, double* r, const double* w,
+                             double* partial, PcgState* st, double* out2, const double* sig_part,
+                             const int* sig_count, cudaStream_t s);
 // x += alpha p, then (unless the solve ended) p = dinv r + beta p
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,
                         PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s);

@@ -297,6 +297,35 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
       : "d"(a), "d"(b));
 }
 
+// One contraction stage: 8 output tiles, two k-steps each.  All operand loads
+// of a group of tiles are issued first, then the k-step-0 DMMAs of every tile,
+// then the k-step-1 DMMAs, then the stores: independent accumulation chains
+// interleave (the straightforward per-tile order serialised load -> DMMA ->
+// DMMA -> store eight times per stage).
+template <class L0, class L1, class MM, class ST>
+__device__ __forceinline__ void f8_stage(L0 l0, L1 l1, MM mm, ST st) {
+  constexpr int TG = 4;   // tiles per group
+#pragma unroll
+  for (int h = 0; h < 8; h += TG) {
+    double x0[TG], x1[TG], d0[TG], d1[TG];
+#pragma unroll
+    for (int u = 0; u < TG; u++) {
+      x0[u] = l0(h + u);
+      x1[u] = l1(h + u);
+    }
+#pragma unroll
+    for (int u = 0; u < TG; u++) {
+      d0[u] = 0.0;
+      d1[u] = 0.0;
+      mm(d0[u], d1[u], 0, x0[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < TG; u++) mm(d0[u], d1[u], 1, x1[u]);
+#pragma unroll
+    for (int u = 0; u < TG; u++) st(h + u, d0[u], d1[u]);
+  }
+}
+
 __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
     int nloc, const double* __restrict__ r, const uint8_t* __restrict__ mult,
     const double* __restrict__ Sg, const double* __restrict__ lamg, const double* __restrict__ xi,
@@ -376,66 +405,54 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
       }
     }
     __syncwarp();
-    // 1. T[a][j][k] = sum_i Sx[i][a] U[i][j][k]
-#pragma unroll
-    for (int t = 0; t < 8; t++) {
-      double d0 = 0.0, d1 = 0.0;
-      dmma884(d0, d1, AX0, U[pad8(q, g, t)]);
-      dmma884(d0, d1, AX1, U[pad8(4 + q, g, t)]);
-      T[pad8(g, 2 * q, t)] = d0;
-      T[pad8(g, 2 * q + 1, t)] = d1;
-    }
+    // 1. T[a][j][k] = sum_i Sx[i][a] U[i][j][k]   (S as the A operand)
+    f8_stage([&](int t) { return U[pad8(q, g, t)]; }, [&](int t) { return U[pad8(4 + q, g, t)]; },
+             [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, s ? AX1 : AX0, x); },
+             [&](int t, double d0, double d1) {
+               T[pad8(g, 2 * q, t)] = d0;
+               T[pad8(g, 2 * q + 1, t)] = d1;
+             });
     __syncwarp();
-    // 2. U[a][b][k] = sum_j T[a][j][k] Sy[j][b]
-#pragma unroll
-    for (int t = 0; t < 8; t++) {
-      double d0 = 0.0, d1 = 0.0;
-      dmma884(d0, d1, T[pad8(g, q, t)], BY0);
-      dmma884(d0, d1, T[pad8(g, 4 + q, t)], BY1);
-      U[pad8(g, 2 * q, t)] = d0;
-      U[pad8(g, 2 * q + 1, t)] = d1;
-    }
+    // 2. U[a][b][k] = sum_j T[a][j][k] Sy[j][b]   (S as the B operand)
+    f8_stage([&](int t) { return T[pad8(g, q, t)]; }, [&](int t) { return T[pad8(g, 4 + q, t)]; },
+             [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, x, s ? BY1 : BY0); },
+             [&](int t, double d0, double d1) {
+               U[pad8(g, 2 * q, t)] = d0;
+               U[pad8(g, 2 * q + 1, t)] = d1;
+             });
     __syncwarp();
     // 3. T[a][b][c] = sum_k U[a][b][k] Sz[k][c] / (lx_a + ly_b + lz_c)
-#pragma unroll
-    for (int t = 0; t < 8; t++) {
-      double d0 = 0.0, d1 = 0.0;
-      dmma884(d0, d1, U[pad8(g, t, q)], BZ0);
-      dmma884(d0, d1, U[pad8(g, t, 4 + q)], BZ1);
-      const double lyt = __ldg(&lx[8 + t]);
-      T[pad8(g, t, 2 * q)] = d0 / (lxg + lyt + lz0);
-      T[pad8(g, t, 2 * q + 1)] = d1 / (lxg + lyt + lz1);
-    }
+    f8_stage([&](int t) { return U[pad8(g, t, q)]; }, [&](int t) { return U[pad8(g, t, 4 + q)]; },
+             [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, x, s ? BZ1 : BZ0); },
+             [&](int t, double d0, double d1) {
+               const double lyt = __ldg(&lx[8 + t]);
+               T[pad8(g, t, 2 * q)] = d0 / (lxg + lyt + lz0);
+               T[pad8(g, t, 2 * q + 1)] = d1 / (lxg + lyt + lz1);
+             });
     __syncwarp();
     // 4. U[a][b][k] = sum_c T[a][b][c] Sz[k][c]
-#pragma unroll
-    for (int t = 0; t < 8; t++) {
-      double d0 = 0.0, d1 = 0.0;
-      dmma884(d0, d1, T[pad8(g, t, q)], CZ0);
-      dmma884(d0, d1, T[pad8(g, t, 4 + q)], CZ1);
-      U[pad8(g, t, 2 * q)] = d0;
-      U[pad8(g, t, 2 * q + 1)] = d1;
-    }
+    f8_stage([&](int t) { return T[pad8(g, t, q)]; }, [&](int t) { return T[pad8(g, t, 4 + q)]; },
+             [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, x, s ? CZ1 : CZ0); },
+             [&](int t, double d0, double d1) {
+               U[pad8(g, t, 2 * q)] = d0;
+               U[pad8(g, t, 2 * q + 1)] = d1;
+             });
     __syncwarp();
     // 5. T[a][j][k] = sum_b U[a][b][k] Sy[j][b]
-#pragma unroll
-    for (int t = 0; t < 8; t++) {
-      double d0 = 0.0, d1 = 0.0;
-      dmma884(d0, d1, U[pad8(g, q, t)], CY0);
-      dmma884(d0, d1, U[pad8(g, 4 + q, t)], CY1);
-      T[pad8(g, 2 * q, t)] = d0;
-      T[pad8(g, 2 * q + 1, t)] = d1;
-    }
+    f8_stage([&](int t) { return U[pad8(g, q, t)]; }, [&](int t) { return U[pad8(g, 4 + q, t)]; },
+             [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, x, s ? CY1 : CY0); },
+             [&](int t, double d0, double d1) {
+               T[pad8(g, 2 * q, t)] = d0;
+               T[pad8(g, 2 * q + 1, t)] = d1;
+             });
     __syncwarp();
     // 6. U[i][j][k] = sum_a Sx[i][a] T[a][j][k]
-#pragma unroll
-    for (int t = 0; t < 8; t++) {
-      double d0 = 0.0, d1 = 0.0;
-      dmma884(d0, d1, CX0, T[pad8(q, g, t)]);
-      dmma884(d0, d1, CX1, T[pad8(4 + q, g, t)]);
-      U[pad8(g, 2 * q, t)] = d0;
-      U[pad8(g, 2 * q + 1, t)] = d1;
-    }
+    f8_stage([&](int t) { return T[pad8(q, g, t)]; }, [&](int t) { return T[pad8(4 + q, g, t)]; },
+             [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, s ? CX1 : CX0, x); },
+             [&](int t, double d0, double d1) {
+               U[pad8(g, 2 * q, t)] = d0;
+               U[pad8(g, 2 * q + 1, t)] = d1;
+             });
     __syncwarp();
     double2* y2 = reinterpret_cast<double2*>(y + (int64_t)el * 512);
 #pragma unroll
@@ -497,10 +514,11 @@ __global__ void __launch_bounds__(kFT) schwarz_combine_kernel(
         const double2* xe = reinterpret_cast<const double2*>(x0 + el * 8);
         const double2 a01 = __ldg(xe), a23 = __ldg(xe + 1), a45 = __ldg(xe + 2), a67 = __ldg(xe + 3);
         const double xv[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+        const double ji[2] = {Js[i][0], Js[i][1]}, jj[2] = {Js[j][0], Js[j][1]};
+        const double jk[2] = {Js[k][0], Js[k][1]};
         double s = 0.0;
 #pragma unroll
-        for (int v = 0; v < 8; v++)
-          s = fma(Js[i][v & 1] * Js[j][(v >> 1) & 1] * Js[k][v >> 2], xv[v], s);
+        for (int v = 0; v < 8; v++) s = fma(ji[v & 1] * jj[(v >> 1) & 1] * jk[v >> 2], xv[v], s);
         if (h == 0) v0 += s;
         else v1 += s;
       }

@@ -392,7 +392,8 @@ def test_pdl_option_identical():
 # ---------------------------------------------------------------- NEXT-3: GMRES and projection
 @pytest.mark.parametrize("spec,N,restart", [(CONFIGS["C1"][0], 3, 30), (tgv_box(6, 6, 6, deform=1), 5, 30),
                                             (tgv_box(6, 6, 6, deform=1), 5, 7),
-                                            (unit_box(3, 2, 4, periodic=(1, 0, 0)), 6, 12)])
+                                            (unit_box(3, 2, 4, periodic=(1, 0, 0)), 6, 12),
+                                            (unit_box(3, 1, 3), 4, 30)])   # odd n_local
 def test_gmres_parity(spec, N, restart):
     o = O.Oracle(spec, N)
     X, Y, Z = o.get("X"), o.get("Y"), o.get("Z")
@@ -442,3 +443,26 @@ def test_projection_pipeline_parity():
         r = c.proj_solve(dev(b), x, 1e-10, 3000, 30, 20)
         assert abs(r["iters"] - ref["iters"]) <= 1 and r["iters"] < its[-1] // 4, (r, ref["iters"])
     assert its[-1] < its[0], its
+
+
+@pytest.mark.parametrize("spec,N", [(CONFIGS["C1"][0], 3), (tgv_box(4, 3, 5, deform=1), 7),
+                                    (unit_box(3, 2, 5, periodic=(1, 0, 0)), 5), (tgv_box(2, 2, 2), 1)])
+def test_gs_update_fusion(spec, N):
+    """One rank: the PCG iteration with the gather-scatter fused into the r
+    update (default) and with separate kernels reach the oracle's iterate; the
+    residual histories agree to rounding (dots per unique point vs c-weighted)."""
+    o = O.Oracle(spec, N)
+    fun = f_tgv if all(spec.periodic) else f_sin
+    b = o.rhs(fun(o.get("X"), o.get("Y"), o.get("Z")))
+    ref = o.pcg(b, 1e-10, 3000)
+    with sem().sem_setup(spec, N) as c:
+        out = []
+        for fuse in (True, False):
+            c.set_gs_update(fuse)
+            x = c.zeros()
+            r = c.pcg_solve(dev(b), x, 1e-10, 3000)
+            assert r["status"] == 0 and abs(r["iters"] - ref["iters"]) <= 1, (fuse, r, ref["iters"])
+            assert np.abs(host(x) - ref["x"]).max() <= 1e-10
+            out.append(c.pcg_history())
+        k = min(len(out[0]), len(out[1]), 10)
+        np.testing.assert_allclose(out[0][:k], out[1][:k], rtol=1e-9)

@@ -96,7 +96,8 @@ def test_schwarz_apply_parity(spec, N):
 
 
 SOLVE_MESHES = [(CONFIGS["C1"][0], 3), (tgv_box(4, 4, 4), 7), (tgv_box(4, 3, 5, deform=1), 5),
-                (unit_box(3, 2, 4, periodic=(1, 0, 0)), 6)]
+                (unit_box(3, 2, 4, periodic=(1, 0, 0)), 6),
+                (unit_box(3, 1, 3), 4)]   # odd n_local: unaligned pair tails
 SOLVE_IDS = [f"{s.ex}x{s.ey}x{s.ez}-p{''.join(map(str, s.periodic))}-d{s.deform}-N{N}"
              for s, N in SOLVE_MESHES]
 
