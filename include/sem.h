@@ -252,6 +252,12 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    separate gather-scatter and update kernels (measured faster on C2: 123 vs
    133 us per iteration).  Same iterates up to summation order. */
 #define SEM_OPT_GS_UPDATE 10
+/* Schwarz coarse level at nranks > 1: 0 = distributed over the ranks (each
+   coarse CG step exchanges and allreduces), 1 = replicated (one all-gather of
+   the restricted right-hand side, then every rank solves the whole N = 1
+   problem; needs an even element partition), -1 (default) = auto (replicated
+   when the coarse problem has <= 2^20 slots).  Collective. */
+#define SEM_OPT_COARSE_REPLICATE 11
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

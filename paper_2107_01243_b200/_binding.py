@@ -266,6 +266,10 @@ class Context:
         """N = 7 Schwarz local solves on the fp64 tensor cores (default) or CUDA cores."""
         _check(load().sem_set_option(self._h, 9, 1 if on else 0))
 
+    def set_coarse_replicate(self, mode: int):
+        """Schwarz coarse level at nranks > 1: -1 auto, 0 distributed, 1 replicated. Collective."""
+        _check(load().sem_set_option(self._h, 11, int(mode)))
+
     def set_coarse_iters(self, k: int):
         """Maximum CG iterations of the Schwarz coarse solve (default 10)."""
         _check(load().sem_set_option(self._h, 7, int(k)))

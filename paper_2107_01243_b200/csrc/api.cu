@@ -114,6 +114,8 @@ struct sem_ctx {
   // single rank: the coarse solve replayed as one CUDA graph (its launches are
   // argument-stable: flat gs schedule, no peer epochs); gate copied to d_gate
   bool coarse_graph = true;
+  int coarse_replicate = -1;   // SEM_OPT_COARSE_REPLICATE: -1 auto, 0 distributed, 1 replicated
+  bool c0_repl = false;        // the coarse context in use is the replicated one
   bool gs_update = false;  // SEM_OPT_GS_UPDATE: one rank, flat gs -> gs + CG update fused
                            // (measured slower on C2: 133 vs 123 us per iteration)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
@@ -924,34 +926,75 @@ struct GateScope {
 // kernels in schwarz.cu).  The coarse space is a second context at N = 1 on
 // the same mesh and element partition (its operator, gather-scatter, PCG
 // kernels and multi-GPU transports are the fine level's, at n = 2).
+// replicated coarse solve (nranks > 1): every rank all-gathers the restricted
+// right-hand side and solves the whole N = 1 problem itself (one NCCL
+// all-gather instead of a gather-scatter exchange and two allreduces in each
+// of the ten coarse CG steps; graph-replayable like one rank).  Auto: when the
+// coarse problem is small (<= kReplicateSlots coarse slots) and the element
+// partition is even (equal all-gather blocks).
+constexpr int64_t kReplicateSlots = 1 << 20;
+static bool coarse_replicated(const sem_ctx* c) {
+  const sem::HostPlan& h = c->hp;
+  if (h.nranks == 1 || h.E % h.nranks != 0) return false;
+  if (c->coarse_replicate >= 0) return c->coarse_replicate == 1;
+  return h.E * 8 <= kReplicateSlots;
+}
+
 static int schwarz_setup(sem_ctx* c) {
   if (c->c0) return SEM_OK;
   const sem::HostPlan& h = c->hp;
   cudaStream_t s = c->stream;
   sem_ctx* c0 = nullptr;
-  SEM_TRY(sem_setup(&h.m, 1, &c0));   // collective for nranks > 1
+  c->c0_repl = coarse_replicated(c);
+  if (c->c0_repl) {   // the whole coarse mesh on this rank
+    sem_mesh m0 = h.m;
+    m0.rank = 0;
+    m0.nranks = 1;
+    m0.nccl_comm = nullptr;
+    SEM_TRY(sem_setup(&m0, 1, &c0));
+  } else {
+    SEM_TRY(sem_setup(&h.m, 1, &c0));   // collective for nranks > 1
+  }
   c->c0 = c0;
-  if (h.nranks == 1) c0->gs_mode = 1;   // flat schedule: graph-stable launches (bit-identical)
+  if (c0->hp.nranks == 1) c0->gs_mode = 1;   // flat schedule: graph-stable launches (bit-identical)
   const size_t nloc = (size_t)h.nloc, n = (size_t)h.n;
-  SEM_TRY(dalloc(&c->d_fS, nloc * 3 * n * n));
-  SEM_TRY(dalloc(&c->d_flam, nloc * 3 * n));
-  SEM_TRY(dalloc(&c->d_sy, (size_t)h.n_local));
+  if (!c->d_fS) {
+    SEM_TRY(dalloc(&c->d_fS, nloc * 3 * n * n));
+    SEM_TRY(dalloc(&c->d_flam, nloc * 3 * n));
+    SEM_TRY(dalloc(&c->d_sy, (size_t)h.n_local));
+    const sem_mesh& m = h.m;
+    const double box[6] = {m.x0, m.x1, m.y0, m.y1, m.z0, m.z1};
+    CUDA_TRY(sem::launch_fdm_setup(h.n, (int)h.nloc, h.e_lo, m.ex, m.ey, m.ez, box, m.deform,
+                                   m.deform_amp, m.periodic, c->d_xi, c->d_w, c->d_D, c->d_fS,
+                                   c->d_flam, s));
+    c->launches++;
+  }
   const size_t n0 = (size_t)c0->hp.n_local;
   SEM_TRY(dalloc(&c->d_b0, n0));
   SEM_TRY(dalloc(&c->d_x0, n0));
-  SEM_TRY(dalloc(&c->d_st0, 1));
+  if (!c->d_st0) SEM_TRY(dalloc(&c->d_st0, 1));
   // plain CG on the coarse level: the "Jacobi" vector is 1 on unmasked slots
   std::vector<double> ones(n0, 1.0);
   SEM_TRY(upload(&c->d_dinv0, ones, s));
   CUDA_TRY(sem::launch_invert_mask(c0->dp, c->d_dinv0, s));
-  const sem_mesh& m = h.m;
-  const double box[6] = {m.x0, m.x1, m.y0, m.y1, m.z0, m.z1};
-  CUDA_TRY(sem::launch_fdm_setup(h.n, (int)h.nloc, h.e_lo, m.ex, m.ey, m.ez, box, m.deform,
-                                 m.deform_amp, m.periodic, c->d_xi, c->d_w, c->d_D, c->d_fS,
-                                 c->d_flam, s));
-  c->launches += 2;
+  c->launches++;
   CUDA_TRY(cudaStreamSynchronize(s));
   return SEM_OK;
+}
+
+// drop the coarse level (rebuilt by the next schwarz_setup)
+static void schwarz_drop_coarse(sem_ctx* c) {
+  if (!c->c0) return;
+  cudaStreamSynchronize(c->stream);
+  free_ctx(c->c0);
+  c->c0 = nullptr;
+  double* bufs[3] = {c->d_b0, c->d_x0, c->d_dinv0};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  c->d_b0 = c->d_x0 = c->d_dinv0 = nullptr;
+  if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
+  c->g0exec = nullptr;
+  c->g0_iters = -1;
 }
 
 // coarse start state: tol set from ||b0|| on the device, at most K0 iterations
@@ -987,7 +1030,7 @@ static int coarse_body(sem_ctx* c, const int* gate) {
 }
 
 static int coarse_solve(sem_ctx* c, const int* gate) {
-  if (c->hp.nranks > 1 || !c->coarse_graph || c->timing) return coarse_body(c, gate);
+  if (c->c0->hp.nranks > 1 || !c->coarse_graph || c->timing) return coarse_body(c, gate);
   cudaStream_t s = c->stream;
   if (!c->g0exec || c->g0_iters != c->coarse_iters) {
     if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
@@ -1041,19 +1084,25 @@ static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, cons
   const sem::HostPlan& h = c->hp;
   cudaStream_t s = c->stream;
   double* y = (which & 1) ? c->d_sy : nullptr;
-  double* b0 = (which & 2) ? c->d_b0 : nullptr;
+  // replicated coarse level: this rank's elements are the block at e_lo
+  const int64_t off0 = c->c0_repl ? h.e_lo * 8 : 0;
+  double* b0 = (which & 2) ? c->d_b0 + off0 : nullptr;
   int tk = timer_begin(c, 7);
   CUDA_TRY(sem::launch_fdm(h.n, (int)h.nloc, r, c->d_mult, c->d_fS, c->d_flam, c->d_xi, y, b0,
                            gate, c->num_sms, c->fdm_tc, s));
   timer_end(c, tk);
   c->launches++;
   if (y) SEM_TRY(gs_op(c, y, 0));
-  if (b0) SEM_TRY(coarse_solve(c, gate));
+  if (b0) {
+    if (c->c0_repl)   // in place: every rank's restricted block -> the whole b0
+      NCCL_TRY(ncclAllGather(b0, c->d_b0, (size_t)h.nloc * 8, ncclDouble, c->nccl, s));
+    SEM_TRY(coarse_solve(c, gate));
+  }
   sem::PcgState* st = c->d_st;
   const bool dist = h.nranks > 1;
   double* dots = w_dot ? (dist ? st->loc_dz : st->dz) : nullptr;
   tk = timer_begin(c, 8);
-  CUDA_TRY(sem::launch_schwarz_combine(h.n, (int)h.nloc, y, b0 ? c->d_x0 : nullptr, c->d_mult,
+  CUDA_TRY(sem::launch_schwarz_combine(h.n, (int)h.nloc, y, b0 ? c->d_x0 + off0 : nullptr, c->d_mult,
                                        c->d_xi, z, r, w_dot, c->d_partial, &c->d_tickets[5], dots,
                                        gate, c->num_sms, s));
   timer_end(c, tk);
@@ -1650,6 +1699,19 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (option == SEM_OPT_FDM_TC) {
     cudaStreamSynchronize(c->stream);
     c->fdm_tc = value != 0;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_COARSE_REPLICATE) {   // collective: same value on every rank
+    if (value < -1 || value > 1) {
+      sem::set_error("sem_set_option: SEM_OPT_COARSE_REPLICATE must be -1, 0 or 1");
+      return SEM_EINVAL;
+    }
+    cudaStreamSynchronize(c->stream);
+    c->coarse_replicate = value;
+    if (c->c0 && c->c0_repl != coarse_replicated(c)) {
+      schwarz_drop_coarse(c);
+      SEM_TRY(schwarz_setup(c));
+    }
     return SEM_OK;
   }
   if (option == SEM_OPT_COARSE_GRAPH) {

@@ -53,10 +53,22 @@ __device__ __forceinline__ void reduce_cols(const double* acc, int K, double* pa
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < K) {
+  // the last block sums the per-block partials of each column with all its
+  // threads (a fixed block-to-thread assignment and a fixed tree: deterministic);
+  // a single thread per column walking all blocks serialised ~600 L2 round trips
+  for (int i = 0; i < K; i++) {
     double v = 0.0;
-    for (unsigned b = 0; b < gridDim.x; b++) v += __ldcg(&part[(size_t)b * K + threadIdx.x]);
-    out[threadIdx.x] = v;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+      v += __ldcg(&part[(size_t)b * K + i]);
+    v = warp_sum(v);
+    __syncthreads();   // s_w reuse
+    if (lane == 0) s_w[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < nw; q++) t += s_w[q];
+      out[i] = t;
+    }
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }

@@ -343,8 +343,13 @@ def schwarz_strong(cfgs=("C3", "C4")):
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
             del X, Y, Z
             res = {"what": f"{cfg}_schwarz_strong", "P": P}
-            for pc, solver in (("jacobi", "pcg"), ("schwarz", "pcg"), ("schwarz", "gmres")):
+            runs = [("jacobi", "pcg", -1), ("schwarz", "pcg", 0), ("schwarz", "gmres", 0)]
+            if P > 1:   # the replicated coarse solve (one all-gather, no per-step collectives)
+                runs += [("schwarz", "pcg", 1), ("schwarz", "gmres", 1)]
+            for pc, solver, rep in runs:
                 c.set_precond(pc)
+                if pc == "schwarz":
+                    c.set_coarse_replicate(rep)
                 x = c.zeros()
                 fn = (lambda: c.pcg_solve(b, x, 1e-10, 3000)) if solver == "pcg" else \
                     (lambda: c.gmres_solve(b, x, 1e-10, 3000, 30))
@@ -357,7 +362,8 @@ def schwarz_strong(cfgs=("C3", "C4")):
                 e1.record(st)
                 torch.cuda.synchronize()
                 ms = mx(e0.elapsed_time(e1))
-                res[f"{solver}_{pc}"] = {"iters": r["iters"], "status": r["status"], "ms": round(ms, 3)}
+                key = f"{solver}_{pc}" + ("_replicated" if rep == 1 else "")
+                res[key] = {"iters": r["iters"], "status": r["status"], "ms": round(ms, 3)}
             c.set_precond("jacobi")
             if rank == 0:
                 out(res)

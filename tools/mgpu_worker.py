@@ -69,16 +69,23 @@ def main():
                 # NEXT-1: two-level Schwarz (fine gs and the N=1 coarse CG run
                 # through the same transport) and flexible PCG with it
                 zs, xs, rs = c.zeros(), c.zeros(), None
+                zs1, xs1, rs1 = c.zeros(), c.zeros(), None
                 if not fused:
                     c.set_precond("schwarz")
+                    c.set_coarse_replicate(0)          # distributed coarse CG
                     c.schwarz_apply(b, zs)
                     rs = c.pcg_solve(b, xs, 1e-10, 3000)
+                    c.set_coarse_replicate(1)          # replicated coarse solve
+                    c.schwarz_apply(b, zs1)
+                    rs1 = c.pcg_solve(b, xs1, 1e-10, 3000)
+                    c.set_coarse_replicate(-1)
                     c.set_precond("jacobi")
                 torch.cuda.synchronize()
                 parts = [None] * P
                 dist.all_gather_object(parts, (w.cpu().numpy(), g.cpu().numpy(), b.cpu().numpy(),
                                                x.cpu().numpy(), r, xg.cpu().numpy(), rg,
-                                               zs.cpu().numpy(), xs.cpu().numpy(), rs))
+                                               zs.cpu().numpy(), xs.cpu().numpy(), rs,
+                                               zs1.cpu().numpy(), xs1.cpu().numpy(), rs1))
                 if rank == 0:
                     W = np.concatenate([p[0] for p in parts])
                     Gs = np.concatenate([p[1] for p in parts])
@@ -118,17 +125,19 @@ def main():
                             fails.append(f"{tag}: gmres x diff {np.abs(Xg - refg['x']).max():.2e}")
                     if rs is not None:
                         schw = o.schwarz(10)
-                        Zs = np.concatenate([p[7] for p in parts])
                         ref_z = schw.apply(B)
-                        e = np.abs(Zs - ref_z).max() / np.abs(ref_z).max()
-                        if not e <= 1e-11:
-                            fails.append(f"{tag}: schwarz apply rel err {e:.2e}")
                         refs = schw.pcg(B, 1e-10, 3000)
-                        Xsch = np.concatenate([p[8] for p in parts])
-                        if abs(rs["iters"] - refs["iters"]) > 1 or rs["status"] != 0:
-                            fails.append(f"{tag}: schwarz pcg iters {rs['iters']} vs {refs['iters']}")
-                        if not np.abs(Xsch - refs["x"]).max() <= 1e-10:
-                            fails.append(f"{tag}: schwarz pcg x diff {np.abs(Xsch - refs['x']).max():.2e}")
+                        for zi, xi, ri, mode in ((7, 8, rs, "distributed"), (10, 11, rs1, "replicated")):
+                            Zs = np.concatenate([p[zi] for p in parts])
+                            e = np.abs(Zs - ref_z).max() / np.abs(ref_z).max()
+                            if not e <= 1e-11:
+                                fails.append(f"{tag}: schwarz ({mode}) apply rel err {e:.2e}")
+                            Xsch = np.concatenate([p[xi] for p in parts])
+                            rr_ = parts[0][xi + 1]
+                            if abs(rr_["iters"] - refs["iters"]) > 1 or rr_["status"] != 0:
+                                fails.append(f"{tag}: schwarz ({mode}) pcg iters {rr_['iters']} vs {refs['iters']}")
+                            if not np.abs(Xsch - refs["x"]).max() <= 1e-10:
+                                fails.append(f"{tag}: schwarz ({mode}) pcg x diff {np.abs(Xsch - refs['x']).max():.2e}")
                     print(f"{tag}: ok-check iters {r['iters']} (oracle {ref['iters']}) "
                           f"dx {dx:.2e}", flush=True)
     sem.nccl_comm_destroy(comm)
