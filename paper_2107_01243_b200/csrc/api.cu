@@ -1152,13 +1152,21 @@ static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, i
   for (int it = 0; it < maxit && !hd; it += kBatch) {
     const int nb = std::min(kBatch, maxit - it);
     for (int q = 0; q < nb; q++) {
-      {
+      if (!dist && !fused(c)) {
+        // w = A p with sigma = sum_l p_l (A_L p)_l reduced by the Ax kernel itself
+        // (reading Q23: equals <p, w>_c for the continuous, masked p)
         GateScope g(c, done);
-        SEM_TRY(apply_op(c, p, w, sem::AX_APPLY));   // w = A p
+        SEM_TRY(run_ax(c, p, w, sem::AX_PCG, 0, (int)h.nloc, 0, 0, &st->sigma));
+        SEM_TRY(gs_pass(c, w));
+      } else {
+        {
+          GateScope g(c, done);
+          SEM_TRY(apply_op(c, p, w, sem::AX_APPLY));   // w = A p
+        }
+        CUDA_TRY(sem::launch_mdot(n, c->d_mult, p, w, n, 1, part, tk,
+                                  dist ? &st->loc[2] : &st->sigma, done, sms, s));
+        if (dist) SEM_TRY(allreduce_to(c, &st->loc[2], &st->sigma, 1));
       }
-      CUDA_TRY(sem::launch_mdot(n, c->d_mult, p, w, n, 1, part, tk,
-                                dist ? &st->loc[2] : &st->sigma, done, sms, s));
-      if (dist) SEM_TRY(allreduce_to(c, &st->loc[2], &st->sigma, 1));
       CUDA_TRY(sem::launch_fcg_scalar(1, st, c->d_hist, s));       // alpha
       CUDA_TRY(sem::launch_maxpy(n, x, p, n, 1, &st->alpha, 1.0, nullptr, c->d_mult, part, tk,
                                  nullptr, done, sms, s));           // x += alpha p
@@ -1356,9 +1364,9 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
       // two classical Gram-Schmidt passes against v_0..v_j, then ||w||_c
       CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, ld, j + 1, part, tk, gs->h1, cyc, sms, s));
       if (dist) SEM_TRY(allreduce(c, gs->h1, j + 1));
-      CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, ld, j + 1, gs->h1, -1.0, nullptr, mult, part, tk,
-                                 nullptr, cyc, sms, s));
-      CUDA_TRY(sem::launch_mdot(n, mult, w, c->d_V, ld, j + 1, part, tk, gs->h2, cyc, sms, s));
+      // second pass fused with the first pass's update: w -= V h1, h2 = V^T w
+      CUDA_TRY(sem::launch_maxpy_mdot(n, w, c->d_V, ld, j + 1, gs->h1, mult, part, tk, gs->h2, cyc,
+                                      sms, s));
       if (dist) SEM_TRY(allreduce(c, gs->h2, j + 1));
       CUDA_TRY(sem::launch_maxpy(n, w, c->d_V, ld, j + 1, gs->h2, -1.0, nullptr, mult, part, tk,
                                  &gs->norm2[0], cyc, sms, s));

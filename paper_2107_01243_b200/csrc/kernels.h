@@ -158,6 +158,11 @@ cudaError_t launch_maxpy(int64_t n, double* y, const double* V, int64_t ldv, int
                          const double* coef, double alpha, const double* dinv, const uint8_t* mult,
                          double* part, unsigned* ticket, double* out_norm, const int* done,
                          int num_sms, cudaStream_t s);
+// y -= sum_i coef[i] V_i, then out[i] = <y, V_i>_c in the same pass (K <= 32)
+cudaError_t launch_maxpy_mdot(int64_t n, double* y, const double* V, int64_t ldv, int K,
+                              const double* coef, const uint8_t* mult, double* part,
+                              unsigned* ticket, double* out, const int* done, int num_sms,
+                              cudaStream_t s);
 cudaError_t launch_resid(int64_t n, const double* b, const double* w, double* v,
                          const uint8_t* mult, double* part, unsigned* ticket, double* out,
                          const int* done, int num_sms, cudaStream_t s);

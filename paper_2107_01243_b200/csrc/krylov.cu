@@ -195,6 +195,63 @@ __global__ void __launch_bounds__(kKT, 2) maxpy_kernel(int64_t n, double* __rest
   if (NORM) reduce_cols<1>(nrm, 1, part, ticket, out_norm, s_w);
 }
 
+// Fused CGS2 middle pass: y -= sum_i coef[i] V_i, then out[i] = <y_new, V_i>_c
+// in the same sweep (each V_i is loaded once for both), so an Arnoldi step
+// reads the basis three times instead of four.  K <= KMAX (no slicing: the
+// dots need the final y).
+template <int KMAX>
+__global__ void __launch_bounds__(kKT, 1) maxpy_mdot_kernel(int64_t n, double* __restrict__ y,
+                                                            const double* __restrict__ V,
+                                                            int64_t ldv, int K,
+                                                            const double* __restrict__ coef,
+                                                            const uint8_t* __restrict__ mult,
+                                                            double* part, unsigned* ticket,
+                                                            double* out, const int* done) {
+  __shared__ double s_w[(kKT / 32) * KMAX];
+  __shared__ double s_c[KMAX];
+  if (done && *done) return;
+  if (threadIdx.x < K) s_c[threadIdx.x] = -coef[threadIdx.x];
+  __syncthreads();
+  double acc[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; i++) acc[i] = 0.0;
+  const int64_t np = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+  double2* y2 = reinterpret_cast<double2*>(y);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < np; q += stride) {
+    double2 vv[KMAX];
+    const double2 yv = y2[q];
+    const uchar2 mv = reinterpret_cast<const uchar2*>(mult)[q];
+#pragma unroll
+    for (int i = 0; i < KMAX; i++)
+      if (i < K) vv[i] = ld2cs(V + i * ldv, q);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++)
+      if (i < K) {
+        s0 = fma(s_c[i], vv[i].x, s0);
+        s1 = fma(s_c[i], vv[i].y, s1);
+      }
+    const double2 v = make_double2(yv.x + s0, yv.y + s1);
+    y2[q] = v;
+    const double cv0 = c_of_k(mv.x) * v.x, cv1 = c_of_k(mv.y) * v.y;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++)
+      if (i < K) acc[i] = fma(cv1, vv[i].y, fma(cv0, vv[i].x, acc[i]));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    double sacc = 0.0;
+    for (int i = 0; i < K; i++) sacc = fma(s_c[i], V[i * ldv + l], sacc);
+    const double v = y[l] + sacc;
+    y[l] = v;
+    const double cv = c_of_k(mult[l]) * v;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++)
+      if (i < K) acc[i] = fma(cv, V[i * ldv + l], acc[i]);
+  }
+  reduce_cols<KMAX>(acc, K, part, ticket, out, s_w);
+}
+
 // v = (b - w) (restart residual) with its c-norm^2, or v = w with its c-norm^2
 __global__ void __launch_bounds__(kKT) resid_kernel(int64_t n, const double* __restrict__ b,
                                                     const double* __restrict__ w,
@@ -393,6 +450,24 @@ cudaError_t launch_maxpy(int64_t n, double* y, const double* V, int64_t ldv, int
     else MAXPY(16, 1);
 #undef MAXPY
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpy_mdot(int64_t n, double* y, const double* V, int64_t ldv, int K,
+                              const double* coef, const uint8_t* mult, double* part,
+                              unsigned* ticket, double* out, const int* done, int num_sms,
+                              cudaStream_t s) {
+  if (K > 32 || (K > 1 && (ldv & 1))) return cudaErrorInvalidValue;
+  const int g = kgrid(n / 2 + 1, num_sms);
+  if (K <= 8)
+    dev::maxpy_mdot_kernel<8><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, mult, part, ticket, out,
+                                                     done);
+  else if (K <= 16)
+    dev::maxpy_mdot_kernel<16><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, mult, part, ticket,
+                                                      out, done);
+  else
+    dev::maxpy_mdot_kernel<32><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, mult, part, ticket,
+                                                      out, done);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@ import paper_2107_01243_b200 as sem  # noqa: E402
 from sem_inputs import CONFIGS, f_tgv  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
+only_gmres = len(sys.argv) > 2 and sys.argv[2] == "gmres"   # one Jacobi GMRES(30) cycle
 spec, N = CONFIGS[cfg]
 torch.cuda.set_device(0)
 with sem.sem_setup(spec, N) as c:
@@ -20,6 +21,12 @@ with sem.sem_setup(spec, N) as c:
     b = c.zeros()
     c.rhs(f_tgv(X, Y, Z, xp=torch), b)
     z = c.zeros()
+    if only_gmres:
+        x = c.zeros()
+        c.gmres_solve(b, x, 0.0, 30, 30)
+        torch.cuda.synchronize()
+        print("prof_schwarz gmres ok")
+        sys.exit(0)
     c.set_coarse_graph(False)   # ncu replays kernels, not graphs
     for _ in range(2):
         c.schwarz_apply(b, z, 3)
