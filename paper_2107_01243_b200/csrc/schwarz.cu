@@ -477,8 +477,14 @@ __global__ void __launch_bounds__(kFT) schwarz_combine_kernel(
   __shared__ int flag;
   __shared__ uint32_t ijk[1728];
   __shared__ double Js[12][2];
+  __shared__ double cinv[256], csq[256];   // 1/m (as __drcp_rn) and its square root
   if (gate && *gate) return;
   const int n3 = n * n * n;
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) {
+    const double c = __drcp_rn((double)(m > 0 ? m : 1));
+    cinv[m] = c;
+    csq[m] = sqrt(c);
+  }
   for (int p = threadIdx.x; p < n3; p += blockDim.x)
     ijk[p] = (uint32_t)(p % n) | ((uint32_t)((p / n) % n) << 8) | ((uint32_t)(p / (n * n)) << 16);
   if (threadIdx.x < n) {
@@ -495,12 +501,12 @@ __global__ void __launch_bounds__(kFT) schwarz_combine_kernel(
     int64_t el = l / n3;
     int p = (int)(l - el * n3);
     const uchar2 mv = *reinterpret_cast<const uchar2*>(mult + l);
-    const double c0 = __drcp_rn((double)mv.x), c1 = __drcp_rn((double)mv.y);
+    const double c0 = cinv[mv.x], c1 = cinv[mv.y];
     double v0 = 0.0, v1 = 0.0;
     if (y) {
       const double2 yv = __ldcs(reinterpret_cast<const double2*>(y) + q);
-      v0 = sqrt(c0) * yv.x;
-      v1 = sqrt(c1) * yv.y;
+      v0 = csq[mv.x] * yv.x;
+      v1 = csq[mv.y] * yv.y;
     }
     if (x0) {
 #pragma unroll
