@@ -84,6 +84,9 @@ def lib():
         L.oracle_proj_solve.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int,
                                         C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.oracle_proj_gram.argtypes = [C.c_void_p, _D]
+        L.oracle_cgcg.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int,
+                                  C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double), C.c_void_p]
         L.oracle_proj_set_schwarz.argtypes = [C.c_void_p, C.c_void_p]
         L.oracle_schwarz_create.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
         L.oracle_schwarz_free.argtypes = [C.c_void_p]
@@ -222,6 +225,18 @@ class Oracle:
                               C.byref(rt), hist.ctypes.data_as(C.c_void_p))
         if st < 0:
             raise OracleError(f"oracle_pcg failed with status {st}")
+        return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
+                "status": st, "hist": hist[: it.value + 1]}
+
+    def cgcg(self, b, tol: float, maxit: int):
+        """Single-reduction (Chronopoulos-Gear) Jacobi PCG (reading Q34)."""
+        x = np.zeros(self.nslots)
+        it, rf, rt = C.c_int(), C.c_double(), C.c_double()
+        hist = np.zeros(maxit + 1)
+        st = lib().oracle_cgcg(self._h, _f64(b), x, tol, maxit, C.byref(it), C.byref(rf),
+                               C.byref(rt), hist.ctypes.data_as(C.c_void_p))
+        if st < 0:
+            raise OracleError(f"oracle_cgcg failed with status {st}")
         return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
                 "status": st, "hist": hist[: it.value + 1]}
 

@@ -646,6 +646,79 @@ int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, 
   return st;
 }
 
+/* Single-reduction PCG (Chronopoulos & Gear 1989; SURVEY 8(f) lower-ranked
+   variant after NEXT-1..4, "addressed with non-blocking or pipelined
+   Krylov solvers"), with the Jacobi preconditioner, reading Q34:
+     x0 = 0, r0 = b, u0 = M r0, w0 = A u0, gamma0 = <r0,u0>_c, delta0 = <w0,u0>_c,
+     eps0 = <r0,r0>_c; stop at once if sqrt(eps0) <= tol; alpha0 = gamma0/delta0, beta0 = 0;
+     for i = 0, 1, ...:
+       p_i = u_i + beta_i p_{i-1};  s_i = w_i + beta_i s_{i-1}   (s_i = A p_i)
+       x_{i+1} = x_i + alpha_i p_i;  r_{i+1} = r_i - alpha_i s_i
+       u_{i+1} = M r_{i+1};  w_{i+1} = A u_{i+1}
+       gamma, delta, eps = <r,u>_c, <w,u>_c, <r,r>_c       (ONE global reduction)
+       stop if sqrt(eps) <= tol (iterations = i + 1)
+       beta_{i+1} = gamma_{i+1}/gamma_i;
+       alpha_{i+1} = gamma_{i+1} / (delta_{i+1} - beta_{i+1} gamma_{i+1} / alpha_i)
+   The iterates equal PCG's in exact arithmetic; hist[k] = sqrt(eps) after k updates. */
+int oracle_cgcg(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+                int* iters, double* res_final, double* res_true, double* hist) {
+  if (!c || maxit < 0) return -1;
+  const int64_t ns = c->nslots;
+  double* r = (double*)malloc(sizeof(double) * ns);
+  double* u = (double*)malloc(sizeof(double) * ns);
+  double* w = (double*)malloc(sizeof(double) * ns);
+  double* p = (double*)calloc(ns, sizeof(double));
+  double* s = (double*)calloc(ns, sizeof(double));
+  if (!r || !u || !w || !p || !s) { free(r); free(u); free(w); free(p); free(s); return -5; }
+  int status = 1, k = 0;
+  for (int64_t l = 0; l < ns; l++) {
+    x[l] = 0.0;
+    r[l] = b[l];
+    u[l] = c->dinv[l] * r[l];
+  }
+  oracle_apply(c, u, w);
+  double gamma = oracle_dot_c(c, r, u);
+  double delta = oracle_dot_c(c, w, u);
+  double eps = oracle_dot_c(c, r, r);
+  if (hist) hist[0] = sqrt(eps);
+  if (sqrt(eps) <= tol) status = 0;
+  double alpha = 0.0, beta = 0.0;
+  if (status == 1) {
+    if (!(delta > 0.0)) status = -6;
+    else alpha = gamma / delta;
+  }
+  while (status == 1 && k < maxit) {
+    for (int64_t l = 0; l < ns; l++) {
+      p[l] = u[l] + beta * p[l];
+      s[l] = w[l] + beta * s[l];
+      x[l] += alpha * p[l];
+      r[l] -= alpha * s[l];
+      u[l] = c->dinv[l] * r[l];
+    }
+    k++;
+    oracle_apply(c, u, w);
+    const double gamma_new = oracle_dot_c(c, r, u);
+    delta = oracle_dot_c(c, w, u);
+    eps = oracle_dot_c(c, r, r);
+    if (hist) hist[k] = sqrt(eps);
+    if (sqrt(eps) <= tol) { status = 0; break; }
+    beta = gamma_new / gamma;
+    const double den = delta - beta * gamma_new / alpha;
+    if (!(den > 0.0)) { status = -6; break; }
+    alpha = gamma_new / den;
+    gamma = gamma_new;
+  }
+  if (iters) *iters = k;
+  if (res_final) *res_final = sqrt(eps);
+  if (res_true) {
+    oracle_apply(c, x, w);
+    for (int64_t l = 0; l < ns; l++) w[l] = b[l] - w[l];
+    *res_true = sqrt(oracle_dot_c(c, w, w));
+  }
+  free(r); free(u); free(w); free(p); free(s);
+  return status;
+}
+
 /* ------------------------------------------------------------------ */
 /* NEXT-3: restarted GMRES and solution projection (Table 2) */
 

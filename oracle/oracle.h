@@ -77,6 +77,10 @@ int oracle_helm_dinv(const oracle_ctx* c, double h1, double h2, double* dinv);
 int oracle_helm_pcg(const oracle_ctx* c, double h1, double h2, const double* b, double* x,
                     double tol, int maxit, int* iters, double* res_final, double* res_true,
                     double* hist);
+/* single-reduction (Chronopoulos-Gear) Jacobi PCG, reading Q34: same iterates
+   as oracle_pcg in exact arithmetic, one global reduction per iteration */
+int oracle_cgcg(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
+                int* iters, double* res_final, double* res_true, double* hist);
 /* NEXT-3 (Table 2): restarted GMRES with right Jacobi
    preconditioning, and the solution-projection space (Fischer 1998). */
 int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
