@@ -258,6 +258,14 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    problem; needs an even element partition), -1 (default) = auto (replicated
    when the coarse problem has <= 2^20 slots).  Collective. */
 #define SEM_OPT_COARSE_REPLICATE 11
+/* Jacobi-PCG recurrences of sem_pcg_solve / sem_helm_pcg_solve /
+   sem_pcg_solve_host: 0 (default) = standard (two reductions per iteration),
+   1 = single-reduction Chronopoulos-Gear form: the dots
+   <r,u>, <r,r> of the update pass and <w,u> of the operator application are
+   reduced together, one allreduce per iteration at nranks > 1 (one extra
+   vector pass per iteration).  Same iterates in exact arithmetic (DESIGN.md
+   reading Q34).  Collective. */
+#define SEM_OPT_PCG_VARIANT 12
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

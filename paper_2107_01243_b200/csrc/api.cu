@@ -116,6 +116,7 @@ struct sem_ctx {
   bool coarse_graph = true;
   int coarse_replicate = -1;   // SEM_OPT_COARSE_REPLICATE: -1 auto, 0 distributed, 1 replicated
   bool c0_repl = false;        // the coarse context in use is the replicated one
+  int pcg_variant = 0;     // SEM_OPT_PCG_VARIANT: 0 standard, 1 single-reduction (Chronopoulos-Gear)
   bool gs_update = false;  // SEM_OPT_GS_UPDATE: one rank, flat gs -> gs + CG update fused
                            // (measured slower on C2: 133 vs 123 us per iteration)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
@@ -882,9 +883,78 @@ static int pcg_finish(sem_ctx* c, const double* b, const double* x, sem_pcg_resu
 }
 
 
+// gate of the operator's Ax kernel (any mode returns early when *g)
+struct GateScope {
+  sem_ctx* c;
+  GateScope(sem_ctx* ctx, const int* g) : c(ctx) { c->ax_gate = g; }
+  ~GateScope() { c->ax_gate = nullptr; }
+};
+
+// single-reduction (Chronopoulos-Gear) Jacobi PCG (reading Q34): one global
+// reduction per iteration -- (gamma, eps) from the update pass and delta from the
+// operator application are reduced together (one allreduce at P > 1)
+static int cgcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                    sem_pcg_result* res) {
+  if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
+  SEM_TRY(ensure_hist(c, maxit));
+  const sem::HostPlan& h = c->hp;
+  const int64_t n = h.n_local;
+  cudaStream_t s = c->stream;
+  const int sms = c->num_sms;
+  const bool dist = h.nranks > 1;
+  if (!c->d_rw) SEM_TRY(dalloc(&c->d_rw, 2 * (size_t)c->ldv));
+  double *u = c->d_rw, *sv = c->d_rw + c->ldv, *p = c->d_p, *r = c->d_r, *w = c->d_wv;
+  const double* dinv = c->helm ? c->d_dinv_helm : c->d_dinv;
+  sem::PcgState* st = c->d_st;
+  const int* done = &st->done;
+  double* out3 = dist ? st->cg3_loc : st->cg3;
+  sem::PcgState init{};
+  init.tol = tol;
+  init.maxit = maxit;
+  std::memcpy(c->h_st, &init, sizeof(init));
+  CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
+  auto op = [&]() -> int {   // w = A u and delta = <w, u>
+    GateScope g(c, done);
+    if (!dist && !fused(c)) {
+      SEM_TRY(run_ax(c, u, w, sem::AX_PCG, 0, (int)h.nloc, 0, 0, &st->cg3[2]));
+      SEM_TRY(gs_pass(c, w));
+    } else {
+      SEM_TRY(apply_op(c, u, w, sem::AX_APPLY));
+      CUDA_TRY(sem::launch_mdot(n, c->d_mult, u, w, n, 1, c->d_partial, &c->d_tickets[6],
+                                &out3[2], done, sms, s));
+      c->launches++;
+    }
+    if (dist) SEM_TRY(allreduce_to(c, st->cg3_loc, st->cg3, 3));   // the one reduction
+    return SEM_OK;
+  };
+  CUDA_TRY(sem::launch_cgcg_init(n, b, dinv, c->d_mult, x, r, u, p, sv, c->d_partial,
+                                 &c->d_tickets[6], out3, sms, s));
+  SEM_TRY(op());
+  CUDA_TRY(sem::launch_cgcg_scalar(0, st, c->d_hist, s));
+  c->launches += 2;
+  int hd = 0;
+  for (int it = 0; it < maxit && !hd; it += kBatch) {
+    const int nb = std::min(kBatch, maxit - it);
+    for (int q = 0; q < nb; q++) {
+      int tk = timer_begin(c, 1);
+      CUDA_TRY(sem::launch_cgcg_update(n, dinv, c->d_mult, u, w, p, sv, x, r, c->d_partial,
+                                       &c->d_tickets[6], out3, st, sms, s));
+      timer_end(c, tk);
+      SEM_TRY(op());
+      CUDA_TRY(sem::launch_cgcg_scalar(1, st, c->d_hist, s));
+      c->launches += 2;
+    }
+    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    hd = c->h_st->done;
+  }
+  return pcg_finish(c, b, x, res);
+}
+
 static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                    sem_pcg_result* res) {
   if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
+  if (c->pcg_variant == 1) return cgcg_run(c, b, x, tol, maxit, res);
   SEM_TRY(ensure_hist(c, maxit));
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
@@ -914,12 +984,6 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   return pcg_finish(c, b, x, res);
 }
 
-// gate of the operator's Ax kernel (any mode returns early when *g)
-struct GateScope {
-  sem_ctx* c;
-  GateScope(sem_ctx* ctx, const int* g) : c(ctx) { c->ax_gate = g; }
-  ~GateScope() { c->ax_gate = nullptr; }
-};
 
 // ---------------------------------------------------------------- NEXT-1: Schwarz
 // two-level additive overlapping Schwarz (readings Q28-Q32;
@@ -1697,6 +1761,15 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     cudaStreamSynchronize(c->stream);
     if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
     c->precond = value;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_PCG_VARIANT) {   // collective for nranks > 1
+    if (value != 0 && value != 1) {
+      sem::set_error("sem_set_option: SEM_OPT_PCG_VARIANT must be 0 or 1");
+      return SEM_EINVAL;
+    }
+    cudaStreamSynchronize(c->stream);
+    c->pcg_variant = value;
     return SEM_OK;
   }
   if (option == SEM_OPT_GS_UPDATE) {

@@ -75,6 +75,8 @@ struct PcgState {
   double alpha, beta;    // flexible PCG (Schwarz) scalars
   double dz[2];          // flexible PCG: <z', r'>_c, <z', w>_c
   double loc_dz[2];      // P > 1: this rank's partials of dz
+  double cg3[3];         // single-reduction PCG: gamma = <r,u>_c, eps = <r,r>_c, delta = <w,u>_c
+  double cg3_loc[3];     // P > 1: this rank's partials of cg3 (one allreduce per iteration)
   int it;                // completed iterations
   int done;              // 0 running, 1 converged, 2 breakdown, 3 NaN, 4 maxit
   int iters;
@@ -163,6 +165,15 @@ cudaError_t launch_maxpy_mdot(int64_t n, double* y, const double* V, int64_t ldv
                               const double* coef, const uint8_t* mult, double* part,
                               unsigned* ticket, double* out, const int* done, int num_sms,
                               cudaStream_t s);
+// single-reduction (Chronopoulos-Gear) Jacobi PCG (krylov.cu, reading Q34)
+cudaError_t launch_cgcg_init(int64_t n, const double* b, const double* dinv, const uint8_t* mult,
+                             double* x, double* r, double* u, double* p, double* s, double* part,
+                             unsigned* ticket, double* out2, int num_sms, cudaStream_t st);
+cudaError_t launch_cgcg_update(int64_t n, const double* dinv, const uint8_t* mult, double* u,
+                               const double* w, double* p, double* s, double* x, double* r,
+                               double* part, unsigned* ticket, double* out2, const PcgState* ps,
+                               int num_sms, cudaStream_t st);
+cudaError_t launch_cgcg_scalar(int stage, PcgState* ps, double* hist, cudaStream_t st);
 cudaError_t launch_resid(int64_t n, const double* b, const double* w, double* v,
                          const uint8_t* mult, double* part, unsigned* ticket, double* out,
                          const int* done, int num_sms, cudaStream_t s);

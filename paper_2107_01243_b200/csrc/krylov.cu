@@ -311,6 +311,115 @@ __global__ void __launch_bounds__(kKT) vnorm_kernel(int64_t n, const double* w, 
   }
 }
 
+// ---- single-reduction (Chronopoulos-Gear) Jacobi PCG (reading Q34)
+// init: x = 0, r = b, u = dinv b, p = s = 0; partials of <r,u>_c and <r,r>_c
+__global__ void __launch_bounds__(kKT) cgcg_init_kernel(int64_t n, const double* __restrict__ b,
+                                                        const double* __restrict__ dinv,
+                                                        const uint8_t* __restrict__ mult,
+                                                        double* __restrict__ x, double* __restrict__ r,
+                                                        double* __restrict__ u, double* __restrict__ p,
+                                                        double* __restrict__ s, double* part,
+                                                        unsigned* ticket, double* out2) {
+  __shared__ double s_w[(kKT / 32) * 2];
+  double acc[2] = {0.0, 0.0};
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const double bl = b[l], ul = dinv[l] * bl, c = c_of_k(mult[l]);
+    x[l] = 0.0;
+    r[l] = bl;
+    u[l] = ul;
+    p[l] = 0.0;
+    s[l] = 0.0;
+    acc[0] = fma(c * bl, ul, acc[0]);
+    acc[1] = fma(c * bl, bl, acc[1]);
+  }
+  reduce_cols<2>(acc, 2, part, ticket, out2, s_w);
+}
+
+// one pass: p = u + beta p; s = w + beta s; x += alpha p; r -= alpha s; u = dinv r;
+// partials of gamma = <r,u>_c and eps = <r,r>_c.  Skipped when st->done.
+__global__ void __launch_bounds__(kKT) cgcg_update_kernel(
+    int64_t n, const double* __restrict__ dinv, const uint8_t* __restrict__ mult,
+    double* __restrict__ u, const double* __restrict__ w, double* __restrict__ p,
+    double* __restrict__ s, double* __restrict__ x, double* __restrict__ r, double* part,
+    unsigned* ticket, double* out2, const PcgState* st) {
+  __shared__ double s_w[(kKT / 32) * 2];
+  if (st->done) return;
+  const double alpha = st->alpha, beta = st->beta;
+  double acc[2] = {0.0, 0.0};
+  const int64_t np = n >> 1;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < np;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 uv = ld2cs(u, q), wv = ld2cs(w, q), dv = ld2cs(dinv, q);
+    double2 pv = ld2cs(p, q), sv = ld2cs(s, q), xv = ld2cs(x, q), rv = ld2cs(r, q);
+    const uchar2 mv = reinterpret_cast<const uchar2*>(mult)[q];
+    pv.x = fma(beta, pv.x, uv.x);
+    pv.y = fma(beta, pv.y, uv.y);
+    sv.x = fma(beta, sv.x, wv.x);
+    sv.y = fma(beta, sv.y, wv.y);
+    xv.x = fma(alpha, pv.x, xv.x);
+    xv.y = fma(alpha, pv.y, xv.y);
+    rv.x = fma(-alpha, sv.x, rv.x);
+    rv.y = fma(-alpha, sv.y, rv.y);
+    const double2 un = make_double2(dv.x * rv.x, dv.y * rv.y);
+    reinterpret_cast<double2*>(p)[q] = pv;
+    reinterpret_cast<double2*>(s)[q] = sv;
+    __stcs(reinterpret_cast<double2*>(x) + q, xv);
+    reinterpret_cast<double2*>(r)[q] = rv;
+    reinterpret_cast<double2*>(u)[q] = un;
+    const double c0 = c_of_k(mv.x), c1 = c_of_k(mv.y);
+    acc[0] = fma(c0 * rv.x, un.x, fma(c1 * rv.y, un.y, acc[0]));
+    acc[1] = fma(c0 * rv.x, rv.x, fma(c1 * rv.y, rv.y, acc[1]));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    const double pl = fma(beta, p[l], u[l]), sl = fma(beta, s[l], w[l]);
+    p[l] = pl;
+    s[l] = sl;
+    x[l] = fma(alpha, pl, x[l]);
+    const double rl = fma(-alpha, sl, r[l]), ul = dinv[l] * rl, c = c_of_k(mult[l]);
+    r[l] = rl;
+    u[l] = ul;
+    acc[0] = fma(c * rl, ul, acc[0]);
+    acc[1] = fma(c * rl, rl, acc[1]);
+  }
+  reduce_cols<2>(acc, 2, part, ticket, out2, s_w);
+}
+
+// scalars: cg3 = (gamma, eps, delta) of the current u, w.  stage 0: start;
+// stage 1: after an update + operator application
+__global__ void cgcg_scalar_kernel(int stage, PcgState* st, double* hist) {
+  const double gamma = st->cg3[0], eps = st->cg3[1], delta = st->cg3[2];
+  const double g = sqrt(eps);
+  if (stage == 0) {
+    st->it = 0;
+    st->iters = 0;
+    st->gamma = eps;
+    hist[0] = g;
+    st->beta = 0.0;
+    st->rho_old = gamma;
+    if (g <= st->tol) { st->done = 1; return; }
+    if (!(delta > 0.0)) { st->done = 2; return; }
+    st->alpha = gamma / delta;
+    st->done = st->maxit == 0 ? 4 : 0;
+    return;
+  }
+  if (st->done) return;
+  const int it = st->it + 1;
+  st->it = it;
+  st->gamma = eps;
+  hist[it] = g;
+  if (!(g == g)) { st->done = 3; st->iters = it; return; }
+  if (g <= st->tol) { st->done = 1; st->iters = it; return; }
+  const double beta = gamma / st->rho_old;
+  const double den = delta - beta * gamma / st->alpha;
+  if (!(den > 0.0)) { st->done = 2; st->iters = it; return; }
+  st->beta = beta;
+  st->alpha = gamma / den;
+  st->rho_old = gamma;
+  if (it >= st->maxit) { st->done = 4; st->iters = it; }
+}
+
 // start of a cycle: beta = sqrt(norm2); converged if beta <= tol
 __global__ void gm_start_kernel(GmresState* gs, PcgState* st, double* hist) {
   if (st->done) return;
@@ -468,6 +577,28 @@ cudaError_t launch_maxpy_mdot(int64_t n, double* y, const double* V, int64_t ldv
   else
     dev::maxpy_mdot_kernel<32><<<g, dev::kKT, 0, s>>>(n, y, V, ldv, K, coef, mult, part, ticket,
                                                       out, done);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgcg_init(int64_t n, const double* b, const double* dinv, const uint8_t* mult,
+                             double* x, double* r, double* u, double* p, double* s, double* part,
+                             unsigned* ticket, double* out2, int num_sms, cudaStream_t st) {
+  dev::cgcg_init_kernel<<<kgrid(n, num_sms), dev::kKT, 0, st>>>(n, b, dinv, mult, x, r, u, p, s,
+                                                                part, ticket, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgcg_update(int64_t n, const double* dinv, const uint8_t* mult, double* u,
+                               const double* w, double* p, double* s, double* x, double* r,
+                               double* part, unsigned* ticket, double* out2, const PcgState* ps,
+                               int num_sms, cudaStream_t st) {
+  dev::cgcg_update_kernel<<<kgrid(n / 2 + 1, num_sms), dev::kKT, 0, st>>>(
+      n, dinv, mult, u, w, p, s, x, r, part, ticket, out2, ps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgcg_scalar(int stage, PcgState* ps, double* hist, cudaStream_t st) {
+  dev::cgcg_scalar_kernel<<<1, 1, 0, st>>>(stage, ps, hist);
   return cudaGetLastError();
 }
 

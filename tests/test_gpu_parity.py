@@ -466,3 +466,33 @@ def test_gs_update_fusion(spec, N):
             out.append(c.pcg_history())
         k = min(len(out[0]), len(out[1]), 10)
         np.testing.assert_allclose(out[0][:k], out[1][:k], rtol=1e-9)
+
+
+@pytest.mark.parametrize("spec,N", [(CONFIGS["C1"][0], 3), (tgv_box(4, 3, 5, deform=1), 7),
+                                    (unit_box(3, 2, 5, periodic=(1, 0, 0)), 5), (tgv_box(2, 2, 2), 1),
+                                    (unit_box(3, 1, 3), 4)])
+def test_pcg_single_reduction_parity(spec, N):
+    """SEM_OPT_PCG_VARIANT = 1 (Chronopoulos-Gear, reading Q34) against the
+    oracle's single-reduction PCG: iterations +-1, x and residuals within 1e-10;
+    also the Helmholtz operator through the same recurrences."""
+    o = O.Oracle(spec, N)
+    fun = f_tgv if all(spec.periodic) else f_sin
+    b = o.rhs(fun(o.get("X"), o.get("Y"), o.get("Z")))
+    ref = o.cgcg(b, 1e-10, 3000)
+    with sem().sem_setup(spec, N) as c:
+        c.set_pcg_variant("single_reduction")
+        x = c.zeros()
+        r = c.pcg_solve(dev(b), x, 1e-10, 3000)
+        assert r["status"] == 0 and abs(r["iters"] - ref["iters"]) <= 1, (r, ref["iters"])
+        assert np.abs(host(x) - ref["x"]).max() <= 1e-10
+        assert abs(r["res_true"] - ref["res_true"]) <= 1e-10
+        h = c.pcg_history()
+        k = min(len(h), len(ref["hist"]), 6)
+        np.testing.assert_allclose(h[:k], ref["hist"][:k], rtol=1e-8, atol=1e-12 * ref["hist"][0])
+        h1, h2 = 1.0 / 1600.0, 2000.0
+        bh = o.rhs_mass(fun(o.get("X"), o.get("Y"), o.get("Z")))
+        refh = o.helm_pcg(h1, h2, bh, 1e-10, 2000)
+        xh = c.zeros()
+        rh = c.helm_pcg_solve(h1, h2, dev(bh), xh, 1e-10, 2000)
+        assert rh["status"] == 0 and abs(rh["iters"] - refh["iters"]) <= 1, (rh, refh["iters"])
+        assert np.abs(host(xh) - refh["x"]).max() <= 1e-10

@@ -64,6 +64,11 @@ def main():
                 c.rhs(fv, b)
                 x = c.zeros()
                 r = c.pcg_solve(b, x, 1e-10, 3000)
+                # single-reduction (Chronopoulos-Gear) PCG: one allreduce per iteration
+                xc = c.zeros()
+                c.set_pcg_variant("single_reduction")
+                rc_ = c.pcg_solve(b, xc, 1e-10, 3000)
+                c.set_pcg_variant("standard")
                 xg = c.zeros()
                 rg = c.gmres_solve(b, xg, 1e-10, 3000, 20) if not fused else None
                 # NEXT-1: two-level Schwarz (fine gs and the N=1 coarse CG run
@@ -85,7 +90,8 @@ def main():
                 dist.all_gather_object(parts, (w.cpu().numpy(), g.cpu().numpy(), b.cpu().numpy(),
                                                x.cpu().numpy(), r, xg.cpu().numpy(), rg,
                                                zs.cpu().numpy(), xs.cpu().numpy(), rs,
-                                               zs1.cpu().numpy(), xs1.cpu().numpy(), rs1))
+                                               zs1.cpu().numpy(), xs1.cpu().numpy(), rs1,
+                                               xc.cpu().numpy(), rc_))
                 if rank == 0:
                     W = np.concatenate([p[0] for p in parts])
                     Gs = np.concatenate([p[1] for p in parts])
@@ -123,6 +129,12 @@ def main():
                             fails.append(f"{tag}: gmres iters {rg['iters']} vs {refg['iters']}")
                         if not np.abs(Xg - refg["x"]).max() <= 1e-9:
                             fails.append(f"{tag}: gmres x diff {np.abs(Xg - refg['x']).max():.2e}")
+                    refc = o.cgcg(ref_b, 1e-10, 3000)
+                    Xc = np.concatenate([p[13] for p in parts])
+                    if abs(rc_["iters"] - refc["iters"]) > 1 or rc_["status"] != 0:
+                        fails.append(f"{tag}: single-reduction pcg iters {rc_['iters']} vs {refc['iters']}")
+                    if not np.abs(Xc - refc["x"]).max() <= 1e-10:
+                        fails.append(f"{tag}: single-reduction pcg x diff {np.abs(Xc - refc['x']).max():.2e}")
                     if rs is not None:
                         schw = o.schwarz(10)
                         ref_z = schw.apply(B)
