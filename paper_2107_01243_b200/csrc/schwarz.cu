@@ -159,6 +159,17 @@ __global__ void fdm_setup_kernel(int n, int nloc, int64_t e_lo, int ex, int ey, 
   }
 }
 
+// 1/x for the (positive, well-scaled) eigenvalue sums: approximate reciprocal
+// and two Newton steps (within an ulp of 1/x; a division costs ~5x the
+// instructions and a subroutine call on its slow path)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
 // y_e = A~_e^-1 (c^1/2 r)_e (fast diagonalisation) and b0_e = (J^T)^3 (c r)_e;
 // either output may be null.  Skipped when *gate.
 template <int n>
@@ -241,7 +252,7 @@ __global__ void __launch_bounds__(kFT) fdm_kernel(int nloc, const double* __rest
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < n; k++) s = fma(S[2][k * n + c], u[a + n * b + n2 * k], s);
-      t[p] = s / (lam[0][a] + lam[1][b] + lam[2][c]);
+      t[p] = s * rcp_nr(lam[0][a] + lam[1][b] + lam[2][c]);
     }
     __syncthreads();
     // backward: u = Sz t along c, t = Sy u along b, y = Sx t along a
@@ -332,7 +343,9 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
     double* __restrict__ y, double* __restrict__ b0, const int* gate) {
   extern __shared__ double f8smem[];
   if (gate && *gate) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp index broadcast from lane 0: provably warp-uniform, so the element
+  // loop and its mma.sync need no divergence handling
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
   const int g = lane >> 2, q = lane & 3;
   double* U = f8smem + warp * 2 * kF8Buf;
   double* T = U + kF8Buf;
@@ -382,16 +395,14 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
     for (int m = 0; m < 8; m++) {
       U[pad8(i0, j0, m)] = csq[mv[m].x] * rv[m].x;
       U[pad8(i0 + 1, j0, m)] = csq[mv[m].y] * rv[m].y;
-      if (b0) {
+      if (b0) {   // separable: sum over the pair along i first, then weight by J_j J_k
         const double xk = __ldg(&xi[m]);
         const double jk[2] = {0.5 * (1.0 - xk), 0.5 * (1.0 + xk)};
         const double cr0 = cinv[mv[m].x] * rv[m].x, cr1 = cinv[mv[m].y] * rv[m].y;
+        const double si[2] = {fma(ja[0], cr0, jb[0] * cr1), fma(ja[1], cr0, jb[1] * cr1)};
 #pragma unroll
-        for (int v = 0; v < 8; v++) {
-          const double wjk = jj[(v >> 1) & 1] * jk[v >> 2];
-          acc[v] = fma(ja[v & 1] * wjk, cr0, acc[v]);
-          acc[v] = fma(jb[v & 1] * wjk, cr1, acc[v]);
-        }
+        for (int v = 0; v < 8; v++)
+          acc[v] = fma(si[v & 1], jj[(v >> 1) & 1] * jk[v >> 2], acc[v]);
       }
     }
     if (b0) {
@@ -426,8 +437,8 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
              [&](double& d0, double& d1, int s, double x) { dmma884(d0, d1, x, s ? BZ1 : BZ0); },
              [&](int t, double d0, double d1) {
                const double lyt = __ldg(&lx[8 + t]);
-               T[pad8(g, t, 2 * q)] = d0 / (lxg + lyt + lz0);
-               T[pad8(g, t, 2 * q + 1)] = d1 / (lxg + lyt + lz1);
+               T[pad8(g, t, 2 * q)] = d0 * rcp_nr(lxg + lyt + lz0);
+               T[pad8(g, t, 2 * q + 1)] = d1 * rcp_nr(lxg + lyt + lz1);
              });
     __syncwarp();
     // 4. U[a][b][k] = sum_c T[a][b][c] Sz[k][c]
