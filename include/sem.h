@@ -266,6 +266,11 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    vector pass per iteration).  Same iterates in exact arithmetic (DESIGN.md
    reading Q34).  Collective. */
 #define SEM_OPT_PCG_VARIANT 12
+/* 1 (default) = in PCG iterations the Ax kernel alone is launched with
+   programmatic dependent launch and its producer warp streams the first
+   geometric-factor planes before waiting for the preceding kernel; 0 = plain
+   order.  Identical results. */
+#define SEM_OPT_AX_PDL 13
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

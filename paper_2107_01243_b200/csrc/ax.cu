@@ -222,10 +222,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     fence_mbar_init();
   }
   __syncthreads();
-  pdl_wait();   // u (= p) and the done flag come from the preceding kernel
-  pdl_trigger();
-  if ((MODE == AX_PCG || a.gate) && *a.done) return;
-
   const int r0lo = a.r0lo, r0hi = a.r0hi, r1lo = a.r1lo, r1hi = a.r1hi;
   const int ng0 = (r0hi - r0lo + NE - 1) / NE, ng1 = (r1hi - r1lo + NE - 1) / NE, ng = ng0 + ng1;
   auto group = [=](int g, int& e0, int& cnt) {
@@ -237,6 +233,33 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       cnt = min(NE, r1hi - e0);
     }
   };
+  // programmatic dependent launch (a.pdl_pref): G does not depend on the
+  // preceding kernel, so the producer streams the first group's G planes into
+  // the (initially free) ring slots BEFORE waiting for the preceding grid --
+  // the ring fill overlaps that kernel's tail.  Only when the group's planes
+  // fit the ring (no wait on a consumer that itself waits for u).
+  constexpr int kPrefPlanes = (n / PPC <= NSG) ? n / PPC : 0;
+  const bool pref = a.pdl_pref && kPrefPlanes > 0 && blockIdx.x < ng;
+  if (pref && producer && tid == TCW) {
+    int e0, cnt;
+    group(blockIdx.x, e0, cnt);
+    const uint64_t pol = policy_evict_first();
+    const uint32_t bP = PPC * 6u * n2 * 8u;
+    for (int kb = 0; kb < kPrefPlanes; kb++) {
+      mbar_arrive_expect_tx(&fullG[kb], bP * (uint32_t)cnt);
+      for (int x = 0; x < cnt; x++)
+        bulk_g2s_hint(sG + kb * Sh::gslot + x * PPC * 6 * n2,
+                      a.G + ((size_t)(e0 + x) * n + kb * PPC) * 6 * n2, bP, &fullG[kb], pol);
+    }
+  }
+  pdl_wait();   // u (= p) and the done flag come from the preceding kernel
+  pdl_trigger();
+  if ((MODE == AX_PCG || a.gate) && *a.done) {
+    // no bulk copy may still target this CTA's shared memory when it exits
+    if (pref && producer && tid == TCW)
+      for (int kb = 0; kb < kPrefPlanes; kb++) mbar_wait(&fullG[kb], 0u);
+    return;
+  }
 
   double acc = 0.0;  // sigma partial (AX_PCG)
 
@@ -246,6 +269,7 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     const uint64_t pol = policy_evict_first();
     int su = 0, sg = 0;
     uint32_t phu = 0, phg = 0;
+    bool first = pref;   // the first group's G planes are already in flight
     for (int g = blockIdx.x; g < ng; g += gridDim.x) {
       int e0, cnt;
       group(g, e0, cnt);
@@ -278,6 +302,10 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       if (++su == NSU) { su = 0; phu ^= 1u; }
       // k-planes of the geometric factors
       for (int kb = 0; kb < n / PPC; kb++) {
+        if (first) {   // prefetched before griddepcontrol.wait
+          if (++sg == NSG) { sg = 0; phg ^= 1u; }
+          continue;
+        }
         mbar_wait(&emptyG[sg], phg ^ 1u);
         if (lane == 0) {
           const uint32_t bP = PPC * 6u * n2 * 8u;
@@ -288,6 +316,7 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
         }
         if (++sg == NSG) { sg = 0; phg ^= 1u; }
       }
+      first = false;
     }
   } else if (gswarp) {
     // ============ gather-scatter warp: last arriver sums shared entities ============

@@ -111,6 +111,8 @@ struct AxLaunch {
   const double* B;
   double h1, h2;
   int gate;                       // 1: any mode returns early when *done (GMRES cycle gate)
+  int pdl_pref;                   // 1: launched with PDL; prefetch the first G planes before
+                                  //    waiting for the preceding grid
 };
 
 // NVLink peer-memory collectives (p2p.cu): mailbox layout and device view

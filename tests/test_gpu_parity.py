@@ -496,3 +496,27 @@ def test_pcg_single_reduction_parity(spec, N):
         rh = c.helm_pcg_solve(h1, h2, dev(bh), xh, 1e-10, 2000)
         assert rh["status"] == 0 and abs(rh["iters"] - refh["iters"]) <= 1, (rh, refh["iters"])
         assert np.abs(host(xh) - refh["x"]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("spec,N", [(CONFIGS["C2"][0], 7), (tgv_box(4, 3, 5, deform=1), 7),
+                                    (unit_box(3, 2, 5, periodic=(1, 0, 0)), 5)])
+def test_ax_pdl_identical(spec, N):
+    """SEM_OPT_AX_PDL (PDL launch of the PCG Ax kernel, G prefetched before the
+    grid wait) gives bit-identical PCG iterates."""
+    o = O.Oracle(spec, N) if spec.E <= 64 else None
+    n = spec.E * (N + 1) ** 3
+    b = random_field(n, seed=21)
+    with sem().sem_setup(spec, N) as c:
+        bd = c.zeros()
+        c.apply(dev(b), bd)          # an assembled, masked right-hand side
+        out = []
+        for on in (False, True, False, True):
+            c.set_ax_pdl(on)
+            x = c.zeros()
+            r = c.pcg_solve(bd, x, 0.0, 25)
+            out.append((host(x), r["res_final"]))
+        assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+        assert np.array_equal(out[1][0], out[3][0])
+        if o is not None:
+            ref = o.pcg(host(bd), 0.0, 25)
+            assert np.abs(out[1][0] - ref["x"]).max() <= 1e-10 * max(1.0, np.abs(ref["x"]).max())
