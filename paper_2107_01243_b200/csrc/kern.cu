@@ -367,11 +367,11 @@ __global__ void __launch_bounds__(kThreads) gs_update_kernel(const DevPlan P,
   pdl_wait();
   pdl_trigger();
   if (st->done) return;
-  if (threadIdx.x < 32) {   // sigma = the Ax kernel's per-CTA partials in a fixed order
+  {   // sigma = the Ax kernel's per-CTA partials in a fixed order (as cg_update)
     const int G = *sig_count;
     double v = 0.0;
-    for (int b = threadIdx.x; b < G; b += 32) v += sig_part[b];
-    v = warp_sum(v);
+    for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(&sig_part[b]);
+    v = block_sum(v, scratch);
     if (threadIdx.x == 0) s_sig = v;
   }
   __syncthreads();
@@ -513,14 +513,15 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
     sigma = s_sig;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->sigma = sigma;
   } else if (sig_part) {
-    // sigma = sum of the Ax kernel's per-CTA partials, in a fixed order
-    if (threadIdx.x < 32) {
-      const int G = *sig_count;
-      double v = 0.0;
-      for (int b = threadIdx.x; b < G; b += 32) v += sig_part[b];
-      v = warp_sum(v);
-      if (threadIdx.x == 0) s_sig = v;
-    }
+    // sigma = sum of the Ax kernel's per-CTA partials in a fixed order (the same
+    // in every block).  All threads load (<= 3 partials each, issued together):
+    // one warp walking ~600 partials put ~5 dependent L2 round trips in front
+    // of every block's streaming loop.
+    const int G = *sig_count;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(&sig_part[b]);
+    v = block_sum(v, scratch);
+    if (threadIdx.x == 0) s_sig = v;
     __syncthreads();
     sigma = s_sig;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->sigma = sigma;

@@ -90,7 +90,16 @@ __device__ __forceinline__ void publish_sigma(const P2P& c, PcgState* st, int np
   if (sig_part) {   // the Ax kernel's per-CTA partials
     const int G = *sig_count;
     double v = 0.0;
-    for (int b = threadIdx.x; b < G; b += 32) v += sig_part[b];
+    for (int b0 = threadIdx.x; b0 < G; b0 += 32 * 8) {   // 8 loads in flight per lane
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int b = b0 + 32 * u;
+        t[u] = b < G ? __ldcg(&sig_part[b]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) v += t[u];
+    }
     sg = warp_sum(v);
   } else {
     sg = st->sigma_part[0];
