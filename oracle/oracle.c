@@ -1236,7 +1236,7 @@ int oracle_schwarz_pcg(const oracle_schwarz* s, const double* b, double* x, doub
   if (!s || maxit < 0) return -1;
   const oracle_ctx* c = s->c;
   const int64_t ns = c->nslots;
-  double* r = (double*)malloc(sizeof(double) * ns);
+  double* r = (double*)calloc(ns, sizeof(double));
   double* z = (double*)malloc(sizeof(double) * ns);
   double* p = (double*)malloc(sizeof(double) * ns);
   double* w = (double*)malloc(sizeof(double) * ns);
