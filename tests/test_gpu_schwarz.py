@@ -256,3 +256,39 @@ def test_variants_identical(spec, N):
         ref = s.apply(r)
         for key, (z, x, it) in out.items():
             assert nrel(z, ref) <= 1e-11, (key, nrel(z, ref))
+
+
+def test_edge_cases_all_solvers():
+    """Zero right-hand side (0 iterations, x = 0), maxit = 0 (not converged),
+    aliasing and bad arguments rejected, for flexible PCG, flexible GMRES,
+    the single-reduction PCG and the projection pipeline."""
+    spec, N = CONFIGS["C1"]
+    o = O.Oracle(spec, N)
+    b = dev(_rhs(o))
+    S = sem()
+    with S.sem_setup(spec, N) as c:
+        for setup in (lambda: c.set_precond("schwarz"),
+                      lambda: (c.set_precond("jacobi"), c.set_pcg_variant("single_reduction"))):
+            setup()
+            for solve in (lambda bb, x, m: c.pcg_solve(bb, x, 1e-10, m),
+                          lambda bb, x, m: c.gmres_solve(bb, x, 1e-10, m, 30)):
+                x = c.zeros()
+                r = solve(c.zeros(), x, 100)
+                assert r["iters"] == 0 and r["status"] == 0, r
+                assert float(x.abs().max()) == 0.0
+                x = c.zeros()
+                r = solve(b, x, 0)
+                assert r["iters"] == 0 and r["status"] == 1, r
+            with pytest.raises(S.SemError):
+                c.pcg_solve(b, b, 1e-10, 10)
+        c.set_pcg_variant("standard")
+        c.set_precond("schwarz")
+        with pytest.raises(S.SemError):
+            c.schwarz_apply(b, b)
+        with pytest.raises(S.SemError):
+            c.schwarz_apply(b, c.zeros(), 4)
+        with pytest.raises(S.SemError):
+            c.set_coarse_replicate(2)
+        x = c.zeros()
+        r = c.proj_solve(c.zeros(), x, 1e-10, 100, 30, 20)
+        assert r["status"] == 0 and r["iters"] == 0
