@@ -477,3 +477,62 @@ def test_tgv_pressure_periodic_convergence():
         errs.append(np.abs(x - p_tgv(X, Y, Z)).max())
     assert errs[0] / errs[1] > 10 and errs[1] / errs[2] > 10, errs
     assert errs[-1] < 1e-5
+
+
+def _analytic_metric(spec, N, xi, w):
+    """Closed-form G and B of the sinusoidal map (reading Q4) at the GLL nodes.
+
+    x_a(r) = X_a + (L_a / 2 pi) amp sin(Xh) sin(Yh) sin(Zh), X_a linear in r_a
+    with dX_a/dr_a = h_a / 2.  The exact Jacobian M_ab = dx_a/dr_b is written out
+    from that formula (no derivative matrix, no interpolation), then
+    G_ab = J w w w sum_m (M^-1)_am (M^-1)_bm and B = J w w w.
+    """
+    ex, ey, ez = spec.ex, spec.ey, spec.ez
+    lo = np.array([spec.x0, spec.y0, spec.z0])
+    L = np.array([spec.x1 - spec.x0, spec.y1 - spec.y0, spec.z1 - spec.z0])
+    h = L / np.array([ex, ey, ez])
+    amp = spec.deform_amp
+    n = N + 1
+    Gs, Bs = [], []
+    for e in range(ex * ey * ez):
+        eidx = np.array([e % ex, (e // ex) % ey, e // (ex * ey)])
+        for k in range(n):
+            for j in range(n):
+                for i in range(n):
+                    X = lo + h * (eidx + 0.5 * (np.array([xi[i], xi[j], xi[k]]) + 1.0))
+                    th = 2 * math.pi * (X - lo) / L
+                    s, c = np.sin(th), np.cos(th)
+                    grad = amp * np.array([c[0] * s[1] * s[2], s[0] * c[1] * s[2],
+                                           s[0] * s[1] * c[2]])   # d dlt / d theta_b
+                    # dx_a/dX_b = delta_ab + (L_a/2pi) grad_b (2pi/L_b); dX_b/dr_b = h_b/2
+                    M = (np.eye(3) + np.outer(L, grad / L)) * (h / 2)[None, :]
+                    J = np.linalg.det(M)
+                    R = np.linalg.inv(M)        # R[b][a] = dr_b/dx_a
+                    wq = w[i] * w[j] * w[k]
+                    g = J * wq * (R @ R.T)
+                    Gs.append([g[0, 0], g[1, 1], g[2, 2], g[0, 1], g[0, 2], g[1, 2]])
+                    Bs.append(J * wq)
+    G = np.array(Gs).reshape(-1, n ** 3, 6).transpose(0, 2, 1)
+    return G, np.array(Bs)
+
+
+def test_deformed_metric_converges_to_closed_form():
+    """Isoparametric G/B (D applied to the node coordinates) converge spectrally
+    to the exact metric of the sinusoidal map.  Pins every deformed-mesh G
+    entry, cross factors included: a transposed inverse, a dropped term of the
+    cofactor expansion or a swapped factor pair leaves an O(1) error that does
+    not decay with N."""
+    spec = tgv_box(2, 2, 2, deform=1)
+    errs = []
+    for N in (3, 5, 7, 9, 11):
+        o = O.Oracle(spec, N)
+        xi, w = O.gll(N)
+        Ga, Ba = _analytic_metric(spec, N, xi, w)
+        G = o.get("G").reshape(o.E, 6, (N + 1) ** 3)
+        B = o.get("B")
+        # scale-free: error relative to the largest entry at this N
+        eg = np.abs(G - Ga).max() / np.abs(Ga).max()
+        eb = np.abs(B - Ba).max() / np.abs(Ba).max()
+        errs.append(max(eg, eb))
+    assert all(b < a / 5 for a, b in zip(errs, errs[1:])), errs
+    assert errs[-1] < 1e-8, errs
