@@ -39,9 +39,10 @@ struct AxCfg;
 #endif
 // PPC: k-planes per bulk copy (divides n).  n=8 tuned with tools/ubench_ax.cu
 // on B200 (NSG=3, PPC=4: 6.2 TB/s on 32^3 elements); n=7, 9, 11, 12 with
-// tools/measure.py sweep over build variants (profiles/r01_measure.md); the
-// others follow the rule of ~2 copies per element and a 2-3 slot ring within
-// ~60 KB of smem.
+// tools/measure.py sweep over build variants (profiles/r01_measure.md); n=2, 3,
+// 5, 6, 10 likewise (profiles/r01d_ax_tuning: NE filling whole warps wins for
+// small n); n=4 follows the rule of ~2 copies per element and a 2-3 slot ring
+// within ~60 KB of smem.
 #ifndef SEM_AX8_NE
 #define SEM_AX8_NE 1
 #endif
@@ -51,11 +52,55 @@ struct AxCfg;
 #ifndef SEM_AX8_PPC
 #define SEM_AX8_PPC 4
 #endif
-template <> struct AxCfg<2> { static constexpr int NE = 16, NSG = 3, PPC = 2; };
-template <> struct AxCfg<3> { static constexpr int NE = 8, NSG = 3, PPC = 3; };
+#ifndef SEM_AX2_NE
+#define SEM_AX2_NE 32
+#endif
+#ifndef SEM_AX2_NSG
+#define SEM_AX2_NSG 3
+#endif
+#ifndef SEM_AX2_PPC
+#define SEM_AX2_PPC 2
+#endif
+template <> struct AxCfg<2> {
+  static constexpr int NE = SEM_AX2_NE, NSG = SEM_AX2_NSG, PPC = SEM_AX2_PPC;
+};
+#ifndef SEM_AX3_NE
+#define SEM_AX3_NE 14
+#endif
+#ifndef SEM_AX3_NSG
+#define SEM_AX3_NSG 3
+#endif
+#ifndef SEM_AX3_PPC
+#define SEM_AX3_PPC 3
+#endif
+template <> struct AxCfg<3> {
+  static constexpr int NE = SEM_AX3_NE, NSG = SEM_AX3_NSG, PPC = SEM_AX3_PPC;
+};
 template <> struct AxCfg<4> { static constexpr int NE = 4, NSG = 3, PPC = 2; };
-template <> struct AxCfg<5> { static constexpr int NE = 2, NSG = 3, PPC = 5; };
-template <> struct AxCfg<6> { static constexpr int NE = 2, NSG = 3, PPC = 3; };
+#ifndef SEM_AX5_NE
+#define SEM_AX5_NE 5
+#endif
+#ifndef SEM_AX5_NSG
+#define SEM_AX5_NSG 3
+#endif
+#ifndef SEM_AX5_PPC
+#define SEM_AX5_PPC 5
+#endif
+template <> struct AxCfg<5> {
+  static constexpr int NE = SEM_AX5_NE, NSG = SEM_AX5_NSG, PPC = SEM_AX5_PPC;
+};
+#ifndef SEM_AX6_NE
+#define SEM_AX6_NE 2
+#endif
+#ifndef SEM_AX6_NSG
+#define SEM_AX6_NSG 3
+#endif
+#ifndef SEM_AX6_PPC
+#define SEM_AX6_PPC 3
+#endif
+template <> struct AxCfg<6> {
+  static constexpr int NE = SEM_AX6_NE, NSG = SEM_AX6_NSG, PPC = SEM_AX6_PPC;
+};
 #ifndef SEM_AX7_NE
 #define SEM_AX7_NE 2
 #endif
@@ -78,7 +123,13 @@ template <> struct AxCfg<8> {
 #define SEM_AX9_PPC 1
 #endif
 template <> struct AxCfg<9> { static constexpr int NE = 1, NSG = SEM_AX9_NSG, PPC = SEM_AX9_PPC; };
-template <> struct AxCfg<10> { static constexpr int NE = 1, NSG = 3, PPC = 5; };
+#ifndef SEM_AX10_NSG
+#define SEM_AX10_NSG 4
+#endif
+#ifndef SEM_AX10_PPC
+#define SEM_AX10_PPC 2
+#endif
+template <> struct AxCfg<10> { static constexpr int NE = 1, NSG = SEM_AX10_NSG, PPC = SEM_AX10_PPC; };
 #ifndef SEM_AX11_NSG
 #define SEM_AX11_NSG 6
 #endif
@@ -121,7 +172,11 @@ struct AxShape {
   static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
   // n >= 7 (and the gs warp): keep 168 registers per thread -- the contraction
   // state does not fit fewer without spilling, which costs far more than residency
-  static constexpr int MINBR = (GS || n >= 7) ? 65536 / (T * 168) : 8;
+#ifndef SEM_AX10_REGS
+#define SEM_AX10_REGS 168
+#endif
+  static constexpr int kRegs = (n == 10 && !GS) ? SEM_AX10_REGS : 168;
+  static constexpr int MINBR = (GS || n >= 7) ? 65536 / (T * kRegs) : 8;
   static constexpr int MINB1 = MINB0 < MINBR ? MINB0 : MINBR;
   static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > 8 ? 8 : MINB1);
 };
