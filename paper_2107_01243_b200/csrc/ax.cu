@@ -102,7 +102,7 @@ template <> struct AxCfg<6> {
   static constexpr int NE = SEM_AX6_NE, NSG = SEM_AX6_NSG, PPC = SEM_AX6_PPC;
 };
 #ifndef SEM_AX7_NE
-#define SEM_AX7_NE 2
+#define SEM_AX7_NE 3
 #endif
 #ifndef SEM_AX7_NSG
 #define SEM_AX7_NSG 6
@@ -122,7 +122,10 @@ template <> struct AxCfg<8> {
 #ifndef SEM_AX9_PPC
 #define SEM_AX9_PPC 1
 #endif
-template <> struct AxCfg<9> { static constexpr int NE = 1, NSG = SEM_AX9_NSG, PPC = SEM_AX9_PPC; };
+#ifndef SEM_AX9_NE
+#define SEM_AX9_NE 1
+#endif
+template <> struct AxCfg<9> { static constexpr int NE = SEM_AX9_NE, NSG = SEM_AX9_NSG, PPC = SEM_AX9_PPC; };
 #ifndef SEM_AX10_NSG
 #define SEM_AX10_NSG 4
 #endif
