@@ -7,14 +7,19 @@ the NVLink peer-memory exchange of shared entities, Alg. 1, and the allreduce),
 the r update with <r,z>_c and <r,r>_c, the convergence test and the x and p
 updates.
 
-Workload (BASELINE.json configs[1]): the 8192-element Cartesian box (32x16x16
-elements, N=7, all 6 geometric factors stored and streamed, BP5 convention)
-per GPU; with N GPUs the box is stacked N times along z and partitioned into
-z-slabs (weak scaling, one slab of 8192 elements per GPU).
+Workload (BASELINE.json configs[1], default --config C2): the 8192-element
+Cartesian box (32x16x16 elements, N=7, all 6 geometric factors stored and
+streamed, BP5 convention) per GPU; with N GPUs the box is stacked N times
+along z and partitioned into z-slabs (weak scaling, one slab of 8192 elements
+per GPU).  --config C4 is the strong-scaling workload (BASELINE configs[3]:
+the 64^3-element deformed mesh split over the N GPUs).  At N=1 the line also
+carries the north-star Ax+gs number on C3 (BASELINE configs[2], working set
+>> L2, rotating operands).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sem|reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...
 
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run (one rank per GPU, rendezvous on 127.0.0.1).
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -34,7 +39,6 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 Ax+gather-scatter GDOF/s and PCG iter/s at 1-8 B200; % HBM roofline"
 UNIT = "GDOF/s"
 E2E_ITERS = 20   # PCG iterations per end-to-end call (one host solve of b -> x)
-FUSED = False    # operator variant timed (SEM_OPT_FUSED_GS); both are reported under ax_gs
 
 
 def parse():
@@ -43,16 +47,38 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="sem", choices=["sem", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C2", "C3"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 Ax+gs block (N=1)")
     return ap.parse_args()
 
 
+def strong(cfg):
+    """C4 (BASELINE configs[3]) is the strong-scaling workload: fixed total mesh."""
+    return cfg == "C4"
+
+
 def workload(cfg, P):
+    """(mesh of the whole job, N, mesh per GPU at N=1)."""
     from sem_inputs import CONFIGS, weak_scaled
     spec, N = CONFIGS[cfg]
-    return weak_scaled(spec, P), N, spec
+    return (spec if strong(cfg) else weak_scaled(spec, P)), N, spec
+
+
+def relaunch(args):
+    """--gpus N > 1 without a torchrun environment: start N ranks ourselves."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.run(cmd, env=env).returncode
 
 
 def bytes_model(N):
@@ -152,7 +178,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    spec_g, N, spec1 = workload(args.config, 1)
+    _, N, spec1 = workload(args.config, 1)
+    if strong(args.config):   # per-GPU share of the strong-scaling mesh
+        from dataclasses import replace
+        ezp = max(1, spec1.ez // max(args.gpus, 1))
+        spec1 = replace(spec1, ez=ezp, z1=spec1.z0 + (spec1.z1 - spec1.z0) * ezp / spec1.ez)
     from dataclasses import replace
     # bounded sample: shrink the z extent so K+W oracle iterations stay ~minutes
     probe = replace(spec1, ez=2, z1=spec1.z0 + (spec1.z1 - spec1.z0) * 2 / spec1.ez)
@@ -176,9 +206,10 @@ def run_reference(args):
             f"-element slice of the {args.config} box, N={N}, {o.nslots} slots")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong" if strong(args.config) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU, N={N}",
+            "config": {"workload": workload_desc(args.config, args.gpus),
                        "step": "one Jacobi-PCG iteration"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle",
                              "sample": desc},
@@ -188,9 +219,76 @@ def run_reference(args):
     return 0
 
 
+def workload_desc(cfg, P):
+    from sem_inputs import CONFIGS
+    spec1, N = CONFIGS[cfg]
+    if strong(cfg):
+        return (f"{cfg}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements in total (strong scaling, "
+                f"z-slabs over {P} GPU(s)), N={N}, periodic, deformed (a={spec1.deform_amp})")
+    return (f"{cfg}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU (box stacked x{P} along z), "
+            f"N={N}, periodic, all 6 G stored")
+
+
+def time_applies(ctx, sets, reps, stream, barrier, max_over_ranks):
+    """sem_apply over rotating (u, w) operand sets; returns ms per apply and the
+    per-kernel split (Ax+mask, gs) from the context's CUDA-event timers."""
+    import torch
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for q in range(3):
+        u, w = sets[q % len(sets)]
+        ctx.apply(u, w)
+    barrier()
+    ev0.record(stream)
+    for q in range(reps):
+        u, w = sets[q % len(sets)]
+        ctx.apply(u, w)
+    ev1.record(stream)
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1)) / reps
+    ctx.timing(True)
+    for q in range(reps):
+        u, w = sets[q % len(sets)]
+        ctx.apply(u, w)
+    ax_ms, ax_n = ctx.timing_read(0)
+    gs_ms, gs_n = ctx.timing_read(4)
+    ctx.timing(False)
+    return ms, ax_ms / max(ax_n, 1), gs_ms / max(gs_n, 1)
+
+
+def c3_block(sem, stream, barrier, peak, reps):
+    """North-star number: fp64 Ax+gs on C3 (32^3 elements, N=7,
+    u and w 134 MB each), two rotating (u, w) sets so no operand is reused
+    while L2-resident (P:L355, P:L361 cold-cache Q)."""
+    import torch
+    from sem_inputs import CONFIGS
+    spec, N = CONFIGS["C3"]
+    ctx = sem.sem_setup(spec, N, stream=stream.cuda_stream)
+    nl = ctx.n_local
+    sets = []
+    for q in range(2):
+        u = torch.empty(nl, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        sets.append((u, ctx.zeros()))
+    ms, ax_ms, gs_ms = time_applies(ctx, sets, reps, stream, barrier, lambda v: v)
+    bm = bytes_model(N)
+    out = {"workload": "C3: 32x32x32 elements, N=7, (0,2pi)^3 periodic; 2 rotating (u, w) sets "
+                       "(536 MB of operands + 805 MB G >> 126 MB L2)",
+           "n_p": nl, "gdofs": nl / (ms / 1e3) / 1e9, "ms": ms,
+           "bytes_per_pt": bm["ax_gs"],
+           "frac_of_8TBps": nl * bm["ax_gs"] / (ms / 1e3) / 8e12,
+           "frac_of_measured": nl * bm["ax_gs"] / (ms / 1e3) / 1e9 / peak,
+           "ax_ms": ax_ms, "gs_ms": gs_ms,
+           "ax_frac_of_measured": nl * 64.0 / (ax_ms / 1e3) / 1e9 / peak,
+           "gs_frac_of_measured": nl * 20.0 * bm["f_b"] / (gs_ms / 1e3) / 1e9 / peak}
+    del sets
+    ctx.close()
+    return out
+
+
 # --------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "sem":
+        return relaunch(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -226,7 +324,6 @@ def main():
         comm = sem.nccl_comm_init(uid[0], rank, P)
     stream = torch.cuda.current_stream()
     ctx = sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm, stream=stream.cuda_stream)
-    ctx.set_fused_gs(FUSED)
     nl = ctx.n_local
     n_p_total = nl * P
 
@@ -285,7 +382,7 @@ def main():
     k_avg = max_over_ranks(k_ms / n_apply)
     bm = bytes_model(N)
     peak, peak_src = peaks()
-    kbytes = bm["ax_gs"] if FUSED else bm["ax"]
+    kbytes = bm["ax"]
     achieved = nl * kbytes / (k_avg / 1e3) / 1e9
     traffic = None
     try:
@@ -297,29 +394,22 @@ def main():
     except Exception:
         pass
 
-    # ---- Ax+gs alone (sem_apply, both variants), and Ax alone, K repetitions each
-    u_rand = torch.empty(nl, dtype=torch.float64, device="cuda").uniform_(-1, 1)
-    w = ctx.zeros()
-    apply_ms = {}
-    for fused in (True, False):
-        ctx.set_fused_gs(fused)
-        for _ in range(3):
-            ctx.apply(u_rand, w)
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            ctx.apply(u_rand, w)
-        ev1.record(stream)
-        barrier()
-        apply_ms[fused] = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
-    ctx.set_fused_gs(FUSED)
+    # ---- Ax+gs alone (sem_apply) over 4 rotating (u, w) sets (268 MB/GPU of
+    # operands > L2 at C2), and Ax alone, K repetitions each
+    sets = []
+    for q in range(4):
+        u = torch.empty(nl, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        sets.append((u, ctx.zeros()))
+    apply_ms, apply_ax_ms, apply_gs_ms = time_applies(ctx, sets, args.steps, stream, barrier,
+                                                      max_over_ranks)
     ev0.record(stream)
-    for _ in range(args.steps):
-        ctx.ax(u_rand, w)
+    for q in range(args.steps):
+        u, w = sets[q % 4]
+        ctx.ax(u, w)
     ev1.record(stream)
     barrier()
     ax_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
-    del u_rand, w
+    del sets
 
     # ---- end to end through the C ABI with HOST buffers (pinned), per step:
     # H2D of b, E2E_ITERS PCG iterations, D2H of x
@@ -353,44 +443,48 @@ def main():
                           f"iterations on a {sample.ex}x{sample.ey}x{sample.ez}-element slice of "
                           f"the {args.config} box, N={N} ({r['n_p']} slots), {r['seconds']:.1f} s")}
 
+    c3 = None
+    if P == 1 and not args.no_c3 and args.config == "C2":
+        c3 = c3_block(sem, stream, barrier, peak, max(args.steps, 20))
+
     if rank == 0:
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if strong(args.config) else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": (f"{args.config}: {spec1.ex}x{spec1.ey}x{spec1.ez} elements per GPU "
-                             f"(box stacked x{P} along z), N={N}, periodic, all 6 G stored"),
+                "workload": workload_desc(args.config, P),
                 "N": N, "elements": spec.E, "n_p": n_p_total, "n_glob": ctx.n_glob,
-                "step": ("one Jacobi-PCG iteration (Ax+mask+<p,Ap>, gs [+ NVLink exchange], "
-                         "r update+dots, x/p update)") if P > 1 else
-                        ("one Jacobi-PCG iteration (Ax+mask+<p,Ap>; gs fused with the r update "
-                         "and dots; x/p update)"),
-                "l2": "no flush: per-iteration working set ~370 MB/GPU > 126 MB L2",
+                "step": ("one Jacobi-PCG iteration: Ax+mask+<p,Ap> kernel, gather-scatter "
+                         "kernel" + (" with the NVLink peer-memory exchange and allreduce"
+                                     if P > 1 else "") +
+                         ", r update + <r,z>_c, <r,r>_c kernel, x/p update kernel"),
+                "l2": (f"no flush: per-iteration working set {nl * 104 / 1e6:.0f} MB/GPU "
+                       "(G, u, w, r, p, x, dinv) > 126 MB L2"),
                 "parallelism": (f"element z-slabs x{P}, NVLink peer-memory gs exchange + "
                                 "allreduce (CUDA IPC)") if P > 1 else "single GPU",
             },
             "pcg_iter_per_s": args.steps / (t_ms / 1e3),
-            "ax_gs": {
-                variant: {"gdofs": n_p_total / (apply_ms[f] / 1e3) / 1e9, "ms": apply_ms[f],
-                          "frac_of_8TBps": nl * bm["ax_gs"] / (apply_ms[f] / 1e3) / 8e12,
-                          "frac_of_measured": nl * bm["ax_gs"] / (apply_ms[f] / 1e3) / 1e9 / peak}
-                for variant, f in (("fused", True), ("two_kernel", False))},
+            "ax_gs": {"gdofs": n_p_total / (apply_ms / 1e3) / 1e9, "ms": apply_ms,
+                      "frac_of_8TBps": nl * bm["ax_gs"] / (apply_ms / 1e3) / 8e12,
+                      "frac_of_measured": nl * bm["ax_gs"] / (apply_ms / 1e3) / 1e9 / peak,
+                      "ax_ms": apply_ax_ms, "gs_ms": apply_gs_ms,
+                      "operands": "4 rotating (u, w) sets"},
+            "ax_gs_c3": c3,
             "ax_only": {"gdofs": n_p_total / (ax_ms / 1e3) / 1e9, "ms": ax_ms,
                         "gbs_64B_per_pt": nl * 64 / (ax_ms / 1e3) / 1e9},
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (f"ax_kernel<{N + 1},AX_PCG,fused={FUSED}> "
-                           + ("(Ax+gs+mask+sigma)" if FUSED else "(Ax+mask+sigma)")),
+                "kernel": f"ax_kernel<{N + 1},AX_PCG> (Ax+mask+sigma)",
                 "bytes_per_pt": kbytes, "hbm_mandatory_bytes_per_pt": 64.0,
                 "avg_ms_per_apply": k_avg, "launches": k_cnt, "applies": n_apply,
                 "peak_source": peak_src,
                 "step_share": k_ms / max(k_ms + u_ms + p_ms + g_ms, 1e-9),
-                "other_kernels_ms_per_step": {"gs": g_ms / n_apply,
-                                              ("gs_update" if g_cnt == 0 else "cg_update"):
-                                                  u_ms / max(u_cnt, 1),
+                "other_kernels_ms_per_step": {"gs": g_ms / max(g_cnt, 1),
+                                              "cg_update": u_ms / max(u_cnt, 1),
                                               "cg_p": p_ms / max(p_cnt, 1)},
             },
             "cpu_baseline": cpu,

@@ -54,7 +54,8 @@ typedef struct {
                                          box rescaled to (0,2pi)^3 (reading Q4) */
   double deform_amp;                  /* a */
   int32_t rank, nranks;               /* this process and the element partition size */
-  void* nccl_comm;                    /* ncclComm_t for nranks > 1 (see sem_nccl_*), else NULL */
+  void* nccl_comm;                    /* nranks > 1: ncclComm_t (sem_nccl_*) or a loopback
+                                         handle (sem_loopback_comm); else NULL */
   void* stream;                       /* cudaStream_t all work is ordered on (NULL = legacy) */
 } sem_mesh;
 
@@ -63,8 +64,11 @@ typedef struct {
    coordinates and the six geometric factors G = J w_i w_j w_k (dr/dx)(dr/dx)^T
    and mass B = J w_i w_j w_k (reading Q5) on the device, the gather-scatter plan
    (element-local entities summed on this GPU, entities shared with
-   other ranks exchanged over NCCL), the Dirichlet mask and the Jacobi inverse
-   diagonal (reading Q14).  Collective, blocking.  N in 1..11. */
+   other ranks exchanged through the multi-rank transport -- NVLink peer memory
+   by default, NCCL, or the single-device loopback of sem_loopback_*), the
+   Dirichlet mask and the Jacobi inverse diagonal (reading Q14).  Collective,
+   blocking.  N in 1..11.  For nranks > 1, nccl_comm is an ncclComm_t
+   (sem_nccl_comm_init) or a loopback handle (sem_loopback_comm). */
 int sem_setup(const sem_mesh* m, int N, sem_ctx** out);
 int sem_destroy(sem_ctx* c);
 /* n_local = local slots, e_local = local elements, n_glob = unique global DOF */
@@ -75,8 +79,11 @@ int sem_sizes(const sem_ctx* c, int64_t* n_local, int64_t* e_local, int64_t* n_g
    sem_gs:    u_L <- Q Q^T u_L in place (Eq. 10), sum over all slots
               sharing a global number, in ascending slot order within a rank and
               ascending rank order across ranks (reading Q10).  Collective.
-   sem_apply: w = mask(Q Q^T A_L u) -- the CG operator, fused in one
-              kernel pass plus the overlapped NCCL exchange (Alg. 1).  Collective.
+   sem_apply: w = mask(Q Q^T A_L u) -- the CG operator: the Ax kernel
+              (mask in its epilogue), then the gather-scatter kernel; at
+              nranks > 1 the shared partials travel through the transport
+              (one peer-memory exchange kernel, or Alg. 1's overlapped
+              pack / send-recv / unpack).  Collective.
    u and w must not alias. */
 int sem_ax(sem_ctx* c, const double* u, double* w);
 int sem_gs(sem_ctx* c, double* u);
@@ -95,12 +102,14 @@ int sem_coords(sem_ctx* c, double* X, double* Y, double* Z);
    recursive residual, res_true = sqrt(<b - A x, b - A x>_c) computed once at the
    end.  Returns SEM_OK, SEM_NOT_CONVERGED or an error.  Collective, blocking.
    sem_pcg_solve takes device b, x; sem_pcg_solve_host takes HOST b, x and does
-   the host<->device copies itself (end-to-end entry point). */
+   the host<->device copies itself (end-to-end entry point); both run the
+   preconditioner selected by SEM_OPT_PRECOND (Jacobi, or flexible PCG with
+   the two-level Schwarz preconditioner). */
 typedef struct {
-  int32_t iters;
-  int32_t status;
-  double res_final;
-  double res_true;
+  int32_t iters;      /* applications of A in the loop (reading Q16) */
+  double res_final;   /* recursive residual sqrt(<r,r>_c) at exit */
+  double res_true;    /* sqrt(<b - A x, b - A x>_c), one extra A at the end (Q17) */
+  int32_t status;     /* SEM_OK, SEM_NOT_CONVERGED or an error code */
 } sem_pcg_result;
 int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                   sem_pcg_result* res);
@@ -186,6 +195,22 @@ int sem_nccl_unique_id(uint8_t id[128]);
 int sem_nccl_comm_init(const uint8_t id[128], int rank, int nranks, void** comm);
 int sem_nccl_comm_destroy(void* comm);
 
+/* ---- loopback multi-rank transport (tests on ONE device) ----
+   P rank contexts in one process on one GPU, each driven by its own host
+   thread with its own stream.  sem_loopback_create makes a world of nranks
+   ranks; sem_loopback_comm returns rank r's handle, passed as
+   sem_mesh.nccl_comm with rank = r, nranks = P.  Every collective runs the
+   NCCL transport's path (pack, neighbour exchange, unpack with ascending-rank
+   sums; allreduces summed in ascending rank order) with device copies and
+   host barriers instead of NCCL; the peer-memory transport is not used.
+   flags & 1: process neighbours in reverse order and delay each rank's
+   arrival randomly (completion order changes, results must not).  A rank
+   that does not reach a collective within flags >> 8 seconds (0: 120 s)
+   makes it fail with SEM_ENCCL on the ranks that did.  Destroy the world after every context using it. */
+int sem_loopback_create(int nranks, int flags, void** world);
+int sem_loopback_comm(void* world, int rank, void** comm);
+int sem_loopback_destroy(void* world);
+
 /* ---- instrumentation ----
    sem_timing(c, 1) records CUDA events on the context stream around every
    launch of kernel class `which` (0 = Ax kernel of apply/PCG, 1 = CG
@@ -210,11 +235,10 @@ int sem_debug_read(sem_ctx* c, int which, int64_t* out, int n);
    while an exchange with that peer is in flight.  Both block. */
 int sem_p2p_pingpong(sem_ctx* c, int peer, int iters, int64_t* rtt_ns);
 int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps);
-/* Operator variants (both compute the same w; results are bit-identical):
-   SEM_OPT_FUSED_GS = 1 -> gather-scatter fused into the Ax kernel (last
-   arriver per face/edge/vertex sums it); 0 (default) -> Ax kernel with the
-   mask in its epilogue followed by one gather-scatter kernel. */
-#define SEM_OPT_FUSED_GS 1
+/* Option numbers 1 (fused Ax+gs kernel), 5 (programmatic dependent launch of
+   every PCG kernel) and 10 (gs fused with the CG update) are retired: those
+   variants were measured slower than the default path and
+   removed; setting them returns SEM_EINVAL. */
 /* Multi-GPU transport of the hot path (nranks > 1): 1 (default) = NVLink peer
    memory (CUDA-IPC mailboxes, see p2p.cu), 0 = NCCL send/recv + allreduce.
    Falls back to NCCL automatically if peer memory cannot be mapped. */
@@ -228,10 +252,6 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    by the blocks (each element's w streamed from HBM about once).  Auto picks
    2 when w exceeds 64 MB. */
 #define SEM_OPT_GS_MODE 4
-/* 1 (default) = the PCG iteration kernels are launched with programmatic
-   dependent launch (each kernel's launch and prologue overlap the previous
-   kernel's tail); 0 = plain stream order.  Results are identical. */
-#define SEM_OPT_PDL 5
 /* Preconditioner of sem_pcg_solve / sem_gmres_solve / sem_proj_solve:
    SEM_PRECOND_JACOBI (default) or SEM_PRECOND_SCHWARZ (NEXT-1; setting it
    builds the Schwarz preconditioner: collective, blocking). */
@@ -246,12 +266,6 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
 /* 1 (default) = at N = 7 the Schwarz local solves run their six 8x8
    contractions on the fp64 tensor cores (DMMA m8n8k4); 0 = CUDA-core kernel */
 #define SEM_OPT_FDM_TC 9
-/* 1 = on one rank, when the gather-scatter runs the flat schedule (w
-   L2-resident), each PCG iteration fuses the gather-scatter of A p with the
-   r update and the two dots (one pass; dots per unique point); 0 (default) =
-   separate gather-scatter and update kernels (measured faster on C2: 123 vs
-   133 us per iteration).  Same iterates up to summation order. */
-#define SEM_OPT_GS_UPDATE 10
 /* Schwarz coarse level at nranks > 1: 0 = distributed over the ranks (each
    coarse CG step exchanges and allreduces), 1 = replicated (one all-gather of
    the restricted right-hand side, then every rank solves the whole N = 1

@@ -35,8 +35,8 @@ class SemMesh(C.Structure):
 
 
 class PcgResult(C.Structure):
-    _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("res_final", C.c_double),
-                ("res_true", C.c_double)]
+    _fields_ = [("iters", C.c_int32), ("res_final", C.c_double), ("res_true", C.c_double),
+                ("status", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -77,6 +77,9 @@ _SIGS = {
     "sem_nccl_unique_id": [_P],
     "sem_nccl_comm_init": [_P, C.c_int, C.c_int, C.POINTER(_P)],
     "sem_nccl_comm_destroy": [_P],
+    "sem_loopback_create": [C.c_int, C.c_int, C.POINTER(_P)],
+    "sem_loopback_comm": [_P, C.c_int, C.POINTER(_P)],
+    "sem_loopback_destroy": [_P],
     "sem_timing": [_P, C.c_int],
     "sem_timing_read": [_P, C.c_int, C.POINTER(C.c_double), _I64P],
     "sem_launch_count": [_P, _I64P],
@@ -266,10 +269,6 @@ class Context:
         """Jacobi-PCG recurrences: 'standard' or 'single_reduction' (Chronopoulos-Gear)."""
         _check(load().sem_set_option(self._h, 12, {"standard": 0, "single_reduction": 1}[kind]))
 
-    def set_gs_update(self, on: bool):
-        """One rank, flat gs: fuse the PCG gather-scatter with the r update (default off)."""
-        _check(load().sem_set_option(self._h, 10, 1 if on else 0))
-
     def set_fdm_tc(self, on: bool):
         """N = 7 Schwarz local solves on the fp64 tensor cores (default) or CUDA cores."""
         _check(load().sem_set_option(self._h, 9, 1 if on else 0))
@@ -333,8 +332,8 @@ class Context:
         _check(load().sem_timing_read(self._h, which, C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
 
-    def set_fused_gs(self, on: bool):
-        _check(load().sem_set_option(self._h, 1, 1 if on else 0))
+    def _set_option(self, option: int, value: int):
+        _check(load().sem_set_option(self._h, int(option), int(value)))
 
     def set_overlap(self, on: bool):
         """Alg. 1 boundary/interior split of the operator at nranks > 1. Collective."""
@@ -343,10 +342,6 @@ class Context:
     def set_gs_mode(self, mode: int):
         """Gather-scatter schedule: 0 auto, 1 flat, 2 element-ordered chunks."""
         _check(load().sem_set_option(self._h, 4, int(mode)))
-
-    def set_pdl(self, on: bool):
-        """Programmatic dependent launch of the PCG iteration kernels (default on)."""
-        _check(load().sem_set_option(self._h, 5, 1 if on else 0))
 
     def set_p2p(self, on: bool):
         """Multi-GPU transport: NVLink peer memory (default) or NCCL. Collective."""
@@ -460,3 +455,24 @@ def nccl_comm_init(uid: bytes, rank: int, nranks: int):
 
 def nccl_comm_destroy(comm):
     _check(load().sem_nccl_comm_destroy(C.c_void_p(comm)))
+
+
+# ------------------------------------------------------------------ loopback (tests)
+def loopback_create(nranks: int, flags: int = 0):
+    """A loopback world: nranks rank contexts on ONE device, one host thread each
+    (ctypes releases the GIL inside every libsem call).  flags & 1 shuffles the
+    neighbour order and the ranks' arrival times."""
+    w = C.c_void_p()
+    _check(load().sem_loopback_create(int(nranks), int(flags), C.byref(w)))
+    return w.value
+
+
+def loopback_comm(world, rank: int):
+    """Rank `rank`'s handle, passed as nccl_comm to sem_setup."""
+    c = C.c_void_p()
+    _check(load().sem_loopback_comm(C.c_void_p(world), int(rank), C.byref(c)))
+    return c.value
+
+
+def loopback_destroy(world):
+    _check(load().sem_loopback_destroy(C.c_void_p(world)))

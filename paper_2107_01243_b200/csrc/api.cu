@@ -1,15 +1,24 @@
 // C ABI of libsem (include/sem.h): context setup, the hot-path entry points
-// (sem_ax, sem_gs, sem_apply, sem_pcg_solve) and the NCCL plumbing.
+// (sem_ax, sem_gs, sem_apply, sem_pcg_solve, ...) and the multi-rank plumbing.
 //
-// Multi-GPU (Alg. 1, P:L367 allreduce): one process per GPU; the
-// element range of this rank is split into boundary elements (incident to an
-// entity shared with another rank) and interior elements.  sem_apply runs the
-// fused Ax+gs kernel on the boundary elements, packs the shared partials,
-// exchanges them with ncclSend/ncclRecv on a communication stream while the
-// interior elements are processed, then adds the partials in ascending rank
-// order and scatters.  The CG inner products are reduced with ncclAllReduce on
-// device-resident scalars (two per iteration); the host never synchronises
-// inside an iteration and polls a device "done" flag every kBatch iterations.
+// The operator w = mask(QQ^T A_L u) is two kernels: the Ax kernel (ax.cu; mask
+// and the CG sigma partials in its epilogue) and the gather-scatter kernel
+// (kern.cu / gs_dev.cuh).  Multi-GPU (Alg. 1, P:L367 allreduce):
+// one process per GPU, three transports for the entities shared with other
+// ranks and for the CG inner products, all summing in ascending rank order:
+//   * NVLink peer memory (default): ONE exchange kernel (p2p.cu) packs this
+//     rank's partials straight into the neighbours' IPC-mapped receive
+//     records, runs the rank-local gs while they travel and unpacks; the
+//     allreduces are mailbox publishes fused into the CG kernels;
+//   * NCCL (SEM_OPT_P2P = 0, or when peer mapping fails): Alg. 1 with Ax on
+//     the boundary elements, pack, ncclSend/ncclRecv on a communication stream
+//     overlapped with Ax on the interior elements and the local gs, unpack;
+//     ncclAllReduce for the dots;
+//   * loopback (sem_loopback_*; tests): P rank contexts on ONE device in one
+//     process, the NCCL transport's pack / copy / unpack and rank-ordered
+//     reductions with device copies instead of NCCL (loopback.cu).
+// The host never synchronises inside a CG iteration: scalars stay on the
+// device and the host polls a "done" flag every kBatch iterations.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -74,6 +83,7 @@ struct sem_ctx {
   int dev = 0, num_sms = 148;
   cudaStream_t stream = nullptr, comm = nullptr;
   ncclComm_t nccl = nullptr;
+  sem::LoopComm* loop = nullptr;   // loopback transport (tests), else NCCL / peer memory
   // device data
   double *d_xi = nullptr, *d_w = nullptr, *d_D = nullptr, *d_G = nullptr, *d_B = nullptr,
          *d_dinv = nullptr;
@@ -86,7 +96,6 @@ struct sem_ctx {
   unsigned long long* d_gsctr = nullptr;   // gs chunk counters (never reset)
   uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
   int gs_mode = 0;                         // SEM_OPT_GS_MODE
-  bool use_pdl = false;                    // SEM_OPT_PDL (measured slower)
   // NEXT-3: GMRES work space, projection space
   const int* ax_gate = nullptr;            // Ax early-exit flag of GMRES Arnoldi steps
   double *d_V = nullptr, *d_gt = nullptr, *d_kpart = nullptr;
@@ -119,8 +128,6 @@ struct sem_ctx {
   bool ax_pdl = true;      // SEM_OPT_AX_PDL (C2: 123.0 -> 121.6 us per PCG iteration)
   bool ax_pdl_now = false; // set around the PCG iteration's Ax launch
   int pcg_variant = 0;     // SEM_OPT_PCG_VARIANT: 0 standard, 1 single-reduction (Chronopoulos-Gear)
-  bool gs_update = false;  // SEM_OPT_GS_UPDATE: one rank, flat gs -> gs + CG update fused
-                           // (measured slower on C2: 133 vs 123 us per iteration)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
   cudaGraphExec_t g0exec = nullptr;
   int g0_iters = -1;
@@ -158,7 +165,6 @@ struct sem_ctx {
   int64_t t_cnt[kTimerClasses] = {};
   bool overlap = false;  // SEM_OPT_OVERLAP: Alg. 1 boundary/interior split (measured slower
                          // on NVLink: the exchange is ~200 KB, the split costs a launch)
-  bool fuse_gs = false;   // SEM_OPT_FUSED_GS
   // NVLink peer-memory transport (nranks > 1)
   bool p2p_ok = false, use_p2p = true;
   sem::P2P p2p;
@@ -239,10 +245,20 @@ int check(cudaError_t e, const char* what) {
   return SEM_OK;
 }
 
-// ---- the operator ----------------------------------------------------------
-// the fused Ax+gs operator is in use (the Helmholtz variant is two-kernel only)
-bool fused(const sem_ctx* c) { return c->fuse_gs && !c->helm; }
+// ---- collectives: NCCL, or the loopback transport (loopback.cu)
+int coll_allreduce(sem_ctx* c, const double* in, double* out, size_t count, cudaStream_t s) {
+  if (c->loop) return sem::loop_allreduce(c->loop, in, out, count, s);
+  NCCL_TRY(ncclAllReduce(in, out, count, ncclDouble, ncclSum, c->nccl, s));
+  return SEM_OK;
+}
 
+int coll_allgather(sem_ctx* c, const double* in, double* out, size_t count, cudaStream_t s) {
+  if (c->loop) return sem::loop_allgather(c->loop, in, out, count * sizeof(double), s);
+  NCCL_TRY(ncclAllGather(in, out, count, ncclDouble, c->nccl, s));
+  return SEM_OK;
+}
+
+// ---- the operator ----------------------------------------------------------
 int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi, int r1lo,
            int r1hi, double* red_out) {
   sem::AxLaunch a{};
@@ -268,7 +284,7 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   const bool pdl = c->ax_pdl_now && !c->timing && !sem::pdl_on();
   a.pdl_pref = pdl ? 1 : 0;
   if (pdl) sem::set_pdl(true);
-  cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream, fused(c),
+  cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream,
                                  c->helm && mode != sem::AX_ONLY);
   if (pdl) sem::set_pdl(false);
   timer_end(c, tk);
@@ -280,6 +296,12 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
 int exchange(sem_ctx* c) {
   CUDA_TRY(cudaEventRecord(c->ev_pack, c->stream));
   CUDA_TRY(cudaStreamWaitEvent(c->comm, c->ev_pack, 0));
+  if (c->loop) {
+    SEM_TRY(sem::loop_sendrecv(c->loop, c->d_send, c->d_recv, c->hp.nbr_rank, c->hp.nbr_off,
+                               c->hp.nbr_cnt, c->comm));
+    CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm));
+    return SEM_OK;
+  }
   NCCL_TRY(ncclGroupStart());
   for (size_t q = 0; q < c->hp.nbr_rank.size(); q++) {
     const int peer = c->hp.nbr_rank[q];
@@ -292,10 +314,9 @@ int exchange(sem_ctx* c) {
   return SEM_OK;
 }
 
-// rank-local gather-scatter pass of the two-kernel operator (masked slots are
-// already zero, so every masked entity point sums to zero)
+// rank-local gather-scatter pass of the operator (masked slots are already
+// zero, so every masked entity point sums to zero)
 int gs_pass(sem_ctx* c, double* w) {
-  if (fused(c)) return SEM_OK;
   int tk = timer_begin(c, 4);
   cudaError_t e = sem::launch_gs_local(c->dp, w, 0, &c->gs_base[0], c->gs_mode, c->stream);
   timer_end(c, tk);
@@ -317,15 +338,14 @@ int allreduce_site(sem_ctx* c, int site, const double* loc, double* glob, int K)
     c->launches += 2;
     return SEM_OK;
   }
-  NCCL_TRY(ncclAllReduce(loc, glob, K, ncclDouble, ncclSum, c->nccl, c->stream));
-  return SEM_OK;
+  return coll_allreduce(c, loc, glob, (size_t)K, c->stream);
 }
 
 // w = mask(QQ^T A_L u) (mode AX_APPLY) or the same plus sigma (AX_PCG)
 int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   const sem::HostPlan& h = c->hp;
   sem::PcgState* st = c->d_st;
-  if (h.nranks > 1 && h.nS > 0 && p2p(c) && !fused(c) && !c->overlap) {
+  if (h.nranks > 1 && h.nS > 0 && p2p(c) && !c->overlap) {
     // one Ax launch, then ONE exchange kernel: pack into the neighbours'
     // receive buffers, rank-local gs while the partials travel, unpack
     const uint64_t e = ++c->ep_gs;
@@ -400,8 +420,7 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   CUDA_TRY(sem::launch_gs_unpack(c->dp, w, c->d_part, c->d_recv, 1,
                                  mode == sem::AX_PCG ? st : nullptr, nparts, c->stream));
   c->launches++;
-  if (mode == sem::AX_PCG)
-    NCCL_TRY(ncclAllReduce(&st->loc[2], &st->sigma, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+  if (mode == sem::AX_PCG) SEM_TRY(coll_allreduce(c, &st->loc[2], &st->sigma, 1, c->stream));
   return SEM_OK;
 }
 
@@ -430,8 +449,7 @@ int gs_op(sem_ctx* c, double* u, int apply_mask) {
 }
 
 int allreduce(sem_ctx* c, double* p, size_t count) {
-  if (c->hp.nranks > 1)
-    NCCL_TRY(ncclAllReduce(p, p, count, ncclDouble, ncclSum, c->nccl, c->stream));
+  if (c->hp.nranks > 1) return coll_allreduce(c, p, p, count, c->stream);
   return SEM_OK;
 }
 
@@ -439,8 +457,7 @@ int allreduce(sem_ctx* c, double* p, size_t count) {
 // to repeat (kernels of converged iterations are no-ops but the collectives
 // still run, re-reducing the same partials)
 int allreduce_to(sem_ctx* c, const double* loc, double* glob, size_t count) {
-  if (c->hp.nranks > 1)
-    NCCL_TRY(ncclAllReduce(loc, glob, count, ncclDouble, ncclSum, c->nccl, c->stream));
+  if (c->hp.nranks > 1) return coll_allreduce(c, loc, glob, count, c->stream);
   return SEM_OK;
 }
 
@@ -499,10 +516,15 @@ int p2p_setup(sem_ctx* c) {
       sem::P2P::kRecvOff + (size_t)std::max<int64_t>(h.nbuf + 1, sem::P2P::kMinRecv) * 2 * 16;
   SEM_TRY(dalloc(&c->d_mbox, bytes));
   CUDA_TRY(cudaMemsetAsync(c->d_mbox, 0, bytes, s));
+  // a rank that cannot export its mailbox still runs every collective below
+  // (with a zeroed handle), so all ranks reach the agreement allreduce and
+  // fall back to NCCL together
+  bool ok = true;
   cudaIpcMemHandle_t mine;
   if (cudaIpcGetMemHandle(&mine, c->d_mbox) != cudaSuccess) {
     cudaGetLastError();
-    return SEM_OK;
+    std::memset(&mine, 0, sizeof(mine));
+    ok = false;
   }
   char* dh = nullptr;
   SEM_TRY(dalloc(&dh, (size_t)64 * (P + 1)));
@@ -523,8 +545,7 @@ int p2p_setup(sem_ctx* c) {
   cudaFree(dh);
   cudaFree(doff);
   std::vector<char*> peers(P, nullptr);
-  bool ok = true;
-  for (int q = 0; q < P; q++) {
+  for (int q = 0; q < P && ok; q++) {
     if (q == me) { peers[q] = c->d_mbox; continue; }
     void* ptr = nullptr;
     if (cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
@@ -596,8 +617,16 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   if (st != SEM_OK) { delete c; return st; }
   const sem::HostPlan& h = c->hp;
   c->stream = static_cast<cudaStream_t>(m->stream);
-  c->nccl = static_cast<ncclComm_t>(m->nccl_comm);
   auto fail = [&](int s) { free_ctx(c); return s; };
+  c->loop = sem::loop_lookup(m->nccl_comm);
+  if (c->loop) {
+    if (sem::loop_rank(c->loop) != m->rank || sem::loop_size(c->loop) != m->nranks) {
+      sem::set_error("loopback communicator rank/size differ from the mesh's rank/nranks");
+      return fail(SEM_EINVAL);
+    }
+  } else {
+    c->nccl = static_cast<ncclComm_t>(m->nccl_comm);
+  }
 #define SETUP_TRY(expr)             \
   do {                              \
     int _s = (expr);                \
@@ -680,7 +709,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_CUDA(cudaMemsetAsync(c->d_tickets, 0, 8 * sizeof(unsigned), s));
   SETUP_TRY(dalloc(&c->d_scal, 8));
 
-  if (h.nranks > 1) SETUP_TRY(p2p_setup(c));
+  if (h.nranks > 1 && !c->loop) SETUP_TRY(p2p_setup(c));   // loopback: device copies only
   c->dp.s_rank = c->d_srank;
 
   // geometry on the device
@@ -698,10 +727,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   if (h.nranks > 1) {
     double flag = bad ? 1.0 : 0.0;
     SETUP_CUDA(cudaMemcpyAsync(c->d_scal, &flag, sizeof(double), cudaMemcpyHostToDevice, s));
-    if (ncclAllReduce(c->d_scal, c->d_scal, 1, ncclDouble, ncclSum, c->nccl, s) != ncclSuccess) {
-      sem::set_error("ncclAllReduce in setup failed");
-      return fail(SEM_ENCCL);
-    }
+    SETUP_TRY(coll_allreduce(c, c->d_scal, c->d_scal, 1, s));
     SETUP_CUDA(cudaMemcpyAsync(&flag, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, s));
     SETUP_CUDA(cudaStreamSynchronize(s));
     bad = flag > 0.0;
@@ -814,20 +840,6 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
 static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const PcgCtl& k) {
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
-  if (c->gs_update && c->hp.nranks == 1 && !fused(c) && sem::gs_flat(c->dp, c->gs_mode)) {
-    // Ax (+ sigma partials), then gather-scatter and update fused in one pass
-    SEM_TRY(run_ax(c, c->d_p, c->d_wv, sem::AX_PCG, 0, (int)c->hp.nloc, 0, 0, nullptr));
-    int tk = timer_begin(c, 1);
-    CUDA_TRY(sem::launch_gs_update(c->dp, dinv, c->d_r, c->d_wv, c->d_partial, st, k.rg_out,
-                                   c->d_partial_ax, c->d_nsig, s));
-    timer_end(c, tk);
-    tk = timer_begin(c, 2);
-    CUDA_TRY(sem::launch_cg_p(c->dp, dinv, c->d_r, c->d_p, x, st, c->d_hist, sem::PeerSync{},
-                              c->red_grid, s));
-    timer_end(c, tk);
-    c->launches += 2;
-    return SEM_OK;
-  }
   c->ax_pdl_now = c->ax_pdl;
   const int sa = apply_op(c, c->d_p, c->d_wv, sem::AX_PCG);
   c->ax_pdl_now = false;
@@ -926,7 +938,7 @@ static int cgcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t 
   CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
   auto op = [&]() -> int {   // w = A u and delta = <w, u>
     GateScope g(c, done);
-    if (!dist && !fused(c)) {
+    if (!dist) {
       SEM_TRY(run_ax(c, u, w, sem::AX_PCG, 0, (int)h.nloc, 0, 0, &st->cg3[2]));
       SEM_TRY(gs_pass(c, w));
     } else {
@@ -979,10 +991,6 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   PcgCtl k;
   SEM_TRY(pcg_enqueue_init(c, dinv, b, x, &k));
   int done = 0;
-  struct PdlScope {   // programmatic dependent launch for the iteration kernels
-    explicit PdlScope(bool on) { sem::set_pdl(on); }
-    ~PdlScope() { sem::set_pdl(false); }
-  } pdl_scope(c->use_pdl && !c->timing);   // per-kernel event timers need plain order
   for (int it = 0; it < maxit && !done; it += kBatch) {
     const int nb = std::min(kBatch, maxit - it);
     for (int q = 0; q < nb; q++) SEM_TRY(pcg_enqueue_iter(c, dinv, x, k));
@@ -991,7 +999,6 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
     CUDA_TRY(cudaEventSynchronize(c->ev_poll));
     done = c->h_st->done;
   }
-  sem::set_pdl(false);
   return pcg_finish(c, b, x, res);
 }
 
@@ -1170,7 +1177,7 @@ static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, cons
   if (y) SEM_TRY(gs_op(c, y, 0));
   if (b0) {
     if (c->c0_repl)   // in place: every rank's restricted block -> the whole b0
-      NCCL_TRY(ncclAllGather(b0, c->d_b0, (size_t)h.nloc * 8, ncclDouble, c->nccl, s));
+      SEM_TRY(coll_allgather(c, b0, c->d_b0, (size_t)h.nloc * 8, s));
     SEM_TRY(coarse_solve(c, gate));
   }
   sem::PcgState* st = c->d_st;
@@ -1227,7 +1234,7 @@ static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, i
   for (int it = 0; it < maxit && !hd; it += kBatch) {
     const int nb = std::min(kBatch, maxit - it);
     for (int q = 0; q < nb; q++) {
-      if (!dist && !fused(c)) {
+      if (!dist) {
         // w = A p with sigma = sum_l p_l (A_L p)_l reduced by the Ax kernel itself
         // (reading Q23: equals <p, w>_c for the continuous, masked p)
         GateScope g(c, done);
@@ -1271,17 +1278,23 @@ extern "C" int sem_schwarz_apply(sem_ctx* c, const double* r, double* z, int32_t
   return schwarz_apply(c, r, z, which, nullptr, nullptr);
 }
 
+// the preconditioner selected by SEM_OPT_PRECOND (sem_pcg_solve and sem_pcg_solve_host)
+static int pcg_dispatch(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
+                        sem_pcg_result* res) {
+  if (c->precond == SEM_PRECOND_SCHWARZ) {
+    SEM_TRY(schwarz_setup(c));
+    return schwarz_pcg_run(c, b, x, tol, maxit, res);
+  }
+  return pcg_run(c, b, x, tol, maxit, res);
+}
+
 extern "C" int sem_pcg_solve(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                              sem_pcg_result* res) {
   if (!c || !b || !x || !aligned16(b) || !aligned16(x) || b == x) {
     sem::set_error("sem_pcg_solve: bad arguments");
     return SEM_EINVAL;
   }
-  if (c->precond == SEM_PRECOND_SCHWARZ) {
-    SEM_TRY(schwarz_setup(c));
-    return schwarz_pcg_run(c, b, x, tol, maxit, res);
-  }
-  return pcg_run(c, b, x, tol, maxit, res);
+  return pcg_dispatch(c, b, x, tol, maxit, res);
 }
 
 // ---------------------------------------------------------------- NEXT-2: Helmholtz
@@ -1633,7 +1646,7 @@ extern "C" int sem_pcg_solve_host(sem_ctx* c, const double* b_host, double* x_ho
   double* db = c->d_tmp;
   double* dx = c->d_tmp + c->ldv;   // 16-byte aligned
   CUDA_TRY(cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, c->stream));
-  int st = pcg_run(c, db, dx, tol, maxit, res);
+  int st = pcg_dispatch(c, db, dx, tol, maxit, res);
   if (st < 0) return st;
   CUDA_TRY(cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1737,18 +1750,15 @@ extern "C" int sem_timing_read(sem_ctx* c, int which, double* total_ms, int64_t*
 
 extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (!c) return SEM_EINVAL;
-  if (option == SEM_OPT_FUSED_GS) {
-    cudaStreamSynchronize(c->stream);
-    c->fuse_gs = value != 0;
-    return SEM_OK;
+  if (option == 1 || option == 5 || option == 10) {
+    // SEM_OPT_FUSED_GS (1), SEM_OPT_PDL (5), SEM_OPT_GS_UPDATE (10): variants
+    // measured slower than the default path in round 1 and removed
+    sem::set_error("sem_set_option: option removed (measured slower variant)");
+    return SEM_EINVAL;
   }
   if (option == SEM_OPT_OVERLAP) {   // collective
     cudaStreamSynchronize(c->stream);
     c->overlap = value != 0;
-    return SEM_OK;
-  }
-  if (option == SEM_OPT_PDL) {
-    c->use_pdl = value != 0;
     return SEM_OK;
   }
   if (option == SEM_OPT_GS_MODE) {
@@ -1786,11 +1796,6 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     }
     cudaStreamSynchronize(c->stream);
     c->pcg_variant = value;
-    return SEM_OK;
-  }
-  if (option == SEM_OPT_GS_UPDATE) {
-    cudaStreamSynchronize(c->stream);
-    c->gs_update = value != 0;
     return SEM_OK;
   }
   if (option == SEM_OPT_FDM_TC) {

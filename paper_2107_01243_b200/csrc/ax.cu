@@ -1,6 +1,6 @@
 // Element stiffness operator  w_L = A_L u_L,  A^e = D^T G^e D  (Eq. 9),
-// optionally with the Dirichlet mask, the CG inner product <p, A p>
-// and the gather-scatter QQ^T (Eq. 10) fused in.
+// optionally with the Dirichlet mask and the CG inner product <p, A p>
+// fused in; the gather-scatter QQ^T (Eq. 10) follows in kern.cu.
 //
 // Design, sm_100a, fp64 on the CUDA cores (the
 // contraction is HBM-bound: 1.7 flop/B at N=7, far below the fp64 ridge):
@@ -15,12 +15,10 @@
 //    t-direction accumulation live in registers; the r and s contractions read
 //    shared memory (padded D and padded w_r/w_s scratch avoid bank conflicts);
 //  * epilogue: mask (per-thread precomputed bits), sigma = sum_l p_l (A_L p)_l
-//    (= p^T A p for a continuous p vanishing on Dirichlet slots), store w;
-//  * FUSE: after storing w_e the compute warps "arrive" on each face / edge /
-//    vertex entity of their elements (one atomic ticket per entity per call);
-//    the last arriver sums the entity's slots in ascending slot order (reading
-//    Q10) while they are L2-resident and resets the ticket.  Otherwise a
-//    separate gather-scatter kernel (kern.cu) follows.
+//    (= p^T A p for a continuous p vanishing on Dirichlet slots), store w.
+//    (A variant with the gather-scatter fused in -- the last CTA to finish an
+//    element of a shared face/edge/vertex summing it -- was measured ~3x
+//    slower than the separate gather-scatter kernel and was removed.)
 #include <algorithm>
 
 #include "dev_common.cuh"
@@ -142,7 +140,7 @@ template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = SEM_AX11_NSG, 
 #endif
 template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = SEM_AX12_NSG, PPC = 3; };
 
-template <int n, bool GS = false>
+template <int n>
 struct AxShape {
   static constexpr int NE = AxCfg<n>::NE, NSG = AxCfg<n>::NSG, PPC = AxCfg<n>::PPC;
   static_assert(n % PPC == 0, "planes per copy must divide n");
@@ -150,8 +148,7 @@ struct AxShape {
   static constexpr int TC = NE * n2;               // computing threads
   static constexpr int TCW = (TC + 31) / 32 * 32;  // compute warps x 32
   static constexpr int NWC = TCW / 32;             // compute warps
-  static constexpr int T = TCW + 32 + (GS ? 32 : 0);  // + producer warp (+ gather-scatter warp)
-  static constexpr int NSD = 4;                    // element-done ring (compute -> gs warp)
+  static constexpr int T = TCW + 32;               // + producer warp
   static constexpr int NSU = 2;                    // u ring depth
   static constexpr bool kBulkU = (n % 2) == 0;     // u block 16-B aligned for any element
   // doubles per u slot (odd n: +2 so the 16-B aligned body can be shifted by one
@@ -165,30 +162,22 @@ struct AxShape {
   static constexpr int wpl = n * rp;               // padded plane pitch
   static constexpr int wel = n * wpl;              // per element
   static constexpr int dpad = n + 1;
-  static constexpr int kMaxList = NE * kRefsPerElem;
-  static constexpr int nbar = 2 * NSG + 2 * NSU + 2 * NSD;
+  static constexpr int nbar = 2 * NSG + 2 * NSU;
   static constexpr size_t smem_bytes =
       sizeof(double) * ((size_t)NSU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32) +
-      sizeof(uint64_t) * nbar + sizeof(int) * (2 * kMaxList + 8) + SEM_AX_SMEM_PAD;
+      sizeof(uint64_t) * nbar + sizeof(int) * 8 + SEM_AX_SMEM_PAD;
   // CTAs per SM the shared memory allows; the register budget is sized to match
-  // (with the gs warp, at most 168 registers per thread: 65536 / (T * 168) CTAs)
   static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
-  // n >= 7 (and the gs warp): keep 168 registers per thread -- the contraction
+  // n >= 7: keep 168 registers per thread -- the contraction
   // state does not fit fewer without spilling, which costs far more than residency
 #ifndef SEM_AX10_REGS
 #define SEM_AX10_REGS 168
 #endif
-  static constexpr int kRegs = (n == 10 && !GS) ? SEM_AX10_REGS : 168;
-  static constexpr int MINBR = (GS || n >= 7) ? 65536 / (T * kRegs) : 8;
+  static constexpr int kRegs = n == 10 ? SEM_AX10_REGS : 168;
+  static constexpr int MINBR = n >= 7 ? 65536 / (T * kRegs) : 8;
   static constexpr int MINB1 = MINB0 < MINBR ? MINB0 : MINBR;
   static constexpr int MINB = MINB1 < 1 ? 1 : (MINB1 > 8 ? 8 : MINB1);
 };
-
-__device__ __forceinline__ int face_s1(int axis, int n) { return axis == 0 ? n : 1; }
-__device__ __forceinline__ int face_s2(int axis, int n) { return axis == 2 ? n : n * n; }
-__device__ __forceinline__ int edge_stride(int axis, int n) {
-  return axis == 0 ? 1 : (axis == 1 ? n : n * n);
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -200,33 +189,15 @@ __device__ __forceinline__ void compute_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-// Sum one entity point over its incidences (ascending slots), write the total.
-__device__ __forceinline__ void sum_point(double* __restrict__ w, const int32_t* base, int nin,
-                                          int off, bool masked) {
-  double v[8];
-#pragma unroll
-  for (int t = 0; t < 8; t++)
-    if (t < nin) v[t] = __ldcg(&w[base[t] + off]);
-  double s = v[0];
-#pragma unroll
-  for (int t = 1; t < 8; t++)
-    if (t < nin) s += v[t];
-  if (masked) s = 0.0;
-#pragma unroll
-  for (int t = 0; t < 8; t++)
-    if (t < nin) __stcg(&w[base[t] + off], s);
-}
-
-template <int n, int MODE, bool FUSE, bool HELM = false>
-__global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
+template <int n, int MODE, bool HELM = false>
+__global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     ax_kernel(const DevPlan P, const AxLaunch a) {
-  using Sh = AxShape<n, FUSE>;
+  using Sh = AxShape<n>;
   constexpr int NE = Sh::NE, n2 = Sh::n2, n3 = Sh::n3, TCW = Sh::TCW;
-  constexpr int NSG = Sh::NSG, NSU = Sh::NSU, NSD = Sh::NSD, PPC = Sh::PPC;
+  constexpr int NSG = Sh::NSG, NSU = Sh::NSU, PPC = Sh::PPC;
   constexpr int dp = Sh::dpad, rp = Sh::rp, wpl = Sh::wpl;
   constexpr bool kBulkU = Sh::kBulkU;
   constexpr bool kMask = MODE != AX_ONLY;   // Dirichlet mask in the epilogue
-  constexpr bool kGs = kMask && FUSE;         // gather-scatter warp in-kernel
 #ifndef SEM_DREG_MAX
 #define SEM_DREG_MAX 12
 #endif
@@ -248,15 +219,10 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
   uint64_t* emptyG = fullG + NSG;
   uint64_t* fullU = emptyG + NSG;
   uint64_t* emptyU = fullU + NSU;
-  uint64_t* doneE = emptyU + NSU;                      // compute warps -> gs warp
-  uint64_t* freeE = doneE + NSD;                       // gs warp -> compute warps
-  int* s_list = reinterpret_cast<int*>(freeE + NSD);   // gs warp: last-arrived entities
-  int* s_pref = s_list + Sh::kMaxList;                 // gs warp: point-count prefix
-  int* s_misc = s_pref + Sh::kMaxList;                 // [1] last-block flag
+  int* s_misc = reinterpret_cast<int*>(emptyU + NSU);  // [1] last-block flag
 
   const int tid = threadIdx.x;
   const bool producer = tid >= TCW && tid < TCW + 32;
-  const bool gswarp = kGs && tid >= TCW + 32;
 
   for (int q = tid; q < n2; q += Sh::T) {
     const int r = q / n, c = q % n;
@@ -272,10 +238,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     for (int s = 0; s < NSU; s++) {
       mbar_init(&fullU[s], kBulkU ? 1 : 2);
       mbar_init(&emptyU[s], Sh::NWC);
-    }
-    for (int s = 0; s < NSD; s++) {
-      mbar_init(&doneE[s], Sh::NWC);
-      mbar_init(&freeE[s], 1);
     }
     fence_mbar_init();
   }
@@ -376,117 +338,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
       }
       first = false;
     }
-  } else if (gswarp) {
-    // ============ gather-scatter warp: last arriver sums shared entities ============
-    // For each group the compute warps have stored, arrive (acq_rel ticket) on
-    // every face / edge / vertex of its elements; for the entities this CTA
-    // completes, sum the incidences' slots in ascending slot order (reading
-    // Q10) while they are L2-resident and broadcast the sum (0 on Dirichlet
-    // points).  Runs concurrently with the compute warps' next elements.
-    const int lane = tid & 31;
-    constexpr int nf = (n - 2) * (n - 2), ne = n - 2;
-    constexpr int Nm1 = n > 2 ? n - 2 : 1;
-    constexpr int K = 2;   // work items per lane per round (loads issued together)
-    int sd = 0;
-    uint32_t phd = 0;
-    for (int g = blockIdx.x; g < ng; g += gridDim.x) {
-      int e0, cnt;
-      group(g, e0, cnt);
-      mbar_wait(&doneE[sd], phd);
-      int nl = 0;
-      for (int q0 = 0; q0 < cnt * kRefsPerElem; q0 += 32) {
-        const int q = q0 + lane;
-        bool last = false;
-        int ref = -1;
-        if (q < cnt * kRefsPerElem) {
-          ref = P.eref[(size_t)(e0 + q / kRefsPerElem) * kRefsPerElem + q % kRefsPerElem];
-          if (ref >= 0) {
-            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
-            const unsigned nin = cls == CLS_FACE ? 2u : (cls == CLS_EDGE ? P.e_nin[idx] : P.v_nin[idx]);
-            unsigned* tk = P.cnt + (cls == CLS_FACE ? idx : (cls == CLS_EDGE ? P.nF + idx : P.nF + P.nEd + idx));
-            // acq_rel: releases the compute warps' w stores (observed through the
-            // done barrier), acquires the other incidences' stores on the last arrival
-            if (atom_add_acq_rel_gpu(tk, 1u) == nin - 1u) {
-              *tk = 0u;
-              last = true;
-            }
-          }
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, last);
-        if (last) s_list[nl + __popc(m & ((1u << lane) - 1u))] = ref;
-        nl += __popc(m);
-      }
-      __syncwarp();
-      if (lane == 0) {   // point-count prefix over the list
-        int acc_p = 0;
-        for (int q = 0; q < nl; q++) {
-          s_pref[q] = acc_p;
-          const int cls = s_list[q] >> kClsShift;
-          acc_p += cls == CLS_FACE ? nf : (cls == CLS_EDGE ? ne : 1);
-        }
-        s_pref[nl] = acc_p;
-      }
-      __syncwarp();
-      const int tot = nl > 0 ? s_pref[nl] : 0;
-      for (int b = 0; b < tot; b += 32 * K) {
-        int addr[K][8], nins[K];
-        bool mk[K];
-#pragma unroll
-        for (int c = 0; c < K; c++) {
-          const int t = b + c * 32 + lane;
-          nins[c] = 0;
-          mk[c] = false;
-          if (t < tot) {
-            int lo = 0, hi = nl - 1;   // entity with s_pref[q] <= t < s_pref[q+1]
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (s_pref[mid] <= t) lo = mid; else hi = mid - 1;
-            }
-            const int ref = s_list[lo], p = t - s_pref[lo];
-            const int cls = ref >> kClsShift, idx = ref & ((1 << kClsShift) - 1);
-            if (cls == CLS_FACE) {
-              const int ax = P.f_axis[idx];
-              const int off = (1 + p % Nm1) * face_s1(ax, n) + (1 + p / Nm1) * face_s2(ax, n);
-              nins[c] = 2;
-              addr[c][0] = P.f_base[2 * idx] + off;
-              addr[c][1] = P.f_base[2 * idx + 1] + off;
-            } else if (cls == CLS_EDGE) {
-              const int off = (1 + p) * edge_stride(P.e_axis[idx], n);
-              nins[c] = P.e_nin[idx];
-              mk[c] = P.e_mask[idx];
-#pragma unroll
-              for (int x = 0; x < 4; x++) addr[c][x] = P.e_base[4 * idx + x] + off;
-            } else {
-              nins[c] = P.v_nin[idx];
-              mk[c] = P.v_mask[idx];
-#pragma unroll
-              for (int x = 0; x < 8; x++) addr[c][x] = P.v_base[8 * idx + x];
-            }
-          }
-        }
-        double v[K][8];
-#pragma unroll
-        for (int c = 0; c < K; c++)
-#pragma unroll
-          for (int x = 0; x < 8; x++)
-            if (x < nins[c]) v[c][x] = __ldcg(&a.w[addr[c][x]]);
-#pragma unroll
-        for (int c = 0; c < K; c++) {
-          if (nins[c] == 0) continue;
-          double s = v[c][0];
-#pragma unroll
-          for (int x = 1; x < 8; x++)
-            if (x < nins[c]) s += v[c][x];
-          if (mk[c]) s = 0.0;
-#pragma unroll
-          for (int x = 0; x < 8; x++)
-            if (x < nins[c]) __stcg(&a.w[addr[c][x]], s);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&freeE[sd]);
-      if (++sd == NSD) { sd = 0; phd ^= 1u; }
-    }
   } else {
     // ======================= compute warps =======================
     const int el = tid / n2, ij = tid - (tid / n2) * n2;
@@ -497,8 +348,8 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
     // (loaded from shared memory per group, right before the phase that uses
     // them, so rows and columns are never live at the same time)
     double Di[n], Dj[n], Dti[n], Dtj[n];
-    int su = 0, sg = 0, sdc = 0;
-    uint32_t phu = 0, phg = 0, phdc = 0;
+    int su = 0, sg = 0;
+    uint32_t phu = 0, phg = 0;
     for (int g = blockIdx.x; g < ng; g += gridDim.x) {
       int e0, cnt;
       group(g, e0, cnt);
@@ -607,15 +458,6 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
         }
       }
 
-      if (kGs) {
-        // hand the stored group to the gs warp (its ring slot must be free)
-        __syncwarp();   // orders this warp's w stores before lane 0's release
-        if (lane == 0) {
-          mbar_wait(&freeE[sdc], phdc ^ 1u);
-          mbar_arrive(&doneE[sdc]);
-        }
-        if (++sdc == NSD) { sdc = 0; phdc ^= 1u; }
-      }
       compute_sync<TCW>();   // w_r / w_s scratch free for the next group
     }
   }
@@ -635,21 +477,23 @@ __global__ void __launch_bounds__(AxShape<n, FUSE>::T, AxShape<n, FUSE>::MINB)
 }
 
 // persistent launch: grid = min(work groups, resident CTAs x SMs) of this variant
-template <int n, int MODE, bool FUSE, bool HELM>
+template <int n, int MODE, bool HELM>
 static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cudaStream_t s) {
-  using Sh = AxShape<n, FUSE>;
-  auto kern = ax_kernel<n, MODE, FUSE, HELM>;
-  static int resident = 0;
+  using Sh = AxShape<n>;
+  auto kern = ax_kernel<n, MODE, HELM>;
+  static std::atomic<int> cache[kMaxDev];   // resident CTAs on each device
+  const int dev = device_index();
+  int resident = cache[dev].load(std::memory_order_relaxed);
   if (resident == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Sh::smem_bytes);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148, nb = 1;
-    cudaGetDevice(&dev);
+    int sms = 148, nb = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Sh::T, Sh::smem_bytes) != cudaSuccess)
       nb = 1;
     resident = std::max(nb, 1) * sms;
+    cache[dev].store(resident, std::memory_order_relaxed);
   }
   const int grid = std::max(1, std::min(groups, resident));
   return launch_k(kern, dim3(grid), dim3(Sh::T), Sh::smem_bytes, s, P, a);
@@ -657,8 +501,8 @@ static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cud
 
 template <int n, int MODE>
 static int occupancy_n() {
-  using Sh = AxShape<n, false>;
-  auto kern = ax_kernel<n, MODE, false>;
+  using Sh = AxShape<n>;
+  auto kern = ax_kernel<n, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::smem_bytes);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Sh::T, Sh::smem_bytes) != cudaSuccess)
@@ -666,24 +510,24 @@ static int occupancy_n() {
   return std::max(nb, 1);
 }
 
-template <int MODE, bool FUSE, bool HELM = false>
+template <int MODE, bool HELM = false>
 static cudaError_t dispatch(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
 #ifdef SEM_AX_ONLY_N8
-  if (P.n == 8) return launch_n<8, MODE, FUSE, HELM>(P, a, grid, s);
+  if (P.n == 8) return launch_n<8, MODE, HELM>(P, a, grid, s);
   return cudaErrorInvalidValue;
 #endif
   switch (P.n) {
-    case 2: return launch_n<2, MODE, FUSE, HELM>(P, a, grid, s);
-    case 3: return launch_n<3, MODE, FUSE, HELM>(P, a, grid, s);
-    case 4: return launch_n<4, MODE, FUSE, HELM>(P, a, grid, s);
-    case 5: return launch_n<5, MODE, FUSE, HELM>(P, a, grid, s);
-    case 6: return launch_n<6, MODE, FUSE, HELM>(P, a, grid, s);
-    case 7: return launch_n<7, MODE, FUSE, HELM>(P, a, grid, s);
-    case 8: return launch_n<8, MODE, FUSE, HELM>(P, a, grid, s);
-    case 9: return launch_n<9, MODE, FUSE, HELM>(P, a, grid, s);
-    case 10: return launch_n<10, MODE, FUSE, HELM>(P, a, grid, s);
-    case 11: return launch_n<11, MODE, FUSE, HELM>(P, a, grid, s);
-    case 12: return launch_n<12, MODE, FUSE, HELM>(P, a, grid, s);
+    case 2: return launch_n<2, MODE, HELM>(P, a, grid, s);
+    case 3: return launch_n<3, MODE, HELM>(P, a, grid, s);
+    case 4: return launch_n<4, MODE, HELM>(P, a, grid, s);
+    case 5: return launch_n<5, MODE, HELM>(P, a, grid, s);
+    case 6: return launch_n<6, MODE, HELM>(P, a, grid, s);
+    case 7: return launch_n<7, MODE, HELM>(P, a, grid, s);
+    case 8: return launch_n<8, MODE, HELM>(P, a, grid, s);
+    case 9: return launch_n<9, MODE, HELM>(P, a, grid, s);
+    case 10: return launch_n<10, MODE, HELM>(P, a, grid, s);
+    case 11: return launch_n<11, MODE, HELM>(P, a, grid, s);
+    case 12: return launch_n<12, MODE, HELM>(P, a, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -741,19 +585,16 @@ int ax_occupancy(int N, int mode) {
 }
 
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
-                      bool fuse_gs, bool helm) {
+                      bool helm) {
   if (grid < 1) grid = 1;
-  if (helm) {   // Helmholtz: two-kernel operator only
-    if (mode == AX_APPLY) return dev::dispatch<AX_APPLY, false, true>(P, a, grid, s);
-    if (mode == AX_PCG) return dev::dispatch<AX_PCG, false, true>(P, a, grid, s);
+  if (helm) {   // Helmholtz: h1 A + h2 B
+    if (mode == AX_APPLY) return dev::dispatch<AX_APPLY, true>(P, a, grid, s);
+    if (mode == AX_PCG) return dev::dispatch<AX_PCG, true>(P, a, grid, s);
     return cudaErrorInvalidValue;
   }
-  if (mode == AX_ONLY) return dev::dispatch<AX_ONLY, false>(P, a, grid, s);
-  if (mode == AX_APPLY)
-    return fuse_gs ? dev::dispatch<AX_APPLY, true>(P, a, grid, s)
-                   : dev::dispatch<AX_APPLY, false>(P, a, grid, s);
-  return fuse_gs ? dev::dispatch<AX_PCG, true>(P, a, grid, s)
-                 : dev::dispatch<AX_PCG, false>(P, a, grid, s);
+  if (mode == AX_ONLY) return dev::dispatch<AX_ONLY>(P, a, grid, s);
+  if (mode == AX_APPLY) return dev::dispatch<AX_APPLY>(P, a, grid, s);
+  return dev::dispatch<AX_PCG>(P, a, grid, s);
 }
 
 }  // namespace sem

@@ -337,161 +337,6 @@ __global__ void cg_start_kernel(PcgState* st, double* hist, const PeerSync ps) {
   st->iters = 0;
 }
 
-// ---------------------------------------------------------------- fused gs + CG update
-// One rank, w L2-resident (the bench's C2): the gather-scatter of w = A_L p and
-// the CG update r -= alpha QQ^T w in ONE pass.  Every slot is visited once:
-// shared points (faces, edges, vertices: the entity plan) sum their incidences
-// of w in ascending slot order -- the gs kernel's arithmetic -- and write the
-// same r_new = r - alpha s to every incidence; element-interior points update
-// directly; the remaining slots lie on Dirichlet faces (masked, r = w = 0).
-// The dots are taken once per unique point (c weighting is implicit), so
-// rho' and gamma equal the two-kernel path's up to summation order.  Saves
-// the gs kernel's write-back of w and the update's re-reads of w, r, dinv at
-// duplicate slots, and one launch.  sigma comes from the Ax kernel's partials.
-template <int n>
-__global__ void __launch_bounds__(kThreads) gs_update_kernel(const DevPlan P,
-                                                             const double* __restrict__ dinv,
-                                                             double* __restrict__ r,
-                                                             const double* __restrict__ w,
-                                                             double* partial, PcgState* st,
-                                                             double* out2,
-                                                             const double* __restrict__ sig_part,
-                                                             const int* sig_count) {
-  constexpr int N = n - 1;
-  constexpr int nf = (N - 1) * (N - 1), ne = N - 1, ni = (N - 1) * (N - 1) * (N - 1);
-  constexpr int Nm1 = N > 1 ? N - 1 : 1;
-  constexpr int F = 4;
-  __shared__ double scratch[32];
-  __shared__ int flag;
-  __shared__ double s_sig;
-  pdl_wait();
-  pdl_trigger();
-  if (st->done) return;
-  {   // sigma = the Ax kernel's per-CTA partials in a fixed order (as cg_update)
-    const int G = *sig_count;
-    double v = 0.0;
-    for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(&sig_part[b]);
-    v = block_sum(v, scratch);
-    if (threadIdx.x == 0) s_sig = v;
-  }
-  __syncthreads();
-  const double sigma = s_sig;
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->sigma = sigma;
-  const bool ok = sigma > 0.0;
-  const double alpha = ok ? st->rho_old / sigma : 0.0;
-  double rz = 0.0, rr = 0.0;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-  if (ok) {
-    // faces: two incidences
-    const int tF = P.nF * nf;
-    if (nf > 0) {
-      for (int t0 = tid; t0 < tF; t0 += nth * F) {
-        int a0[F], a1[F];
-        bool okq[F];
-#pragma unroll
-        for (int q = 0; q < F; q++) {
-          const int t = t0 + q * nth;
-          okq[q] = t < tF;
-          const int f = okq[q] ? t / (nf > 0 ? nf : 1) : 0;
-          const int pp = t - f * nf;
-          const int ax = P.f_axis[f];
-          const int off = (1 + pp % Nm1) * f_s1(ax, n) + (1 + pp / Nm1) * f_s2(ax, n);
-          const int2 b2 = reinterpret_cast<const int2*>(P.f_base)[f];
-          a0[q] = b2.x + off;
-          a1[q] = b2.y + off;
-        }
-        double v0[F], v1[F], rv[F], dv[F];
-#pragma unroll
-        for (int q = 0; q < F; q++)
-          if (okq[q]) {
-            v0[q] = w[a0[q]];
-            v1[q] = w[a1[q]];
-            rv[q] = r[a0[q]];
-            dv[q] = dinv[a0[q]];
-          }
-#pragma unroll
-        for (int q = 0; q < F; q++)
-          if (okq[q]) {
-            const double rn = fma(-alpha, v0[q] + v1[q], rv[q]);
-            r[a0[q]] = rn;
-            r[a1[q]] = rn;
-            rz = fma(rn, dv[q] * rn, rz);
-            rr = fma(rn, rn, rr);
-          }
-      }
-    }
-    // edges and vertices: up to 8 incidences
-    const int tE = P.nEd * ne, tot = tF + tE + P.nV;
-    for (int t = tF + tid; t < tot; t += nth) {
-      int32_t base[8];
-      int nin, off;
-      if (ne > 0 && t < tF + tE) {
-        const int q = t - tF, e = q / (ne > 0 ? ne : 1);
-        const int pp = q - e * ne;
-        off = (1 + pp) * e_sd(P.e_axis[e], n);
-        nin = P.e_nin[e];
-        const int4 b4 = reinterpret_cast<const int4*>(P.e_base)[e];
-        base[0] = b4.x; base[1] = b4.y; base[2] = b4.z; base[3] = b4.w;
-      } else {
-        const int v = t - tF - tE;
-        off = 0;
-        nin = P.v_nin[v];
-        const int4 b0 = reinterpret_cast<const int4*>(P.v_base)[2 * v];
-        const int4 b1 = reinterpret_cast<const int4*>(P.v_base)[2 * v + 1];
-        base[0] = b0.x; base[1] = b0.y; base[2] = b0.z; base[3] = b0.w;
-        base[4] = b1.x; base[5] = b1.y; base[6] = b1.z; base[7] = b1.w;
-      }
-      double v[8];
-#pragma unroll
-      for (int x = 0; x < 8; x++)
-        if (x < nin) v[x] = w[base[x] + off];
-      const double r0 = r[base[0] + off], d0 = dinv[base[0] + off];
-      double sacc = v[0];
-#pragma unroll
-      for (int x = 1; x < 8; x++)
-        if (x < nin) sacc += v[x];
-      const double rn = fma(-alpha, sacc, r0);
-#pragma unroll
-      for (int x = 0; x < 8; x++)
-        if (x < nin) r[base[x] + off] = rn;
-      rz = fma(rn, d0 * rn, rz);
-      rr = fma(rn, rn, rr);
-    }
-  }
-  if (ok && ni > 0) {
-    // element-interior points (multiplicity 1), one row of N-1 points per thread
-    constexpr int nr = (N - 1) * (N - 1);
-    const int64_t tR = (int64_t)P.nloc * nr;
-    for (int64_t t = tid; t < tR; t += nth) {
-      const int64_t el = t / nr;
-      const int pp = (int)(t - el * nr);
-      const int j = 1 + pp % Nm1, k = 1 + pp / Nm1;
-      const int64_t l0 = el * (n * n * n) + 1 + n * j + n * n * k;
-      double wv[Nm1], rv[Nm1], dv[Nm1];
-#pragma unroll
-      for (int i = 0; i < Nm1; i++) {
-        wv[i] = __ldcs(&w[l0 + i]);
-        rv[i] = __ldcs(&r[l0 + i]);
-        dv[i] = __ldcs(&dinv[l0 + i]);
-      }
-#pragma unroll
-      for (int i = 0; i < Nm1; i++) {
-        const double rn = fma(-alpha, wv[i], rv[i]);
-        __stcg(&r[l0 + i], rn);
-        rz = fma(rn, dv[i] * rn, rz);
-        rr = fma(rn, rn, rr);
-      }
-    }
-  }
-  double v2[2] = {rz, rr};
-  if (grid_reduce<2>(v2, partial, &st->tickets[2], out2, scratch, &flag)) {
-    if (threadIdx.x == 0 && !ok) {
-      st->done = 2;
-      st->iters = st->it + 1;
-    }
-  }
-}
-
 // alpha = rho / sigma; r -= alpha w; partials of rho' = <r, dinv r>_c and
 // gamma = <r, r>_c (z is never stored).  x += alpha p is deferred to the p
 // kernel, which streams p anyway (same operation, one pass less over p and x).
@@ -769,15 +614,19 @@ cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_
   const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
   if (tot == 0) return cudaSuccess;
   // co-resident grid (x SEM_GS_GRIDX); chunk mode: blocks pull element chunks
-  static int resident[2] = {0, 0};
-  if (resident[0] == 0) {
-    int dev = 0, sms = 148, nb0 = 1, nb1 = 1;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cache[kMaxDev][2];
+  const int dev = device_index();
+  int resident[2] = {cache[dev][0].load(std::memory_order_relaxed),
+                     cache[dev][1].load(std::memory_order_relaxed)};
+  if (resident[0] == 0 || resident[1] == 0) {
+    int sms = 148, nb0 = 1, nb1 = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, dev::gs_local_kernel<8, false>, kThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, dev::gs_local_kernel<8, true>, kThreads, 0);
     resident[0] = std::max(nb0, 1) * sms * SEM_GS_GRIDX;
     resident[1] = std::max(nb1, 1) * sms * SEM_GS_GRIDX;
+    cache[dev][0].store(resident[0], std::memory_order_relaxed);
+    cache[dev][1].store(resident[1], std::memory_order_relaxed);
   }
   const int ce = dev::gs_mode_ce(P, mode);
   const int g = ce > 0 ? std::max(1, std::min(resident[1], (P.nloc + ce - 1) / ce))
@@ -856,28 +705,6 @@ cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double
 }
 
 bool gs_flat(const DevPlan& P, int mode) { return dev::gs_mode_ce(P, mode) == 0; }
-
-cudaError_t launch_gs_update(const DevPlan& P, const double* dinv, double* r, const double* w,
-                             double* partial, PcgState* st, double* out2, const double* sig_part,
-                             const int* sig_count, cudaStream_t s) {
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, sms = 148, nb = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::gs_update_kernel<8>, kThreads, 0);
-    grid = std::max(nb, 1) * sms;
-  }
-#define GSU(NN)                                                                                \
-  case NN:                                                                                     \
-    return launch_k(dev::gs_update_kernel<NN>, dim3(grid), dim3(kThreads), 0, s, P, dinv, r, w, \
-                    partial, st, out2, sig_part, sig_count);
-  switch (P.n) {
-    GSU(2) GSU(3) GSU(4) GSU(5) GSU(6) GSU(7) GSU(8) GSU(9) GSU(10) GSU(11) GSU(12)
-  }
-#undef GSU
-  return cudaErrorInvalidValue;
-}
 
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,
                         PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s) {

@@ -2,6 +2,8 @@
 #pragma once
 #include <utility>
 #include <cstdint>
+#include <vector>
+#include <atomic>
 #include <cuda_runtime.h>
 
 namespace sem {
@@ -28,6 +30,16 @@ cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   cfg.attrs = at;
   cfg.numAttrs = pdl_on() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+// Launch geometry and function attributes belong to a device: the launchers
+// cache them per device index (kMaxDev) in atomics (loopback ranks launch from
+// several host threads).
+constexpr int kMaxDev = 16;
+inline int device_index() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDev) ? d : 0;
 }
 
 struct DevPlan {
@@ -219,9 +231,9 @@ cudaError_t launch_ar_finish(const P2P& c, int site, uint64_t epoch, double* out
 
 // returns max resident CTAs/SM for the Ax kernel of this N and mode
 int ax_occupancy(int N, int mode);
-// helm: the Helmholtz variant (a.B, a.h1, a.h2), AX_APPLY / AX_PCG, two-kernel operator
+// helm: the Helmholtz variant (a.B, a.h1, a.h2), AX_APPLY / AX_PCG
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
-                      bool fuse_gs, bool helm = false);
+                      bool helm = false);
 int ax_groups(int N, int nelem);   // element groups processed per launch
 
 // setup
@@ -272,16 +284,23 @@ cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
                              int grid, cudaStream_t s);
 bool gs_flat(const DevPlan& P, int mode);   // the gs schedule `mode` resolves to the flat sweep
-// one rank, flat gs schedule: gather-scatter of w and the CG update in one pass
-// (sigma from the Ax kernel's partials; rho', gamma into out2)
-cudaError_t launch_gs_update(const DevPlan& P, const double* dinv, double* r, const double* w,
-                             double* partial, PcgState* st, double* out2, const double* sig_part,
-                             const int* sig_count, cudaStream_t s);
 // x += alpha p, then (unless the solve ended) p = dinv r + beta p
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,
                         PcgState* st, double* hist, const PeerSync& ps, int grid, cudaStream_t s);
 cudaError_t launch_cg_residual(const DevPlan& P, const uint8_t* mult, const double* b,
                                const double* w, double* partial, PcgState* st, double* out1,
                                const PeerSync& ps, int grid, cudaStream_t s);
+
+// loopback multi-rank transport (loopback.cu; tests): P rank contexts on one
+// device, collectives by device copies with rank-ordered sums
+struct LoopComm;
+LoopComm* loop_lookup(const void* handle);   // nullptr unless a live loopback handle
+int loop_rank(const LoopComm* c);
+int loop_size(const LoopComm* c);
+// Alg. 1 exchange: send + off[k] (cnt[k] doubles) to nbr[k], receive into recv + off[k]
+int loop_sendrecv(LoopComm* c, const double* send, double* recv, const std::vector<int32_t>& nbr,
+                  const std::vector<int64_t>& off, const std::vector<int64_t>& cnt, cudaStream_t s);
+int loop_allreduce(LoopComm* c, const double* in, double* out, size_t count, cudaStream_t s);
+int loop_allgather(LoopComm* c, const void* in, void* out, size_t bytes, cudaStream_t s);
 
 }  // namespace sem

@@ -244,15 +244,19 @@ static cudaError_t launch_exchange_n(const DevPlan& P, double* u, double* part, 
                                      uint64_t epoch, int apply_mask, PcgState* st, int nparts,
                                      uint64_t e_sig, const double* sig_part, const int* sig_count,
                                      uint64_t* base, int mode, cudaStream_t s) {
-  static int resident[2] = {0, 0};
-  if (resident[0] == 0) {
-    int dev = 0, sms = 148, nb0 = 1, nb1 = 1;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cache[kMaxDev][2];
+  const int dev = device_index();
+  int resident[2] = {cache[dev][0].load(std::memory_order_relaxed),
+                     cache[dev][1].load(std::memory_order_relaxed)};
+  if (resident[0] == 0 || resident[1] == 0) {
+    int sms = 148, nb0 = 1, nb1 = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, dev::gs_exchange_p2p_kernel<n, false>, 256, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, dev::gs_exchange_p2p_kernel<n, true>, 256, 0);
     resident[0] = std::max(nb0, 1) * sms;
     resident[1] = std::max(nb1, 1) * sms;
+    cache[dev][0].store(resident[0], std::memory_order_relaxed);
+    cache[dev][1].store(resident[1], std::memory_order_relaxed);
   }
   const int ce = dev::gs_mode_ce(P, mode);
   // co-resident grid (the waits must not starve unscheduled blocks)

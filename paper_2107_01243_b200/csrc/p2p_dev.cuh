@@ -48,31 +48,32 @@ __device__ __forceinline__ uint64_t* mb_ping(char* mb, int r) {
 __device__ __forceinline__ uint4* mb_ll(char* mb, int64_t o, uint64_t epoch) {
   return reinterpret_cast<uint4*>(mb + P2P::kRecvOff) + 2 * o + (epoch & 1);
 }
-// "LL" store: each 8-byte half {32 data bits, 32-bit epoch flag} of the 16-byte
-// record is written by one single-copy-atomic 8-byte access, so a reader that
-// sees both flags equal to the epoch holds both halves of this epoch's value --
-// no fence and no separate flag are needed
+// "LL" store: the 16-byte record is two 8-byte halves, each packing 32 data
+// bits with the 32-bit epoch flag as ONE u64 element ((flag << 32) | data).
+// st.volatile.v2.u64 makes each half an aligned 8-byte element access, which
+// the PTX memory model makes single-copy atomic, so a reader that sees both
+// flags equal to the epoch holds both halves of this epoch's value -- no
+// fence and no separate flag are needed
 __device__ __forceinline__ void ll_store(uint4* p, double v, uint32_t flag) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p),
-               "r"((uint32_t)b), "r"(flag), "r"((uint32_t)(b >> 32)), "r"(flag)
-               : "memory");
+  const unsigned long long h0 = ((unsigned long long)flag << 32) | (b & 0xffffffffull);
+  const unsigned long long h1 = ((unsigned long long)flag << 32) | (b >> 32);
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(h0), "l"(h1) : "memory");
 }
 // spin until the record carries this epoch (bounded; on timeout raise err, return 0)
 __device__ __forceinline__ double ll_load(const uint4* p, uint32_t flag, int* err) {
-  uint32_t lo, f1, hi, f2;
+  unsigned long long h0, h1;
   long long t0 = -1;
   for (;;) {
-    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(lo), "=r"(f1), "=r"(hi), "=r"(f2) : "l"(p) : "memory");
-    if (f1 == flag && f2 == flag) break;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(h0), "=l"(h1) : "l"(p) : "memory");
+    if ((uint32_t)(h0 >> 32) == flag && (uint32_t)(h1 >> 32) == flag) break;
     if (t0 < 0) t0 = clock64();
     else if (clock64() - t0 > (1ll << 33)) {
       atomicExch(err, 1);
       return 0.0;
     }
   }
-  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+  return __longlong_as_double((long long)(((h1 & 0xffffffffull) << 32) | (h0 & 0xffffffffull)));
 }
 
 // one thread: publish K partials of this rank to every rank

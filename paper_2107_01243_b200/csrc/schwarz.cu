@@ -676,10 +676,13 @@ cudaError_t launch_fdm(int n, int nloc, const double* r, const uint8_t* mult, co
   if (nloc == 0) return cudaSuccess;
   if (n == 8 && y && tensor_cores) {   // fp64 tensor-core path (N = 7)
     const size_t smem = (size_t)dev::kF8Smem * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dev::fdm8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
+    static std::atomic<bool> attr[kMaxDev];   // function attributes are per device
+    const int d = device_index();
+    if (!attr[d].load(std::memory_order_relaxed)) {
+      cudaError_t e = cudaFuncSetAttribute(dev::fdm8_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr[d].store(true, std::memory_order_relaxed);
     }
     const int grid8 = std::min((nloc + dev::kF8W - 1) / dev::kF8W, num_sms * 4);
     dev::fdm8_kernel<<<grid8, dev::kF8W * 32, smem, s>>>(nloc, r, mult, S, lam, xi, y, b0, gate);

@@ -80,13 +80,11 @@ def test_setup_exports(spec, N):
             assert np.abs(host(t) - o.get(name)).max() < 1e-13
 
 
-@pytest.mark.parametrize("fused", [False, True], ids=["2kernel", "fused"])
 @pytest.mark.parametrize("spec,N", MESHES, ids=IDS)
-def test_ax_gs_apply_parity(spec, N, fused):
+def test_ax_gs_apply_parity(spec, N):
     o = O.Oracle(spec, N)
     u = random_field(o.nslots, seed=11)
     with sem().sem_setup(spec, N) as c:
-        c.set_fused_gs(fused)
         du, dw = dev(u), c.zeros()
         c.ax(du, dw)
         w_ax = host(dw)
@@ -95,7 +93,7 @@ def test_ax_gs_apply_parity(spec, N, fused):
         dv = dev(u)
         c.gs(dv)
         assert np.array_equal(host(dv), o.gs(u))
-        # fused Ax + gs + mask
+        # the operator: Ax (+ mask) then gs
         dw.zero_()
         c.apply(du, dw)
         w_ap, ref = host(dw), o.apply(u)
@@ -108,14 +106,14 @@ def test_ax_gs_apply_parity(spec, N, fused):
         assert np.array_equal(first[gid], w_ap)
 
 
-def test_apply_is_deterministic_and_variants_agree_bitwise():
+def test_apply_is_deterministic_and_schedules_agree_bitwise():
     spec, N = tgv_box(6, 5, 4, deform=1), 7
     u = random_field(spec.n_slots(N), seed=5)
     with sem().sem_setup(spec, N) as c:
         du = dev(u)
         outs = []
-        for fused in (False, True, False, True):
-            c.set_fused_gs(fused)
+        for mode in (0, 1, 2, 0):
+            c.set_gs_mode(mode)
             w = c.zeros()
             c.apply(du, w)
             outs.append(host(w))
@@ -170,8 +168,8 @@ def test_full_size_apply(cfg):
         c.ax(du, dw)
         assert nrel(host(dw), o.ax(u)) <= 1e-12
         ref = o.apply(u)
-        for fused in (False, True):
-            c.set_fused_gs(fused)
+        for mode in (1, 2):
+            c.set_gs_mode(mode)
             dw.zero_()
             c.apply(du, dw)
             assert nrel(host(dw), ref) <= 1e-12
@@ -227,15 +225,13 @@ PCG_CASES = [
 ]
 
 
-@pytest.mark.parametrize("fused", [False, True], ids=["2kernel", "fused"])
 @pytest.mark.parametrize("spec,N,fun,tol", PCG_CASES)
-def test_pcg_parity(spec, N, fun, tol, fused):
+def test_pcg_parity(spec, N, fun, tol):
     o = O.Oracle(spec, N)
     f = fun(o.get("X"), o.get("Y"), o.get("Z"))
     b = o.rhs(f)
     ref = o.pcg(b, tol, 5000)
     with sem().sem_setup(spec, N) as c:
-        c.set_fused_gs(fused)
         x = c.zeros()
         r = c.pcg_solve(dev(b), x, tol, 5000)
         xs = host(x)
@@ -300,11 +296,12 @@ def test_launch_counts_and_native_library_loaded():
     with sem().sem_setup(spec, N) as c:
         u = c.zeros()
         w = c.zeros()
-        for fused, k in ((True, 1), (False, 2)):   # kernels per apply at P=1
-            c.set_fused_gs(fused)
-            n0 = c.launch_count()
-            c.apply(u, w)
-            assert c.launch_count() == n0 + k
+        n0 = c.launch_count()
+        c.apply(u, w)
+        assert c.launch_count() == n0 + 2   # Ax, gs at P=1
+        for opt in (1, 5, 10):   # retired slower variants are rejected
+            with pytest.raises(sem().SemError):
+                c._set_option(opt, 1)
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libsem.so" in maps
 
@@ -372,23 +369,6 @@ def test_ring_release_stress():
             assert nrel(host(w), ref_p) <= 1e-12
 
 
-def test_pdl_option_identical():
-    """SEM_OPT_PDL (programmatic dependent launch of the iteration kernels, off
-    by default) changes scheduling only: bit-identical PCG iterates."""
-    spec, N = tgv_box(8, 8, 8), 7
-    o = O.Oracle(spec, N)
-    X, Y, Z = o.get("X"), o.get("Y"), o.get("Z")
-    b = dev(o.rhs(f_tgv(X, Y, Z)))
-    with sem().sem_setup(spec, N) as c:
-        xs = []
-        for on in (False, True):
-            c.set_pdl(on)
-            x = c.zeros()
-            r = c.pcg_solve(b, x, 1e-10, 500)
-            xs.append((host(x), r["iters"]))
-        assert xs[0][1] == xs[1][1] and np.array_equal(xs[0][0], xs[1][0])
-
-
 # ---------------------------------------------------------------- NEXT-3: GMRES and projection
 @pytest.mark.parametrize("spec,N,restart", [(CONFIGS["C1"][0], 3, 30), (tgv_box(6, 6, 6, deform=1), 5, 30),
                                             (tgv_box(6, 6, 6, deform=1), 5, 7),
@@ -443,29 +423,6 @@ def test_projection_pipeline_parity():
         r = c.proj_solve(dev(b), x, 1e-10, 3000, 30, 20)
         assert abs(r["iters"] - ref["iters"]) <= 1 and r["iters"] < its[-1] // 4, (r, ref["iters"])
     assert its[-1] < its[0], its
-
-
-@pytest.mark.parametrize("spec,N", [(CONFIGS["C1"][0], 3), (tgv_box(4, 3, 5, deform=1), 7),
-                                    (unit_box(3, 2, 5, periodic=(1, 0, 0)), 5), (tgv_box(2, 2, 2), 1)])
-def test_gs_update_fusion(spec, N):
-    """One rank: the PCG iteration with the gather-scatter fused into the r
-    update (default) and with separate kernels reach the oracle's iterate; the
-    residual histories agree to rounding (dots per unique point vs c-weighted)."""
-    o = O.Oracle(spec, N)
-    fun = f_tgv if all(spec.periodic) else f_sin
-    b = o.rhs(fun(o.get("X"), o.get("Y"), o.get("Z")))
-    ref = o.pcg(b, 1e-10, 3000)
-    with sem().sem_setup(spec, N) as c:
-        out = []
-        for fuse in (True, False):
-            c.set_gs_update(fuse)
-            x = c.zeros()
-            r = c.pcg_solve(dev(b), x, 1e-10, 3000)
-            assert r["status"] == 0 and abs(r["iters"] - ref["iters"]) <= 1, (fuse, r, ref["iters"])
-            assert np.abs(host(x) - ref["x"]).max() <= 1e-10
-            out.append(c.pcg_history())
-        k = min(len(out[0]), len(out[1]), 10)
-        np.testing.assert_allclose(out[0][:k], out[1][:k], rtol=1e-9)
 
 
 @pytest.mark.parametrize("spec,N", [(CONFIGS["C1"][0], 3), (tgv_box(4, 3, 5, deform=1), 7),

@@ -1,32 +1,23 @@
 """Multi-GPU parity worker (launched by tests/test_multigpu.py under torchrun).
 
-Every rank builds its z-slab (lexicographic element range) of the mesh through
-the C ABI with an NCCL communicator; rank 0 gathers the local E-vectors and
-compares them with the oracle run with the SAME number of ranks (so the
-gather-scatter summation order -- ascending slots within a rank, ascending
-ranks across -- is identical):
-  * gs: bit-exact;  apply / rhs: normwise 1e-12;  PCG: iterations +-1, x within 1e-10.
-Exits non-zero on any mismatch.
+One process per GPU with an NCCL communicator; every rank runs the cases of
+tools/mgpu_common.py through the C ABI with both transports (NVLink peer
+memory, NCCL) and both gather-scatter schedules; rank 0 gathers the local
+E-vectors and compares them with the oracle run with the same number of ranks
+(bars in mgpu_common).  Exits non-zero on any mismatch.
 """
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2107_01243_b200 as sem  # noqa: E402
-from sem_inputs import f_sin, f_tgv, random_field, tgv_box, unit_box  # noqa: E402
-
-CASES = [
-    (tgv_box(4, 4, 8), 5, f_tgv),                    # z-slabs, periodic: 2 planes shared
-    (unit_box(3, 2, 5), 4, f_sin),                   # Dirichlet, slabs cut mid-layer
-    (tgv_box(4, 4, 8, deform=1), 7, f_tgv),          # curvilinear, overlap path
-    (unit_box(4, 3, 8, periodic=(1, 0, 0)), 3, f_sin),
-]
+from mgpu_common import CASES, OracleRefs, case_field, check, rank_run, rank_slice  # noqa: E402
 
 
 def main():
@@ -39,119 +30,23 @@ def main():
     comm = sem.nccl_comm_init(uid[0], rank, P)
     fails = []
     for ci, (spec, N, fun) in enumerate(CASES):
-        E, n3 = spec.E, (N + 1) ** 3
-        lo, hi = rank * E // P, (rank + 1) * E // P
-        o = None
-        if rank == 0:
-            import oracle as O
-            o = O.Oracle(spec, N, nranks=P)
-        u = random_field(E * n3, seed=100 + ci)
-        ul = np.ascontiguousarray(u[lo * n3:hi * n3])
-        for fused, p2p, gsm in ((False, True, 0), (False, True, 2), (True, True, 0), (False, False, 2)):
+        u = case_field(ci, spec, N)
+        lo, hi = rank_slice(spec, N, rank, P)
+        ref = OracleRefs(spec, N, fun, u, P) if rank == 0 else None
+        for p2p, gsm in ((True, 0), (True, 2), (False, 2)):
             with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm) as c:
-                c.set_fused_gs(fused)
                 c.set_p2p(p2p)
                 c.set_gs_mode(gsm)
-                assert c.n_local == (hi - lo) * n3
-                du = torch.from_numpy(ul).cuda()
-                w = c.zeros()
-                c.apply(du, w)
-                g = du.clone()
-                c.gs(g)
-                X, Y, Z = c.coords()
-                fv = fun(X, Y, Z, xp=torch)
-                b = c.zeros()
-                c.rhs(fv, b)
-                x = c.zeros()
-                r = c.pcg_solve(b, x, 1e-10, 3000)
-                # single-reduction (Chronopoulos-Gear) PCG: one allreduce per iteration
-                xc = c.zeros()
-                c.set_pcg_variant("single_reduction")
-                rc_ = c.pcg_solve(b, xc, 1e-10, 3000)
-                c.set_pcg_variant("standard")
-                xg = c.zeros()
-                rg = c.gmres_solve(b, xg, 1e-10, 3000, 20) if not fused else None
-                # NEXT-1: two-level Schwarz (fine gs and the N=1 coarse CG run
-                # through the same transport) and flexible PCG with it
-                zs, xs, rs = c.zeros(), c.zeros(), None
-                zs1, xs1, rs1 = c.zeros(), c.zeros(), None
-                if not fused:
-                    c.set_precond("schwarz")
-                    c.set_coarse_replicate(0)          # distributed coarse CG
-                    c.schwarz_apply(b, zs)
-                    rs = c.pcg_solve(b, xs, 1e-10, 3000)
-                    c.set_coarse_replicate(1)          # replicated coarse solve
-                    c.schwarz_apply(b, zs1)
-                    rs1 = c.pcg_solve(b, xs1, 1e-10, 3000)
-                    c.set_coarse_replicate(-1)
-                    c.set_precond("jacobi")
-                torch.cuda.synchronize()
+                assert c.n_local == hi - lo
+                out = rank_run(c, u[lo:hi], fun)
                 parts = [None] * P
-                dist.all_gather_object(parts, (w.cpu().numpy(), g.cpu().numpy(), b.cpu().numpy(),
-                                               x.cpu().numpy(), r, xg.cpu().numpy(), rg,
-                                               zs.cpu().numpy(), xs.cpu().numpy(), rs,
-                                               zs1.cpu().numpy(), xs1.cpu().numpy(), rs1,
-                                               xc.cpu().numpy(), rc_))
+                dist.all_gather_object(parts, out)
                 if rank == 0:
-                    W = np.concatenate([p[0] for p in parts])
-                    Gs = np.concatenate([p[1] for p in parts])
-                    B = np.concatenate([p[2] for p in parts])
-                    Xs = np.concatenate([p[3] for p in parts])
-                    ref_w = o.apply(u)
-                    tag = f"case{ci} P={P} fused={fused} p2p={p2p} gs_mode={gsm}"
-                    e = np.abs(W - ref_w).max() / np.abs(ref_w).max()
-                    if not e <= 1e-12:
-                        fails.append(f"{tag}: apply rel err {e:.2e}")
-                    if not np.array_equal(Gs, o.gs(u)):
-                        fails.append(f"{tag}: gs not bit-exact "
-                                     f"(max diff {np.abs(Gs - o.gs(u)).max():.2e})")
-                    fo = fun(o.get("X"), o.get("Y"), o.get("Z"))
-                    ref_b = o.rhs(fo)
-                    e = np.abs(B - ref_b).max() / np.abs(ref_b).max()
-                    if not e <= 1e-12:
-                        fails.append(f"{tag}: rhs rel err {e:.2e}")
-                    ref = o.pcg(ref_b, 1e-10, 3000)
-                    if abs(r["iters"] - ref["iters"]) > 1 or r["status"] != 0:
-                        fails.append(f"{tag}: pcg iters {r['iters']} vs {ref['iters']} st {r['status']}")
-                    dx = np.abs(Xs - ref["x"]).max()
-                    if not dx <= 1e-10:
-                        fails.append(f"{tag}: pcg x diff {dx:.2e}")
-                    if not abs(r["res_final"] - ref["res_final"]) <= 1e-10:
-                        fails.append(f"{tag}: pcg res {r['res_final']:.3e} vs {ref['res_final']:.3e}")
-                    if rg is not None:   # GMRES(20) through the same transport
-                        Xg = np.concatenate([p[5] for p in parts])
-                        refg = o.gmres(ref_b, 1e-10, 3000, 20)
-                        # restarted GMRES amplifies the rounding of rank-partitioned dots
-                        # across restarts (reading Q27): iterations within max(1, 5 %),
-                        # x within 1e-9 (both converge to the 1e-10 residual)
-                        if (abs(rg["iters"] - refg["iters"]) > max(1, 0.05 * refg["iters"])
-                                or rg["status"] != 0):
-                            fails.append(f"{tag}: gmres iters {rg['iters']} vs {refg['iters']}")
-                        if not np.abs(Xg - refg["x"]).max() <= 1e-9:
-                            fails.append(f"{tag}: gmres x diff {np.abs(Xg - refg['x']).max():.2e}")
-                    refc = o.cgcg(ref_b, 1e-10, 3000)
-                    Xc = np.concatenate([p[13] for p in parts])
-                    if abs(rc_["iters"] - refc["iters"]) > 1 or rc_["status"] != 0:
-                        fails.append(f"{tag}: single-reduction pcg iters {rc_['iters']} vs {refc['iters']}")
-                    if not np.abs(Xc - refc["x"]).max() <= 1e-10:
-                        fails.append(f"{tag}: single-reduction pcg x diff {np.abs(Xc - refc['x']).max():.2e}")
-                    if rs is not None:
-                        schw = o.schwarz(10)
-                        ref_z = schw.apply(B)
-                        refs = schw.pcg(B, 1e-10, 3000)
-                        for zi, xi, ri, mode in ((7, 8, rs, "distributed"), (10, 11, rs1, "replicated")):
-                            Zs = np.concatenate([p[zi] for p in parts])
-                            e = np.abs(Zs - ref_z).max() / np.abs(ref_z).max()
-                            if not e <= 1e-11:
-                                fails.append(f"{tag}: schwarz ({mode}) apply rel err {e:.2e}")
-                            Xsch = np.concatenate([p[xi] for p in parts])
-                            rr_ = parts[0][xi + 1]
-                            if abs(rr_["iters"] - refs["iters"]) > 1 or rr_["status"] != 0:
-                                fails.append(f"{tag}: schwarz ({mode}) pcg iters {rr_['iters']} vs {refs['iters']}")
-                            if not np.abs(Xsch - refs["x"]).max() <= 1e-10:
-                                fails.append(f"{tag}: schwarz ({mode}) pcg x diff {np.abs(Xsch - refs['x']).max():.2e}")
-                    print(f"{tag}: ok-check iters {r['iters']} (oracle {ref['iters']}) "
-                          f"dx {dx:.2e}", flush=True)
+                    tag = f"case{ci} P={P} p2p={p2p} gs_mode={gsm}"
+                    f = check(parts, ref, tag)
+                    fails += f
+                    print(f"{tag}: {'FAIL' if f else 'ok'} pcg iters {out['r']['iters']} "
+                          f"(oracle {ref.pcg['iters']})", flush=True)
     sem.nccl_comm_destroy(comm)
     dist.barrier()
     dist.destroy_process_group()

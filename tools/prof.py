@@ -1,5 +1,5 @@
 """Short, deterministic workload for ncu: C2 mesh (8192 elements, N=7).
-Runs apply (two-kernel and fused), Ax alone, and a 4-iteration PCG."""
+Runs apply (Ax+mask kernel, gs kernel), Ax alone, and a 4-iteration PCG."""
 import os
 import sys
 
@@ -17,13 +17,10 @@ torch.cuda.set_device(0)
 with sem.sem_setup(spec, N) as c:
     u = torch.empty(c.n_local, dtype=torch.float64, device="cuda").uniform_(-1, 1)
     w = c.zeros()
-    for fused in (False, True):
-        c.set_fused_gs(fused)
-        for _ in range(3):
-            c.apply(u, w)
+    for _ in range(3):
+        c.apply(u, w)
     for _ in range(3):
         c.ax(u, w)
-    c.set_fused_gs(False)
     x = c.zeros()
     c.pcg_solve(u, x, 0.0, 4)
     torch.cuda.synchronize()
