@@ -1762,8 +1762,8 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     return SEM_OK;
   }
   if (option == SEM_OPT_GS_MODE) {
-    if (value < 0 || value > 2) {
-      sem::set_error("sem_set_option: SEM_OPT_GS_MODE must be 0, 1 or 2");
+    if (value < 0 || value > 5) {
+      sem::set_error("sem_set_option: SEM_OPT_GS_MODE must be in 0..5");
       return SEM_EINVAL;
     }
     c->gs_mode = value;

@@ -116,6 +116,105 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
   }
 }
 
+// Flat variant 2 (high memory-level parallelism): the kernel is L2-latency
+// bound, so every thread issues ALL its loads of a round before any use: the
+// index records of F face points and FE edge points first, then their 2F +
+// 4 FE data loads, then the sums and the broadcast stores (fire and forget).
+// A round covers nth*F face points and nth*FE edge points (consecutive
+// threads on consecutive points of an entity: coalesced where the layout
+// allows); vertices (few) follow in a grid-stride loop.
+template <int n, int F, int FE>
+__device__ __forceinline__ void gs_flat2_body(const DevPlan& P, double* __restrict__ u,
+                                               int apply_mask, int tid, int nth) {
+  constexpr int N = n - 1;
+  constexpr int nf = (N - 1) * (N - 1), ne = N - 1;
+  constexpr int Nm1 = N > 1 ? N - 1 : 1;
+  constexpr int nfd = nf > 0 ? nf : 1, ned = ne > 0 ? ne : 1;
+  const int tF = P.nF * nf, tE = P.nEd * ne;
+  const int rF = nf > 0 ? (tF + nth * F - 1) / (nth * F) : 0;
+  const int rE = ne > 0 ? (tE + nth * FE - 1) / (nth * FE) : 0;
+  const int rounds = rF > rE ? rF : rE;
+  for (int r = 0; r < rounds; r++) {
+    int a0[F], a1[F];
+    bool fok[F];
+    int eb[FE][4], eoff[FE], enin[FE];
+    bool emk[FE];
+#pragma unroll
+    for (int q = 0; q < F; q++) {
+      const int t = (r * F + q) * nth + tid;
+      fok[q] = nf > 0 && t < tF;
+      const int f = fok[q] ? t / nfd : 0;
+      const int p = t - f * nf;
+      const int ax = fok[q] ? P.f_axis[f] : 0;
+      const int off = (1 + p % Nm1) * f_s1(ax, n) + (1 + p / Nm1) * f_s2(ax, n);
+      const int2 b2 = fok[q] ? reinterpret_cast<const int2*>(P.f_base)[f] : make_int2(0, 0);
+      a0[q] = b2.x + off;
+      a1[q] = b2.y + off;
+    }
+#pragma unroll
+    for (int q = 0; q < FE; q++) {
+      const int t = (r * FE + q) * nth + tid;
+      const bool ok = ne > 0 && t < tE;
+      const int e = ok ? t / ned : 0;
+      const int p = t - e * ne;
+      enin[q] = ok ? P.e_nin[e] : 0;
+      eoff[q] = ok ? (1 + p) * e_sd(P.e_axis[e], n) : 0;
+      emk[q] = ok && P.e_mask[e];
+      const int4 b4 = ok ? reinterpret_cast<const int4*>(P.e_base)[e] : make_int4(0, 0, 0, 0);
+      eb[q][0] = b4.x; eb[q][1] = b4.y; eb[q][2] = b4.z; eb[q][3] = b4.w;
+    }
+    double v0[F], v1[F], ve[FE][4];
+#pragma unroll
+    for (int q = 0; q < F; q++)
+      if (fok[q]) {
+        v0[q] = gs_ld(&u[a0[q]]);
+        v1[q] = gs_ld(&u[a1[q]]);
+      }
+#pragma unroll
+    for (int q = 0; q < FE; q++)
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+        if (x < enin[q]) ve[q][x] = gs_ld(&u[eb[q][x] + eoff[q]]);
+#pragma unroll
+    for (int q = 0; q < F; q++)
+      if (fok[q]) {
+        const double s = v0[q] + v1[q];
+        gs_st(&u[a0[q]], s);
+        gs_st(&u[a1[q]], s);
+      }
+#pragma unroll
+    for (int q = 0; q < FE; q++) {
+      if (enin[q] == 0) continue;
+      double s = ve[q][0];
+#pragma unroll
+      for (int x = 1; x < 4; x++)
+        if (x < enin[q]) s += ve[q][x];
+      if (apply_mask && emk[q]) s = 0.0;
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+        if (x < enin[q]) gs_st(&u[eb[q][x] + eoff[q]], s);
+    }
+  }
+  for (int v = tid; v < P.nV; v += nth) {
+    const int nin = P.v_nin[v];
+    const int4 b0 = reinterpret_cast<const int4*>(P.v_base)[2 * v];
+    const int4 b1 = reinterpret_cast<const int4*>(P.v_base)[2 * v + 1];
+    const int base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    double vv[8];
+#pragma unroll
+    for (int x = 0; x < 8; x++)
+      if (x < nin) vv[x] = gs_ld(&u[base[x]]);
+    double s = vv[0];
+#pragma unroll
+    for (int x = 1; x < 8; x++)
+      if (x < nin) s += vv[x];
+    if (apply_mask && P.v_mask[v]) s = 0.0;
+#pragma unroll
+    for (int x = 0; x < 8; x++)
+      if (x < nin) gs_st(&u[base[x]], s);
+  }
+}
+
 // Rank-local gather-scatter, one sweep in element order.  The planner creates
 // every entity from its smallest local element, in element order, so the faces,
 // edges and vertices created by elements [e0, e1) are three contiguous index
