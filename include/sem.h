@@ -285,12 +285,6 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    geometric-factor planes before waiting for the preceding kernel; 0 = plain
    order.  Identical results. */
 #define SEM_OPT_AX_PDL 13
-/* 1 (default) = for N >= 7 the operator's Ax kernel sums the element faces
-   normal to x inside runs of consecutive elements (each CTA takes runs of
-   ceil(E_local / resident CTAs) elements) and the gather-scatter kernel skips
-   those faces; 0 = the gather-scatter sums every face.  Bit-identical results
-   (a face point has exactly two incidences).  sem_ax is never affected. */
-#define SEM_OPT_XFACE 14
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

@@ -261,10 +261,6 @@ class Context:
         """Replay the one-rank Schwarz coarse solve as a CUDA graph (default on)."""
         _check(load().sem_set_option(self._h, 8, 1 if on else 0))
 
-    def set_xface(self, on: bool):
-        """N >= 7: x-faces inside runs of elements summed by the Ax kernel (default on)."""
-        _check(load().sem_set_option(self._h, 14, 1 if on else 0))
-
     def set_ax_pdl(self, on: bool):
         """PDL launch of the PCG Ax kernel with G prefetched before the grid wait."""
         _check(load().sem_set_option(self._h, 13, 1 if on else 0))

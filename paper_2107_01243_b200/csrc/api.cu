@@ -88,22 +88,14 @@ struct sem_ctx {
   double *d_xi = nullptr, *d_w = nullptr, *d_D = nullptr, *d_G = nullptr, *d_B = nullptr,
          *d_dinv = nullptr;
   uint8_t *d_mult = nullptr, *d_bmask = nullptr;
-  int32_t *d_fb = nullptr, *d_eb = nullptr, *d_vb = nullptr;
+  int32_t *d_eref = nullptr, *d_fb = nullptr, *d_eb = nullptr, *d_vb = nullptr;
   uint8_t *d_fax = nullptr, *d_eax = nullptr, *d_enin = nullptr, *d_emask = nullptr,
           *d_vnin = nullptr, *d_vmask = nullptr;
+  unsigned* d_cnt = nullptr;
   int32_t *d_fst = nullptr, *d_est = nullptr, *d_vst = nullptr;
   unsigned long long* d_gsctr = nullptr;   // gs chunk counters (never reset)
   uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
   int gs_mode = 0;                         // SEM_OPT_GS_MODE
-  // x-face fusion (SEM_OPT_XFACE): the Ax kernel sums the
-  // x-faces inside runs of xrun consecutive elements; dp_fx is the plan
-  // without those faces, used by the gather-scatter that follows such an Ax
-  bool xface = true;
-  int xrun = 1;
-  bool xf_last = false;                    // the last masked Ax launch fused x-faces
-  sem::DevPlan dp_fx;
-  int32_t *d_fb_fx = nullptr, *d_fst_fx = nullptr;
-  uint8_t* d_fax_fx = nullptr;
   // NEXT-3: GMRES work space, projection space
   const int* ax_gate = nullptr;            // Ax early-exit flag of GMRES Arnoldi steps
   double *d_V = nullptr, *d_gt = nullptr, *d_kpart = nullptr;
@@ -284,12 +276,6 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.B = c->d_B;
   a.h1 = c->h1;
   a.h2 = c->h2;
-  // x-face fusion: masked modes over the whole local range in one launch
-  c->xf_last = c->xface && c->xrun > 1 && mode != sem::AX_ONLY && r0lo == 0 &&
-               r0hi == (int)c->hp.nloc && r1lo == r1hi;
-  a.xrun = c->xf_last ? c->xrun : 1;
-  a.Ex = c->hp.m.ex;
-  a.e_lo = c->hp.e_lo;
   const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
   const int groups = std::max(ng, 1);   // the launcher caps the grid at residency
   int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
@@ -332,9 +318,7 @@ int exchange(sem_ctx* c) {
 // zero, so every masked entity point sums to zero)
 int gs_pass(sem_ctx* c, double* w) {
   int tk = timer_begin(c, 4);
-  cudaError_t e = sem::launch_gs_local(c->xf_last ? c->dp_fx : c->dp, w, 0, &c->gs_base[0],
-                                       c->gs_mode, c->stream);
-  c->xf_last = false;
+  cudaError_t e = sem::launch_gs_local(c->dp, w, 0, &c->gs_base[0], c->gs_mode, c->stream);
   timer_end(c, tk);
   c->launches++;
   return check(e, "gs kernel");
@@ -369,9 +353,7 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
     SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, nullptr));
     c->cur_e_sig = mode == sem::AX_PCG ? ++c->ep_ar[sem::AR_SIG] : 0;
     int tk = timer_begin(c, 4);
-    const bool xf = c->xf_last;
-    c->xf_last = false;
-    CUDA_TRY(sem::launch_gs_exchange_p2p(xf ? c->dp_fx : c->dp, w, c->d_part, c->p2p, e, 1,
+    CUDA_TRY(sem::launch_gs_exchange_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
                                          mode == sem::AX_PCG ? st : nullptr, 1, c->cur_e_sig,
                                          c->d_partial_ax, c->d_nsig, &c->gs_base[1], c->gs_mode,
                                          c->stream));
@@ -489,15 +471,15 @@ int ensure_hist(sem_ctx* c, int maxit) {
 void free_ctx(sem_ctx* c) {
   if (!c) return;
   void* ptrs[] = {c->d_xi, c->d_w, c->d_D, c->d_G, c->d_B, c->d_dinv, c->d_mult, c->d_bmask,
-                  c->d_fb, c->d_eb, c->d_vb, c->d_fax, c->d_eax, c->d_enin,
-                  c->d_emask, c->d_vnin, c->d_vmask, c->d_sslot, c->d_soff,
+                  c->d_eref, c->d_fb, c->d_eb, c->d_vb, c->d_fax, c->d_eax, c->d_enin,
+                  c->d_emask, c->d_vnin, c->d_vmask, c->d_cnt, c->d_sslot, c->d_soff,
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
                   c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank, c->d_fst, c->d_est,
                   c->d_vst, c->d_gsctr, c->d_dinv_helm,
                   c->d_V, c->d_gt, c->d_kpart, c->d_Z, c->d_AZ, c->d_pdelta, c->d_pbd,
                   c->d_fS, c->d_flam, c->d_sy, c->d_b0, c->d_x0, c->d_dinv0, c->d_st0,
-                  c->d_rw, c->d_z, c->d_Zs, c->d_fb_fx, c->d_fst_fx, c->d_fax_fx};
+                  c->d_rw, c->d_z, c->d_Zs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->d_gs) cudaFree(c->d_gs);
@@ -520,46 +502,6 @@ void free_ctx(sem_ctx* c) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-// x-face fusion plan: runs of R = ceil(nloc / resident Ax CTAs)
-// consecutive elements; the face between local elements el and el + 1 (el's x+
-// face, el + 1's x- face, same run, not across a periodic wrap) is summed by
-// the Ax kernel.  dp_fx = the plan with those faces removed (order kept, so
-// the element-ordered chunk ranges f_start stay valid).  Only for the NE == 1
-// Ax shapes (N >= 7).
-int xface_setup(sem_ctx* c) {
-  const sem::HostPlan& h = c->hp;
-  c->dp_fx = c->dp;
-  c->xrun = 1;
-  if (sem::ax_ne(h.N) != 1 || h.nloc < 2) return SEM_OK;
-  const int R = (int)((h.nloc + c->ax_grid - 1) / c->ax_grid);
-  if (R < 2) return SEM_OK;
-  const int64_t n3 = h.n3;
-  std::vector<int32_t> fb, fst(h.nloc + 1, 0);
-  std::vector<uint8_t> fax;
-  int64_t el_cur = 0;
-  for (int64_t f = 0; f < h.nF; f++) {
-    while (el_cur < h.nloc && h.f_start[el_cur + 1] <= f) fst[++el_cur] = (int32_t)fax.size();
-    const int32_t b0 = h.f_base[2 * f], b1 = h.f_base[2 * f + 1];
-    const int64_t e0 = b0 / n3, e1 = b1 / n3;
-    const bool fused = h.f_axis[f] == 0 && e1 == e0 + 1 && b0 % n3 == h.n - 1 && b1 % n3 == 0 &&
-                       e0 / R == e1 / R && (h.e_lo + e0) % h.m.ex != h.m.ex - 1;
-    if (fused) continue;
-    fb.push_back(b0);
-    fb.push_back(b1);
-    fax.push_back(h.f_axis[f]);
-  }
-  while (el_cur < h.nloc) fst[++el_cur] = (int32_t)fax.size();
-  SEM_TRY(upload(&c->d_fb_fx, fb, c->stream));
-  SEM_TRY(upload(&c->d_fax_fx, fax, c->stream));
-  SEM_TRY(upload(&c->d_fst_fx, fst, c->stream));
-  c->dp_fx.nF = (int)fax.size();
-  c->dp_fx.f_base = c->d_fb_fx;
-  c->dp_fx.f_axis = c->d_fax_fx;
-  c->dp_fx.f_start = c->d_fst_fx;
-  c->xrun = R;
-  return SEM_OK;
-}
 
 // Map every rank's mailbox into this process (CUDA IPC over NVLink); handles and
 // receive-buffer offsets are exchanged once with NCCL all-gathers.  Returns
@@ -703,6 +645,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(upload(&c->d_w, h.w, s));
   SETUP_TRY(upload(&c->d_D, h.D, s));
   SETUP_TRY(upload(&c->d_bmask, h.bmask, s));
+  SETUP_TRY(upload(&c->d_eref, h.eref, s));
   SETUP_TRY(upload(&c->d_fb, h.f_base, s));
   SETUP_TRY(upload(&c->d_fax, h.f_axis, s));
   SETUP_TRY(upload(&c->d_eb, h.e_base, s));
@@ -724,6 +667,9 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(upload(&c->d_smask, h.s_mask, s));
   SETUP_TRY(upload(&c->d_smult, h.s_mult, s));
   SETUP_TRY(upload(&c->d_srank, h.s_rank, s));
+  const size_t nent = (size_t)(h.nF + h.nEd + h.nV);
+  SETUP_TRY(dalloc(&c->d_cnt, nent));
+  SETUP_CUDA(cudaMemsetAsync(c->d_cnt, 0, std::max<size_t>(nent, 1) * sizeof(unsigned), s));
   SETUP_TRY(dalloc(&c->d_part, (size_t)h.nS));
   SETUP_TRY(dalloc(&c->d_send, (size_t)h.nbuf));
   SETUP_TRY(dalloc(&c->d_recv, (size_t)h.nbuf));
@@ -744,10 +690,11 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   sem::DevPlan& P = c->dp;
   P.N = h.N; P.n = h.n; P.nloc = (int)h.nloc; P.n_local = h.n_local;
   P.nF = (int)h.nF; P.nEd = (int)h.nEd; P.nV = (int)h.nV; P.nS = (int)h.nS;
-  P.D = c->d_D; P.bmask = c->d_bmask;
+  P.D = c->d_D; P.bmask = c->d_bmask; P.eref = c->d_eref;
   P.f_base = c->d_fb; P.f_axis = c->d_fax;
   P.e_base = c->d_eb; P.e_axis = c->d_eax; P.e_nin = c->d_enin; P.e_mask = c->d_emask;
   P.v_base = c->d_vb; P.v_nin = c->d_vnin; P.v_mask = c->d_vmask;
+  P.cnt = c->d_cnt;
   P.f_start = c->d_fst; P.e_start = c->d_est; P.v_start = c->d_vst; P.gs_ctr = c->d_gsctr;
   P.s_slot = c->d_sslot; P.s_off = c->d_soff; P.s_nloc = c->d_snloc; P.s_nr = c->d_snr;
   P.s_mask = c->d_smask; P.s_mult = c->d_smult;
@@ -764,7 +711,6 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
 
   if (h.nranks > 1 && !c->loop) SETUP_TRY(p2p_setup(c));   // loopback: device copies only
   c->dp.s_rank = c->d_srank;
-  SETUP_TRY(xface_setup(c));
 
   // geometry on the device
   int* d_bad = nullptr;
@@ -1836,11 +1782,6 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     cudaStreamSynchronize(c->stream);
     if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
     c->precond = value;
-    return SEM_OK;
-  }
-  if (option == SEM_OPT_XFACE) {
-    cudaStreamSynchronize(c->stream);
-    c->xface = value != 0;
     return SEM_OK;
   }
   if (option == SEM_OPT_AX_PDL) {

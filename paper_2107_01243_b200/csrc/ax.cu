@@ -164,8 +164,7 @@ struct AxShape {
   static constexpr int dpad = n + 1;
   static constexpr int nbar = 2 * NSG + 2 * NSU;
   static constexpr size_t smem_bytes =
-      sizeof(double) * ((size_t)NSU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32 +
-                        (NE == 1 ? 2 * n2 : 0)) +
+      sizeof(double) * ((size_t)NSU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32) +
       sizeof(uint64_t) * nbar + sizeof(int) * 8 + SEM_AX_SMEM_PAD;
   // CTAs per SM the shared memory allows; the register budget is sized to match
   static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
@@ -216,8 +215,7 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
   double* sD = sWs + NE * Sh::wel;                     // sD[i*dp+m]  = D[i][m]
   double* sDt = sD + n * dp;                           // sDt[i*dp+m] = D[m][i]
   double* s_red = sDt + n * dp;                        // 32 doubles
-  double* sXf = s_red + 32;                            // [2][n][n] x-face stash (NE == 1)
-  uint64_t* fullG = reinterpret_cast<uint64_t*>(sXf + (NE == 1 ? 2 * n2 : 0));
+  uint64_t* fullG = reinterpret_cast<uint64_t*>(s_red + 32);
   uint64_t* emptyG = fullG + NSG;
   uint64_t* fullU = emptyG + NSG;
   uint64_t* emptyU = fullU + NSU;
@@ -255,21 +253,16 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
       cnt = min(NE, r1hi - e0);
     }
   };
-  // group order: CTA b takes runs b, b + grid, ... of R = a.xrun consecutive
-  // groups, each run in ascending order (R = 1: plain grid stride)
-  const int R = a.xrun > 1 ? a.xrun : 1;
-  const int g_first = blockIdx.x * R;
-  auto g_next = [=](int g) { return ((g + 1) % R != 0) ? g + 1 : (g / R + (int)gridDim.x) * R; };
   // programmatic dependent launch (a.pdl_pref): G does not depend on the
   // preceding kernel, so the producer streams the first group's G planes into
   // the (initially free) ring slots BEFORE waiting for the preceding grid --
   // the ring fill overlaps that kernel's tail.  Only when the group's planes
   // fit the ring (no wait on a consumer that itself waits for u).
   constexpr int kPrefPlanes = (n / PPC <= NSG) ? n / PPC : 0;
-  const bool pref = a.pdl_pref && kPrefPlanes > 0 && g_first < ng;
+  const bool pref = a.pdl_pref && kPrefPlanes > 0 && blockIdx.x < ng;
   if (pref && producer && tid == TCW) {
     int e0, cnt;
-    group(g_first, e0, cnt);
+    group(blockIdx.x, e0, cnt);
     const uint64_t pol = policy_evict_first();
     const uint32_t bP = PPC * 6u * n2 * 8u;
     for (int kb = 0; kb < kPrefPlanes; kb++) {
@@ -297,7 +290,7 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     int su = 0, sg = 0;
     uint32_t phu = 0, phg = 0;
     bool first = pref;   // the first group's G planes are already in flight
-    for (int g = g_first; g < ng; g = g_next(g)) {
+    for (int g = blockIdx.x; g < ng; g += gridDim.x) {
       int e0, cnt;
       group(g, e0, cnt);
       // u block of the group
@@ -357,21 +350,10 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     double Di[n], Dj[n], Dti[n], Dtj[n];
     int su = 0, sg = 0;
     uint32_t phu = 0, phg = 0;
-    for (int g = g_first; g < ng; g = g_next(g)) {
+    for (int g = blockIdx.x; g < ng; g += gridDim.x) {
       int e0, cnt;
       group(g, e0, cnt);
       const bool active = el < cnt;
-      // x-face fusion (a.xrun > 1, NE == 1, one range from element 0; DESIGN.md
-      // 5.2): the face between this element and the next one of the run (its
-      // x+ neighbour) is summed here instead of by the gather-scatter kernel.
-      // xnext: stash this element's x+ face-interior values; xprev: add the
-      // stashed values of the previous element to this element's x- face.
-      const bool xf = NE == 1 && kMask && R > 1;
-      const bool xnext = xf && (g + 1) % R != 0 && g + 1 < ng &&
-                         (int)((a.e_lo + e0 + 1) % a.Ex) != 0;
-      const bool xprev = xf && g % R != 0 && (int)((a.e_lo + e0) % a.Ex) != 0;
-      double* xs_put = sXf + (g & 1) * n2;         // written for the next element
-      const double* xs_get = sXf + ((g & 1) ^ 1) * n2;   // written by the previous one
       // the element's Dirichlet face bits, fetched now, used by the epilogue
       const unsigned bm = (kMask && active) ? (unsigned)__ldg(P.bmask + e0 + el) : 0u;
       const int uoff = kBulkU ? 0 : (int)((reinterpret_cast<uintptr_t>(a.u + (size_t)e0 * n3) >> 3) & 1u);
@@ -471,17 +453,8 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
           if (HELM)   // h1 A_L u + h2 B_L u
             v = a.h1 * v + a.h2 * ((kBpre ? rb[kBpre ? k : 0] : __ldg(Bc + n2 * k)) * ru[k]);
           if (kMask && ((kmask >> k) & 1u)) v = 0.0;
-          if (MODE == AX_PCG) acc = fma(ru[k], v, acc);   // sigma: unassembled A_L p
-          const bool fpt = j >= 1 && j <= n - 2 && k >= 1 && k <= n - 2;   // face interior
-          if (i == n - 1 && xnext && fpt) {
-            xs_put[j * n + k] = v;        // summed (and stored) by the next element
-          } else if (i == 0 && xprev && fpt) {
-            const double sum = xs_get[j * n + k] + v;   // slots e-1 (i = n-1) and e (i = 0)
-            wg[ij + n2 * k] = sum;
-            wg[(n - 1) + n * j + n2 * k - n3] = sum;
-          } else {
-            wg[ij + n2 * k] = v;
-          }
+          if (MODE == AX_PCG) acc = fma(ru[k], v, acc);
+          wg[ij + n2 * k] = v;
         }
       }
 
@@ -522,8 +495,7 @@ static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cud
     resident = std::max(nb, 1) * sms;
     cache[dev].store(resident, std::memory_order_relaxed);
   }
-  const int runs = (groups + std::max(a.xrun, 1) - 1) / std::max(a.xrun, 1);
-  const int grid = std::max(1, std::min(runs, resident));
+  const int grid = std::max(1, std::min(groups, resident));
   return launch_k(kern, dim3(grid), dim3(Sh::T), Sh::smem_bytes, s, P, a);
 }
 
@@ -599,8 +571,6 @@ static int ne_of(int n) {
     default: return 1;
   }
 }
-
-int ax_ne(int N) { return ne_of(N + 1); }
 
 int ax_groups(int N, int nelem) {
   const int ne = ne_of(N + 1);

@@ -48,6 +48,7 @@ struct DevPlan {
   int nF = 0, nEd = 0, nV = 0, nS = 0;
   const double* D = nullptr;        // [n*n]
   const uint8_t* bmask = nullptr;   // [nloc]
+  const int32_t* eref = nullptr;    // [nloc*26]
   const int32_t* f_base = nullptr;  // [nF][2]
   const uint8_t* f_axis = nullptr;
   const int32_t* e_base = nullptr;  // [nEd][4]
@@ -57,6 +58,7 @@ struct DevPlan {
   const int32_t* v_base = nullptr;  // [nV][8]
   const uint8_t* v_nin = nullptr;
   const uint8_t* v_mask = nullptr;
+  unsigned* cnt = nullptr;          // [nF + nEd + nV] last-arriver tickets
   const int32_t* f_start = nullptr; // [nloc+1] entities created by each element (gs_dev.cuh)
   const int32_t* e_start = nullptr;
   const int32_t* v_start = nullptr;
@@ -123,12 +125,6 @@ struct AxLaunch {
   int gate;                       // 1: any mode returns early when *done (GMRES cycle gate)
   int pdl_pref;                   // 1: launched with PDL; prefetch the first G planes before
                                   //    waiting for the preceding grid
-  // x-face fusion (NE == 1 shapes, masked modes, one element range from 0):
-  // runs of xrun consecutive elements per CTA; the x-faces inside a run are
-  // summed by the kernel (the gather-scatter then uses the plan without them)
-  int xrun;                       // <= 1: off
-  int Ex;                         // elements per x row
-  int64_t e_lo;                   // global index of local element 0
 };
 
 // NVLink peer-memory collectives (p2p.cu): mailbox layout and device view
@@ -239,7 +235,6 @@ int ax_occupancy(int N, int mode);
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
                       bool helm = false);
 int ax_groups(int N, int nelem);   // element groups processed per launch
-int ax_ne(int N);                  // elements per CTA group (x-face fusion needs 1)
 
 // setup
 cudaError_t launch_geom(const DevPlan& P, const double* xi, const double* wq, int64_t e_lo,
