@@ -53,6 +53,16 @@ def main():
                     if q >= 3:
                         tot += e0.elapsed_time(e1)
                 ms = tot / reps
+                tot2 = 0.0   # gs right after a gs (w certainly L2-resident)
+                for q in range(reps + 3):
+                    c.gs(w)
+                    e0.record(st)
+                    c.gs(w)
+                    e1.record(st)
+                    e1.synchronize()
+                    if q >= 3:
+                        tot2 += e0.elapsed_time(e1)
+                ms2 = tot2 / reps
                 e0.record(st)
                 for q in range(reps):
                     c.apply(u, w)
@@ -60,7 +70,7 @@ def main():
                 e1.synchronize()
                 ap = e0.elapsed_time(e1) / reps
                 fb = 1.0 - ((N - 1) / (N + 1)) ** 3
-                print(json.dumps({"cfg": cfg, "N": N, "n_p": nl, "mode": mode, "gs_us": ms * 1e3,
+                print(json.dumps({"cfg": cfg, "N": N, "n_p": nl, "mode": mode, "gs_us": ms * 1e3, "gs_after_gs_us": ms2 * 1e3,
                                   "gs_gbs_alg": nl * 20 * fb / (ms / 1e3) / 1e9,
                                   "apply_us": ap * 1e3, "apply_gdofs": nl / (ap / 1e3) / 1e9,
                                   "bit_identical_to_first": same}), flush=True)
