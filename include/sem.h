@@ -171,13 +171,23 @@ int sem_export_field(const sem_ctx* c, int which, double* host_dst);
 /* which: 0 multiplicity[n_local], 1 mask[n_local] (1 = Dirichlet slot) */
 int sem_export_int(const sem_ctx* c, int which, int64_t* host_dst);
 
+typedef struct sem_plan sem_plan;
+/* Live plan export (P:L107 global numbering, P:L231 pairs / segments, Alg. 1
+   shared lists): a planner handle (query it with the sem_plan_* accessors
+   below, free it with sem_plan_destroy) built from the gather-scatter
+   records the context's kernels use, copied back from the device: the face /
+   edge / vertex incidence records and the shared-point lists expand into the
+   pairs, segments and per-neighbour lists; multiplicity and mask are the
+   device arrays; global numbers come from the lattice formula (reading Q6,
+   never stored on the device).  Blocking. */
+int sem_export_plan(const sem_ctx* c, sem_plan** out);
+
 /* ---- host-only planner (no device needed; used by CPU tests) ----
    Exposes the gather-scatter plan a rank would build for this mesh: lattice
    global numbering (reading Q6), multiplicity, mask, the injective pairs
    (l_a < l_b) sorted by l_a and the non-injective segments sorted by first
    slot, the neighbour ranks and, per neighbour, the shared global
    numbers in ascending order (Alg. 1 buffers). */
-typedef struct sem_plan sem_plan;
 int sem_plan_create(const sem_mesh* m, int N, sem_plan** out);
 int sem_plan_destroy(sem_plan* p);
 int sem_plan_sizes(const sem_plan* p, int64_t* n_local, int64_t* npairs, int64_t* nseg,
@@ -250,7 +260,7 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    0 (default) auto, 1 = flat (each entity class swept over the whole grid;
    best while w is L2-resident), 2 = element-ordered chunks pulled dynamically
    by the blocks (each element's w streamed from HBM about once).  Auto picks
-   2 when w exceeds 64 MB. */
+   2 when w exceeds 256 MB. */
 #define SEM_OPT_GS_MODE 4
 /* Preconditioner of sem_pcg_solve / sem_gmres_solve / sem_proj_solve:
    SEM_PRECOND_JACOBI (default) or SEM_PRECOND_SCHWARZ (NEXT-1; setting it

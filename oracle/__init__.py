@@ -72,6 +72,7 @@ def lib():
         L.oracle_helm_pcg.argtypes = [C.c_void_p, C.c_double, C.c_double, _D, _D, C.c_double,
                                       C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.c_void_p]
+        L.oracle_arnoldi.argtypes = [C.c_void_p, _D, C.c_int, _D, _D]
         L.oracle_gmres.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int,
                                    C.POINTER(C.c_int), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.c_void_p]
@@ -278,6 +279,16 @@ class Oracle:
             raise OracleError(f"oracle_gmres failed with status {st}")
         return {"x": x, "iters": it.value, "res_final": rf.value, "res_true": rt.value,
                 "status": st, "hist": hist[: it.value + 1]}
+
+    def arnoldi(self, b, m: int):
+        """Test access: m Arnoldi steps of the GMRES above from b; returns (V, H),
+        V [(m+1), nslots], H [(m+1), m]."""
+        V = np.zeros((m + 1, self.nslots))
+        H = np.zeros((m + 1, m))
+        st = lib().oracle_arnoldi(self._h, _f64(b), m, V, H)
+        if st < 0:
+            raise OracleError(f"oracle_arnoldi failed with status {st}")
+        return V, H
 
     def proj(self, m: int = 20):
         return Proj(self, m)

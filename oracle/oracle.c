@@ -731,6 +731,48 @@ int oracle_cgcg(const oracle_ctx* c, const double* b, double* x, double tol, int
    |g_{j+1}| is the residual norm; stop when it is <= tol or at maxit; then
    y = H^-1 g (upper triangular), x += M^-1 V y.  hist[k] = |g| after iteration
    k (hist[0] = ||b - A x0||_c).  Returns 0 converged, 1 not converged. */
+/* One Arnoldi step of right-Jacobi-preconditioned GMRES (Table 2,
+   reading Q25): w = A M^-1 v_j, then modified Gram-Schmidt against
+   v_0..v_j applied twice (one reorthogonalisation pass, which keeps the
+   basis orthogonal over long cycles), H(0:j+1, j) and v_{j+1} = w / ||w||_c.
+   Returns ||w||_c.  t, w: scratch of nslots. */
+static double arnoldi_step(const oracle_ctx* c, double* V, int j, int m, double* t, double* w,
+                           double* H) {
+  const int64_t ns = c->nslots;
+  double* vj = V + (int64_t)j * ns;
+  for (int64_t l = 0; l < ns; l++) t[l] = c->dinv[l] * vj[l];
+  oracle_apply(c, t, w);
+  for (int i = 0; i <= j; i++) H[i * m + j] = 0.0;
+  for (int pass = 0; pass < 2; pass++)
+    for (int i = 0; i <= j; i++) {
+      const double* vi = V + (int64_t)i * ns;
+      const double h = oracle_dot_c(c, w, vi);
+      H[i * m + j] += h;
+      for (int64_t l = 0; l < ns; l++) w[l] -= h * vi[l];
+    }
+  const double hn = sqrt(oracle_dot_c(c, w, w));
+  H[(j + 1) * m + j] = hn;
+  double* vn = V + (int64_t)(j + 1) * ns;
+  for (int64_t l = 0; l < ns; l++) vn[l] = hn > 0.0 ? w[l] / hn : 0.0;
+  return hn;
+}
+
+/* test access: m Arnoldi steps from v_0 = b / ||b||_c with the same step as
+   oracle_gmres; V [(m+1) x nslots], H [(m+1) x m] row-major (H[i*m + j]) */
+int oracle_arnoldi(const oracle_ctx* c, const double* b, int m, double* V, double* H) {
+  if (!c || m < 1) return -1;
+  const int64_t ns = c->nslots;
+  double* w = (double*)malloc(sizeof(double) * ns);
+  double* t = (double*)malloc(sizeof(double) * ns);
+  if (!w || !t) { free(w); free(t); return -5; }
+  for (int i = 0; i < (m + 1) * m; i++) H[i] = 0.0;
+  const double beta = sqrt(oracle_dot_c(c, b, b));
+  for (int64_t l = 0; l < ns; l++) V[l] = b[l] / beta;
+  for (int j = 0; j < m; j++) arnoldi_step(c, V, j, m, t, w, H);
+  free(w); free(t);
+  return 0;
+}
+
 int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
                  int restart, int* iters, double* res_final, double* res_true, double* hist) {
   if (!c || maxit < 0 || restart < 1) return -1;
@@ -764,24 +806,8 @@ int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, in
     g[0] = beta;
     int j = 0;
     for (; j < m && k < maxit; j++) {
-      double* vj = V + (int64_t)j * ns;
-      for (int64_t l = 0; l < ns; l++) t[l] = c->dinv[l] * vj[l];
-      oracle_apply(c, t, w);
+      const double hn = arnoldi_step(c, V, j, m, t, w, H);
       k++;
-      /* modified Gram-Schmidt, applied twice (one reorthogonalisation pass,
-         reading Q25): keeps the basis orthogonal over long cycles */
-      for (int i = 0; i <= j; i++) H[i * m + j] = 0.0;
-      for (int pass = 0; pass < 2; pass++)
-        for (int i = 0; i <= j; i++) {
-          const double* vi = V + (int64_t)i * ns;
-          const double h = oracle_dot_c(c, w, vi);
-          H[i * m + j] += h;
-          for (int64_t l = 0; l < ns; l++) w[l] -= h * vi[l];
-        }
-      const double hn = sqrt(oracle_dot_c(c, w, w));
-      H[(j + 1) * m + j] = hn;
-      double* vn = V + (int64_t)(j + 1) * ns;
-      for (int64_t l = 0; l < ns; l++) vn[l] = hn > 0.0 ? w[l] / hn : 0.0;
       for (int i = 0; i < j; i++) {   /* previous rotations */
         const double a = H[i * m + j], bb = H[(i + 1) * m + j];
         H[i * m + j] = cs[i] * a + sn[i] * bb;

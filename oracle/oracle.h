@@ -83,6 +83,8 @@ int oracle_cgcg(const oracle_ctx* c, const double* b, double* x, double tol, int
                 int* iters, double* res_final, double* res_true, double* hist);
 /* NEXT-3 (Table 2): restarted GMRES with right Jacobi
    preconditioning, and the solution-projection space (Fischer 1998). */
+/* test access: m Arnoldi steps (the oracle_gmres step) from b; V [(m+1) x nslots], H [(m+1) x m] */
+int oracle_arnoldi(const oracle_ctx* c, const double* b, int m, double* V, double* H);
 int oracle_gmres(const oracle_ctx* c, const double* b, double* x, double tol, int maxit,
                  int restart, int* iters, double* res_final, double* res_true, double* hist);
 typedef struct oracle_proj oracle_proj;

@@ -66,6 +66,7 @@ _SIGS = {
     "sem_pcg_history": [_P, _P, C.c_int32, C.POINTER(C.c_int32)],
     "sem_export_field": [_P, C.c_int, _P],
     "sem_export_int": [_P, C.c_int, _P],
+    "sem_export_plan": [_P, C.POINTER(_P)],
     "sem_plan_create": [C.POINTER(SemMesh), C.c_int, C.POINTER(_P)],
     "sem_plan_destroy": [_P],
     "sem_plan_sizes": [_P, _I64P, _I64P, _I64P, _I64P, C.POINTER(C.c_int32)],
@@ -317,6 +318,12 @@ class Context:
         _check(load().sem_export_field(self._h, which, C.c_void_p(out.ctypes.data)))
         return out.reshape(self.n, self.n) if name == "D" else out
 
+    def export_plan(self):
+        """The gather-scatter plan the kernels use, read back from the device (a Plan)."""
+        h = C.c_void_p()
+        _check(load().sem_export_plan(self._h, C.byref(h)))
+        return Plan._from_handle(h, self.N)
+
     def export_int(self, name):
         which = {"mult": 0, "mask": 1}[name]
         out = np.zeros(self.n_local, dtype=np.int64)
@@ -382,6 +389,16 @@ class Plan:
         m = _mesh(spec, rank, nranks)
         h = C.c_void_p()
         _check(L.sem_plan_create(C.byref(m), N, C.byref(h)))
+        self._init(h, N)
+
+    @classmethod
+    def _from_handle(cls, h, N):
+        self = cls.__new__(cls)
+        self._init(h, N)
+        return self
+
+    def _init(self, h, N):
+        L = load()
         self._h = h
         self.N = N
         a, b, c, d, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()

@@ -1710,6 +1710,52 @@ extern "C" int sem_export_int(const sem_ctx* c, int which, int64_t* host_dst) {
   return SEM_OK;
 }
 
+// live plan export: the gather-scatter records the kernels use, read back from
+// the device into a planner handle (its pairs / segments / shared lists are
+// expanded from these records; multiplicity and mask from the device arrays)
+extern "C" int sem_export_plan(const sem_ctx* c, sem_plan** out) {
+  if (!c || !out) { sem::set_error("sem_export_plan: NULL argument"); return SEM_EINVAL; }
+  *out = nullptr;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  sem::HostPlan p = c->hp;
+  auto get = [](auto& v, const auto* d) -> cudaError_t {
+    if (v.empty()) return cudaSuccess;
+    return cudaMemcpy(v.data(), d, v.size() * sizeof(v[0]), cudaMemcpyDeviceToHost);
+  };
+  // overwrite every record with the device copy (sizes from the host plan)
+  std::fill(p.f_base.begin(), p.f_base.end(), -7);
+  std::fill(p.e_base.begin(), p.e_base.end(), -7);
+  std::fill(p.v_base.begin(), p.v_base.end(), -7);
+  std::fill(p.s_slot.begin(), p.s_slot.end(), -7);
+  CUDA_TRY(get(p.f_base, c->d_fb));
+  CUDA_TRY(get(p.f_axis, c->d_fax));
+  CUDA_TRY(get(p.e_base, c->d_eb));
+  CUDA_TRY(get(p.e_axis, c->d_eax));
+  CUDA_TRY(get(p.e_nin, c->d_enin));
+  CUDA_TRY(get(p.e_mask, c->d_emask));
+  CUDA_TRY(get(p.v_base, c->d_vb));
+  CUDA_TRY(get(p.v_nin, c->d_vnin));
+  CUDA_TRY(get(p.v_mask, c->d_vmask));
+  CUDA_TRY(get(p.s_slot, c->d_sslot));
+  CUDA_TRY(get(p.s_off, c->d_soff));
+  CUDA_TRY(get(p.s_nloc, c->d_snloc));
+  CUDA_TRY(get(p.s_nr, c->d_snr));
+  CUDA_TRY(get(p.s_mult, c->d_smult));
+  const size_t nl = (size_t)p.n_local;
+  std::vector<uint8_t> mult(nl), mask(nl);
+  CUDA_TRY(cudaMemcpy(mult.data(), c->d_mult, nl, cudaMemcpyDeviceToHost));
+  uint8_t* d = nullptr;
+  SEM_TRY(dalloc(&d, nl));
+  CUDA_TRY(sem::launch_export_mask(c->dp, d, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(mask.data(), d, nl, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  p.x_mult.assign(mult.begin(), mult.end());
+  p.x_mask.assign(mask.begin(), mask.end());
+  *out = sem::plan_wrap(p);
+  return *out ? SEM_OK : SEM_ENOMEM;
+}
+
 extern "C" int sem_nccl_unique_id(uint8_t id[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   ncclUniqueId u;
@@ -1762,8 +1808,8 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     return SEM_OK;
   }
   if (option == SEM_OPT_GS_MODE) {
-    if (value < 0 || value > 5) {
-      sem::set_error("sem_set_option: SEM_OPT_GS_MODE must be in 0..5");
+    if (value < 0 || value > 2) {
+      sem::set_error("sem_set_option: SEM_OPT_GS_MODE must be 0, 1 or 2");
       return SEM_EINVAL;
     }
     c->gs_mode = value;

@@ -34,97 +34,19 @@ __device__ __forceinline__ int f_s1(int axis, int n) { return axis == 0 ? n : 1;
 __device__ __forceinline__ int f_s2(int axis, int n) { return axis == 2 ? n : n * n; }
 __device__ __forceinline__ int e_sd(int axis, int n) { return axis == 0 ? 1 : (axis == 1 ? n : n * n); }
 
-// Flat variant for meshes whose w fits in L2 (no DRAM re-streaming to avoid):
-// every thread takes its share of each class in turn, tid-strided over the whole
-// grid (perfect balance).  Face points (2 incidences, ~85% of the points) are
-// processed F = 4 per thread with all 2F loads issued before any use (the
-// kernel is L2-latency bound); edges and vertices one per thread.
-template <int n>
+// Flat schedule (w L2-resident or moderately larger): each entity class is
+// spread over the whole grid.  The kernel is latency bound (scattered 8-byte
+// accesses), so every thread issues ALL its loads of a round before any use:
+// the index records of F face points and FE edge points first, then their
+// 2F + 4FE data loads, then the sums and the broadcast stores (fire and
+// forget).  A round covers nth*F face points and nth*FE edge points
+// (consecutive threads on consecutive points of an entity: coalesced where
+// the layout allows); vertices (few) follow in a grid-stride loop.  F = 6,
+// FE = 2 measured best of (4,1), (6,2), (8,2) and of the earlier
+// faces-then-edges loop on C2 / C3 (profiles/r02_experiments/gs_*.jsonl).
+constexpr int kGsF = 6, kGsFE = 2;
+template <int n, int F = kGsF, int FE = kGsFE>
 __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restrict__ u,
-                                              int apply_mask, int tid, int nth) {
-  constexpr int N = n - 1;
-  constexpr int nf = (N - 1) * (N - 1), ne = N - 1;
-  constexpr int Nm1 = N > 1 ? N - 1 : 1;
-  constexpr int F = 4;
-  const int tF = P.nF * nf, tE = P.nEd * ne, tot = tF + tE + P.nV;
-  if (nf > 0) {
-    for (int t0 = tid; t0 < tF; t0 += nth * F) {
-      int a0[F], a1[F];
-      bool ok[F];
-#pragma unroll
-      for (int q = 0; q < F; q++) {
-        const int t = t0 + q * nth;
-        ok[q] = t < tF;
-        const int f = ok[q] ? t / (nf > 0 ? nf : 1) : 0;
-        const int p = t - f * nf;
-        const int ax = P.f_axis[f];
-        const int off = (1 + p % Nm1) * f_s1(ax, n) + (1 + p / Nm1) * f_s2(ax, n);
-        const int2 b2 = reinterpret_cast<const int2*>(P.f_base)[f];
-        a0[q] = b2.x + off;
-        a1[q] = b2.y + off;
-      }
-      double v0[F], v1[F];
-#pragma unroll
-      for (int q = 0; q < F; q++)
-        if (ok[q]) {
-          v0[q] = gs_ld(&u[a0[q]]);
-          v1[q] = gs_ld(&u[a1[q]]);
-        }
-#pragma unroll
-      for (int q = 0; q < F; q++)
-        if (ok[q]) {
-          const double s = v0[q] + v1[q];
-          gs_st(&u[a0[q]], s);
-          gs_st(&u[a1[q]], s);
-        }
-    }
-  }
-  for (int t = tF + tid; t < tot; t += nth) {
-    int32_t base[8];
-    int nin, off;
-    bool mk = false;
-    if (ne > 0 && t < tF + tE) {
-      const int q = t - tF, e = q / (ne > 0 ? ne : 1);
-      const int p = q - e * ne;
-      off = (1 + p) * e_sd(P.e_axis[e], n);
-      nin = P.e_nin[e];
-      const int4 b4 = reinterpret_cast<const int4*>(P.e_base)[e];
-      base[0] = b4.x; base[1] = b4.y; base[2] = b4.z; base[3] = b4.w;
-      mk = P.e_mask[e];
-    } else {
-      const int v = t - tF - tE;
-      off = 0;
-      nin = P.v_nin[v];
-      const int4 b0 = reinterpret_cast<const int4*>(P.v_base)[2 * v];
-      const int4 b1 = reinterpret_cast<const int4*>(P.v_base)[2 * v + 1];
-      base[0] = b0.x; base[1] = b0.y; base[2] = b0.z; base[3] = b0.w;
-      base[4] = b1.x; base[5] = b1.y; base[6] = b1.z; base[7] = b1.w;
-      mk = P.v_mask[v];
-    }
-    double v[8];
-#pragma unroll
-    for (int x = 0; x < 8; x++)
-      if (x < nin) v[x] = gs_ld(&u[base[x] + off]);
-    double s = v[0];
-#pragma unroll
-    for (int x = 1; x < 8; x++)
-      if (x < nin) s += v[x];
-    if (apply_mask && mk) s = 0.0;
-#pragma unroll
-    for (int x = 0; x < 8; x++)
-      if (x < nin) gs_st(&u[base[x] + off], s);
-  }
-}
-
-// Flat variant 2 (high memory-level parallelism): the kernel is L2-latency
-// bound, so every thread issues ALL its loads of a round before any use: the
-// index records of F face points and FE edge points first, then their 2F +
-// 4 FE data loads, then the sums and the broadcast stores (fire and forget).
-// A round covers nth*F face points and nth*FE edge points (consecutive
-// threads on consecutive points of an entity: coalesced where the layout
-// allows); vertices (few) follow in a grid-stride loop.
-template <int n, int F, int FE>
-__device__ __forceinline__ void gs_flat2_body(const DevPlan& P, double* __restrict__ u,
                                                int apply_mask, int tid, int nth) {
   constexpr int N = n - 1;
   constexpr int nf = (N - 1) * (N - 1), ne = N - 1;
@@ -230,7 +152,7 @@ __device__ __forceinline__ void gs_flat2_body(const DevPlan& P, double* __restri
 // elements per chunk: ~SEM_GS_CHUNK_PTS entity points (3 faces, 3 edges and one
 // vertex per element in the interior of a box)
 #ifndef SEM_GS_FLAT_BYTES
-#define SEM_GS_FLAT_BYTES (64ll << 20)   // auto mode: flat sweep while w fits in ~half of L2
+#define SEM_GS_FLAT_BYTES (256ll << 20)   // auto mode: flat schedule up to 256 MB of w (C3: 134 MB)
 #endif
 // mode 0 auto, 1 flat, 2 element-ordered chunks -> ce (0 = flat)
 int gs_chunk_elems(int N);

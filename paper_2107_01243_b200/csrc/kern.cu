@@ -223,15 +223,6 @@ __global__ void __launch_bounds__(256, SEM_GS_MINB) gs_local_kernel(const DevPla
   gs_local_body<n, SWEEP>(P, u, apply_mask, P.gs_ctr, base, ce);
 }
 
-template <int n, int F, int FE>
-__global__ void __launch_bounds__(256) gs_flat2_kernel(const DevPlan P, double* __restrict__ u,
-                                                       int apply_mask) {
-  pdl_wait();
-  pdl_trigger();
-  gs_flat2_body<n, F, FE>(P, u, apply_mask, blockIdx.x * blockDim.x + threadIdx.x,
-                          gridDim.x * blockDim.x);
-}
-
 // Alg. 1 lines 6-7: this rank's partial for every shared point (ascending local
 // slots), copied into the send buffer of every neighbour that shares it.
 __global__ void gs_pack_kernel(const DevPlan P, const double* __restrict__ u, double* part,
@@ -617,54 +608,11 @@ cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStre
   return cudaGetLastError();
 }
 
-template <int n, int F, int FE>
-static cudaError_t launch_flat2_n(const DevPlan& P, double* u, int apply_mask, cudaStream_t s) {
-  auto kern = dev::gs_flat2_kernel<n, F, FE>;
-  static std::atomic<int> cache[kMaxDev];
-  const int dev = device_index();
-  int resident = cache[dev].load(std::memory_order_relaxed);
-  if (resident == 0) {
-    int sms = 148, nb = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, 0);
-    resident = std::max(nb, 1) * sms;
-    cache[dev].store(resident, std::memory_order_relaxed);
-  }
-  const int64_t N = P.N;
-  const int64_t need = std::max(std::max<int64_t>((P.nF * (N - 1) * (N - 1) + F - 1) / F,
-                                                 (P.nEd * (N - 1) + FE - 1) / FE),
-                                (int64_t)P.nV);
-  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(resident, (need + kThreads - 1) / kThreads));
-  return launch_k(kern, dim3(g), dim3(kThreads), 0, s, P, u, apply_mask);
-}
-
-template <int F, int FE>
-static cudaError_t launch_flat2(const DevPlan& P, double* u, int apply_mask, cudaStream_t s) {
-  switch (P.n) {
-    case 2: return launch_flat2_n<2, F, FE>(P, u, apply_mask, s);
-    case 3: return launch_flat2_n<3, F, FE>(P, u, apply_mask, s);
-    case 4: return launch_flat2_n<4, F, FE>(P, u, apply_mask, s);
-    case 5: return launch_flat2_n<5, F, FE>(P, u, apply_mask, s);
-    case 6: return launch_flat2_n<6, F, FE>(P, u, apply_mask, s);
-    case 7: return launch_flat2_n<7, F, FE>(P, u, apply_mask, s);
-    case 8: return launch_flat2_n<8, F, FE>(P, u, apply_mask, s);
-    case 9: return launch_flat2_n<9, F, FE>(P, u, apply_mask, s);
-    case 10: return launch_flat2_n<10, F, FE>(P, u, apply_mask, s);
-    case 11: return launch_flat2_n<11, F, FE>(P, u, apply_mask, s);
-    case 12: return launch_flat2_n<12, F, FE>(P, u, apply_mask, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
 cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_t* base,
                             int mode, cudaStream_t s) {
   const int64_t N = P.N;
   const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
   if (tot == 0) return cudaSuccess;
-  // experimental flat variant 2 schedules (SEM_OPT_GS_MODE 3..5)
-  if (mode == 3) return launch_flat2<4, 1>(P, u, apply_mask, s);
-  if (mode == 4) return launch_flat2<6, 2>(P, u, apply_mask, s);
-  if (mode == 5) return launch_flat2<8, 2>(P, u, apply_mask, s);
   // co-resident grid (x SEM_GS_GRIDX); chunk mode: blocks pull element chunks
   static std::atomic<int> cache[kMaxDev][2];
   const int dev = device_index();
@@ -681,8 +629,12 @@ cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_
     cache[dev][1].store(resident[1], std::memory_order_relaxed);
   }
   const int ce = dev::gs_mode_ce(P, mode);
+  // flat: enough threads for one round (F face points, FE edge points, one vertex each)
+  const int64_t need = std::max(std::max<int64_t>((P.nF * (N - 1) * (N - 1) + dev::kGsF - 1) / dev::kGsF,
+                                                 (P.nEd * (N - 1) + dev::kGsFE - 1) / dev::kGsFE),
+                                (int64_t)P.nV);
   const int g = ce > 0 ? std::max(1, std::min(resident[1], (P.nloc + ce - 1) / ce))
-                       : grid_for(tot, resident[0]);
+                       : grid_for(need, resident[0]);
   const unsigned long long b = *base;
   *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
 #define GS_LAUNCH(k)                                                                        \

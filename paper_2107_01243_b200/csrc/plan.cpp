@@ -499,6 +499,12 @@ extern "C" int sem_plan_create(const sem_mesh* m, int N, sem_plan** out) {
   return SEM_OK;
 }
 
+sem_plan* sem::plan_wrap(const sem::HostPlan& p) {
+  sem_plan* h = new (std::nothrow) sem_plan();
+  if (h) h->p = p;
+  return h;
+}
+
 extern "C" int sem_plan_destroy(sem_plan* h) {
   delete h;
   return SEM_OK;
@@ -577,6 +583,13 @@ extern "C" int sem_plan_slots(const sem_plan* h, int64_t* gid, int64_t* mult, in
           if (mask) mask[l] = sem::slot_masked(p, p.e_lo + el, i, j, k) ? 1 : 0;
           if (mult) mult[l] = 1;
         }
+  if (!p.x_mult.empty()) {   // live export: the device's multiplicity and mask
+    for (int64_t l = 0; l < p.n_local; l++) {
+      if (mult) mult[l] = p.x_mult[l];
+      if (mask) mask[l] = p.x_mask[l];
+    }
+    return SEM_OK;
+  }
   if (mult) {
     std::vector<std::vector<int64_t>> g;
     expand(p, &g);

@@ -55,7 +55,12 @@ struct HostPlan {
   int64_t nbuf = 0;
   // Alg. 1 overlap: boundary elements [b0lo,b0hi) U [b1lo,b1hi), interior [ilo,ihi)
   int64_t b0lo = 0, b0hi = 0, b1lo = 0, b1hi = 0, ilo = 0, ihi = 0;
+  // live-context export (sem_export_plan): multiplicity and mask read back from
+  // the device (empty for a host-only plan, which derives them itself)
+  std::vector<int64_t> x_mult, x_mask;
 };
+// a planner handle around a copy of p (sem_export_plan; destroyed by sem_plan_destroy)
+sem_plan* plan_wrap(const HostPlan& p);
 
 int build_plan(const sem_mesh* m, int N, HostPlan* p);   // returns SEM_* status
 // device G layout (see dev_common.cuh g_index): G[e][k][f][i + n j]

@@ -477,3 +477,58 @@ def test_ax_pdl_identical(spec, N):
         if o is not None:
             ref = o.pcg(host(bd), 0.0, 25)
             assert np.abs(out[1][0] - ref["x"]).max() <= 1e-10 * max(1.0, np.abs(ref["x"]).max())
+
+
+# ---------------------------------------------------------------- live plan export
+LIVE_PLAN = [(unit_box(2, 2, 2), 3, 1), (tgv_box(3, 4, 2), 5, 1), (tgv_box(4, 4, 4, deform=1), 7, 1),
+             (unit_box(3, 2, 4, periodic=(1, 0, 0)), 2, 1), (tgv_box(2, 2, 4), 3, 2),
+             (unit_box(3, 2, 5), 3, 3), (tgv_box(4, 2, 2), 4, 4)]
+
+
+@pytest.mark.parametrize("spec,N,P", LIVE_PLAN, ids=[f"{s.ex}x{s.ey}x{s.ez}-N{N}-P{P}" for s, N, P in LIVE_PLAN])
+def test_live_plan_export_bit_exact(spec, N, P):
+    """sem_export_plan: the gather-scatter records the device kernels use, read
+    back from a live context (P > 1: each rank of a loopback world), expand to
+    the oracle's numbering, multiplicity, mask, pairs, segments and shared
+    lists bit-exactly (Alg. 1)."""
+    import threading
+    import torch
+    o = O.Oracle(spec, N, nranks=P)
+    plans = [None] * P
+    if P == 1:
+        with sem().sem_setup(spec, N) as c:
+            plans[0] = c.export_plan()
+    else:
+        world = sem().loopback_create(P)
+        errs = []
+
+        def rank(r):
+            try:
+                st = torch.cuda.Stream()
+                with sem().sem_setup(spec, N, rank=r, nranks=P, nccl_comm=sem().loopback_comm(world, r),
+                                     stream=st.cuda_stream) as c:
+                    plans[r] = c.export_plan()
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+        th = [threading.Thread(target=rank, args=(r,)) for r in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        sem().loopback_destroy(world)
+        assert not errs, errs
+    orank = o.get_int("rank")
+    for r, p in enumerate(plans):
+        sel = orank == r
+        gid, mult, mask = p.slots()
+        assert np.array_equal(gid, o.get_int("gid")[sel])
+        assert np.array_equal(mult, o.get_int("mult")[sel])
+        assert np.array_equal(mask, o.get_int("mask")[sel])
+        ranks, counts = p.neighbors()
+        assert ranks.tolist() == [q for q in range(P) if q != r and len(o.shared(r, q))]
+        for q in ranks:
+            assert np.array_equal(p.shared(int(q)), o.shared(r, int(q)))
+    if P == 1:
+        op, ooff, oslots = o.plan()
+        pp, poff, pslots = plans[0].pairs()
+        assert np.array_equal(pp, op) and np.array_equal(poff, ooff) and np.array_equal(pslots, oslots)

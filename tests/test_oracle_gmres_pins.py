@@ -139,3 +139,36 @@ def test_projection_pipeline_repeated_and_sequence():
         it_proj.append(pp.solve(bt, 1e-10, 500)["iters"])
         it_plain.append(o.gmres(bt, 1e-10, 500)["iters"])
     assert sum(it_proj[1:]) < sum(it_plain[1:]), (it_proj, it_plain)
+
+
+def test_arnoldi_basis_orthonormal_where_single_pass_mgs_is_not():
+    """Reading Q25 pin: the oracle's Arnoldi step (modified Gram-Schmidt applied
+    twice) keeps V^T C V = I to ~1e-13 on a case where the same Arnoldi process
+    with ONE MGS pass -- written out here in numpy on the dense assembled
+    operator -- loses orthogonality by orders of magnitude more (the Krylov
+    space nearly captures an invariant subspace, kappa(K) ~ 1/eps^(1/2)).  Also
+    A M^-1 V_m = V_{m+1} H (the Arnoldi relation) to rounding."""
+    o = O.Oracle(tgv_box(2, 2, 2, deform=1), 3)
+    Q, A, keep, gid, first = _reduced(o)
+    Minv = 1.0 / np.diag(A)
+    bk = random_field(o.nglob, seed=11)[keep]
+    m = 40
+    V, H = o.arnoldi(_to_slots(o, keep, gid, bk), m)
+    c = 1.0 / o.get_int("mult")
+    gram = (V * c) @ V.T
+    loss2 = np.abs(gram - np.eye(m + 1)).max()
+    # single-pass MGS on the unique DOFs (Euclidean = the c-weighted slot norm)
+    W = np.zeros((len(bk), m + 1))
+    W[:, 0] = bk / np.linalg.norm(bk)
+    for j in range(m):
+        w = A @ (Minv * W[:, j])
+        for i in range(j + 1):
+            w -= (w @ W[:, i]) * W[:, i]
+        W[:, j + 1] = w / np.linalg.norm(w)
+    loss1 = np.abs(W.T @ W - np.eye(m + 1)).max()
+    assert loss2 <= 1e-12, loss2
+    assert loss1 >= 1e3 * loss2, (loss1, loss2)
+    # Arnoldi relation on the unique DOFs: A M^-1 V_m = V_{m+1} H
+    Vk = np.stack([v[first][keep] for v in V], axis=1)
+    R = A @ (Minv[:, None] * Vk[:, :m]) - Vk @ H
+    assert np.abs(R).max() <= 1e-11 * np.abs(A).max()
