@@ -295,6 +295,11 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    geometric-factor planes before waiting for the preceding kernel; 0 = plain
    order.  Identical results. */
 #define SEM_OPT_AX_PDL 13
+/* 1 (default) = on one rank with the flat gather-scatter schedule, the
+   kernels of each batch of 8 Jacobi-PCG iterations are captured once into a
+   CUDA graph (cached per x / Jacobi operand) and replayed; 0 = stream
+   launches.  Identical results. */
+#define SEM_OPT_PCG_GRAPH 14
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

@@ -130,6 +130,11 @@ struct sem_ctx {
   int pcg_variant = 0;     // SEM_OPT_PCG_VARIANT: 0 standard, 1 single-reduction (Chronopoulos-Gear)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
   cudaGraphExec_t g0exec = nullptr;
+  // SEM_OPT_PCG_GRAPH: one-rank PCG batches replayed as a CUDA graph
+  bool pcg_graph = true;
+  cudaGraphExec_t pg_exec = nullptr;
+  double pg_key[4] = {0, 0, 0, 0};
+  int64_t pg_launches = 0;
   int g0_iters = -1;
   int64_t g0_launches = 0;
   int* d_gate = nullptr;
@@ -486,6 +491,7 @@ void free_ctx(sem_ctx* c) {
   if (c->d_ktick) cudaFree(c->d_ktick);
   if (c->c0) free_ctx(c->c0);
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
+  if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
   if (c->d_gate) cudaFree(c->d_gate);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -974,6 +980,52 @@ static int cgcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t 
   return pcg_finish(c, b, x, res);
 }
 
+// One rank, flat gather-scatter schedule: the kernels of kBatch PCG iterations
+// have fixed arguments (no gs chunk tickets, no peer-memory epochs), so the
+// batch is captured once into a CUDA graph (SEM_OPT_PCG_GRAPH) and replayed;
+// the graph is keyed by the operands that enter the kernel arguments.
+// Returns nullptr (plain stream launches) when not applicable.
+static cudaGraphExec_t pcg_batch_graph(sem_ctx* c, const double* dinv, double* x, const PcgCtl& k) {
+  if (!c->pcg_graph || c->hp.nranks > 1 || c->timing || c->ax_gate ||
+      !sem::gs_flat(c->dp, c->gs_mode))
+    return nullptr;
+  const double key[4] = {(double)(uintptr_t)x, (double)(uintptr_t)dinv, c->helm ? c->h1 : -1.0,
+                         c->helm ? c->h2 : -1.0};
+  if (c->pg_exec && std::memcmp(key, c->pg_key, sizeof(key)) == 0) return c->pg_exec;
+  if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
+  c->pg_exec = nullptr;
+  if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  // capture on a private stream (the context stream may be the legacy one)
+  cudaStream_t s_save = c->stream;
+  c->stream = c->cap_stream;
+  const int64_t l0 = c->launches;
+  cudaGraph_t graph = nullptr;
+  int st = SEM_OK;
+  if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    for (int q = 0; q < kBatch && st == SEM_OK; q++) st = pcg_enqueue_iter(c, dinv, x, k);
+    if (cudaStreamEndCapture(c->cap_stream, &graph) != cudaSuccess) st = SEM_ECUDA;
+  } else {
+    st = SEM_ECUDA;
+  }
+  c->stream = s_save;
+  c->pg_launches = c->launches - l0;
+  c->launches = l0;
+  cudaGraphExec_t ge = nullptr;
+  if (st == SEM_OK && graph && cudaGraphInstantiate(&ge, graph, 0) != cudaSuccess) ge = nullptr;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (!ge) {
+    c->pcg_graph = false;   // not capturable here: plain stream launches from now on
+    return nullptr;
+  }
+  c->pg_exec = ge;
+  std::memcpy(c->pg_key, key, sizeof(key));
+  return ge;
+}
+
 static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                    sem_pcg_result* res) {
   if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
@@ -993,7 +1045,13 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   int done = 0;
   for (int it = 0; it < maxit && !done; it += kBatch) {
     const int nb = std::min(kBatch, maxit - it);
-    for (int q = 0; q < nb; q++) SEM_TRY(pcg_enqueue_iter(c, dinv, x, k));
+    cudaGraphExec_t ge = nb == kBatch ? pcg_batch_graph(c, dinv, x, k) : nullptr;
+    if (ge) {
+      CUDA_TRY(cudaGraphLaunch(ge, s));
+      c->launches += c->pg_launches;
+    } else {
+      for (int q = 0; q < nb; q++) SEM_TRY(pcg_enqueue_iter(c, dinv, x, k));
+    }
     CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaEventRecord(c->ev_poll, s));
     CUDA_TRY(cudaEventSynchronize(c->ev_poll));
@@ -1828,6 +1886,13 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     cudaStreamSynchronize(c->stream);
     if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
     c->precond = value;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_PCG_GRAPH) {
+    cudaStreamSynchronize(c->stream);
+    c->pcg_graph = value != 0;
+    if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
+    c->pg_exec = nullptr;
     return SEM_OK;
   }
   if (option == SEM_OPT_AX_PDL) {

@@ -41,10 +41,17 @@ __device__ __forceinline__ int e_sd(int axis, int n) { return axis == 0 ? 1 : (a
 // 2F + 4FE data loads, then the sums and the broadcast stores (fire and
 // forget).  A round covers nth*F face points and nth*FE edge points
 // (consecutive threads on consecutive points of an entity: coalesced where
-// the layout allows); vertices (few) follow in a grid-stride loop.  F = 6,
-// FE = 2 measured best of (4,1), (6,2), (8,2) and of the earlier
-// faces-then-edges loop on C2 / C3 (profiles/r02_experiments/gs_*.jsonl).
-constexpr int kGsF = 6, kGsFE = 2;
+// the layout allows); vertices (few) follow in a grid-stride loop.  F = 3,
+// FE = 1 measured best of (2,1), (3,1), (4,1), (6,2), (8,2) and of the
+// round-1 faces-then-edges loop, inside the PCG iteration on C2 and C3
+// (profiles/r02_experiments/gs_flat_ab.jsonl).
+#ifndef SEM_GS_FF
+#define SEM_GS_FF 3
+#endif
+#ifndef SEM_GS_FFE
+#define SEM_GS_FFE 1
+#endif
+constexpr int kGsF = SEM_GS_FF, kGsFE = SEM_GS_FFE;
 template <int n, int F = kGsF, int FE = kGsFE>
 __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restrict__ u,
                                                int apply_mask, int tid, int nth) {

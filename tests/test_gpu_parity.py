@@ -532,3 +532,24 @@ def test_live_plan_export_bit_exact(spec, N, P):
         op, ooff, oslots = o.plan()
         pp, poff, pslots = plans[0].pairs()
         assert np.array_equal(pp, op) and np.array_equal(poff, ooff) and np.array_equal(pslots, oslots)
+
+
+@pytest.mark.parametrize("spec,N", [(tgv_box(8, 8, 8), 7), (CONFIGS["C1"][0], 3), (tgv_box(4, 3, 5, deform=1), 5)])
+def test_pcg_graph_identical(spec, N):
+    """SEM_OPT_PCG_GRAPH: 8-iteration batches replayed as a CUDA graph give the
+    stream-launched iterates bit for bit (and the graph is reused by a second
+    solve with the same operands)."""
+    o = O.Oracle(spec, N)
+    fun = f_tgv if all(spec.periodic) else f_sin
+    b = dev(o.rhs(fun(o.get("X"), o.get("Y"), o.get("Z"))))
+    ref = o.pcg(host(b), 1e-10, 3000)
+    with sem().sem_setup(spec, N) as c:
+        outs = []
+        for g in (False, True, True):
+            c.set_pcg_graph(g)
+            x = c.zeros()
+            r = c.pcg_solve(b, x, 1e-10, 3000)
+            outs.append((host(x), r["iters"], c.pcg_history()))
+        for x_, it, h in outs[1:]:
+            assert it == outs[0][1] and np.array_equal(x_, outs[0][0]) and np.array_equal(h, outs[0][2])
+        assert abs(outs[0][1] - ref["iters"]) <= 1 and np.abs(outs[0][0] - ref["x"]).max() <= 1e-10

@@ -54,6 +54,8 @@ def main():
                                   "ax_frac_copy": nl * 64 / (ax / 1e3) / 1e9 / 6550.7,
                                   "apply_us": ap * 1e3}), flush=True)
                 continue
+            if os.environ.get("PCG_GRAPH") == "0":
+                c.set_pcg_graph(False)
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
