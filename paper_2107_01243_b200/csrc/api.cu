@@ -88,10 +88,9 @@ struct sem_ctx {
   double *d_xi = nullptr, *d_w = nullptr, *d_D = nullptr, *d_G = nullptr, *d_B = nullptr,
          *d_dinv = nullptr;
   uint8_t *d_mult = nullptr, *d_bmask = nullptr;
-  int32_t *d_eref = nullptr, *d_fb = nullptr, *d_eb = nullptr, *d_vb = nullptr;
+  int32_t *d_fb = nullptr, *d_eb = nullptr, *d_vb = nullptr;
   uint8_t *d_fax = nullptr, *d_eax = nullptr, *d_enin = nullptr, *d_emask = nullptr,
           *d_vnin = nullptr, *d_vmask = nullptr;
-  unsigned* d_cnt = nullptr;
   int32_t *d_fst = nullptr, *d_est = nullptr, *d_vst = nullptr;
   unsigned long long* d_gsctr = nullptr;   // gs chunk counters (never reset)
   uint64_t gs_base[2] = {0, 0};            // host copies: tickets taken so far
@@ -476,8 +475,8 @@ int ensure_hist(sem_ctx* c, int maxit) {
 void free_ctx(sem_ctx* c) {
   if (!c) return;
   void* ptrs[] = {c->d_xi, c->d_w, c->d_D, c->d_G, c->d_B, c->d_dinv, c->d_mult, c->d_bmask,
-                  c->d_eref, c->d_fb, c->d_eb, c->d_vb, c->d_fax, c->d_eax, c->d_enin,
-                  c->d_emask, c->d_vnin, c->d_vmask, c->d_cnt, c->d_sslot, c->d_soff,
+                  c->d_fb, c->d_eb, c->d_vb, c->d_fax, c->d_eax, c->d_enin,
+                  c->d_emask, c->d_vnin, c->d_vmask, c->d_sslot, c->d_soff,
                   c->d_snloc, c->d_snr, c->d_smask, c->d_smult, c->d_part, c->d_send,
                   c->d_recv, c->d_r, c->d_p, c->d_wv, c->d_tmp, c->d_partial, c->d_tickets,
                   c->d_scal, c->d_st, c->d_hist, c->d_partial_ax, c->d_nsig, c->d_srank, c->d_fst, c->d_est,
@@ -651,7 +650,6 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(upload(&c->d_w, h.w, s));
   SETUP_TRY(upload(&c->d_D, h.D, s));
   SETUP_TRY(upload(&c->d_bmask, h.bmask, s));
-  SETUP_TRY(upload(&c->d_eref, h.eref, s));
   SETUP_TRY(upload(&c->d_fb, h.f_base, s));
   SETUP_TRY(upload(&c->d_fax, h.f_axis, s));
   SETUP_TRY(upload(&c->d_eb, h.e_base, s));
@@ -673,9 +671,6 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   SETUP_TRY(upload(&c->d_smask, h.s_mask, s));
   SETUP_TRY(upload(&c->d_smult, h.s_mult, s));
   SETUP_TRY(upload(&c->d_srank, h.s_rank, s));
-  const size_t nent = (size_t)(h.nF + h.nEd + h.nV);
-  SETUP_TRY(dalloc(&c->d_cnt, nent));
-  SETUP_CUDA(cudaMemsetAsync(c->d_cnt, 0, std::max<size_t>(nent, 1) * sizeof(unsigned), s));
   SETUP_TRY(dalloc(&c->d_part, (size_t)h.nS));
   SETUP_TRY(dalloc(&c->d_send, (size_t)h.nbuf));
   SETUP_TRY(dalloc(&c->d_recv, (size_t)h.nbuf));
@@ -696,11 +691,10 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
   sem::DevPlan& P = c->dp;
   P.N = h.N; P.n = h.n; P.nloc = (int)h.nloc; P.n_local = h.n_local;
   P.nF = (int)h.nF; P.nEd = (int)h.nEd; P.nV = (int)h.nV; P.nS = (int)h.nS;
-  P.D = c->d_D; P.bmask = c->d_bmask; P.eref = c->d_eref;
+  P.D = c->d_D; P.bmask = c->d_bmask;
   P.f_base = c->d_fb; P.f_axis = c->d_fax;
   P.e_base = c->d_eb; P.e_axis = c->d_eax; P.e_nin = c->d_enin; P.e_mask = c->d_emask;
   P.v_base = c->d_vb; P.v_nin = c->d_vnin; P.v_mask = c->d_vmask;
-  P.cnt = c->d_cnt;
   P.f_start = c->d_fst; P.e_start = c->d_est; P.v_start = c->d_vst; P.gs_ctr = c->d_gsctr;
   P.s_slot = c->d_sslot; P.s_off = c->d_soff; P.s_nloc = c->d_snloc; P.s_nr = c->d_snr;
   P.s_mask = c->d_smask; P.s_mult = c->d_smult;

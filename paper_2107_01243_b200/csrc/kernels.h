@@ -48,7 +48,6 @@ struct DevPlan {
   int nF = 0, nEd = 0, nV = 0, nS = 0;
   const double* D = nullptr;        // [n*n]
   const uint8_t* bmask = nullptr;   // [nloc]
-  const int32_t* eref = nullptr;    // [nloc*26]
   const int32_t* f_base = nullptr;  // [nF][2]
   const uint8_t* f_axis = nullptr;
   const int32_t* e_base = nullptr;  // [nEd][4]
@@ -58,7 +57,6 @@ struct DevPlan {
   const int32_t* v_base = nullptr;  // [nV][8]
   const uint8_t* v_nin = nullptr;
   const uint8_t* v_mask = nullptr;
-  unsigned* cnt = nullptr;          // [nF + nEd + nV] last-arriver tickets
   const int32_t* f_start = nullptr; // [nloc+1] entities created by each element (gs_dev.cuh)
   const int32_t* e_start = nullptr;
   const int32_t* v_start = nullptr;

@@ -294,7 +294,6 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
   const int64_t n3 = p.n3;
   const int nf_pts = (N - 1) * (N - 1), ne_pts = N - 1;
   p.bmask.assign(p.nloc, 0);
-  p.eref.assign(p.nloc * kRefsPerElem, -1);
   std::vector<uint8_t> boundary(p.nloc, 0);
 
   struct SP {
@@ -358,29 +357,23 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
             if (!K.fixed[a]) span0 += stride[a];   // spanning coords start at 1
           base[t] = (int32_t)((inc[t].e - p.e_lo) * n3 + off0 - span0);
         }
-        int32_t ref;
         if (L.cls == CLS_FACE) {
-          int64_t idx = p.nF++;
+          p.nF++;
           p.f_base.push_back(base[0]);
           p.f_base.push_back(base[1]);
           p.f_axis.push_back((uint8_t)L.axis);
-          ref = (int32_t)((CLS_FACE << kClsShift) | idx);
         } else if (L.cls == CLS_EDGE) {
-          int64_t idx = p.nEd++;
+          p.nEd++;
           for (int t = 0; t < 4; t++) p.e_base.push_back(t < nin ? base[t] : -1);
           p.e_axis.push_back((uint8_t)L.axis);
           p.e_nin.push_back((uint8_t)nin);
           p.e_mask.push_back(masked ? 1 : 0);
-          ref = (int32_t)((CLS_EDGE << kClsShift) | idx);
         } else {
-          int64_t idx = p.nV++;
+          p.nV++;
           for (int t = 0; t < 8; t++) p.v_base.push_back(t < nin ? base[t] : -1);
           p.v_nin.push_back((uint8_t)nin);
           p.v_mask.push_back(masked ? 1 : 0);
-          ref = (int32_t)((CLS_VERT << kClsShift) | idx);
         }
-        for (int t = 0; t < nin; t++)
-          p.eref[(inc[t].e - p.e_lo) * kRefsPerElem + inc[t].lid] = ref;
       } else {
         // shared with other ranks: one record per point
         int npts = L.cls == CLS_FACE ? nf_pts : (L.cls == CLS_EDGE ? ne_pts : 1);

@@ -20,7 +20,6 @@ void set_error(const std::string& msg);
 // box mesh), so a point's slot in incidence t is base[t] + offset(kind, p).
 enum EntClass { CLS_FACE = 0, CLS_EDGE = 1, CLS_VERT = 2 };
 constexpr int kRefsPerElem = 26;   // 6 faces + 12 edges + 8 vertices
-constexpr int kClsShift = 28;      // ref = (cls << 28) | index
 
 struct HostPlan {
   sem_mesh m{};
@@ -31,7 +30,6 @@ struct HostPlan {
   bool fully_periodic = false;
   std::vector<double> xi, w, D;           // GLL rule, D[i*n+j] = l_j'(xi_i)
   std::vector<uint8_t> bmask;             // [nloc] bit (2a+b): face (axis a, side b) Dirichlet
-  std::vector<int32_t> eref;              // [nloc*26] local-entity refs, -1 none
   // local entities (all incidences on this rank), SoA
   int64_t nF = 0, nEd = 0, nV = 0;
   std::vector<int32_t> f_base;            // [2][nF]

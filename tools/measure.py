@@ -278,6 +278,45 @@ def sweep(Ns, st=None, tri=None):
         torch.cuda.empty_cache()
 
 
+def c5(Ns):
+    """BASELINE configs[4] at its stated size: per N, E_axis = round(1000/(N+1)) in x, y and z
+    rounded to a multiple of 8 (sem_inputs.c5_mesh), n_p ~ 1e9 local points on ONE GPU:
+    Ax, Ax+gs (both gs schedules) and a 20-iteration Jacobi-PCG (b = A u, tol 0)."""
+    from sem_inputs import c5_mesh
+    torch.cuda.set_device(0)
+    st = torch.cuda.current_stream()
+    tri = triad(st)
+    for N in Ns:
+        spec = c5_mesh(N)
+        t0 = time.perf_counter()
+        with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
+            setup_s = time.perf_counter() - t0
+            fb, _, baxgs = bytes_model(N)
+            res = {"what": "c5", "N": N, "mesh": [spec.ex, spec.ey, spec.ez], "E": spec.E,
+                   "n_p": c.n_local, "f_b": round(fb, 3), "ax_gs_B_per_pt": round(baxgs, 1),
+                   "setup_s": round(setup_s, 1), "triad_GBps": round(tri, 0),
+                   **op_rates(c, N, st, 5, tri)}
+            u = torch.empty(c.n_local, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+            b = c.zeros()
+            c.apply(u, b)
+            del u
+            x = c.zeros()
+            c.pcg_solve(b, x, 0.0, 4)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            r = c.pcg_solve(b, x, 0.0, 20)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            res["pcg"] = {"iters": r["iters"], "ms": round(ms, 2),
+                          "iter_per_s": round(r["iters"] / (ms * 1e-3), 2),
+                          "gdofs": round(c.n_local * r["iters"] / (ms * 1e-3) / 1e9, 2)}
+            del b, x
+            out(res)
+        torch.cuda.empty_cache()
+
+
 def strong():
     import torch.distributed as dist
     rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -378,6 +417,8 @@ if __name__ == "__main__":
         strong()
     elif mode == "sweep":
         sweep([int(v) for v in sys.argv[2].split(",")])
+    elif mode == "c5":
+        c5([int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else range(1, 12))
     elif mode == "schwarz_strong":
         schwarz_strong(tuple(sys.argv[2].split(",")) if len(sys.argv) > 2 else ("C3", "C4"))
     elif mode == "schwarz":
