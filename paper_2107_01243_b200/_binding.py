@@ -266,6 +266,10 @@ class Context:
         """One rank: replay 8-iteration PCG batches as a CUDA graph (default on)."""
         _check(load().sem_set_option(self._h, 14, 1 if on else 0))
 
+    def set_pcg_fuse(self, on: bool):
+        """One rank: p update fused into the next Ax kernel (default on)."""
+        _check(load().sem_set_option(self._h, 15, 1 if on else 0))
+
     def set_ax_pdl(self, on: bool):
         """PDL launch of the PCG Ax kernel with G prefetched before the grid wait."""
         _check(load().sem_set_option(self._h, 13, 1 if on else 0))

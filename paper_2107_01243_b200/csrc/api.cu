@@ -126,6 +126,11 @@ struct sem_ctx {
   bool c0_repl = false;        // the coarse context in use is the replicated one
   bool ax_pdl = true;      // SEM_OPT_AX_PDL (C2: 123.0 -> 121.6 us per PCG iteration)
   bool ax_pdl_now = false; // set around the PCG iteration's Ax launch
+  // SEM_OPT_PCG_FUSE: one-rank Jacobi-PCG with the p update fused into the Ax
+  // kernel (and x += alpha p into the CG update): three kernels per iteration
+  bool pcg_fuse = true;
+  bool pf_now = false;            // set around the PCG iteration's Ax launch
+  const double* pf_dinv = nullptr;
   int pcg_variant = 0;     // SEM_OPT_PCG_VARIANT: 0 standard, 1 single-reduction (Chronopoulos-Gear)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
   cudaGraphExec_t g0exec = nullptr;
@@ -194,6 +199,9 @@ int dalloc(T** p, size_t count) {
     sem::set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? SEM_ENOMEM : SEM_ECUDA;
   }
+#if SEM_CHECKED   // poison (checked builds): NaN doubles, -1 indices
+  cudaMemset(*p, 0xFF, count * sizeof(T));
+#endif
   return SEM_OK;
 }
 
@@ -288,8 +296,15 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   const bool pdl = c->ax_pdl_now && !c->timing && !sem::pdl_on();
   a.pdl_pref = pdl ? 1 : 0;
   if (pdl) sem::set_pdl(true);
+  const bool pf = c->pf_now && mode == sem::AX_PCG;
+  if (pf) {   // u is p: p_old in, p_new out (in place)
+    a.rr = c->d_r;
+    a.dinv = c->pf_dinv;
+    a.pout = const_cast<double*>(u);
+    a.beta = &c->d_st->beta;
+  }
   cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream,
-                                 c->helm && mode != sem::AX_ONLY);
+                                 c->helm && mode != sem::AX_ONLY, pf);
   if (pdl) sem::set_pdl(false);
   timer_end(c, tk);
   c->launches++;
@@ -690,7 +705,7 @@ extern "C" int sem_setup(const sem_mesh* m, int N, sem_ctx** out) {
 
   sem::DevPlan& P = c->dp;
   P.N = h.N; P.n = h.n; P.nloc = (int)h.nloc; P.n_local = h.n_local;
-  P.nF = (int)h.nF; P.nEd = (int)h.nEd; P.nV = (int)h.nV; P.nS = (int)h.nS;
+  P.nF = (int)h.nF; P.nEd = (int)h.nEd; P.nV = (int)h.nV; P.nS = (int)h.nS; P.nbuf = h.nbuf;
   P.D = c->d_D; P.bmask = c->d_bmask;
   P.f_base = c->d_fb; P.f_axis = c->d_fax;
   P.e_base = c->d_eb; P.e_axis = c->d_eax; P.e_nin = c->d_enin; P.e_mask = c->d_emask;
@@ -813,6 +828,7 @@ extern "C" int sem_rhs(sem_ctx* c, const double* f, double* b) {
 // ---- PCG building blocks (pcg_run and the Schwarz coarse solve)
 struct PcgCtl {
   bool dist = false, pp = false;
+  bool pf = false;   // p update fused into the Ax kernel (one rank)
   double* rg_out = nullptr;
 };
 
@@ -822,6 +838,7 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
   k->dist = c->hp.nranks > 1;
+  k->pf = c->pcg_fuse && !k->dist;
   k->rg_out = k->dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   // peer-memory allreduces fused into the CG kernels (nranks > 1 with NVLink mailboxes)
   k->pp = p2p(c);
@@ -829,7 +846,7 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
   if (k->pp) ps.c = c->p2p;
   ps.e_pub = ps.e_wait = k->pp ? ++c->ep_ar[sem::AR_RG] : 0;
   CUDA_TRY(sem::launch_cg_init(c->dp, c->d_mult, dinv, b, x, c->d_r, c->d_p, c->d_partial,
-                               st, k->rg_out, ps, c->red_grid, s));
+                               st, k->rg_out, ps, c->red_grid, s, k->pf ? 1 : 0));
   if (!k->pp) SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
   CUDA_TRY(sem::launch_cg_start(st, c->d_hist, ps, s));
   c->launches += 2;
@@ -841,9 +858,21 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
   c->ax_pdl_now = c->ax_pdl;
+  c->pf_now = k.pf;
+  c->pf_dinv = dinv;
   const int sa = apply_op(c, c->d_p, c->d_wv, sem::AX_PCG);
   c->ax_pdl_now = false;
+  c->pf_now = false;
   SEM_TRY(sa);
+  if (k.pf) {   // r, x updates and the end of the iteration in one kernel
+    int tk = timer_begin(c, 1);
+    CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv, c->d_partial, st,
+                                   k.rg_out, c->d_partial_ax, c->d_nsig, sem::PeerSync{},
+                                   c->red_grid, s, x, c->d_p, c->d_hist));
+    timer_end(c, tk);
+    c->launches++;
+    return SEM_OK;
+  }
   sem::PeerSync psu, psp;
   if (k.pp) {
     psu.c = psp.c = c->p2p;
@@ -1880,6 +1909,13 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     cudaStreamSynchronize(c->stream);
     if (value == SEM_PRECOND_SCHWARZ) SEM_TRY(schwarz_setup(c));
     c->precond = value;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_PCG_FUSE) {
+    cudaStreamSynchronize(c->stream);
+    c->pcg_fuse = value != 0;
+    if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
+    c->pg_exec = nullptr;
     return SEM_OK;
   }
   if (option == SEM_OPT_PCG_GRAPH) {

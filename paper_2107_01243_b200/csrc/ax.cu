@@ -140,9 +140,21 @@ template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = SEM_AX11_NSG, 
 #endif
 template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = SEM_AX12_NSG, PPC = 3; };
 
-template <int n>
+// PF (one-rank Jacobi-PCG with the p update fused in): the u ring carries p_old,
+// r and dinv (NU = 3 blocks per slot); at n = 8 the G ring shrinks to 3 slots
+// of 2 planes so four CTAs still fit per SM (measured as fast as 3 x 4 planes)
+#ifndef SEM_AX8PF_NSG
+#define SEM_AX8PF_NSG 3
+#endif
+#ifndef SEM_AX8PF_PPC
+#define SEM_AX8PF_PPC 2
+#endif
+template <int n, bool PF = false>
 struct AxShape {
-  static constexpr int NE = AxCfg<n>::NE, NSG = AxCfg<n>::NSG, PPC = AxCfg<n>::PPC;
+  static constexpr int NE = AxCfg<n>::NE;
+  static constexpr int NSG = (PF && n == 8) ? SEM_AX8PF_NSG : AxCfg<n>::NSG;
+  static constexpr int PPC = (PF && n == 8) ? SEM_AX8PF_PPC : AxCfg<n>::PPC;
+  static constexpr int NU = PF ? 3 : 1;            // blocks per u slot (p_old, r, dinv)
   static_assert(n % PPC == 0, "planes per copy must divide n");
   static constexpr int n2 = n * n, n3 = n2 * n;
   static constexpr int TC = NE * n2;               // computing threads
@@ -164,7 +176,7 @@ struct AxShape {
   static constexpr int dpad = n + 1;
   static constexpr int nbar = 2 * NSG + 2 * NSU;
   static constexpr size_t smem_bytes =
-      sizeof(double) * ((size_t)NSU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32) +
+      sizeof(double) * ((size_t)NSU * NU * uslot + (size_t)NSG * gslot + 2 * NE * wel + 2 * n * dpad + 32) +
       sizeof(uint64_t) * nbar + sizeof(int) * 8 + SEM_AX_SMEM_PAD;
   // CTAs per SM the shared memory allows; the register budget is sized to match
   static constexpr int MINB0 = (int)((227u * 1024u) / (smem_bytes + 1024u));
@@ -189,10 +201,12 @@ __device__ __forceinline__ void compute_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-template <int n, int MODE, bool HELM = false>
-__global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
+template <int n, int MODE, bool HELM = false, bool PF = false>
+__global__ void __launch_bounds__(AxShape<n, PF>::T, AxShape<n, PF>::MINB)
     ax_kernel(const DevPlan P, const AxLaunch a) {
-  using Sh = AxShape<n>;
+  using Sh = AxShape<n, PF>;
+  static_assert(!PF || MODE == AX_PCG, "the fused p update is a PCG-iteration mode");
+  constexpr int NU = Sh::NU;
   constexpr int NE = Sh::NE, n2 = Sh::n2, n3 = Sh::n3, TCW = Sh::TCW;
   constexpr int NSG = Sh::NSG, NSU = Sh::NSU, PPC = Sh::PPC;
   constexpr int dp = Sh::dpad, rp = Sh::rp, wpl = Sh::wpl;
@@ -209,7 +223,7 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
 
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;                                   // [NSU][NE*n3]
-  double* sG = sU + NSU * Sh::uslot;                   // [NSG][NE][6][n2]
+  double* sG = sU + NSU * NU * Sh::uslot;              // [NSG][NE][6][n2]
   double* sWr = sG + NSG * Sh::gslot;                  // [NE][n][n][rp]
   double* sWs = sWr + NE * Sh::wel;
   double* sD = sWs + NE * Sh::wel;                     // sD[i*dp+m]  = D[i][m]
@@ -282,6 +296,7 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
   }
 
   double acc = 0.0;  // sigma partial (AX_PCG)
+  const double beta = PF ? *a.beta : 0.0;   // written by the preceding CG update
 
   if (producer) {
     // ======================= producer warp: TMA bulk copies =======================
@@ -293,31 +308,38 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
     for (int g = blockIdx.x; g < ng; g += gridDim.x) {
       int e0, cnt;
       group(g, e0, cnt);
-      // u block of the group
+      // u block of the group (PF: p_old, r and dinv blocks)
+      const double* usrc[3] = {a.u, a.rr, a.dinv};
       mbar_wait(&emptyU[su], phu ^ 1u);
       if (kBulkU) {
         if (lane == 0) {
           const uint32_t bU = (uint32_t)cnt * n3 * 8u;
-          mbar_arrive_expect_tx(&fullU[su], bU);
-          bulk_g2s(sU + su * Sh::uslot, a.u + (size_t)e0 * n3, bU, &fullU[su]);
+          mbar_arrive_expect_tx(&fullU[su], bU * NU);
+#pragma unroll
+          for (int b = 0; b < NU; b++)
+            bulk_g2s(sU + (su * NU + b) * Sh::uslot, usrc[b] + (size_t)e0 * n3, bU, &fullU[su]);
         }
       } else {
         // odd n: the group's u block starts 8 mod 16 for every other element.
         // Bulk-copy its 16-B aligned body; lane 1 copies the (at most two) end
         // doubles.  The block lands h doubles into the slot (h = source
         // misalignment), which keeps the bulk destination 16-B aligned.
-        const double* src = a.u + (size_t)e0 * n3;
-        const int h = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1u);
+        // (PF: the three arrays share the allocation alignment, hence h)
+        const int h = (int)((reinterpret_cast<uintptr_t>(a.u + (size_t)e0 * n3) >> 3) & 1u);
         const int cntd = cnt * n3, nb = ((cntd - h) >> 1) << 1;
-        double* dst = sU + su * Sh::uslot + h;
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&fullU[su], (uint32_t)nb * 8u);
-          bulk_g2s(dst + h, src + h, (uint32_t)nb * 8u, &fullU[su]);
-        } else if (lane == 1) {
-          if (h) dst[0] = __ldg(src);
-          if (h + nb < cntd) dst[cntd - 1] = __ldg(src + cntd - 1);
-          mbar_arrive(&fullU[su]);   // release: this lane's stores
+        if (lane == 0) mbar_arrive_expect_tx(&fullU[su], (uint32_t)nb * 8u * NU);
+#pragma unroll
+        for (int b = 0; b < NU; b++) {
+          const double* src = usrc[b] + (size_t)e0 * n3;
+          double* dst = sU + (su * NU + b) * Sh::uslot + h;
+          if (lane == 0) {
+            bulk_g2s(dst + h, src + h, (uint32_t)nb * 8u, &fullU[su]);
+          } else if (lane == 1) {
+            if (h) dst[0] = __ldg(src);
+            if (h + nb < cntd) dst[cntd - 1] = __ldg(src + cntd - 1);
+          }
         }
+        if (lane == 1) mbar_arrive(&fullU[su]);   // release: this lane's stores
       }
       if (++su == NSU) { su = 0; phu ^= 1u; }
       // k-planes of the geometric factors
@@ -357,7 +379,7 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
       // the element's Dirichlet face bits, fetched now, used by the epilogue
       const unsigned bm = (kMask && active) ? (unsigned)__ldg(P.bmask + e0 + el) : 0u;
       const int uoff = kBulkU ? 0 : (int)((reinterpret_cast<uintptr_t>(a.u + (size_t)e0 * n3) >> 3) & 1u);
-      const double* sUe = sU + su * Sh::uslot + uoff + el * n3;
+      double* sUe = sU + su * NU * Sh::uslot + uoff + el * n3;   // (PF: p_old, then r, dinv)
       double* wr_s = sWr + el * Sh::wel;
       double* ws_s = sWs + el * Sh::wel;
       mbar_wait(&fullU[su], phu);
@@ -379,10 +401,32 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
 #pragma unroll
         for (int k = 0; k < n; k++) rb[kBpre ? k : 0] = active ? __ldg(Bc + n2 * k) : 0.0;
       }
+      if (PF) {
+        // fused p update (one-rank PCG): p = dinv r + beta p_old for this thread's
+        // column, in place in the slot's p part (the contractions read it across
+        // threads) and to global memory; beta = 0 on the first iteration (p_old = 0)
+        const double* sRe = sUe + Sh::uslot;
+        const double* sDe = sUe + 2 * Sh::uslot;
+        double* pg = a.pout + (size_t)(e0 + el) * n3 + ij;
 #pragma unroll
-      for (int k = 0; k < n; k++) {
-        ru[k] = active ? sUe[ij + n2 * k] : 0.0;
-        rw[k] = 0.0;
+        for (int k = 0; k < n; k++) {
+          double pn = 0.0;
+          if (active) {
+            const int l = ij + n2 * k;
+            pn = fma(beta, sUe[l], sDe[l] * sRe[l]);
+            sUe[l] = pn;
+            pg[n2 * k] = pn;
+          }
+          ru[k] = pn;
+          rw[k] = 0.0;
+        }
+        compute_sync<TCW>();   // the whole group's p in shared memory
+      } else {
+#pragma unroll
+        for (int k = 0; k < n; k++) {
+          ru[k] = active ? sUe[ij + n2 * k] : 0.0;
+          rw[k] = 0.0;
+        }
       }
 #ifndef SEM_KU
 #define SEM_KU 2
@@ -423,6 +467,9 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
           if (++sg == NSG) { sg = 0; phg ^= 1u; }
         }
       }
+      // PF wrote the slot with generic stores: order them before the producer's
+      // next bulk copy (async proxy) into it
+      if (PF) fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyU[su]);   // u slot consumed
       if (++su == NSU) { su = 0; phu ^= 1u; }
@@ -477,10 +524,10 @@ __global__ void __launch_bounds__(AxShape<n>::T, AxShape<n>::MINB)
 }
 
 // persistent launch: grid = min(work groups, resident CTAs x SMs) of this variant
-template <int n, int MODE, bool HELM>
+template <int n, int MODE, bool HELM, bool PF>
 static cudaError_t launch_n(const DevPlan& P, const AxLaunch& a, int groups, cudaStream_t s) {
-  using Sh = AxShape<n>;
-  auto kern = ax_kernel<n, MODE, HELM>;
+  using Sh = AxShape<n, PF>;
+  auto kern = ax_kernel<n, MODE, HELM, PF>;
   static std::atomic<int> cache[kMaxDev];   // resident CTAs on each device
   const int dev = device_index();
   int resident = cache[dev].load(std::memory_order_relaxed);
@@ -510,24 +557,24 @@ static int occupancy_n() {
   return std::max(nb, 1);
 }
 
-template <int MODE, bool HELM = false>
+template <int MODE, bool HELM = false, bool PF = false>
 static cudaError_t dispatch(const DevPlan& P, const AxLaunch& a, int grid, cudaStream_t s) {
 #ifdef SEM_AX_ONLY_N8
-  if (P.n == 8) return launch_n<8, MODE, HELM>(P, a, grid, s);
+  if (P.n == 8) return launch_n<8, MODE, HELM, PF>(P, a, grid, s);
   return cudaErrorInvalidValue;
 #endif
   switch (P.n) {
-    case 2: return launch_n<2, MODE, HELM>(P, a, grid, s);
-    case 3: return launch_n<3, MODE, HELM>(P, a, grid, s);
-    case 4: return launch_n<4, MODE, HELM>(P, a, grid, s);
-    case 5: return launch_n<5, MODE, HELM>(P, a, grid, s);
-    case 6: return launch_n<6, MODE, HELM>(P, a, grid, s);
-    case 7: return launch_n<7, MODE, HELM>(P, a, grid, s);
-    case 8: return launch_n<8, MODE, HELM>(P, a, grid, s);
-    case 9: return launch_n<9, MODE, HELM>(P, a, grid, s);
-    case 10: return launch_n<10, MODE, HELM>(P, a, grid, s);
-    case 11: return launch_n<11, MODE, HELM>(P, a, grid, s);
-    case 12: return launch_n<12, MODE, HELM>(P, a, grid, s);
+    case 2: return launch_n<2, MODE, HELM, PF>(P, a, grid, s);
+    case 3: return launch_n<3, MODE, HELM, PF>(P, a, grid, s);
+    case 4: return launch_n<4, MODE, HELM, PF>(P, a, grid, s);
+    case 5: return launch_n<5, MODE, HELM, PF>(P, a, grid, s);
+    case 6: return launch_n<6, MODE, HELM, PF>(P, a, grid, s);
+    case 7: return launch_n<7, MODE, HELM, PF>(P, a, grid, s);
+    case 8: return launch_n<8, MODE, HELM, PF>(P, a, grid, s);
+    case 9: return launch_n<9, MODE, HELM, PF>(P, a, grid, s);
+    case 10: return launch_n<10, MODE, HELM, PF>(P, a, grid, s);
+    case 11: return launch_n<11, MODE, HELM, PF>(P, a, grid, s);
+    case 12: return launch_n<12, MODE, HELM, PF>(P, a, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -585,8 +632,13 @@ int ax_occupancy(int N, int mode) {
 }
 
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
-                      bool helm) {
+                      bool helm, bool pf) {
   if (grid < 1) grid = 1;
+  if (pf) {   // one-rank PCG iteration with the p update fused in
+    if (mode != AX_PCG) return cudaErrorInvalidValue;
+    return helm ? dev::dispatch<AX_PCG, true, true>(P, a, grid, s)
+                : dev::dispatch<AX_PCG, false, true>(P, a, grid, s);
+  }
   if (helm) {   // Helmholtz: h1 A + h2 B
     if (mode == AX_APPLY) return dev::dispatch<AX_APPLY, true>(P, a, grid, s);
     if (mode == AX_PCG) return dev::dispatch<AX_PCG, true>(P, a, grid, s);

@@ -10,6 +10,21 @@ namespace dev {
 // grid has completed and its writes are visible, then let the next grid's CTAs
 // be scheduled (they run their prologue and wait in turn).  Both are no-ops
 // when the kernel was launched without the PDL attribute.
+// Checked builds (build.py --variant checked -DSEM_CHECKED=1): the substitute
+// for compute-sanitizer, which this pool does not allow.
+// Every computed slot / buffer index of the gather-scatter, pack / unpack and
+// exchange kernels is range-checked (and incidence slots must be ascending);
+// a violation traps the kernel, so the next CUDA call fails loudly.  Device
+// allocations are poisoned with 0xFF bytes (NaN doubles, -1 indices, 255
+// multiplicities) so a read of never-written memory cannot go unnoticed.
+#ifndef SEM_CHECKED
+#define SEM_CHECKED 0
+#endif
+#define SEM_CHK(cond)                      \
+  do {                                     \
+    if (SEM_CHECKED && !(cond)) __trap();  \
+  } while (0)
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

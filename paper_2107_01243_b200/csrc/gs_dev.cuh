@@ -79,6 +79,7 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
       const int2 b2 = fok[q] ? reinterpret_cast<const int2*>(P.f_base)[f] : make_int2(0, 0);
       a0[q] = b2.x + off;
       a1[q] = b2.y + off;
+      SEM_CHK(!fok[q] || (a0[q] >= 0 && a0[q] < a1[q] && a1[q] < P.n_local));
     }
 #pragma unroll
     for (int q = 0; q < FE; q++) {
@@ -91,6 +92,10 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
       emk[q] = ok && P.e_mask[e];
       const int4 b4 = ok ? reinterpret_cast<const int4*>(P.e_base)[e] : make_int4(0, 0, 0, 0);
       eb[q][0] = b4.x; eb[q][1] = b4.y; eb[q][2] = b4.z; eb[q][3] = b4.w;
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+        SEM_CHK(x >= enin[q] || (eb[q][x] + eoff[q] >= 0 && eb[q][x] + eoff[q] < P.n_local &&
+                                 (x == 0 || eb[q][x] > eb[q][x - 1])));
     }
     double v0[F], v1[F], ve[FE][4];
 #pragma unroll
@@ -129,6 +134,9 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
     const int4 b0 = reinterpret_cast<const int4*>(P.v_base)[2 * v];
     const int4 b1 = reinterpret_cast<const int4*>(P.v_base)[2 * v + 1];
     const int base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int x = 0; x < 8; x++)
+      SEM_CHK(x >= nin || (base[x] >= 0 && base[x] < P.n_local && (x == 0 || base[x] > base[x - 1])));
     double vv[8];
 #pragma unroll
     for (int x = 0; x < 8; x++)
@@ -199,6 +207,7 @@ __device__ __forceinline__ void gs_chunk_body(const DevPlan& P, double* __restri
         const int2 b2 = reinterpret_cast<const int2*>(P.f_base)[f];
         a0[q] = b2.x + off;
         a1[q] = b2.y + off;
+        SEM_CHK(!ok[q] || (a0[q] >= 0 && a0[q] < a1[q] && a1[q] < P.n_local));
       }
       double v0[F], v1[F];
 #pragma unroll
@@ -242,6 +251,10 @@ __device__ __forceinline__ void gs_chunk_body(const DevPlan& P, double* __restri
       base[4] = b1.x; base[5] = b1.y; base[6] = b1.z; base[7] = b1.w;
       mk = P.v_mask[v];
     }
+#pragma unroll
+    for (int x = 0; x < 8; x++)
+      SEM_CHK(x >= nin || (base[x] + off >= 0 && base[x] + off < P.n_local &&
+                           (x == 0 || base[x] > base[x - 1])));
     double v[8];
 #pragma unroll
     for (int x = 0; x < 8; x++)

@@ -230,12 +230,18 @@ __global__ void gs_pack_kernel(const DevPlan P, const double* __restrict__ u, do
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < P.nS;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int nl = P.s_nloc[s];
+#pragma unroll 1
+    for (int x = 0; x < nl; x++) {
+      const int32_t l = P.s_slot[(int64_t)x * P.nS + s];
+      SEM_CHK(l >= 0 && l < P.n_local && (x == 0 || l > P.s_slot[(int64_t)(x - 1) * P.nS + s]));
+    }
     double v = u[P.s_slot[s]];
     for (int x = 1; x < nl; x++) v += u[P.s_slot[(int64_t)x * P.nS + s]];
     part[s] = v;
     const int nr = P.s_nr[s];
     for (int x = 0; x < nr; x++) {
       const int o = P.s_off[(int64_t)x * P.nS + s];
+      SEM_CHK(o < P.nbuf);
       if (o >= 0) sendbuf[o] = v;
     }
   }
@@ -257,12 +263,16 @@ __global__ void gs_unpack_kernel(const DevPlan P, double* __restrict__ u, const 
     double tot = 0.0;
     for (int x = 0; x < nr; x++) {
       const int o = P.s_off[(int64_t)x * P.nS + s];
+      SEM_CHK(o < P.nbuf);
       const double v = o < 0 ? part[s] : recvbuf[o];
       tot = x == 0 ? v : tot + v;
     }
     if (apply_mask && P.s_mask[s]) tot = 0.0;
     const int nl = P.s_nloc[s];
-    for (int x = 0; x < nl; x++) u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
+    for (int x = 0; x < nl; x++) {
+      SEM_CHK(P.s_slot[(int64_t)x * P.nS + s] >= 0 && P.s_slot[(int64_t)x * P.nS + s] < P.n_local);
+      u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
+    }
   }
 }
 
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint
                                const double* __restrict__ dinv, const double* __restrict__ b,
                                double* __restrict__ x, double* __restrict__ r,
                                double* __restrict__ p, double* partial, PcgState* st,
-                               double* out2, const PeerSync ps) {
+                               double* out2, const PeerSync ps, int pzero) {
   __shared__ double scratch[32];
   __shared__ int flag;
   double rz = 0.0, rr = 0.0;
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(kThreads) cg_init_kernel(int64_t n, const uint
     const double bl = b[l], z = dinv[l] * bl, c = c_of(mult[l]);
     x[l] = 0.0;
     r[l] = bl;
-    p[l] = z;
+    p[l] = pzero ? 0.0 : z;   // pzero: the fused Ax kernel forms p_0 = dinv r + 0 p
     rz = fma(c * bl, z, rz);
     rr = fma(c * bl, bl, rr);
   }
@@ -330,6 +340,7 @@ __global__ void cg_start_kernel(PcgState* st, double* hist, const PeerSync ps) {
     st->gamma = g2[1];
   }
   st->rho_old = st->rho_new;
+  st->beta = 0.0;   // fused p update: p_0 = dinv r
   st->it = 0;
   const double g = sqrt(st->gamma);
   hist[0] = g;
@@ -338,13 +349,20 @@ __global__ void cg_start_kernel(PcgState* st, double* hist, const PeerSync ps) {
 }
 
 // alpha = rho / sigma; r -= alpha w; partials of rho' = <r, dinv r>_c and
-// gamma = <r, r>_c (z is never stored).  x += alpha p is deferred to the p
-// kernel, which streams p anyway (same operation, one pass less over p and x).
+// gamma = <r, r>_c (z is never stored).  Unfused: x += alpha p is deferred to
+// the p kernel, which streams p anyway (same operation, one pass less over p
+// and x).  PF (one rank, p update fused into the next Ax kernel): x += alpha p
+// here, and the last block ends the iteration -- convergence test on
+// sqrt(gamma), beta = rho'/rho for the next Ax kernel, history -- as the p
+// kernel's last block does otherwise.
+template <bool PF>
 __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                  const double* __restrict__ dinv, double* __restrict__ r,
                                  const double* __restrict__ w, double* partial, PcgState* st,
                                  double* out2, const double* __restrict__ sig_part,
-                                 const int* sig_count, const PeerSync ps) {
+                                 const int* sig_count, const PeerSync ps,
+                                 double* __restrict__ x, const double* __restrict__ p,
+                                 double* hist) {
   __shared__ double scratch[32];
   __shared__ int flag;
   __shared__ double s_sig;
@@ -382,12 +400,21 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
     const double2* d2 = reinterpret_cast<const double2*>(dinv);
     double2* r2 = reinterpret_cast<double2*>(r);
     const uchar2* m2 = reinterpret_cast<const uchar2*>(mult);
+    double2* x2 = reinterpret_cast<double2*>(x);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
          q += (int64_t)gridDim.x * blockDim.x) {
       const double2 wv = __ldcs(&w2[q]);
       const double2 dv = __ldcs(&d2[q]);
       double2 rv = __ldcs(&r2[q]);
       const uchar2 mv = m2[q];
+      if (PF) {
+        const double2 pv = __ldcs(&p2[q]);
+        double2 xv = __ldcs(&x2[q]);
+        xv.x = fma(alpha, pv.x, xv.x);
+        xv.y = fma(alpha, pv.y, xv.y);
+        __stcs(&x2[q], xv);
+      }
       rv.x = fma(-alpha, wv.x, rv.x);
       rv.y = fma(-alpha, wv.y, rv.y);
       __stcg(&r2[q], rv);
@@ -401,6 +428,7 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
       const int64_t l = n - 1;
       const double rl = fma(-alpha, w[l], r[l]);
       r[l] = rl;
+      if (PF) x[l] = fma(alpha, p[l], x[l]);
       const double c = c_of(mult[l]);
       rz = fma(c * rl, dinv[l] * rl, rz);
       rr = fma(c * rl, rl, rr);
@@ -413,6 +441,28 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
       st->iters = st->it + 1;
     }
     if (threadIdx.x == 0 && ps.c.P > 1) ar_publish(ps.c, AR_RG, ps.e_pub, out2, 2);
+    if (PF && ok && threadIdx.x == 0) {   // end of the iteration (one rank: out2 = st->rho_new)
+      __threadfence();
+      const double rho_new = st->rho_new, gamma = st->gamma;
+      const double g = sqrt(gamma);
+      const int it = st->it + 1;
+      st->it = it;
+      hist[it] = g;
+      if (!(g == g) || !(rho_new == rho_new)) {
+        st->done = 3;
+        st->iters = it;
+      } else if (g <= st->tol) {
+        st->done = 1;
+        st->iters = it;
+      } else {
+        st->beta = rho_new / st->rho_old;
+        st->rho_old = rho_new;
+        if (it >= st->maxit) {
+          st->done = 4;
+          st->iters = it;
+        }
+      }
+    }
   }
 }
 
@@ -689,9 +739,9 @@ cudaError_t launch_sum_c(const DevPlan& P, const uint8_t* mult, const double* a,
 
 cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv, const double* b,
                            double* x, double* r, double* p, double* partial, PcgState* st,
-                           double* out2, const PeerSync& ps, int grid, cudaStream_t s) {
+                           double* out2, const PeerSync& ps, int grid, cudaStream_t s, int pzero) {
   dev::cg_init_kernel<<<grid, kThreads, 0, s>>>(P.n_local, mult, dinv, b, x, r, p, partial, st, out2,
-                                                ps);
+                                                ps, pzero);
   return cudaGetLastError();
 }
 
@@ -703,9 +753,12 @@ cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cuda
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* r,
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
-                             int grid, cudaStream_t s) {
-  return launch_k(dev::cg_update_kernel, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult, dinv, r,
-                  w, partial, st, out2, sig_part, sig_count, ps);
+                             int grid, cudaStream_t s, double* x, const double* p, double* hist) {
+  if (x)
+    return launch_k(dev::cg_update_kernel<true>, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult,
+                    dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist);
+  return launch_k(dev::cg_update_kernel<false>, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult,
+                  dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist);
 }
 
 bool gs_flat(const DevPlan& P, int mode) { return dev::gs_mode_ce(P, mode) == 0; }

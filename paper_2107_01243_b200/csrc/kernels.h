@@ -46,6 +46,7 @@ struct DevPlan {
   int N = 0, n = 0, nloc = 0;
   int64_t n_local = 0;
   int nF = 0, nEd = 0, nV = 0, nS = 0;
+  int64_t nbuf = 0;                 // receive / send buffer entries (P > 1)
   const double* D = nullptr;        // [n*n]
   const uint8_t* bmask = nullptr;   // [nloc]
   const int32_t* f_base = nullptr;  // [nF][2]
@@ -123,6 +124,12 @@ struct AxLaunch {
   int gate;                       // 1: any mode returns early when *done (GMRES cycle gate)
   int pdl_pref;                   // 1: launched with PDL; prefetch the first G planes before
                                   //    waiting for the preceding grid
+  // PF (one-rank Jacobi-PCG, p update fused): u = p_old (in place), rr = r,
+  // dinv, pout = p (= u), beta = the CG state's beta (0 on the first iteration)
+  const double* rr;
+  const double* dinv;
+  double* pout;
+  const double* beta;
 };
 
 // NVLink peer-memory collectives (p2p.cu): mailbox layout and device view
@@ -230,8 +237,9 @@ cudaError_t launch_ar_finish(const P2P& c, int site, uint64_t epoch, double* out
 // returns max resident CTAs/SM for the Ax kernel of this N and mode
 int ax_occupancy(int N, int mode);
 // helm: the Helmholtz variant (a.B, a.h1, a.h2), AX_APPLY / AX_PCG
+// pf: AX_PCG with the p update fused in (p = dinv r + beta p, see AxLaunch)
 cudaError_t launch_ax(const DevPlan& P, const AxLaunch& a, int mode, int grid, cudaStream_t s,
-                      bool helm = false);
+                      bool helm = false, bool pf = false);
 int ax_groups(int N, int nelem);   // element groups processed per launch
 
 // setup
@@ -273,14 +281,17 @@ cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStre
 cudaError_t launch_cg_init(const DevPlan& P, const uint8_t* mult, const double* dinv,
                            const double* b, double* x, double* r, double* p, double* partial,
                            PcgState* st, double* out2, const PeerSync& ps, int grid,
-                           cudaStream_t s);
+                           cudaStream_t s, int pzero = 0);
 cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cudaStream_t s);
 // sig_part/sig_count: the Ax kernel's per-CTA sigma partials (P = 1; every block
-// re-sums them in a fixed order) or nullptr (P > 1: sigma is already allreduced)
+// re-sums them in a fixed order) or nullptr (P > 1: sigma is already allreduced).
+// x != nullptr (one rank, p update fused into the Ax kernel): also x += alpha p,
+// and the last block ends the iteration (convergence, beta, history)
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* r,
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
-                             int grid, cudaStream_t s);
+                             int grid, cudaStream_t s, double* x = nullptr,
+                             const double* p = nullptr, double* hist = nullptr);
 bool gs_flat(const DevPlan& P, int mode);   // the gs schedule `mode` resolves to the flat sweep
 // x += alpha p, then (unless the solve ended) p = dinv r + beta p
 cudaError_t launch_cg_p(const DevPlan& P, const double* dinv, const double* r, double* p, double* x,

@@ -54,6 +54,9 @@ __device__ unsigned long long g_xts[5 * kXtsBlocks];
 __device__ __forceinline__ void pack_point(const DevPlan& P, const double* u, double* part,
                                            const P2P& c, uint64_t epoch, int s) {
   const int nl = P.s_nloc[s];
+  for (int x = 0; x < nl; x++)
+    SEM_CHK(P.s_slot[(int64_t)x * P.nS + s] >= 0 && P.s_slot[(int64_t)x * P.nS + s] < P.n_local &&
+            (x == 0 || P.s_slot[(int64_t)x * P.nS + s] > P.s_slot[(int64_t)(x - 1) * P.nS + s]));
   double v = u[P.s_slot[s]];
   for (int x = 1; x < nl; x++) v += u[P.s_slot[(int64_t)x * P.nS + s]];
   part[s] = v;
@@ -73,6 +76,7 @@ __device__ __forceinline__ void unpack_point(const DevPlan& P, double* u, const 
   double tot = 0.0;
   for (int x = 0; x < nr; x++) {
     const int o = P.s_off[(int64_t)x * P.nS + s];
+    SEM_CHK(o < P.nbuf);
     const double v = o < 0 ? part[s] : ll_load(mb_ll(c.local, o, epoch), (uint32_t)epoch, c.err);
     tot = x == 0 ? v : tot + v;
   }

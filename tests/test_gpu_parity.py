@@ -553,3 +553,44 @@ def test_pcg_graph_identical(spec, N):
         for x_, it, h in outs[1:]:
             assert it == outs[0][1] and np.array_equal(x_, outs[0][0]) and np.array_equal(h, outs[0][2])
         assert abs(outs[0][1] - ref["iters"]) <= 1 and np.abs(outs[0][0] - ref["x"]).max() <= 1e-10
+
+
+PF_CASES = [(CONFIGS["C1"][0], 3), (tgv_box(8, 8, 8), 7), (tgv_box(4, 3, 5, deform=1), 6),
+            (unit_box(3, 2, 5, periodic=(1, 0, 0)), 5), (tgv_box(3, 3, 2, deform=1), 8),
+            (unit_box(2, 3, 2), 10), (tgv_box(2, 2, 2), 1), (tgv_box(3, 2, 2), 11)]
+
+
+@pytest.mark.parametrize("spec,N", PF_CASES, ids=[f"{s.ex}x{s.ey}x{s.ez}-N{N}" for s, N in PF_CASES])
+def test_pcg_fused_p_update(spec, N):
+    """SEM_OPT_PCG_FUSE: the p update fused into the Ax kernel (p = dinv r +
+    beta p in the kernel's prologue, x += alpha p in the r update) reaches the
+    oracle's iterate like the four-kernel iteration (every n incl. odd ones,
+    Dirichlet and periodic, Helmholtz); same iteration count."""
+    o = O.Oracle(spec, N)
+    fun = f_tgv if all(spec.periodic) else f_sin
+    b = o.rhs(fun(o.get("X"), o.get("Y"), o.get("Z")))
+    ref = o.pcg(b, 1e-10, 3000)
+    with sem().sem_setup(spec, N) as c:
+        res = {}
+        for fuse in (True, False):
+            c.set_pcg_fuse(fuse)
+            x = c.zeros()
+            r = c.pcg_solve(dev(b), x, 1e-10, 3000)
+            res[fuse] = (host(x), r)
+            assert r["status"] == 0 and abs(r["iters"] - ref["iters"]) <= 1, (fuse, r, ref["iters"])
+            assert np.abs(host(x) - ref["x"]).max() <= 1e-10
+            assert abs(r["res_true"] - ref["res_true"]) <= 1e-10
+        assert abs(res[True][1]["iters"] - res[False][1]["iters"]) <= 1
+        # Helmholtz PCG through the same fused kernel
+        bh = c.zeros()
+        c.rhs_mass(dev(fun(o.get("X"), o.get("Y"), o.get("Z"))), bh)
+        refh = o.helm_pcg(0.5, 3.0, host(bh), 1e-10, 2000)
+        xs = []
+        for fuse in (True, False):
+            c.set_pcg_fuse(fuse)
+            xh = c.zeros()
+            rh = c.helm_pcg_solve(0.5, 3.0, bh, xh, 1e-10, 2000)
+            assert rh["status"] == 0 and abs(rh["iters"] - refh["iters"]) <= 1
+            assert np.abs(host(xh) - refh["x"]).max() <= 1e-10
+            xs.append((host(xh), rh["iters"]))
+        assert abs(xs[0][1] - xs[1][1]) <= 1 and np.abs(xs[0][0] - xs[1][0]).max() <= 1e-10

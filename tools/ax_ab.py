@@ -56,6 +56,8 @@ def main():
                 continue
             if os.environ.get("PCG_GRAPH") == "0":
                 c.set_pcg_graph(False)
+            if os.environ.get("PCG_FUSE") == "0":
+                c.set_pcg_fuse(False)
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
