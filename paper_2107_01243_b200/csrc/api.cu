@@ -199,8 +199,11 @@ int dalloc(T** p, size_t count) {
     sem::set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? SEM_ENOMEM : SEM_ECUDA;
   }
-#if SEM_CHECKED   // poison (checked builds): NaN doubles, -1 indices
+#if SEM_CHECKED || SEM_POISON   // poison (checked builds): NaN doubles, -1 indices
+  // (completed before returning: the caller's stream may be a non-blocking one
+  // that does not order after the legacy stream the memset runs on)
   cudaMemset(*p, 0xFF, count * sizeof(T));
+  cudaDeviceSynchronize();
 #endif
   return SEM_OK;
 }

@@ -141,10 +141,11 @@ template <> struct AxCfg<11> { static constexpr int NE = 1, NSG = SEM_AX11_NSG, 
 template <> struct AxCfg<12> { static constexpr int NE = 1, NSG = SEM_AX12_NSG, PPC = 3; };
 
 // PF (one-rank Jacobi-PCG with the p update fused in): the u ring carries p_old,
-// r and dinv (NU = 3 blocks per slot); at n = 8 the G ring shrinks to 3 slots
-// of 2 planes so four CTAs still fit per SM (measured as fast as 3 x 4 planes)
+// r and dinv (NU = 3 blocks per slot); at n = 8 the G ring is 4 slots of 2
+// planes (3 CTAs per SM; best of 3x2, 3x4, 4x1, 4x2, 5x1, 2x2 on C2 and C3,
+// profiles/r02_experiments/pcg_fuse_ab.jsonl)
 #ifndef SEM_AX8PF_NSG
-#define SEM_AX8PF_NSG 3
+#define SEM_AX8PF_NSG 4
 #endif
 #ifndef SEM_AX8PF_PPC
 #define SEM_AX8PF_PPC 2
