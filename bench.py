@@ -84,7 +84,7 @@ def relaunch(args):
 def bytes_model(N):
     """SURVEY 8(d) per-point algorithmic bytes (paper Eq. 12 Q, cold cache)."""
     fb = 1.0 - ((N - 1) / (N + 1)) ** 3           # fraction of slots on element faces
-    return {"f_b": fb, "ax": 64.0, "ax_gs": 64.0 + 20.0 * fb,
+    return {"f_b": fb, "ax": 64.0, "ax_pf": 88.0, "ax_gs": 64.0 + 20.0 * fb,
             "pcg_iter_fused": 152.0 + 20.0 * fb, "flops_ax": 12 * (N + 1) + 15}
 
 
@@ -382,7 +382,9 @@ def main():
     k_avg = max_over_ranks(k_ms / n_apply)
     bm = bytes_model(N)
     peak, peak_src = peaks()
-    kbytes = bm["ax"]
+    # P = 1: the Ax kernel also performs the p update (PF): p_old, r, dinv in, p out
+    pf = P == 1
+    kbytes = bm["ax_pf"] if pf else bm["ax"]
     achieved = nl * kbytes / (k_avg / 1e3) / 1e9
     traffic = None
     try:
@@ -457,10 +459,12 @@ def main():
             "config": {
                 "workload": workload_desc(args.config, P),
                 "N": N, "elements": spec.E, "n_p": n_p_total, "n_glob": ctx.n_glob,
-                "step": ("one Jacobi-PCG iteration: Ax+mask+<p,Ap> kernel, gather-scatter "
-                         "kernel" + (" with the NVLink peer-memory exchange and allreduce"
-                                     if P > 1 else "") +
-                         ", r update + <r,z>_c, <r,r>_c kernel, x/p update kernel"),
+                "step": (("one Jacobi-PCG iteration: Ax+mask+<p,Ap> kernel, gather-scatter kernel "
+                          "with the NVLink peer-memory exchange and allreduce, r update + "
+                          "<r,z>_c, <r,r>_c kernel, x/p update kernel") if P > 1 else
+                         ("one Jacobi-PCG iteration, three kernels replayed as a CUDA graph: "
+                          "p update + Ax + mask + <p,Ap> kernel, gather-scatter kernel, "
+                          "r and x update + <r,z>_c, <r,r>_c + convergence kernel")),
                 "l2": (f"no flush: per-iteration working set {nl * 104 / 1e6:.0f} MB/GPU "
                        "(G, u, w, r, p, x, dinv) > 126 MB L2"),
                 "parallelism": (f"element z-slabs x{P}, NVLink peer-memory gs exchange + "
@@ -478,7 +482,8 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": f"ax_kernel<{N + 1},AX_PCG> (Ax+mask+sigma)",
+                "kernel": (f"ax_kernel<{N + 1},AX_PCG,PF> (p = dinv r + beta p, Ax, mask, sigma)"
+                           if pf else f"ax_kernel<{N + 1},AX_PCG> (Ax+mask+sigma)"),
                 "bytes_per_pt": kbytes, "hbm_mandatory_bytes_per_pt": 64.0,
                 "avg_ms_per_apply": k_avg, "launches": k_cnt, "applies": n_apply,
                 "peak_source": peak_src,
