@@ -371,14 +371,16 @@ def main():
     # ---- dominant kernel (Ax + mask + sigma), CUDA events on the context stream
     ctx.timing(True)
     ctx.pcg_solve(b, x, 0.0, args.steps)
-    k_ms, k_cnt = ctx.timing_read(0)
+    # P = 1: the PF Ax kernel is timer class 9 (the final true-residual apply,
+    # class 0, is excluded); P > 1: class 0 over the K iterations + 1 apply
+    k_ms, k_cnt = ctx.timing_read(9 if P == 1 else 0)
     u_ms, u_cnt = ctx.timing_read(1)
     p_ms, p_cnt = ctx.timing_read(2)
     g_ms, g_cnt = ctx.timing_read(4)
     ctx.timing(False)
     # per operator application (the split Alg. 1 operator launches the kernel
     # twice per application at N > 1): steps iterations + 1 true-residual apply
-    n_apply = args.steps + 1
+    n_apply = args.steps if P == 1 else args.steps + 1
     k_avg = max_over_ranks(k_ms / n_apply)
     bm = bytes_model(N)
     peak, peak_src = peaks()

@@ -226,7 +226,8 @@ int sem_loopback_destroy(void* world);
    launch of kernel class `which` (0 = Ax kernel of apply/PCG, 1 = CG
    update, 2 = p update, 3 = Ax only, 4 = gather-scatter kernel of apply/PCG,
    5 = peer-memory pack, 6 = peer-memory unpack, 7 = Schwarz local-solve kernel,
-   8 = Schwarz combine kernel); sem_timing_read returns the summed
+   8 = Schwarz combine kernel, 9 = Ax kernel with the fused p update of the
+   one-rank PCG iteration); sem_timing_read returns the summed
    device time in ms and the number of timed launches since the last reset.
    sem_launch_count returns the number of kernels this context has launched. */
 int sem_timing(sem_ctx* c, int enable);

@@ -67,7 +67,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 namespace {
 
 constexpr int kBatch = 8;            // iterations enqueued between host polls
-constexpr int kTimerClasses = 9;
+constexpr int kTimerClasses = 10;
 
 struct Timer {
   std::vector<cudaEvent_t> pool;     // pairs
@@ -293,7 +293,7 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   a.h2 = c->h2;
   const int ng = sem::ax_groups(c->hp.N, (r0hi - r0lo)) + sem::ax_groups(c->hp.N, (r1hi - r1lo));
   const int groups = std::max(ng, 1);   // the launcher caps the grid at residency
-  int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : 0);
+  int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : (c->pf_now && mode == sem::AX_PCG ? 9 : 0));
   // PCG iterations: programmatic dependent launch of the Ax kernel alone, its
   // producer prefetching G before waiting for the preceding kernel (SEM_OPT_AX_PDL)
   const bool pdl = c->ax_pdl_now && !c->timing && !sem::pdl_on();

@@ -94,10 +94,12 @@ def main():
     open(out, "w").write("\n".join(lines) + "\n")
     # traffic of the PCG Ax kernel (AX_PCG = mode 2, n = 8)
     traffic = {}
-    for name, r in seen.items():
-        if "ax_kernel" in name:
+    # prefer the one-rank PCG kernel with the fused p update (<8, 2, 0, 1>)
+    cands = [r for name, r in seen.items() if "ax_kernel" in name and "<8, 2" in r[ki]]
+    cands.sort(key=lambda r: 0 if "<8, 2, 0, 1>" in r[ki] or "true>" in r[ki] else 1)
+    for r in cands[:1]:
+        if True:
             full = r[ki]
-            if "<8, 2" in full or "(int)8, (int)2" in full:
                 b = float(r[h.index("dram__bytes_read.sum")]) + float(r[h.index("dram__bytes_write.sum")])
                 scale = 1e6 if units[h.index("dram__bytes_read.sum")].lower().startswith("m") else 1.0
                 traffic["C2_N7_P1"] = {"kernel": full[:80], "dram_bytes_per_launch": b * scale,
