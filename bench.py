@@ -486,7 +486,7 @@ def main():
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": (f"ax_kernel<{N + 1},AX_PCG,PF> (p = dinv r + beta p, Ax, mask, sigma)"
                            if pf else f"ax_kernel<{N + 1},AX_PCG> (Ax+mask+sigma)"),
-                "bytes_per_pt": kbytes, "hbm_mandatory_bytes_per_pt": 64.0,
+                "bytes_per_pt": kbytes, "hbm_mandatory_bytes_per_pt": kbytes,
                 "avg_ms_per_apply": k_avg, "launches": k_cnt, "applies": n_apply,
                 "peak_source": peak_src,
                 "step_share": k_ms / max(k_ms + u_ms + p_ms + g_ms, 1e-9),

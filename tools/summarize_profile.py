@@ -96,14 +96,13 @@ def main():
     traffic = {}
     # prefer the one-rank PCG kernel with the fused p update (<8, 2, 0, 1>)
     cands = [r for name, r in seen.items() if "ax_kernel" in name and "<8, 2" in r[ki]]
-    cands.sort(key=lambda r: 0 if "<8, 2, 0, 1>" in r[ki] or "true>" in r[ki] else 1)
+    cands.sort(key=lambda r: 0 if ("<8, 2, 0, 1>" in r[ki] or "true>" in r[ki]) else 1)
     for r in cands[:1]:
-        if True:
-            full = r[ki]
-                b = float(r[h.index("dram__bytes_read.sum")]) + float(r[h.index("dram__bytes_write.sum")])
-                scale = 1e6 if units[h.index("dram__bytes_read.sum")].lower().startswith("m") else 1.0
-                traffic["C2_N7_P1"] = {"kernel": full[:80], "dram_bytes_per_launch": b * scale,
-                                       "source": os.path.basename(rep)}
+        full = r[ki]
+        b = float(r[h.index("dram__bytes_read.sum")]) + float(r[h.index("dram__bytes_write.sum")])
+        scale = 1e6 if units[h.index("dram__bytes_read.sum")].lower().startswith("m") else 1.0
+        traffic["C2_N7_P1"] = {"kernel": full[:80], "dram_bytes_per_launch": b * scale,
+                               "source": os.path.basename(rep)}
     if traffic:
         json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
     print(out)
