@@ -841,7 +841,7 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
   cudaStream_t s = c->stream;
   sem::PcgState* st = c->d_st;
   k->dist = c->hp.nranks > 1;
-  k->pf = c->pcg_fuse && !k->dist;
+  k->pf = c->pcg_fuse;
   k->rg_out = k->dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   // peer-memory allreduces fused into the CG kernels (nranks > 1 with NVLink mailboxes)
   k->pp = p2p(c);
@@ -867,13 +867,25 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
   c->ax_pdl_now = false;
   c->pf_now = false;
   SEM_TRY(sa);
-  if (k.pf) {   // r, x updates and the end of the iteration in one kernel
+  if (k.pf) {   // r, x updates and (one rank, peer memory) the end of the iteration
+    sem::PeerSync ps;
+    if (k.pp) {
+      ps.c = c->p2p;
+      ps.e_wait = c->cur_e_sig;
+      ps.e_pub = ++c->ep_ar[sem::AR_RG];
+    }
+    const bool end_here = !k.dist || k.pp;
     int tk = timer_begin(c, 1);
     CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv, c->d_partial, st,
-                                   k.rg_out, c->d_partial_ax, c->d_nsig, sem::PeerSync{},
-                                   c->red_grid, s, x, c->d_p, c->d_hist));
+                                   k.rg_out, k.dist ? nullptr : c->d_partial_ax, c->d_nsig, ps,
+                                   c->red_grid, s, x, c->d_p, c->d_hist, end_here ? 1 : 0));
     timer_end(c, tk);
     c->launches++;
+    if (!end_here) {   // NCCL / loopback: reduce (rho', gamma), then end the iteration
+      SEM_TRY(allreduce_site(c, sem::AR_RG, &st->loc[0], &st->rho_new, 2));
+      CUDA_TRY(sem::launch_cg_end_iter(st, c->d_hist, s));
+      c->launches++;
+    }
     return SEM_OK;
   }
   sem::PeerSync psu, psp;

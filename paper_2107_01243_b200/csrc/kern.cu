@@ -348,13 +348,39 @@ __global__ void cg_start_kernel(PcgState* st, double* hist, const PeerSync ps) {
   st->iters = 0;
 }
 
+// end of a PCG iteration from the reduced (rho', gamma) in the state:
+// convergence test on sqrt(gamma) (reading Q15), NaN guard, beta = rho'/rho,
+// rho <- rho', residual history (the p kernel's last block does the same)
+__device__ __forceinline__ void pcg_end_iteration(PcgState* st, double* hist) {
+  const double rho_new = st->rho_new, gamma = st->gamma;
+  const double g = sqrt(gamma);
+  const int it = st->it + 1;
+  st->it = it;
+  hist[it] = g;
+  if (!(g == g) || !(rho_new == rho_new)) {
+    st->done = 3;
+    st->iters = it;
+  } else if (g <= st->tol) {
+    st->done = 1;
+    st->iters = it;
+  } else {
+    st->beta = rho_new / st->rho_old;
+    st->rho_old = rho_new;
+    if (it >= st->maxit) {
+      st->done = 4;
+      st->iters = it;
+    }
+  }
+}
+
 // alpha = rho / sigma; r -= alpha w; partials of rho' = <r, dinv r>_c and
 // gamma = <r, r>_c (z is never stored).  Unfused: x += alpha p is deferred to
 // the p kernel, which streams p anyway (same operation, one pass less over p
 // and x).  PF (one rank, p update fused into the next Ax kernel): x += alpha p
 // here, and the last block ends the iteration -- convergence test on
 // sqrt(gamma), beta = rho'/rho for the next Ax kernel, history -- as the p
-// kernel's last block does otherwise.
+// kernel's last block does otherwise (end_here = 0: NCCL / loopback, where
+// cg_end_iter_kernel does it after the host-side allreduce).
 template <bool PF>
 __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                  const double* __restrict__ dinv, double* __restrict__ r,
@@ -362,7 +388,7 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
                                  double* out2, const double* __restrict__ sig_part,
                                  const int* sig_count, const PeerSync ps,
                                  double* __restrict__ x, const double* __restrict__ p,
-                                 double* hist) {
+                                 double* hist, int end_here) {
   __shared__ double scratch[32];
   __shared__ int flag;
   __shared__ double s_sig;
@@ -441,29 +467,25 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
       st->iters = st->it + 1;
     }
     if (threadIdx.x == 0 && ps.c.P > 1) ar_publish(ps.c, AR_RG, ps.e_pub, out2, 2);
-    if (PF && ok && threadIdx.x == 0) {   // end of the iteration (one rank: out2 = st->rho_new)
+    if (PF && ok && end_here && threadIdx.x == 0) {
+      // end of the iteration: one rank -- out2 is st->rho_new; peer memory --
+      // the ranks' partials summed in ascending rank order first
       __threadfence();
-      const double rho_new = st->rho_new, gamma = st->gamma;
-      const double g = sqrt(gamma);
-      const int it = st->it + 1;
-      st->it = it;
-      hist[it] = g;
-      if (!(g == g) || !(rho_new == rho_new)) {
-        st->done = 3;
-        st->iters = it;
-      } else if (g <= st->tol) {
-        st->done = 1;
-        st->iters = it;
-      } else {
-        st->beta = rho_new / st->rho_old;
-        st->rho_old = rho_new;
-        if (it >= st->maxit) {
-          st->done = 4;
-          st->iters = it;
-        }
+      if (ps.c.P > 1) {
+        double g2[2];
+        ar_wait_sum(ps.c, AR_RG, ps.e_pub, 2, g2);
+        st->rho_new = g2[0];
+        st->gamma = g2[1];
       }
+      pcg_end_iteration(st, hist);
     }
   }
+}
+
+// PF over NCCL / loopback: the end of the iteration after the host-side allreduce
+__global__ void cg_end_iter_kernel(PcgState* st, double* hist) {
+  if (st->done) return;
+  pcg_end_iteration(st, hist);
 }
 
 // x += alpha p (this iteration's alpha, always); convergence test on
@@ -753,12 +775,18 @@ cudaError_t launch_cg_start(PcgState* st, double* hist, const PeerSync& ps, cuda
 cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double* dinv, double* r,
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
-                             int grid, cudaStream_t s, double* x, const double* p, double* hist) {
+                             int grid, cudaStream_t s, double* x, const double* p, double* hist,
+                             int end_here) {
   if (x)
     return launch_k(dev::cg_update_kernel<true>, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult,
-                    dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist);
+                    dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist, end_here);
   return launch_k(dev::cg_update_kernel<false>, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult,
-                  dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist);
+                  dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist, end_here);
+}
+
+cudaError_t launch_cg_end_iter(PcgState* st, double* hist, cudaStream_t s) {
+  dev::cg_end_iter_kernel<<<1, 1, 0, s>>>(st, hist);
+  return cudaGetLastError();
 }
 
 bool gs_flat(const DevPlan& P, int mode) { return dev::gs_mode_ce(P, mode) == 0; }
