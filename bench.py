@@ -371,21 +371,21 @@ def main():
     # ---- dominant kernel (Ax + mask + sigma), CUDA events on the context stream
     ctx.timing(True)
     ctx.pcg_solve(b, x, 0.0, args.steps)
-    # P = 1: the PF Ax kernel is timer class 9 (the final true-residual apply,
-    # class 0, is excluded); P > 1: class 0 over the K iterations + 1 apply
-    k_ms, k_cnt = ctx.timing_read(9 if P == 1 else 0)
+    # the Ax kernel with the fused p update is timer class 9 (the final
+    # true-residual apply, class 0, is excluded); per iteration
+    k_ms, k_cnt = ctx.timing_read(9)
     u_ms, u_cnt = ctx.timing_read(1)
     p_ms, p_cnt = ctx.timing_read(2)
     g_ms, g_cnt = ctx.timing_read(4)
     ctx.timing(False)
     # per operator application (the split Alg. 1 operator launches the kernel
     # twice per application at N > 1): steps iterations + 1 true-residual apply
-    n_apply = args.steps if P == 1 else args.steps + 1
+    n_apply = args.steps
     k_avg = max_over_ranks(k_ms / n_apply)
     bm = bytes_model(N)
     peak, peak_src = peaks()
-    # P = 1: the Ax kernel also performs the p update (PF): p_old, r, dinv in, p out
-    pf = P == 1
+    # the Ax kernel also performs the p update (PF): p_old, r, dinv in, p out
+    pf = True
     kbytes = bm["ax_pf"] if pf else bm["ax"]
     achieved = nl * kbytes / (k_avg / 1e3) / 1e9
     traffic = None
@@ -461,9 +461,10 @@ def main():
             "config": {
                 "workload": workload_desc(args.config, P),
                 "N": N, "elements": spec.E, "n_p": n_p_total, "n_glob": ctx.n_glob,
-                "step": (("one Jacobi-PCG iteration: Ax+mask+<p,Ap> kernel, gather-scatter kernel "
-                          "with the NVLink peer-memory exchange and allreduce, r update + "
-                          "<r,z>_c, <r,r>_c kernel, x/p update kernel") if P > 1 else
+                "step": (("one Jacobi-PCG iteration, three kernels: p update + Ax + mask + <p,Ap> "
+                          "kernel, gather-scatter kernel with the NVLink peer-memory exchange and "
+                          "sigma allreduce, r and x update + <r,z>_c, <r,r>_c + allreduce + "
+                          "convergence kernel") if P > 1 else
                          ("one Jacobi-PCG iteration, three kernels replayed as a CUDA graph: "
                           "p update + Ax + mask + <p,Ap> kernel, gather-scatter kernel, "
                           "r and x update + <r,z>_c, <r,r>_c + convergence kernel")),
