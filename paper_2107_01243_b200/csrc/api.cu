@@ -23,6 +23,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -186,6 +187,10 @@ struct sem_ctx {
   uint64_t ep_gs = 0, ep_ar[sem::P2P::kSites] = {0, 0, 0, 0};
   std::vector<uint64_t> ep_ping;   // per peer: ping-pong flag epochs
   uint64_t cur_e_sig = 0;   // sigma epoch published by the last PCG apply
+  // PCG at P > 1 over peer memory, graph-replayed: the iteration kernels take
+  // their epochs from the device state (PcgState::ep0 + iteration) instead of
+  // kernel arguments, so a captured batch is argument-stable
+  bool dev_ep = false;
 };
 
 namespace {
@@ -370,10 +375,11 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
   if (h.nranks > 1 && h.nS > 0 && p2p(c) && !c->overlap) {
     // one Ax launch, then ONE exchange kernel: pack into the neighbours'
     // receive buffers, rank-local gs while the partials travel, unpack
-    const uint64_t e = ++c->ep_gs;
+    const bool dev_ep = c->dev_ep && mode == sem::AX_PCG;   // epochs from the device state
+    const uint64_t e = dev_ep ? 0 : ++c->ep_gs;
     // PCG: the Ax kernel leaves per-CTA sigma partials; the exchange kernel sums them
     SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0, nullptr));
-    c->cur_e_sig = mode == sem::AX_PCG ? ++c->ep_ar[sem::AR_SIG] : 0;
+    c->cur_e_sig = mode == sem::AX_PCG ? (dev_ep ? 0 : ++c->ep_ar[sem::AR_SIG]) : 0;
     int tk = timer_begin(c, 4);
     CUDA_TRY(sem::launch_gs_exchange_p2p(c->dp, w, c->d_part, c->p2p, e, 1,
                                          mode == sem::AX_PCG ? st : nullptr, 1, c->cur_e_sig,
@@ -871,8 +877,12 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
     sem::PeerSync ps;
     if (k.pp) {
       ps.c = c->p2p;
-      ps.e_wait = c->cur_e_sig;
-      ps.e_pub = ++c->ep_ar[sem::AR_RG];
+      if (c->dev_ep) {
+        ps.dev = st;
+      } else {
+        ps.e_wait = c->cur_e_sig;
+        ps.e_pub = ++c->ep_ar[sem::AR_RG];
+      }
     }
     const bool end_here = !k.dist || k.pp;
     int tk = timer_begin(c, 1);
@@ -1024,7 +1034,7 @@ static int cgcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t 
 // the graph is keyed by the operands that enter the kernel arguments.
 // Returns nullptr (plain stream launches) when not applicable.
 static cudaGraphExec_t pcg_batch_graph(sem_ctx* c, const double* dinv, double* x, const PcgCtl& k) {
-  if (!c->pcg_graph || c->hp.nranks > 1 || c->timing || c->ax_gate ||
+  if (!c->pcg_graph || (c->hp.nranks > 1 && !c->dev_ep) || c->timing || c->ax_gate ||
       !sem::gs_flat(c->dp, c->gs_mode))
     return nullptr;
   const double key[4] = {(double)(uintptr_t)x, (double)(uintptr_t)dinv, c->helm ? c->h1 : -1.0,
@@ -1078,8 +1088,20 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
   std::memcpy(c->h_st, &init, sizeof(init));   // h_st is idle: every solve ends synchronised
   CUDA_TRY(cudaMemcpyAsync(st, c->h_st, sizeof(init), cudaMemcpyHostToDevice, s));
   const double* dinv = c->helm ? c->d_dinv_helm : c->d_dinv;   // Jacobi of the operator in use
+  static_assert(offsetof(sem::PcgState, done) == offsetof(sem::PcgState, it) + sizeof(int),
+                "the host polls (it, done) with one copy");
   PcgCtl k;
+  c->dev_ep = false;
   SEM_TRY(pcg_enqueue_init(c, dinv, b, x, &k));
+  // P > 1 over peer memory with graph replay: device-side epochs from here on
+  c->dev_ep = k.pp && k.pf && c->pcg_graph && !c->timing && !c->ax_gate && !c->overlap &&
+              sem::gs_flat(c->dp, c->gs_mode);
+  if (c->dev_ep) {
+    c->h_st->ep0[0] = c->ep_gs;
+    c->h_st->ep0[1] = c->ep_ar[sem::AR_SIG];
+    c->h_st->ep0[2] = c->ep_ar[sem::AR_RG];
+    CUDA_TRY(cudaMemcpyAsync(st->ep0, c->h_st->ep0, sizeof(st->ep0), cudaMemcpyHostToDevice, s));
+  }
   int done = 0;
   for (int it = 0; it < maxit && !done; it += kBatch) {
     const int nb = std::min(kBatch, maxit - it);
@@ -1090,10 +1112,18 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
     } else {
       for (int q = 0; q < nb; q++) SEM_TRY(pcg_enqueue_iter(c, dinv, x, k));
     }
-    CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    // (it, done) adjacent in the state: the iteration count advances the epochs
+    CUDA_TRY(cudaMemcpyAsync(&c->h_st->it, &st->it, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaEventRecord(c->ev_poll, s));
     CUDA_TRY(cudaEventSynchronize(c->ev_poll));
     done = c->h_st->done;
+  }
+  if (c->dev_ep) {   // the host's epoch counters continue after the device-side ones
+    const uint64_t kit = (uint64_t)c->h_st->it;
+    c->ep_gs = c->h_st->ep0[0] + kit;
+    c->ep_ar[sem::AR_SIG] = c->h_st->ep0[1] + kit;
+    c->ep_ar[sem::AR_RG] = c->h_st->ep0[2] + kit;
+    c->dev_ep = false;
   }
   return pcg_finish(c, b, x, res);
 }

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
                                  const double* __restrict__ dinv, double* __restrict__ r,
                                  const double* __restrict__ w, double* partial, PcgState* st,
                                  double* out2, const double* __restrict__ sig_part,
-                                 const int* sig_count, const PeerSync ps,
+                                 const int* sig_count, const PeerSync ps_in,
                                  double* __restrict__ x, const double* __restrict__ p,
                                  double* hist, int end_here) {
   __shared__ double scratch[32];
@@ -395,6 +395,12 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
   pdl_wait();
   pdl_trigger();
   if (st->done) return;
+  PeerSync ps = ps_in;
+  if (ps.dev) {   // device-side epochs (graph-replayed iterations at P > 1)
+    const uint64_t kit = (uint64_t)st->it + 1;
+    ps.e_wait = st->ep0[1] + kit;
+    ps.e_pub = st->ep0[2] + kit;
+  }
   double sigma;
   if (ps.c.P > 1) {   // global sigma from the peers' mailboxes (rank-ordered sum)
     if (threadIdx.x == 0) ar_wait_sum(ps.c, AR_SIG, ps.e_wait, 1, &s_sig);

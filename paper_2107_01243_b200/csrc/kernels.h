@@ -88,6 +88,8 @@ struct PcgState {
   double loc_dz[2];      // P > 1: this rank's partials of dz
   double cg3[3];         // single-reduction PCG: gamma = <r,u>_c, eps = <r,r>_c, delta = <w,u>_c
   double cg3_loc[3];     // P > 1: this rank's partials of cg3 (one allreduce per iteration)
+  uint64_t ep0[3];       // device-side epochs (graph-replayed PCG at P > 1): iteration k
+                         // uses ep0[site] + k for the gs exchange, sigma and (rho', gamma)
   int it;                // completed iterations
   int done;              // 0 running, 1 converged, 2 breakdown, 3 NaN, 4 maxit
   int iters;
@@ -156,6 +158,7 @@ enum ArSite { AR_SIG = 0, AR_RG = 1, AR_RES = 2, AR_MISC = 3 };
 struct PeerSync {
   P2P c;
   uint64_t e_wait = 0, e_pub = 0;
+  const PcgState* dev = nullptr;   // non-null: the epochs come from dev->ep0 and dev->it
 };
 
 cudaError_t launch_gs_pack_p2p(const DevPlan& P, const double* u, double* part, const P2P& c,

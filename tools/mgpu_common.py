@@ -49,13 +49,20 @@ def rank_run(c, u_local, fun, schwarz=True):
     c.rhs(fv, b)
     x = c.zeros()
     r = c.pcg_solve(b, x, 1e-10, 3000)
+    # the same solve with stream launches instead of the replayed CUDA graph
+    # (P > 1 over peer memory: device-side epochs in the graph)
+    xs_ = c.zeros()
+    c.set_pcg_graph(False)
+    rs_ = c.pcg_solve(b, xs_, 1e-10, 3000)
+    c.set_pcg_graph(True)
     xc = c.zeros()
     c.set_pcg_variant("single_reduction")   # one allreduce per iteration
     rc = c.pcg_solve(b, xc, 1e-10, 3000)
     c.set_pcg_variant("standard")
     xg = c.zeros()
     rg = c.gmres_solve(b, xg, 1e-10, 3000, 20)
-    out = {"w": w, "g": g, "b": b, "x": x, "r": r, "xc": xc, "rc": rc, "xg": xg, "rg": rg}
+    out = {"w": w, "g": g, "b": b, "x": x, "r": r, "xc": xc, "rc": rc, "xg": xg, "rg": rg,
+           "x_nograph": xs_, "r_nograph": rs_}
     if schwarz:
         # NEXT-1: the fine gs and the N = 1 coarse CG run through the same transport
         c.set_precond("schwarz")
@@ -118,6 +125,8 @@ def check(parts, ref, tag, schwarz=True):
         fails.append(f"{tag}: pcg x diff {dx:.2e}")
     if not abs(r["res_final"] - ref.pcg["res_final"]) <= 1e-10:
         fails.append(f"{tag}: pcg res {r['res_final']:.3e} vs {ref.pcg['res_final']:.3e}")
+    if parts[0]["r_nograph"]["iters"] != r["iters"] or not np.array_equal(cat("x_nograph"), X):
+        fails.append(f"{tag}: graph-replayed and stream-launched PCG differ")
     rc = parts[0]["rc"]
     if abs(rc["iters"] - ref.cgcg["iters"]) > 1 or rc["status"] != 0:
         fails.append(f"{tag}: single-reduction pcg iters {rc['iters']} vs {ref.cgcg['iters']}")
