@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
   pdl_wait();
   pdl_trigger();
   XTS(0);
-  if (st) {   // PCG iteration: a finished solve consumes no epochs (same on every rank)
-    if (st->done) return;
+  if (st) {   // PCG iteration: a finished solve consumes no epochs (same on every rank);
+              // the chunk schedule must still take its tickets (host-tracked base)
+    if (!SWEEP && st->done) return;
     if (epoch == 0) {   // device-side epochs (graph-replayed iterations)
       const uint64_t k = (uint64_t)st->it + 1;
       epoch = st->ep0[0] + k;
