@@ -301,9 +301,10 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   int tk = timer_begin(c, mode == sem::AX_ONLY ? 3 : (c->pf_now && mode == sem::AX_PCG ? 9 : 0));
   // PCG iterations: programmatic dependent launch of the Ax kernel alone, its
   // producer prefetching G before waiting for the preceding kernel (SEM_OPT_AX_PDL)
-  const bool pdl = c->ax_pdl_now && !c->timing && !sem::pdl_on();
+  const bool pdl = c->ax_pdl_now && !c->timing;
+  const bool pdl_set = pdl && !sem::pdl_on();   // (already on: every iteration kernel uses PDL)
   a.pdl_pref = pdl ? 1 : 0;
-  if (pdl) sem::set_pdl(true);
+  if (pdl_set) sem::set_pdl(true);
   const bool pf = c->pf_now && mode == sem::AX_PCG;
   if (pf) {   // u is p: p_old in, p_new out (in place)
     a.rr = c->d_r;
@@ -313,7 +314,7 @@ int run_ax(sem_ctx* c, const double* u, double* w, int mode, int r0lo, int r0hi,
   }
   cudaError_t e = sem::launch_ax(c->dp, a, mode, groups, c->stream,
                                  c->helm && mode != sem::AX_ONLY, pf);
-  if (pdl) sem::set_pdl(false);
+  if (pdl_set) sem::set_pdl(false);
   timer_end(c, tk);
   c->launches++;
   return check(e, "ax kernel");
