@@ -288,17 +288,26 @@ __global__ void __launch_bounds__(kFT) fdm_kernel(int nloc, const double* __rest
 // (D[8x8] += A[8x4] B[4x8]).  The S factors are operands held in registers
 // (2 per stage per lane, read once from global/L2); the element's data moves
 // between two shared-memory buffers with the padded layout
-// a(i,j,k) = i + 12 j + 100 k, which makes every fragment load and store of
-// the six stages (strides 1/12/100 against the lane fields g = lane/4,
-// q = lane%4 and the accumulator columns 2q+e) hit each bank pair exactly
-// twice: conflict-free.  The same smem traffic as one CUDA-core stage moves
+// a(i,j,k) = (i ^ 4 [bit 2 of j != bit 2 of k]) + 12 j + 100 k (pad8), which
+// makes every fragment load and store of the six stages (strides 1/12/100
+// against the lane fields g = lane/4, q = lane%4 and the accumulator columns
+// 2q+e) conflict-free.  The same smem traffic as one CUDA-core stage moves
 // 8x the arithmetic, which is what takes the kernel from shared-memory bound
 // (15 % of HBM bandwidth) towards the HBM roofline.
 constexpr int kF8W = 4;          // warps (elements in flight) per CTA
 constexpr int kF8Buf = 800;      // doubles per padded buffer (max index 791)
 constexpr int kF8Smem = kF8W * 2 * kF8Buf + 2 * 256;   // + 1/m and (1/m)^1/2 tables
 
-__device__ __forceinline__ int pad8(int i, int j, int k) { return i + 12 * j + 100 * k; }
+// swizzled padded layout: i is XOR-ed with 4 when bit 2 of j and bit 2 of k
+// differ.  The plain pad i + 12 j + 100 k made every fragment LOAD of the six
+// stages conflict-free but the accumulator STORES (columns 2q + e) 2-way
+// conflicted within each half warp (lanes q and q + 2 on one bank pair):
+// ~8 M excess wavefronts per C3 launch in ncu.  The swizzle makes loads and
+// stores hit 16 distinct bank pairs per half warp (checked for every stage
+// pattern and for the 128-bit load / store phases) in the same 792 doubles.
+__device__ __forceinline__ int pad8(int i, int j, int k) {
+  return (i ^ (4 * (((j >> 2) ^ (k >> 2)) & 1))) + 12 * j + 100 * k;
+}
 
 // not volatile: the tiles of a stage are independent and the scheduler may
 // interleave their DMMAs (a volatile asm keeps program order)
@@ -356,9 +365,18 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
     cinv[m] = c;
     csq[m] = sqrt(c);
   }
-  // this lane's points in the load phase: p = 2 (lane + 32 m) -> i = 2 lane % 8,
-  // j = lane / 4, k = m: the restriction weights J_ia J_jb J_kc factor per lane
-  const int i0 = (2 * lane) & 7, j0 = lane >> 2;
+  // this lane's point pair in the load / store phases: pair q of plane m
+  // (points 2q, 2q + 1: i = 2 (q % 4), j = q / 4, k = m).  The lane -> pair map
+  // is a permutation within the warp's 512-B segment (still one coalesced
+  // access) chosen so that the eight lanes of every quarter warp hit eight
+  // distinct 16-B bank groups of the padded buffer (pad8 = i + 12 j + 100 k):
+  // quarter warp G takes the rows j in {jt[G], jt[G] + 2}, jt = {0, 1, 4, 5}
+  // (the identity map, j = lane / 4, put two lanes on every group: 2-way
+  // conflicts on the LDS.128 / STS of these phases, ~9 M excess wavefronts
+  // per C3 launch in ncu).  The restriction weights J_ia J_jb J_kc factor per lane.
+  const int qp = ((lane >> 3) == 0 ? 0 : (lane >> 3) == 1 ? 1 : (lane >> 3) == 2 ? 4 : 5) * 4 +
+                 ((lane >> 2) & 1) * 8 + (lane & 3);
+  const int i0 = 2 * (qp & 3), j0 = qp >> 2;
   const double xa = __ldg(&xi[i0]), xb = __ldg(&xi[i0 + 1]), xj = __ldg(&xi[j0]);
   const double ja[2] = {0.5 * (1.0 - xa), 0.5 * (1.0 + xa)};
   const double jb[2] = {0.5 * (1.0 - xb), 0.5 * (1.0 + xb)};
@@ -372,8 +390,8 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
     uchar2 mv[8];
 #pragma unroll
     for (int m = 0; m < 8; m++) {
-      rv[m] = __ldcs(&r2[lane + 32 * m]);
-      mv[m] = m2[lane + 32 * m];
+      rv[m] = __ldcs(&r2[qp + 32 * m]);
+      mv[m] = m2[qp + 32 * m];
     }
     const double* Sx = Sg + (size_t)el * 192;
     const double* Sy = Sx + 64;
@@ -468,7 +486,7 @@ __global__ void __launch_bounds__(kF8W * 32) fdm8_kernel(
     double2* y2 = reinterpret_cast<double2*>(y + (int64_t)el * 512);
 #pragma unroll
     for (int m = 0; m < 8; m++)
-      __stcs(&y2[lane + 32 * m], make_double2(U[pad8(i0, j0, m)], U[pad8(i0 + 1, j0, m)]));
+      __stcs(&y2[qp + 32 * m], make_double2(U[pad8(i0, j0, m)], U[pad8(i0 + 1, j0, m)]));
     __syncwarp();   // U is refilled by the next element
   }
 }
