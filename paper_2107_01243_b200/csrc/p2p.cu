@@ -276,10 +276,11 @@ static cudaError_t launch_exchange_n(const DevPlan& P, double* u, double* part, 
   const int g = resident[ce > 0 ? 1 : 0];
   const unsigned long long b = *base;
   *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
+  // cooperative: the packers' receive-record waits need every CTA co-resident
   if (ce > 0)
-    return launch_k(dev::gs_exchange_p2p_kernel<n, true>, dim3(g), dim3(256), 0, s, P, u, part, c,
-                    epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
-  return launch_k(dev::gs_exchange_p2p_kernel<n, false>, dim3(g), dim3(256), 0, s, P, u, part, c,
+    return launch_coop(dev::gs_exchange_p2p_kernel<n, true>, dim3(g), dim3(256), 0, s, P, u, part, c,
+                       epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
+  return launch_coop(dev::gs_exchange_p2p_kernel<n, false>, dim3(g), dim3(256), 0, s, P, u, part, c,
                   epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
 }
 
