@@ -32,27 +32,6 @@ cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
-// Cooperative launch: the runtime guarantees that every CTA of the grid is
-// co-resident (or fails the launch) -- for kernels whose CTAs wait on each
-// other's (or another GPU's) progress, e.g. the peer-memory exchange kernel
-template <typename... KArgs, typename... Args>
-cudaError_t launch_coop(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                        Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_on() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
-}
-
 // Launch geometry and function attributes belong to a device: the launchers
 // cache them per device index (kMaxDev) in atomics (loopback ranks launch from
 // several host threads).

@@ -276,11 +276,16 @@ static cudaError_t launch_exchange_n(const DevPlan& P, double* u, double* part, 
   const int g = resident[ce > 0 ? 1 : 0];
   const unsigned long long b = *base;
   *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
-  // cooperative: the packers' receive-record waits need every CTA co-resident
+  // The packers' receive-record waits need every CTA co-resident: the grid is
+  // capped at the occupancy-computed residency.  A cooperative launch (the
+  // runtime's guarantee) was measured 10 us slower per exchange (C2, 2 GPUs:
+  // 39.4 vs 29.4 us, profiles/r02_experiments/coop_launch.txt); a kernel that
+  // cannot become co-resident (another stream occupying the SMs) times out
+  // after ~4 s and the call returns SEM_ENCCL instead of hanging.
   if (ce > 0)
-    return launch_coop(dev::gs_exchange_p2p_kernel<n, true>, dim3(g), dim3(256), 0, s, P, u, part, c,
-                       epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
-  return launch_coop(dev::gs_exchange_p2p_kernel<n, false>, dim3(g), dim3(256), 0, s, P, u, part, c,
+    return launch_k(dev::gs_exchange_p2p_kernel<n, true>, dim3(g), dim3(256), 0, s, P, u, part, c,
+                    epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
+  return launch_k(dev::gs_exchange_p2p_kernel<n, false>, dim3(g), dim3(256), 0, s, P, u, part, c,
                   epoch, apply_mask, st, nparts, e_sig, sig_part, sig_count, b, ce);
 }
 
