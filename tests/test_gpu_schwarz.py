@@ -123,6 +123,10 @@ def test_schwarz_pcg_parity(spec, N):
         h = c.pcg_history()
         k = min(len(h), len(ref["hist"]), 4)
         np.testing.assert_allclose(h[:k], ref["hist"][:k], rtol=1e-8)
+        # the host-buffer entry point runs the same (Schwarz) solve
+        xh = np.zeros(c.n_local)
+        rh = c.pcg_solve_host(np.ascontiguousarray(b), xh, 1e-10, 500)
+        assert rh["iters"] == r["iters"] and np.array_equal(xh, host(x))
         # back to Jacobi: the plain PCG again
         c.set_precond("jacobi")
         rj = o.pcg(b, 1e-10, 3000)
