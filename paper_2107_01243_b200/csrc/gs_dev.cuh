@@ -52,14 +52,18 @@ __device__ __forceinline__ int e_sd(int axis, int n) { return axis == 0 ? 1 : (a
 #define SEM_GS_FFE 1
 #endif
 constexpr int kGsF = SEM_GS_FF, kGsFE = SEM_GS_FFE;
+// the rounds over the entity ranges [f0, f0 + nFr), [e0, e0 + nEr), [v0, v0 + nVr)
+// by threads tid of nth (the flat schedule: every entity, the whole grid; the
+// chunk schedule: one chunk's entities, one block)
 template <int n, int F = kGsF, int FE = kGsFE>
-__device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restrict__ u,
-                                               int apply_mask, int tid, int nth) {
+__device__ __forceinline__ void gs_round_body(const DevPlan& P, double* __restrict__ u,
+                                              int apply_mask, int tid, int nth, int f0, int nFr,
+                                              int e0, int nEr, int v0, int nVr) {
   constexpr int N = n - 1;
   constexpr int nf = (N - 1) * (N - 1), ne = N - 1;
   constexpr int Nm1 = N > 1 ? N - 1 : 1;
   constexpr int nfd = nf > 0 ? nf : 1, ned = ne > 0 ? ne : 1;
-  const int tF = P.nF * nf, tE = P.nEd * ne;
+  const int tF = nFr * nf, tE = nEr * ne;
   const int rF = nf > 0 ? (tF + nth * F - 1) / (nth * F) : 0;
   const int rE = ne > 0 ? (tE + nth * FE - 1) / (nth * FE) : 0;
   const int rounds = rF > rE ? rF : rE;
@@ -72,8 +76,9 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
     for (int q = 0; q < F; q++) {
       const int t = (r * F + q) * nth + tid;
       fok[q] = nf > 0 && t < tF;
-      const int f = fok[q] ? t / nfd : 0;
-      const int p = t - f * nf;
+      const int fl = fok[q] ? t / nfd : 0;
+      const int p = t - fl * nf;
+      const int f = f0 + fl;
       const int ax = fok[q] ? P.f_axis[f] : 0;
       const int off = (1 + p % Nm1) * f_s1(ax, n) + (1 + p / Nm1) * f_s2(ax, n);
       const int2 b2 = fok[q] ? reinterpret_cast<const int2*>(P.f_base)[f] : make_int2(0, 0);
@@ -85,8 +90,9 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
     for (int q = 0; q < FE; q++) {
       const int t = (r * FE + q) * nth + tid;
       const bool ok = ne > 0 && t < tE;
-      const int e = ok ? t / ned : 0;
-      const int p = t - e * ne;
+      const int el = ok ? t / ned : 0;
+      const int p = t - el * ne;
+      const int e = e0 + el;
       enin[q] = ok ? P.e_nin[e] : 0;
       eoff[q] = ok ? (1 + p) * e_sd(P.e_axis[e], n) : 0;
       emk[q] = ok && P.e_mask[e];
@@ -129,7 +135,8 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
         if (x < enin[q]) gs_st(&u[eb[q][x] + eoff[q]], s);
     }
   }
-  for (int v = tid; v < P.nV; v += nth) {
+  for (int vl = tid; vl < nVr; vl += nth) {
+    const int v = v0 + vl;
     const int nin = P.v_nin[v];
     const int4 b0 = reinterpret_cast<const int4*>(P.v_base)[2 * v];
     const int4 b1 = reinterpret_cast<const int4*>(P.v_base)[2 * v + 1];
@@ -150,6 +157,12 @@ __device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restric
     for (int x = 0; x < 8; x++)
       if (x < nin) gs_st(&u[base[x]], s);
   }
+}
+
+template <int n>
+__device__ __forceinline__ void gs_flat_body(const DevPlan& P, double* __restrict__ u,
+                                             int apply_mask, int tid, int nth) {
+  gs_round_body<n>(P, u, apply_mask, tid, nth, 0, P.nF, 0, P.nEd, 0, P.nV);
 }
 
 // Rank-local gather-scatter, one sweep in element order.  The planner creates
@@ -289,6 +302,8 @@ __device__ __forceinline__ void gs_sweep_body(const DevPlan& P, double* __restri
     unsigned long long nx = 0;
     if (threadIdx.x == 0) nx = atomicAdd(ctr, 1ull);
     const int e0 = (int)c * ce;
+    // (the flat schedule's load-all-first rounds over the chunk's entity ranges were
+    // measured 10-40 % slower here: profiles/r02_experiments/gs_chunk_rounds.jsonl)
     gs_chunk_body<n>(P, u, apply_mask, e0, min(e0 + ce, P.nloc));
     if (threadIdx.x == 0) s_next = (long long)(nx - base);
     __syncthreads();
