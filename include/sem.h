@@ -308,6 +308,14 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    value is computed by the same expression), iterates equal up to the
    sigma partial-sum order. */
 #define SEM_OPT_PCG_FUSE 15
+/* 1 = on one rank with SEM_OPT_PCG_FUSE, the PCG iteration launches no
+   gather-scatter kernel: the r update sums the unassembled w = A_L p over each
+   shared point's incidences on read (ascending slots, the gs kernel's sum)
+   through a per-element incidence table (496 B per element, built on the
+   first solve); 0 = separate gs kernel; -1 (default) = auto, 1 when the
+   vector exceeds 128 MiB (the L2 size: below it the separate gs kernel on an
+   L2-resident w is faster).  Identical results. */
+#define SEM_OPT_PCG_GSU 16
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

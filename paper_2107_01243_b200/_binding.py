@@ -270,6 +270,12 @@ class Context:
         """One rank: p update fused into the next Ax kernel (default on)."""
         _check(load().sem_set_option(self._h, 15, 1 if on else 0))
 
+    def set_pcg_gsu(self, mode):
+        """One rank, fused PCG: gather-scatter performed on read by the r update
+        instead of a separate gs kernel: True, False or -1 (default: auto, on
+        when a vector exceeds 128 MiB)."""
+        _check(load().sem_set_option(self._h, 16, -1 if mode == -1 else (1 if mode else 0)))
+
     def set_ax_pdl(self, on: bool):
         """PDL launch of the PCG Ax kernel with G prefetched before the grid wait."""
         _check(load().sem_set_option(self._h, 13, 1 if on else 0))

@@ -132,6 +132,12 @@ struct sem_ctx {
   bool pcg_fuse = true;
   bool pf_now = false;            // set around the PCG iteration's Ax launch
   const double* pf_dinv = nullptr;
+  // SEM_OPT_PCG_GSU: one-rank fused PCG with the gather-scatter performed on
+  // read by the r update (per-element incidence table d_gu, built on first use);
+  // -1 auto: when w exceeds the L2
+  int pcg_gsu = -1;
+  bool gsu_now = false;           // set around the PCG iteration's operator
+  int32_t* d_gu = nullptr;
   int pcg_variant = 0;     // SEM_OPT_PCG_VARIANT: 0 standard, 1 single-reduction (Chronopoulos-Gear)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
   cudaGraphExec_t g0exec = nullptr;
@@ -426,7 +432,8 @@ int apply_op(sem_ctx* c, const double* u, double* w, int mode) {
     // single rank: the CG update kernel sums the per-CTA sigma partials itself
     SEM_TRY(run_ax(c, u, w, mode, 0, (int)h.nloc, 0, 0,
                    (mode == sem::AX_PCG && h.nranks == 1) ? nullptr : &st->sigma));
-    SEM_TRY(gs_pass(c, w));
+    // SEM_OPT_PCG_GSU: w stays unassembled, the r update gathers on read
+    if (!(c->gsu_now && mode == sem::AX_PCG)) SEM_TRY(gs_pass(c, w));
     return SEM_OK;
   }
   int nparts = 1;
@@ -513,6 +520,7 @@ void free_ctx(sem_ctx* c) {
     if (p) cudaFree(p);
   if (c->d_gs) cudaFree(c->d_gs);
   if (c->d_ktick) cudaFree(c->d_ktick);
+  if (c->d_gu) cudaFree(c->d_gu);
   if (c->c0) free_ctx(c->c0);
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
@@ -838,9 +846,17 @@ extern "C" int sem_rhs(sem_ctx* c, const double* f, double* b) {
 // ---- PCG building blocks (pcg_run and the Schwarz coarse solve)
 struct PcgCtl {
   bool dist = false, pp = false;
-  bool pf = false;   // p update fused into the Ax kernel (one rank)
+  bool pf = false;   // p update fused into the Ax kernel
+  bool gu = false;   // one rank: gather-scatter on read in the r update
   double* rg_out = nullptr;
 };
+
+// SEM_OPT_PCG_GSU auto: gather on read once w (8 B per slot) exceeds the 126 MB
+// L2.  Below, the gs kernel runs on an L2-resident w and the separate pass is
+// cheaper (C2, 34 MB: 115 vs 123 us per iteration); above, the fused update
+// saves the gs kernel's DRAM round trip (C3, 134 MB: 451 -> 440 us; 1.2e8
+// points at N = 5 / 9: 2-3 %), profiles/r02_experiments/gsu_ab.jsonl
+constexpr int64_t kGsuAutoBytes = 64ll << 20;
 
 // x = 0, r = b, p = dinv b, (rho, gamma), start state; the host wrote tol/maxit
 static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, double* x,
@@ -849,6 +865,14 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
   sem::PcgState* st = c->d_st;
   k->dist = c->hp.nranks > 1;
   k->pf = c->pcg_fuse;
+  k->gu = k->pf && c->hp.nranks == 1 &&
+          (c->pcg_gsu > 0 || (c->pcg_gsu < 0 && c->hp.n_local * 8 > kGsuAutoBytes));
+  if (k->gu && !c->d_gu) {   // the incidence table, once per context
+    std::vector<int32_t> tab;
+    sem::build_gu_table(c->hp, &tab);
+    CUDA_TRY(cudaMalloc(&c->d_gu, std::max<size_t>(tab.size(), 1) * sizeof(int32_t)));
+    CUDA_TRY(cudaMemcpy(c->d_gu, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   k->rg_out = k->dist ? &st->loc[0] : &st->rho_new;   // (rho_new, gamma)
   // peer-memory allreduces fused into the CG kernels (nranks > 1 with NVLink mailboxes)
   k->pp = p2p(c);
@@ -870,9 +894,11 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
   c->ax_pdl_now = c->ax_pdl;
   c->pf_now = k.pf;
   c->pf_dinv = dinv;
+  c->gsu_now = k.gu;
   const int sa = apply_op(c, c->d_p, c->d_wv, sem::AX_PCG);
   c->ax_pdl_now = false;
   c->pf_now = false;
+  c->gsu_now = false;
   SEM_TRY(sa);
   if (k.pf) {   // r, x updates and (one rank, peer memory) the end of the iteration
     sem::PeerSync ps;
@@ -889,7 +915,8 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
     int tk = timer_begin(c, 1);
     CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv, c->d_partial, st,
                                    k.rg_out, k.dist ? nullptr : c->d_partial_ax, c->d_nsig, ps,
-                                   c->red_grid, s, x, c->d_p, c->d_hist, end_here ? 1 : 0));
+                                   c->red_grid, s, x, c->d_p, c->d_hist, end_here ? 1 : 0,
+                                   k.gu ? c->d_gu : nullptr));
     timer_end(c, tk);
     c->launches++;
     if (!end_here) {   // NCCL / loopback: reduce (rho', gamma), then end the iteration
@@ -1960,6 +1987,17 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
   if (option == SEM_OPT_PCG_FUSE) {
     cudaStreamSynchronize(c->stream);
     c->pcg_fuse = value != 0;
+    if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
+    c->pg_exec = nullptr;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_PCG_GSU) {
+    cudaStreamSynchronize(c->stream);
+    if (value < -1 || value > 1) {
+      sem::set_error("sem_set_option: SEM_OPT_PCG_GSU must be -1 (auto), 0 or 1");
+      return SEM_EINVAL;
+    }
+    c->pcg_gsu = value;
     if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
     c->pg_exec = nullptr;
     return SEM_OK;

@@ -381,14 +381,92 @@ __device__ __forceinline__ void pcg_end_iteration(PcgState* st, double* hist) {
 // sqrt(gamma), beta = rho'/rho for the next Ax kernel, history -- as the p
 // kernel's last block does otherwise (end_here = 0: NCCL / loopback, where
 // cg_end_iter_kernel does it after the host-side allreduce).
-template <bool PF>
-__global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
+//
+// GN = n > 0 (SEM_OPT_PCG_GSU): w is the UNASSEMBLED A_L p and this kernel
+// performs the gather-scatter on read.  A slot with multiplicity > 1 sums its
+// point's incidences of w in ascending slot order -- the gs kernel's sum,
+// bit for bit (v0 + v1 for faces, left to right for edges and vertices) --
+// through the per-element incidence table gu; every other slot
+// takes its own w.  The streamed vectors keep their coalesced pair access; only
+// the partner values are gathered (mostly L2 hits: the partners lie in
+// elements e +- 1, e +- ex, e +- ex ey of the slab).  The gs kernel and its
+// write-back of w disappear; r, rho', gamma are bitwise the two-kernel ones.
+// the point's incidence bases (all -1: take its own w) and offset along the
+// entity; depends on the slot index only, so the table load issues with the
+// streamed loads instead of after them
+struct GuRef {
+  int4 a, b;
+  int off;
+};
+template <int n>
+__device__ __forceinline__ GuRef gu_ref(const int32_t* __restrict__ gu, int64_t s) {
+  constexpr int N = n - 1, n2 = n * n, n3 = n2 * n;
+  const int64_t el = s / n3;
+  const int l = (int)(s - el * n3);
+  const int i = l % n, j = (l / n) % n, k = l / n2;
+  const bool bi = i == 0 || i == N, bj = j == 0 || j == N, bk = k == 0 || k == N;
+  const int nb = (int)bi + (int)bj + (int)bk;
+  GuRef g;
+  g.a = g.b = make_int4(-1, -1, -1, -1);
+  g.off = 0;
+  const int32_t* rec = gu + el * kGuInts;
+  if (nb == 1) {   // face interior point: normal axis a
+    const int a = bi ? 0 : (bj ? 1 : 2);
+    const int ca = a == 0 ? i : (a == 1 ? j : k);
+    const int2 bb = reinterpret_cast<const int2*>(rec)[2 * a + (ca == N)];
+    g.a.x = bb.x;
+    g.a.y = bb.y;
+    g.off = l - ca * (a == 0 ? 1 : (a == 1 ? n : n2));
+  } else if (nb == 2) {   // edge interior point: direction a, the other two fixed
+    const int a = !bi ? 0 : (!bj ? 1 : 2);
+    const int lo = a == 0 ? j : i, hi = a == 2 ? j : k;
+    g.a = reinterpret_cast<const int4*>(rec + kGuEdge)[4 * a + (lo == N) + 2 * (hi == N)];
+    g.off = a == 0 ? i : (a == 1 ? j * n : k * n2);
+  } else if (nb == 3) {   // vertex: up to 8 incidences, two groups of 4
+    const int sub = (i == N) + 2 * (j == N) + 4 * (k == N);
+    g.a = reinterpret_cast<const int4*>(rec + kGuVert)[2 * sub];
+    g.b = reinterpret_cast<const int4*>(rec + kGuVert)[2 * sub + 1];
+  }
+  return g;
+}
+
+// ascending incidences, summed left to right (the gs kernel's order); a point
+// that is not on a local entity (interior, Dirichlet side, or shared with
+// another rank) keeps its own value
+__device__ __forceinline__ double gu_sum(const double* __restrict__ w, const GuRef& g,
+                                         double own) {
+  if (g.a.x < 0) return own;
+  const int off = g.off;
+  double acc = w[g.a.x + off];
+  {
+    const double v1 = w[g.a.y + off];
+    const double v2 = g.a.z >= 0 ? w[g.a.z + off] : 0.0;
+    const double v3 = g.a.w >= 0 ? w[g.a.w + off] : 0.0;
+    acc += v1;
+    if (g.a.z >= 0) acc += v2;
+    if (g.a.w >= 0) acc += v3;
+  }
+  if (g.b.x >= 0) {
+    const double v4 = w[g.b.x];
+    const double v5 = g.b.y >= 0 ? w[g.b.y] : 0.0;
+    const double v6 = g.b.z >= 0 ? w[g.b.z] : 0.0;
+    const double v7 = g.b.w >= 0 ? w[g.b.w] : 0.0;
+    acc += v4;
+    if (g.b.y >= 0) acc += v5;
+    if (g.b.z >= 0) acc += v6;
+    if (g.b.w >= 0) acc += v7;
+  }
+  return acc;
+}
+
+template <bool PF, int GN>
+__global__ void __launch_bounds__(kThreads, 4) cg_update_kernel(int64_t n, const uint8_t* __restrict__ mult,
                                  const double* __restrict__ dinv, double* __restrict__ r,
                                  const double* __restrict__ w, double* partial, PcgState* st,
                                  double* out2, const double* __restrict__ sig_part,
                                  const int* sig_count, const PeerSync ps_in,
                                  double* __restrict__ x, const double* __restrict__ p,
-                                 double* hist, int end_here) {
+                                 double* hist, int end_here, const int32_t* __restrict__ gu) {
   __shared__ double scratch[32];
   __shared__ int flag;
   __shared__ double s_sig;
@@ -436,10 +514,15 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
     const double2* p2 = reinterpret_cast<const double2*>(p);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n2;
          q += (int64_t)gridDim.x * blockDim.x) {
-      const double2 wv = __ldcs(&w2[q]);
+      double2 wv = GN ? w2[q] : __ldcs(&w2[q]);
       const double2 dv = __ldcs(&d2[q]);
       double2 rv = __ldcs(&r2[q]);
       const uchar2 mv = m2[q];
+      if (GN) {
+        const GuRef g0 = gu_ref<GN ? GN : 2>(gu, 2 * q), g1 = gu_ref<GN ? GN : 2>(gu, 2 * q + 1);
+        wv.x = gu_sum(w, g0, wv.x);
+        wv.y = gu_sum(w, g1, wv.y);
+      }
       if (PF) {
         const double2 pv = __ldcs(&p2[q]);
         double2 xv = __ldcs(&x2[q]);
@@ -458,7 +541,9 @@ __global__ void __launch_bounds__(kThreads) cg_update_kernel(int64_t n, const ui
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
       const int64_t l = n - 1;
-      const double rl = fma(-alpha, w[l], r[l]);
+      double wl = w[l];
+      if (GN) wl = gu_sum(w, gu_ref<GN ? GN : 2>(gu, l), wl);
+      const double rl = fma(-alpha, wl, r[l]);
       r[l] = rl;
       if (PF) x[l] = fma(alpha, p[l], x[l]);
       const double c = c_of(mult[l]);
@@ -782,12 +867,27 @@ cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
                              int grid, cudaStream_t s, double* x, const double* p, double* hist,
-                             int end_here) {
+                             int end_here, const int32_t* gu) {
+  if (gu) {   // gather-scatter on read (PF iterations only)
+    if (!x) return cudaErrorInvalidValue;
+#define GUK(NN)                                                                                  \
+  case NN:                                                                                       \
+    return launch_k(dev::cg_update_kernel<true, NN>, dim3(grid), dim3(kThreads), 0, s, P.n_local, \
+                    mult, dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist,    \
+                    end_here, gu);
+    switch (P.n) {
+      GUK(2) GUK(3) GUK(4) GUK(5) GUK(6) GUK(7) GUK(8) GUK(9) GUK(10) GUK(11) GUK(12)
+    }
+#undef GUK
+    return cudaErrorInvalidValue;
+  }
   if (x)
-    return launch_k(dev::cg_update_kernel<true>, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult,
-                    dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist, end_here);
-  return launch_k(dev::cg_update_kernel<false>, dim3(grid), dim3(kThreads), 0, s, P.n_local, mult,
-                  dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist, end_here);
+    return launch_k(dev::cg_update_kernel<true, 0>, dim3(grid), dim3(kThreads), 0, s, P.n_local,
+                    mult, dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist,
+                    end_here, gu);
+  return launch_k(dev::cg_update_kernel<false, 0>, dim3(grid), dim3(kThreads), 0, s, P.n_local,
+                  mult, dinv, r, w, partial, st, out2, sig_part, sig_count, ps, x, p, hist,
+                  end_here, gu);
 }
 
 cudaError_t launch_cg_end_iter(PcgState* st, double* hist, cudaStream_t s) {

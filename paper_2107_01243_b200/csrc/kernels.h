@@ -294,7 +294,8 @@ cudaError_t launch_cg_update(const DevPlan& P, const uint8_t* mult, const double
                              const double* w, double* partial, PcgState* st, double* out2,
                              const double* sig_part, const int* sig_count, const PeerSync& ps,
                              int grid, cudaStream_t s, double* x = nullptr,
-                             const double* p = nullptr, double* hist = nullptr, int end_here = 1);
+                             const double* p = nullptr, double* hist = nullptr, int end_here = 1,
+                             const int32_t* gu = nullptr);
 // PF over NCCL / loopback: end of the iteration after the host-side allreduce
 cudaError_t launch_cg_end_iter(PcgState* st, double* hist, cudaStream_t s);
 bool gs_flat(const DevPlan& P, int mode);   // the gs schedule `mode` resolves to the flat sweep

@@ -124,6 +124,50 @@ bool slot_masked(const HostPlan& p, int64_t e, int i, int j, int k) {
   return false;
 }
 
+// per-element incidence table of the local entities (sem_internal.h kGu*): each
+// incidence's element and sub-entity follow from its base (element block +
+// the fixed coordinates; the spanning ones are 0 in a base)
+void build_gu_table(const HostPlan& p, std::vector<int32_t>* tab) {
+  const int n = p.n, N = p.N;
+  const int64_t n3 = p.n3;
+  tab->assign((size_t)p.nloc * kGuInts, -1);
+  int32_t* T = tab->data();
+  auto split = [&](int32_t b, int64_t* el, int c[3]) {
+    *el = b / n3;
+    const int64_t r = b - *el * n3;
+    c[0] = (int)(r % n);
+    c[1] = (int)((r / n) % n);
+    c[2] = (int)(r / ((int64_t)n * n));
+  };
+  int c[3];
+  int64_t el;
+  for (int64_t f = 0; f < p.nF; f++) {
+    const int a = p.f_axis[f];
+    for (int t = 0; t < 2; t++) {
+      split(p.f_base[2 * f + t], &el, c);
+      int32_t* r = T + el * kGuInts + 2 * (2 * a + (c[a] == N));
+      r[0] = p.f_base[2 * f];
+      r[1] = p.f_base[2 * f + 1];
+    }
+  }
+  for (int64_t e = 0; e < p.nEd; e++) {
+    const int a = p.e_axis[e];
+    const int lo = a == 0 ? 1 : 0, hi = a == 2 ? 1 : 2;
+    for (int t = 0; t < p.e_nin[e]; t++) {
+      split(p.e_base[4 * e + t], &el, c);
+      int32_t* r = T + el * kGuInts + kGuEdge + 4 * (4 * a + (c[lo] == N) + 2 * (c[hi] == N));
+      for (int x = 0; x < 4; x++) r[x] = p.e_base[4 * e + x];
+    }
+  }
+  for (int64_t v = 0; v < p.nV; v++) {
+    for (int t = 0; t < p.v_nin[v]; t++) {
+      split(p.v_base[8 * v + t], &el, c);
+      int32_t* r = T + el * kGuInts + kGuVert + 8 * ((c[0] == N) + 2 * (c[1] == N) + 4 * (c[2] == N));
+      for (int x = 0; x < 8; x++) r[x] = p.v_base[8 * v + x];
+    }
+  }
+}
+
 // local entity id (0..25) <-> kind / sides
 //   faces 0..5: 2a + side_a ; edges 6..17: 6 + 4a + s_f1 + 2 s_f2 (f1<f2 the
 //   fixed axes) ; vertices 18..25: 18 + sx + 2 sy + 4 sz

@@ -20,6 +20,15 @@ void set_error(const std::string& msg);
 // box mesh), so a point's slot in incidence t is base[t] + offset(kind, p).
 enum EntClass { CLS_FACE = 0, CLS_EDGE = 1, CLS_VERT = 2 };
 constexpr int kRefsPerElem = 26;   // 6 faces + 12 edges + 8 vertices
+// Per-element incidence table of the gather-on-read CG update (SEM_OPT_PCG_GSU,
+// kern.cu gu_gather): for each of the element's sub-entities the slot bases of
+// ALL incidences of its local entity, ascending, -1 padded (all -1: not a
+// local entity).  Faces 2a+b (normal axis a, side b) x 2 bases at [0, 12);
+// edges 4a + s_lo + 2 s_hi (direction a, sides of the two other axes in
+// ascending order) x 4 at [12, 60); vertices s_x + 2 s_y + 4 s_z x 8 at
+// [60, 124).  A point's slot in incidence t is base[t] + its offset along the
+// entity (the spanning coordinates), as in the gs kernel.
+constexpr int kGuEdge = 12, kGuVert = 60, kGuInts = 124;
 
 struct HostPlan {
   sem_mesh m{};
@@ -61,6 +70,8 @@ struct HostPlan {
 sem_plan* plan_wrap(const HostPlan& p);
 
 int build_plan(const sem_mesh* m, int N, HostPlan* p);   // returns SEM_* status
+// the kGuInts-per-element incidence table of the local entities
+void build_gu_table(const HostPlan& p, std::vector<int32_t>* tab);
 // device G layout (see dev_common.cuh g_index): G[e][k][f][i + n j]
 inline int64_t g_index_host(int64_t el, int f, int p, int n) {
   const int n2 = n * n, k = p / n2, ij = p - k * n2;

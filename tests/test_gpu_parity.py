@@ -594,3 +594,35 @@ def test_pcg_fused_p_update(spec, N):
             assert np.abs(host(xh) - refh["x"]).max() <= 1e-10
             xs.append((host(xh), rh["iters"]))
         assert abs(xs[0][1] - xs[1][1]) <= 1 and np.abs(xs[0][0] - xs[1][0]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("spec,N", PF_CASES, ids=[f"{s.ex}x{s.ey}x{s.ez}-N{N}" for s, N in PF_CASES])
+def test_pcg_gather_on_read_identical(spec, N):
+    """SEM_OPT_PCG_GSU: the r update sums the unassembled w over each shared
+    point's incidences (ascending slots) instead of a separate gs kernel -- the
+    same sums in the same order, so the PCG iterates (x, iteration count, final
+    residual) are bitwise those of the gs-kernel iteration, for Poisson and
+    Helmholtz, with and without graph replay."""
+    o = O.Oracle(spec, N)
+    fun = f_tgv if all(spec.periodic) else f_sin
+    f = fun(o.get("X"), o.get("Y"), o.get("Z"))
+    b = o.rhs(f)
+    with sem().sem_setup(spec, N) as c:
+        bh = c.zeros()
+        c.rhs_mass(dev(f), bh)
+        for graph in (True, False):
+            c.set_pcg_graph(graph)
+            out = {}
+            for gsu in (True, False):
+                c.set_pcg_gsu(gsu)
+                x = c.zeros()
+                r = c.pcg_solve(dev(b), x, 1e-10, 3000)
+                xh = c.zeros()
+                rh = c.helm_pcg_solve(0.5, 3.0, bh, xh, 1e-10, 2000)
+                out[gsu] = (host(x), r, host(xh), rh)
+            (x1, r1, xh1, rh1), (x0, r0, xh0, rh0) = out[True], out[False]
+            assert r1["status"] == 0 and r1["iters"] == r0["iters"], (graph, r1, r0)
+            assert r1["res_final"] == r0["res_final"] and np.array_equal(x1, x0), graph
+            assert rh1["iters"] == rh0["iters"] and np.array_equal(xh1, xh0), graph
+        c.set_pcg_graph(True)
+        c.set_pcg_gsu(-1)

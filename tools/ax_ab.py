@@ -40,6 +40,9 @@ def main():
             N = int(cfg[1:])
             ea = max(2, int(round(256 / (N + 1))))
             spec = tgv_box(ea, ea, ea)
+        elif cfg.startswith("B"):    # B<ex>x<ey>x<ez>: periodic box at N = 7
+            N = 7
+            spec = tgv_box(*[int(v) for v in cfg[1:].split("x")])
         else:
             spec, N = CONFIGS[cfg]
         with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
@@ -58,6 +61,8 @@ def main():
                 c.set_pcg_graph(False)
             if os.environ.get("PCG_FUSE") == "0":
                 c.set_pcg_fuse(False)
+            if os.environ.get("PCG_GSU") == "0":
+                c.set_pcg_gsu(False)
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
