@@ -77,19 +77,26 @@ def last_json(path):
         return None
 
 
-def kernels_per_point(N):
-    """W (flops) and Q (bytes) per local point of one PCG iteration as built."""
+def kernels_per_point(N, built="r02"):
+    """W (flops) and Q (bytes) per local point of one PCG iteration as built.
+
+    r02 (DESIGN.md 5.1/5.3): the operator kernel also forms p = dinv r + beta p_old
+    from TMA-staged p_old, r, dinv and the per-CTA p.w partials (88 B/pt); the
+    r update also does x += alpha p (57 B/pt: w, dinv, r, p, x, mult read; r, x
+    written).  r01: separate p kernel, x updated in it."""
     n = N + 1
     fb = 1.0 - ((N - 1) / (N + 1)) ** 3
+    if built == "r01":
+        return {"Ax": (12 * n + 15, 64.0), "gs": (fb, 20.0 * fb),
+                "cg_update": (8.0, 33.0), "cg_p": (5.0, 48.0)}
     return {
-        "Ax": (12 * n + 15, 64.0),
+        "Ax+p": (12 * n + 15 + 5, 88.0),
         "gs": (fb, 20.0 * fb),
-        "cg_update": (8.0, 33.0),
-        "cg_p": (5.0, 48.0),
+        "cg_update+x": (10.0, 57.0),
     }
 
 
-def model(probe_path, mdir, out_path=None):
+def model(probe_path, mdir, out_path=None, built="r02"):
     import random
     pr = json.loads([l for l in open(probe_path) if l.startswith("{")][-1])
     single = [json.loads(l) for l in open(os.path.join(mdir, "measure_single.jsonl")) if l.startswith("{")]
@@ -124,7 +131,7 @@ def model(probe_path, mdir, out_path=None):
 
     def predict(n_per_gpu, N, P, n_s, paper_levels):
         ta = 0.0
-        for W, Q in kernels_per_point(N).values():
+        for W, Q in kernels_per_point(N, built).values():
             ta += max(W * n_per_gpu / PI_FP64, Q * n_per_gpu / triad)
         tc = 2 * allreduce(P, paper_levels) + gs(P, n_s)
         return ta, tc
@@ -138,7 +145,7 @@ def model(probe_path, mdir, out_path=None):
       "; ".join(f"peer {q}: mean {v['mean_us']:.2f} us, p50 {v['p50_us']:.2f}, p99 {v['p99_us']:.2f}, max {v['max_us']:.2f}"
                 for q, v in pr["pingpong"].items()) + "\n")
     w("Per-point costs of one PCG iteration as built (W flops, Q bytes): " +
-      ", ".join(f"{k} ({W:.0f}, {Q:.1f})" for k, (W, Q) in kernels_per_point(7).items()) + " at N=7.\n")
+      ", ".join(f"{k} ({W:.0f}, {Q:.1f})" for k, (W, Q) in kernels_per_point(7, built).items()) + f" at N=7 (iteration as built in {built}).\n")
 
     # weak scaling: C2 per GPU (bench.py)
     N = 7
@@ -198,4 +205,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "probe":
         probe()
     else:
-        model(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
+        model(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None,
+              os.environ.get("SEM_MODEL_BUILT", "r02"))
