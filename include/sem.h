@@ -316,6 +316,12 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    vector exceeds 128 MiB (the L2 size: below it the separate gs kernel on an
    L2-resident w is faster).  Identical results. */
 #define SEM_OPT_PCG_GSU 16
+/* Schwarz coarse solve when the coarse level is single-rank (one rank, or
+   the replicated level): -1 (default) / 1 = CG on the ASSEMBLED N = 1 operator
+   over the unique unmasked vertices (ELL, built once at Schwarz setup from the
+   element matrices), 0 = CG on the element operator + gather-scatter over the
+   E-vector slots.  Same iterates in exact arithmetic (reading Q35). */
+#define SEM_OPT_COARSE_ASM 17
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

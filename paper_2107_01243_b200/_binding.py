@@ -292,6 +292,11 @@ class Context:
         """Schwarz coarse level at nranks > 1: -1 auto, 0 distributed, 1 replicated. Collective."""
         _check(load().sem_set_option(self._h, 11, int(mode)))
 
+    def set_coarse_asm(self, mode):
+        """Single-rank Schwarz coarse level: CG on the assembled N = 1 operator
+        (True / -1 auto, the default) or on the element operator + gs (False)."""
+        _check(load().sem_set_option(self._h, 17, -1 if mode == -1 else (1 if mode else 0)))
+
     def set_coarse_iters(self, k: int):
         """Maximum CG iterations of the Schwarz coarse solve (default 10)."""
         _check(load().sem_set_option(self._h, 7, int(k)))

@@ -14,7 +14,7 @@ SO = os.path.join(HERE, "libsem.so")
 ROOT = os.path.dirname(HERE)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SRCS = ["ax.cu", "kern.cu", "p2p.cu", "krylov.cu", "schwarz.cu", "loopback.cu", "api.cu"]
+CUDA_SRCS = ["ax.cu", "kern.cu", "p2p.cu", "krylov.cu", "schwarz.cu", "coarse.cu", "loopback.cu", "api.cu"]
 CXX_SRCS = ["plan.cpp"]
 
 

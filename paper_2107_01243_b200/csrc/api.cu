@@ -125,6 +125,15 @@ struct sem_ctx {
   bool coarse_graph = true;
   int coarse_replicate = -1;   // SEM_OPT_COARSE_REPLICATE: -1 auto, 0 distributed, 1 replicated
   bool c0_repl = false;        // the coarse context in use is the replicated one
+  // SEM_OPT_COARSE_ASM: the one-rank coarse level as an assembled operator on
+  // its unique vertices (coarse.cu); -1 auto = on whenever the coarse level is single-rank
+  int coarse_asm = -1;
+  bool casm_ok = false;
+  sem::CoarseAsm casm;
+  int casm_grid = 1;
+  int32_t *d_ccol = nullptr, *d_cu2sp = nullptr, *d_cu2s = nullptr, *d_cuidx = nullptr;
+  double *d_cval = nullptr, *d_cvec = nullptr, *d_cpart = nullptr;
+  sem::CoarseCg* d_ccg = nullptr;
   bool ax_pdl = true;      // SEM_OPT_AX_PDL (C2: 123.0 -> 121.6 us per PCG iteration)
   bool ax_pdl_now = false; // set around the PCG iteration's Ax launch
   // SEM_OPT_PCG_FUSE: one-rank Jacobi-PCG with the p update fused into the Ax
@@ -504,6 +513,17 @@ int ensure_hist(sem_ctx* c, int maxit) {
   return dalloc(&c->d_hist, (size_t)c->hist_cap);
 }
 
+void casm_free(sem_ctx* c) {
+  void* ptrs[] = {c->d_ccol, c->d_cu2sp, c->d_cu2s, c->d_cuidx, c->d_cval, c->d_cvec, c->d_cpart,
+                  c->d_ccg};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  c->d_ccol = c->d_cu2sp = c->d_cu2s = c->d_cuidx = nullptr;
+  c->d_cval = c->d_cvec = c->d_cpart = nullptr;
+  c->d_ccg = nullptr;
+  c->casm_ok = false;
+}
+
 void free_ctx(sem_ctx* c) {
   if (!c) return;
   void* ptrs[] = {c->d_xi, c->d_w, c->d_D, c->d_G, c->d_B, c->d_dinv, c->d_mult, c->d_bmask,
@@ -521,6 +541,7 @@ void free_ctx(sem_ctx* c) {
   if (c->d_gs) cudaFree(c->d_gs);
   if (c->d_ktick) cudaFree(c->d_ktick);
   if (c->d_gu) cudaFree(c->d_gu);
+  casm_free(c);
   if (c->c0) free_ctx(c->c0);
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
@@ -1176,6 +1197,8 @@ static bool coarse_replicated(const sem_ctx* c) {
   return h.E * 8 <= kReplicateSlots;
 }
 
+static int coarse_assemble(sem_ctx* c);
+
 static int schwarz_setup(sem_ctx* c) {
   if (c->c0) return SEM_OK;
   const sem::HostPlan& h = c->hp;
@@ -1215,6 +1238,146 @@ static int schwarz_setup(sem_ctx* c) {
   CUDA_TRY(sem::launch_invert_mask(c0->dp, c->d_dinv0, s));
   c->launches++;
   CUDA_TRY(cudaStreamSynchronize(s));
+  return coarse_assemble(c);
+}
+
+// The single-rank coarse level as an assembled operator (coarse.cu, reading
+// Q35): the element matrices A_e of the N = 1 operator, column by column
+// (A_e e_a through the element kernel, no gs, no mask), summed on the host in
+// ascending element order into A0 on the unmasked unique vertices (ascending
+// global lattice number); ELL on the device with each row's entries in
+// ascending column order.  Plus the slot <-> unique maps for the restriction
+// (ascending-slot sums) and the prolongation.
+static int coarse_assemble(sem_ctx* c) {
+  sem_ctx* c0 = c->c0;
+  if (!c0 || c->casm_ok || c0->hp.nranks != 1 || c->coarse_asm == 0) return SEM_OK;
+  const sem::HostPlan& h0 = c0->hp;
+  const int64_t n0 = h0.n_local, E = h0.nloc;
+  cudaStream_t s = c0->stream;
+  double *du = nullptr, *dw = nullptr;
+  SEM_TRY(dalloc(&du, (size_t)n0));
+  int st = dalloc(&dw, (size_t)n0);
+  std::vector<double> u((size_t)n0), Ae((size_t)8 * n0);
+  for (int a = 0; a < 8 && st == SEM_OK; a++) {
+    for (int64_t q = 0; q < n0; q++) u[q] = (q % 8 == a) ? 1.0 : 0.0;
+    if (cudaMemcpyAsync(du, u.data(), n0 * sizeof(double), cudaMemcpyHostToDevice, s) != cudaSuccess)
+      st = SEM_ECUDA;
+    if (st == SEM_OK) st = sem_ax(c0, du, dw);
+    if (st == SEM_OK &&
+        (cudaMemcpyAsync(Ae.data() + (size_t)a * n0, dw, n0 * sizeof(double), cudaMemcpyDeviceToHost,
+                         s) != cudaSuccess ||
+         cudaStreamSynchronize(s) != cudaSuccess))
+      st = SEM_ECUDA;
+  }
+  cudaFree(du);
+  cudaFree(dw);
+  if (st != SEM_OK) {
+    cudaGetLastError();
+    sem::set_error("coarse_assemble: element matrices");
+    return st;
+  }
+  // unique numbering of the unmasked vertices, ascending global number
+  std::vector<int64_t> gid((size_t)n0);
+  std::vector<int32_t> cidx((size_t)h0.nglob, -1), uidx((size_t)n0, -1);
+  for (int64_t el = 0; el < E; el++)
+    for (int a = 0; a < 8; a++) {
+      const int i = a & 1, j = (a >> 1) & 1, k = a >> 2;
+      const int64_t sl = el * 8 + a;
+      gid[sl] = sem::lattice_gid(h0, h0.e_lo + el, i, j, k);
+      if (sem::slot_masked(h0, h0.e_lo + el, i, j, k)) gid[sl] = -1;
+      else cidx[gid[sl]] = -2;
+    }
+  int nu = 0;
+  for (int64_t g = 0; g < h0.nglob; g++)
+    if (cidx[g] == -2) cidx[g] = nu++;
+  std::vector<int32_t> u2sp((size_t)nu + 1, 0), u2s;
+  for (int64_t sl = 0; sl < n0; sl++)
+    if (gid[sl] >= 0) {
+      uidx[sl] = cidx[gid[sl]];
+      u2sp[uidx[sl] + 1]++;
+    }
+  for (int g = 0; g < nu; g++) u2sp[g + 1] += u2sp[g];
+  u2s.assign((size_t)u2sp[nu], 0);
+  {
+    std::vector<int32_t> fill(u2sp.begin(), u2sp.end() - 1);
+    for (int64_t sl = 0; sl < n0; sl++)   // ascending slots per unique vertex
+      if (uidx[sl] >= 0) u2s[fill[uidx[sl]]++] = (int32_t)sl;
+  }
+  // A0 rows: <= 27 distinct columns on the vertex lattice
+  constexpr int kW = 27;
+  std::vector<int32_t> rc((size_t)nu * kW, -1);
+  std::vector<double> rv((size_t)nu * kW, 0.0);
+  std::vector<uint8_t> rn((size_t)nu, 0);
+  for (int64_t el = 0; el < E; el++)
+    for (int b = 0; b < 8; b++) {
+      const int row = uidx[el * 8 + b];
+      if (row < 0) continue;
+      int32_t* cr = &rc[(size_t)row * kW];
+      double* vr = &rv[(size_t)row * kW];
+      for (int a = 0; a < 8; a++) {
+        const int col = uidx[el * 8 + a];
+        if (col < 0) continue;
+        const double v = Ae[(size_t)a * n0 + el * 8 + b];
+        int q = 0;
+        while (q < rn[row] && cr[q] != col) q++;
+        if (q == rn[row]) {
+          if (q == kW) {
+            sem::set_error("coarse_assemble: more than 27 columns in a row");
+            return SEM_EINVAL;
+          }
+          cr[q] = col;
+          vr[q] = v;
+          rn[row]++;
+        } else {
+          vr[q] += v;
+        }
+      }
+    }
+  int K = 1;
+  for (int g = 0; g < nu; g++) K = std::max<int>(K, rn[g]);
+  std::vector<int32_t> ecol((size_t)K * nu);
+  std::vector<double> eval((size_t)K * nu);
+  for (int g = 0; g < nu; g++) {
+    int ord[kW];
+    const int m = rn[g];
+    for (int q = 0; q < m; q++) ord[q] = q;
+    const int32_t* cr = &rc[(size_t)g * kW];
+    std::sort(ord, ord + m, [&](int x, int y) { return cr[x] < cr[y]; });
+    for (int q = 0; q < K; q++) {
+      ecol[(size_t)q * nu + g] = q < m ? cr[ord[q]] : g;
+      eval[(size_t)q * nu + g] = q < m ? rv[(size_t)g * kW + ord[q]] : 0.0;
+    }
+  }
+  cudaStream_t sc = c->stream;
+  c->casm_grid = sem::coarse_asm_grid(nu, c->num_sms);
+  SEM_TRY(upload(&c->d_ccol, ecol, sc));
+  SEM_TRY(upload(&c->d_cval, eval, sc));
+  SEM_TRY(upload(&c->d_cu2sp, u2sp, sc));
+  SEM_TRY(upload(&c->d_cu2s, u2s, sc));
+  SEM_TRY(upload(&c->d_cuidx, uidx, sc));
+  SEM_TRY(dalloc(&c->d_cvec, (size_t)5 * std::max(nu, 1)));
+  SEM_TRY(dalloc(&c->d_cpart, (size_t)c->casm_grid));
+  SEM_TRY(dalloc(&c->d_ccg, 1));
+  CUDA_TRY(cudaMemsetAsync(c->d_ccg, 0, sizeof(sem::CoarseCg), sc));
+  CUDA_TRY(cudaStreamSynchronize(sc));
+  sem::CoarseAsm& A = c->casm;
+  A.nu = nu;
+  A.K = K;
+  A.n0 = n0;
+  A.periodic = h0.fully_periodic ? 1 : 0;
+  A.col = c->d_ccol;
+  A.val = c->d_cval;
+  A.u2s_ptr = c->d_cu2sp;
+  A.u2s = c->d_cu2s;
+  A.uidx = c->d_cuidx;
+  A.b = c->d_cvec;
+  A.x = A.b + nu;
+  A.r = A.x + nu;
+  A.p = A.r + nu;
+  A.q = A.p + nu;
+  A.partial = c->d_cpart;
+  A.st = c->d_ccg;
+  c->casm_ok = true;
   return SEM_OK;
 }
 
@@ -1228,6 +1391,7 @@ static void schwarz_drop_coarse(sem_ctx* c) {
   for (double* p : bufs)
     if (p) cudaFree(p);
   c->d_b0 = c->d_x0 = c->d_dinv0 = nullptr;
+  casm_free(c);
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   c->g0exec = nullptr;
   c->g0_iters = -1;
@@ -1247,6 +1411,11 @@ static int coarse_state(sem_ctx* c) {
 static int coarse_body(sem_ctx* c, const int* gate) {
   sem_ctx* c0 = c->c0;
   cudaStream_t s = c0->stream;
+  if (c->casm_ok && c->coarse_asm != 0) {   // assembled operator on the unique vertices
+    CUDA_TRY(sem::launch_coarse_asm_solve(c->casm, c->d_b0, c->d_x0, gate, c->coarse_iters, 1e-12,
+                                          c->casm_grid, s, &c0->launches));
+    return SEM_OK;
+  }
   SEM_TRY(gs_op(c0, c->d_b0, 1));
   if (c0->hp.fully_periodic) {   // b0 in range(A0): remove the unique-DOF mean
     CUDA_TRY(sem::launch_sum_c(c0->dp, c0->d_mult, c->d_b0, c0->d_partial, &c0->d_tickets[0],
@@ -2039,6 +2208,19 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
       schwarz_drop_coarse(c);
       SEM_TRY(schwarz_setup(c));
     }
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_COARSE_ASM) {
+    if (value < -1 || value > 1) {
+      sem::set_error("sem_set_option: SEM_OPT_COARSE_ASM must be -1, 0 or 1");
+      return SEM_EINVAL;
+    }
+    cudaStreamSynchronize(c->stream);
+    c->coarse_asm = value;
+    if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
+    c->g0exec = nullptr;
+    c->g0_iters = -1;
+    SEM_TRY(coarse_assemble(c));
     return SEM_OK;
   }
   if (option == SEM_OPT_COARSE_GRAPH) {

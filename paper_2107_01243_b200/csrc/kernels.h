@@ -226,6 +226,32 @@ cudaError_t launch_gate_state(PcgState* st, const int* gate, cudaStream_t s);
 cudaError_t launch_rel_tol(PcgState* st, double rtol, cudaStream_t s);
 cudaError_t launch_copy_gate(int* dst, const int* gate, cudaStream_t s);
 
+// assembled coarse operator (coarse.cu): CG state and operands on the nu unique
+// unmasked N = 1 vertices
+struct CoarseCg {
+  double gamma, sigma, alpha, beta, tol, mean, red;
+  int it, done, maxit;     // done: 0 running, 1 converged, 2 breakdown, 3 NaN, 4 maxit, 5 gated
+  unsigned ticket[4];
+};
+struct CoarseAsm {
+  int nu = 0, K = 0;       // unknowns, ELL width
+  int64_t n0 = 0;          // coarse E-vector slots
+  int periodic = 0;        // fully periodic: remove the mean of the right-hand side
+  const int32_t* col = nullptr;      // [K][nu] ELL, ascending per row, padded (row, 0.0)
+  const double* val = nullptr;
+  const int32_t* u2s_ptr = nullptr;  // [nu + 1] unique -> slots (ascending)
+  const int32_t* u2s = nullptr;
+  const int32_t* uidx = nullptr;     // [n0] slot -> unique, -1 masked
+  double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;   // [nu]
+  double* partial = nullptr;         // [grid]
+  CoarseCg* st = nullptr;
+};
+int coarse_asm_grid(int nu, int num_sms);
+// x0 = A0^-1 b0 by <= maxit CG steps on the assembled operator (b0, x0: E-vectors)
+cudaError_t launch_coarse_asm_solve(const CoarseAsm& A, const double* b0, double* x0,
+                                    const int* gate, int maxit, double rtol, int grid,
+                                    cudaStream_t s, int64_t* launches);
+
 // interconnect probes for the performance model: one-thread ping-pong
 // with `peer` (round-trip ns per sample), and one-sided peer writes (bandwidth)
 cudaError_t launch_p2p_pingpong(const P2P& c, int peer, int iters, uint64_t e0, long long* out,

@@ -141,13 +141,16 @@ def schwarz(cfgs=("C3", "C4")):
         n1 = N + 1
         with sem.sem_setup(spec, N, stream=st.cuda_stream) as c:
             n = c.n_local
+            if os.environ.get("COARSE_ASM") == "0":   # A/B: element-operator coarse CG
+                c.set_coarse_asm(False)
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
             del X, Y, Z
             z = c.zeros()
             c.schwarz_apply(b, z, 3)
-            res = {"what": f"{cfg}_schwarz", "n_local": n}
+            res = {"what": f"{cfg}_schwarz", "n_local": n,
+                   "coarse": "element" if os.environ.get("COARSE_ASM") == "0" else "assembled"}
             for which, name in ((1, "local"), (2, "coarse"), (3, "both")):
                 ms = timed(lambda: c.schwarz_apply(b, z, which), st, 20)   # graph on
                 c.timing(True)
