@@ -21,11 +21,19 @@ __device__ __forceinline__ double ld_volatile(const double* p) {
   return v;
 }
 
+// has any wait of this rank already timed out?  (checked only on the slow path:
+// after one timeout every later wait gives up at once, so a rank whose peer
+// never arrives fails in ~4 s instead of ~4 s per wait)
+__device__ __forceinline__ bool p2p_failed(const int* err) {
+  return *reinterpret_cast<const volatile int*>(err) != 0;
+}
+
 // spin until *flag >= epoch (bounded); returns false on timeout
 __device__ __forceinline__ bool wait_flag(const uint64_t* flag, uint64_t epoch, int* err) {
   if (ld_acquire_sys(flag) >= epoch) return true;
   const long long t0 = clock64();
   while (ld_acquire_sys(flag) < epoch) {
+    if (p2p_failed(err)) return false;
     if (clock64() - t0 > (1ll << 33)) {   // ~4 s at 2 GHz
       atomicExch(err, 1);
       return false;
@@ -68,6 +76,7 @@ __device__ __forceinline__ double ll_load(const uint4* p, uint32_t flag, int* er
     asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(h0), "=l"(h1) : "l"(p) : "memory");
     if ((uint32_t)(h0 >> 32) == flag && (uint32_t)(h1 >> 32) == flag) break;
     if (t0 < 0) t0 = clock64();
+    else if (p2p_failed(err)) return 0.0;
     else if (clock64() - t0 > (1ll << 33)) {
       atomicExch(err, 1);
       return 0.0;

@@ -8,6 +8,7 @@ E-vectors and compares them with the oracle run with the same number of ranks
 """
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -18,6 +19,33 @@ import torch.distributed as dist  # noqa: E402
 
 import paper_2107_01243_b200 as sem  # noqa: E402
 from mgpu_common import CASES, OracleRefs, case_field, check, rank_run, rank_slice  # noqa: E402
+
+
+def failure_path(rank, P, comm):
+    """A rank that enters a peer-memory collective alone gets SEM_ENCCL after
+    the bounded wait (~4 s; every later wait of that rank gives up at once),
+    instead of hanging the GPU.  The other ranks keep their contexts (and
+    mailboxes) alive until it returns."""
+    spec, N, _ = CASES[1]
+    fails = []
+    with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm) as c:
+        c.set_p2p(True)
+        if rank == 0:
+            b = torch.rand(c.n_local, dtype=torch.float64, device="cuda")
+            x = c.zeros()
+            t0 = time.time()
+            try:
+                c.pcg_solve(b, x, 1e-10, 100)
+                fails.append("failure path: a lone rank's PCG returned without error")
+            except sem.SemError as e:
+                if e.status != sem.SEM_ENCCL:
+                    fails.append(f"failure path: status {e.status}, expected SEM_ENCCL")
+            dt = time.time() - t0
+            print(f"failure path: lone rank 0 PCG returned after {dt:.1f} s", flush=True)
+            if dt > 30:
+                fails.append(f"failure path took {dt:.1f} s")
+        dist.barrier()
+    return fails
 
 
 def main():
@@ -47,6 +75,7 @@ def main():
                     fails += f
                     print(f"{tag}: {'FAIL' if f else 'ok'} pcg iters {out['r']['iters']} "
                           f"(oracle {ref.pcg['iters']})", flush=True)
+    fails += failure_path(rank, P, comm)
     sem.nccl_comm_destroy(comm)
     dist.barrier()
     dist.destroy_process_group()
