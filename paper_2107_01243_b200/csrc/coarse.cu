@@ -46,6 +46,9 @@ __global__ void __launch_bounds__(kCT) casm_gather_kernel(const CoarseAsm A, con
   double s = 0.0;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < A.nu; g += gridDim.x * blockDim.x) {
     const int q0 = A.u2s_ptr[g], q1 = A.u2s_ptr[g + 1];
+    SEM_CHK(q1 > q0 && q1 - q0 <= 8);
+    for (int q = q0; q < q1; q++)
+      SEM_CHK(A.u2s[q] >= 0 && A.u2s[q] < A.n0 && (q == q0 || A.u2s[q] > A.u2s[q - 1]));
     double v = b0[A.u2s[q0]];
     for (int q = q0 + 1; q < q1; q++) v += b0[A.u2s[q]];
     A.b[g] = v;
@@ -87,6 +90,7 @@ __global__ void __launch_bounds__(kCT) casm_spmv_kernel(const CoarseAsm A) {
     double acc = 0.0;
     for (int k = 0; k < A.K; k++) {
       const int64_t e = (int64_t)k * A.nu + g;
+      SEM_CHK(A.col[e] >= 0 && A.col[e] < A.nu);
       acc = fma(A.val[e], A.p[A.col[e]], acc);
     }
     A.q[g] = acc;
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(kCT) casm_scatter_kernel(const CoarseAsm A, do
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < A.n0;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int g = A.uidx[s];
+    SEM_CHK(g >= -1 && g < A.nu);
     x0[s] = g >= 0 ? A.x[g] : 0.0;
   }
 }

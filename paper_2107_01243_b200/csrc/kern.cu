@@ -437,6 +437,8 @@ __device__ __forceinline__ double gu_sum(const double* __restrict__ w, const GuR
                                          double own) {
   if (g.a.x < 0) return own;
   const int off = g.off;
+  SEM_CHK(g.a.y > g.a.x && (g.a.z < 0 || g.a.z > g.a.y) && (g.a.w < 0 || g.a.w > g.a.z) &&
+          (g.b.x < 0 || g.b.x > g.a.w));
   double acc = w[g.a.x + off];
   {
     const double v1 = w[g.a.y + off];
