@@ -313,8 +313,9 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    shared point's incidences on read (ascending slots, the gs kernel's sum)
    through a per-element incidence table (496 B per element, built on the
    first solve); 0 = separate gs kernel; -1 (default) = auto, 1 when the
-   vector exceeds 128 MiB (the L2 size: below it the separate gs kernel on an
-   L2-resident w is faster).  Identical results. */
+   vector exceeds 64 MiB (below, the separate gs kernel on an L2-resident w is
+   faster) and one z-layer of elements holds at most 8 MiB of it (beyond, the
+   +z face partners fall out of the L2 before reuse).  Identical results. */
 #define SEM_OPT_PCG_GSU 16
 /* Schwarz coarse solve when the coarse level is single-rank (one rank, or
    the replicated level): -1 (default) / 1 = CG on the ASSEMBLED N = 1 operator

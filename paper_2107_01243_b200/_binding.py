@@ -273,7 +273,7 @@ class Context:
     def set_pcg_gsu(self, mode):
         """One rank, fused PCG: gather-scatter performed on read by the r update
         instead of a separate gs kernel: True, False or -1 (default: auto, on
-        when a vector exceeds 128 MiB)."""
+        when a vector exceeds 64 MiB and a z-layer of elements holds <= 8 MiB of it)."""
         _check(load().sem_set_option(self._h, 16, -1 if mode == -1 else (1 if mode else 0)))
 
     def set_ax_pdl(self, on: bool):

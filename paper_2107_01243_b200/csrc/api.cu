@@ -872,12 +872,16 @@ struct PcgCtl {
   double* rg_out = nullptr;
 };
 
-// SEM_OPT_PCG_GSU auto: gather on read once w (8 B per slot) exceeds the 126 MB
-// L2.  Below, the gs kernel runs on an L2-resident w and the separate pass is
-// cheaper (C2, 34 MB: 115 vs 123 us per iteration); above, the fused update
-// saves the gs kernel's DRAM round trip (C3, 134 MB: 451 -> 440 us; 1.2e8
-// points at N = 5 / 9: 2-3 %), profiles/r02_experiments/gsu_ab.jsonl
-constexpr int64_t kGsuAutoBytes = 64ll << 20;
+// SEM_OPT_PCG_GSU auto: gather on read when w (8 B per slot) exceeds 64 MiB --
+// below, the gs kernel runs on an L2-resident w and the separate pass is
+// cheaper (C2, 34 MB: 115 vs 123 us per iteration) -- and one z-layer of
+// elements holds at most 8 MiB of w: the update streams ~7x the w bytes
+// (57 B per slot) between an element and its +z neighbour, whose face
+// partners must still be in the L2 then.  N = 7 measurements
+// (profiles/r02_experiments/gsu_ab*.jsonl): 32^3 (4 MiB layers) 451 -> 441 us,
+// 40^3 (6.5 MiB) -5.7 %, 48^3 (9.4 MiB) -0.7 %, 64x64x32 and C4 (16.8 MiB)
+// +9 / +13 %.
+constexpr int64_t kGsuAutoBytes = 64ll << 20, kGsuLayerBytes = 8ll << 20;
 
 // x = 0, r = b, p = dinv b, (rho, gamma), start state; the host wrote tol/maxit
 static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, double* x,
@@ -887,7 +891,9 @@ static int pcg_enqueue_init(sem_ctx* c, const double* dinv, const double* b, dou
   k->dist = c->hp.nranks > 1;
   k->pf = c->pcg_fuse;
   k->gu = k->pf && c->hp.nranks == 1 &&
-          (c->pcg_gsu > 0 || (c->pcg_gsu < 0 && c->hp.n_local * 8 > kGsuAutoBytes));
+          (c->pcg_gsu > 0 ||
+           (c->pcg_gsu < 0 && c->hp.n_local * 8 > kGsuAutoBytes &&
+            (int64_t)c->hp.m.ex * c->hp.m.ey * c->hp.n3 * 8 <= kGsuLayerBytes));
   if (k->gu && !c->d_gu) {   // the incidence table, once per context
     std::vector<int32_t> tab;
     sem::build_gu_table(c->hp, &tab);

@@ -63,6 +63,8 @@ def main():
                 c.set_pcg_fuse(False)
             if os.environ.get("PCG_GSU") == "0":
                 c.set_pcg_gsu(False)
+            if os.environ.get("PCG_GSU_FORCE") in ("0", "1"):
+                c.set_pcg_gsu(os.environ["PCG_GSU_FORCE"] == "1")
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
