@@ -1259,6 +1259,9 @@ static int coarse_assemble(sem_ctx* c) {
   if (!c0 || c->casm_ok || c0->hp.nranks != 1 || c->coarse_asm == 0) return SEM_OK;
   const sem::HostPlan& h0 = c0->hp;
   const int64_t n0 = h0.n_local, E = h0.nloc;
+  // the host assembly holds the 8 columns of every element matrix (64 B per
+  // coarse slot): beyond 2^26 slots the coarse level stays in E-vector form
+  if (n0 > (int64_t(1) << 26)) return SEM_OK;
   cudaStream_t s = c0->stream;
   double *du = nullptr, *dw = nullptr;
   SEM_TRY(dalloc(&du, (size_t)n0));
