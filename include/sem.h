@@ -321,7 +321,8 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    the replicated level): -1 (default) / 1 = CG on the ASSEMBLED N = 1 operator
    over the unique unmasked vertices (ELL, built once at Schwarz setup from the
    element matrices), 0 = CG on the element operator + gather-scatter over the
-   E-vector slots.  Same iterates in exact arithmetic (reading Q35). */
+   E-vector slots (also beyond 2^26 coarse slots).  Same iterates in exact
+   arithmetic (reading Q35). */
 #define SEM_OPT_COARSE_ASM 17
 int sem_set_option(sem_ctx* c, int option, int value);
 
