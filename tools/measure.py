@@ -2,6 +2,7 @@
 
   python tools/measure.py single            # one GPU: triad, C3, C4, N-sweep
   torchrun --nproc-per-node P tools/measure.py strong   # C3/C4 strong scaling
+  torchrun --nproc-per-node P tools/measure.py c5_strong|c5_weak [N,...]   # C5 at ~1e9 DOF
 
 Each result is one JSON line on stdout (rank 0).  All timings are CUDA events
 on the context stream after warm-up, max over ranks for P > 1.  Denominators:
@@ -357,6 +358,60 @@ def strong():
     dist.destroy_process_group()
 
 
+def c5_scale(Ns, kind):
+    """BASELINE configs[4] scaling at ~1e9 DOF (torchrun, one rank per GPU):
+    strong = the ~1e9-point C5 mesh of order N over P GPUs; weak = ~1e9 points per
+    GPU (the C5 mesh stacked P times along z).  Per N: operator (Ax + gs with the
+    exchange) and a 20-iteration Jacobi-PCG (b = A u, tol 0), max over ranks."""
+    import torch.distributed as dist
+    from sem_inputs import c5_mesh, weak_scaled
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = [sem.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = sem.nccl_comm_init(uid[0], rank, P)
+    st = torch.cuda.current_stream()
+
+    def mx(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for N in Ns:
+        spec = c5_mesh(N) if kind == "strong" else weak_scaled(c5_mesh(N), P)
+        t0 = time.perf_counter()
+        with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm, stream=st.cuda_stream) as c:
+            setup_s = mx(time.perf_counter() - t0)
+            n_tot = spec.E * (N + 1) ** 3
+            u = torch.empty(c.n_local, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+            b = c.zeros()
+            ms = mx(timed(lambda: c.apply(u, b), st, 5, sync=dist.barrier))
+            del u
+            x = c.zeros()
+            c.pcg_solve(b, x, 0.0, 3)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            r = c.pcg_solve(b, x, 0.0, 20)
+            e1.record(st)
+            torch.cuda.synchronize()
+            pms = mx(e0.elapsed_time(e1))
+            if rank == 0:
+                out({"what": f"c5_{kind}", "P": P, "N": N, "mesh": [spec.ex, spec.ey, spec.ez],
+                     "n_p_total": n_tot, "setup_s": round(setup_s, 1),
+                     "ax_gs_ms": round(ms, 3), "ax_gs_gdofs": round(n_tot / (ms * 1e-3) / 1e9, 2),
+                     "pcg_iters": r["iters"], "pcg_ms": round(pms, 2),
+                     "pcg_gdofs": round(n_tot * r["iters"] / (pms * 1e-3) / 1e9, 2)})
+            del b, x
+        torch.cuda.empty_cache()
+        dist.barrier()
+    sem.nccl_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
 def schwarz_strong(cfgs=("C3", "C4")):
     """NEXT-1 at P ranks: time-to-solution (tol 1e-10, TGV pressure RHS) of
     Jacobi-PCG, Schwarz flexible PCG and Schwarz flexible GMRES(30); the
@@ -422,6 +477,9 @@ if __name__ == "__main__":
         sweep([int(v) for v in sys.argv[2].split(",")])
     elif mode == "c5":
         c5([int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else range(1, 12))
+    elif mode in ("c5_strong", "c5_weak"):   # torchrun: C5 scaling at ~1e9 DOF
+        c5_scale([int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else (3, 7, 11),
+                 mode[3:])
     elif mode == "schwarz_strong":
         schwarz_strong(tuple(sys.argv[2].split(",")) if len(sys.argv) > 2 else ("C3", "C4"))
     elif mode == "schwarz":
