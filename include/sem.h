@@ -281,7 +281,8 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    coarse CG step exchanges and allreduces), 1 = replicated (one all-gather of
    the restricted right-hand side, then every rank solves the whole N = 1
    problem; needs an even element partition), -1 (default) = auto (replicated
-   when the coarse problem has <= 2^20 slots).  Collective. */
+   when the coarse problem has <= 2^26 slots, the bound of the assembled
+   coarse operator).  Collective. */
 #define SEM_OPT_COARSE_REPLICATE 11
 /* Jacobi-PCG recurrences of sem_pcg_solve / sem_helm_pcg_solve /
    sem_pcg_solve_host: 0 (default) = standard (two reductions per iteration),

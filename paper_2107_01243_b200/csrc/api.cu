@@ -1195,7 +1195,11 @@ static int pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t m
 // of the ten coarse CG steps; graph-replayable like one rank).  Auto: when the
 // coarse problem is small (<= kReplicateSlots coarse slots) and the element
 // partition is even (equal all-gather blocks).
-constexpr int64_t kReplicateSlots = 1 << 20;
+// With the assembled coarse operator (Q35) the replicated solve is cheap up to
+// the assembly bound: C4 (2.1 M coarse slots) Schwarz PCG 134.0 -> 126.8 ms at
+// 2 GPUs, 81.7 -> 75.7 ms at 4 (profiles/r02_schwarz_scale/); it was 2^20
+// slots with the E-vector coarse CG.
+constexpr int64_t kReplicateSlots = int64_t(1) << 26;
 static bool coarse_replicated(const sem_ctx* c) {
   const sem::HostPlan& h = c->hp;
   if (h.nranks == 1 || h.E % h.nranks != 0) return false;
