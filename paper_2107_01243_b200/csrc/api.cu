@@ -198,6 +198,7 @@ struct sem_ctx {
   int64_t* d_rdelta = nullptr;
   int32_t* d_nbrs = nullptr;
   int* d_perr = nullptr;
+  uint64_t* d_xflag = nullptr;   // exchange kernel: per packer block, the epoch of its finished pack
   std::vector<char*> ipc_opened;
   uint64_t ep_gs = 0, ep_ar[sem::P2P::kSites] = {0, 0, 0, 0};
   std::vector<uint64_t> ep_ping;   // per peer: ping-pong flag epochs
@@ -549,7 +550,7 @@ void free_ctx(sem_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->h_st) cudaFreeHost(c->h_st);
   for (char* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
-  void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_perr};
+  void* p2ps[] = {c->d_mbox, c->d_peers, c->d_rdelta, c->d_nbrs, c->d_perr, c->d_xflag};
   for (void* p : p2ps)
     if (p) cudaFree(p);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
@@ -635,11 +636,14 @@ int p2p_setup(sem_ctx* c) {
   SEM_TRY(upload(&c->d_nbrs, h.nbr_rank, s));
   SEM_TRY(dalloc(&c->d_perr, 1));
   CUDA_TRY(cudaMemsetAsync(c->d_perr, 0, sizeof(int), s));
+  SEM_TRY(dalloc(&c->d_xflag, sem::P2P::kXflags));
+  CUDA_TRY(cudaMemsetAsync(c->d_xflag, 0, sizeof(uint64_t) * sem::P2P::kXflags, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   sem::P2P& p = c->p2p;
   p.P = P; p.me = me; p.nnbr = (int)h.nbr_rank.size();
   p.local = c->d_mbox; p.peers = c->d_peers; p.rdelta = c->d_rdelta; p.nbrs = c->d_nbrs;
   p.err = c->d_perr;
+  p.xflag = c->d_xflag;
   c->ep_ping.assign(P, 0);
   c->p2p_ok = true;
   return SEM_OK;

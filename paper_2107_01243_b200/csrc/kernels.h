@@ -151,6 +151,8 @@ struct P2P {
   const int64_t* rdelta = nullptr;  // [P] neighbour recv offset - own send offset
   const int32_t* nbrs = nullptr;    // [nnbr] neighbour ranks
   int* err = nullptr;               // raised on a wait timeout
+  uint64_t* xflag = nullptr;        // [kXflags] per packer block: epoch of its finished pack
+  static constexpr int kXflags = 8192;
 };
 enum ArSite { AR_SIG = 0, AR_RG = 1, AR_RES = 2, AR_MISC = 3 };
 // peer-memory allreduce fused into a CG kernel (c.P <= 1: unused): the kernel

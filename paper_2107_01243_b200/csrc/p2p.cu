@@ -45,6 +45,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // 3 unpack done, 4 end
 constexpr int kXtsBlocks = 2048;
 __device__ unsigned long long g_xts[5 * kXtsBlocks];
+#ifndef SEM_XUNPACK
+#define SEM_XUNPACK 1   // exchange kernel: the non-packer blocks unpack (0: the packers)
+#endif
 #define XTS(ph) \
   do { if (threadIdx.x == 0 && blockIdx.x < kXtsBlocks) g_xts[(ph) * kXtsBlocks + blockIdx.x] = gtimer(); } while (0)
 
@@ -70,18 +73,27 @@ __device__ __forceinline__ void pack_point(const DevPlan& P, const double* u, do
 }
 
 // the rank partials of s in ascending rank order, masked, scattered to its slots
+// (OWN: this rank's partial recomputed from its slots, in pack_point's order,
+// instead of read from part[] -- the slots are unchanged until this write)
+template <bool OWN = false>
 __device__ __forceinline__ void unpack_point(const DevPlan& P, double* u, const double* part,
                                              const P2P& c, uint64_t epoch, int apply_mask, int s) {
   const int nr = P.s_nr[s];
+  const int nl = P.s_nloc[s];
+  double self = 0.0;
+  if (OWN) {
+    self = u[P.s_slot[s]];
+    for (int x = 1; x < nl; x++) self += u[P.s_slot[(int64_t)x * P.nS + s]];
+  }
   double tot = 0.0;
   for (int x = 0; x < nr; x++) {
     const int o = P.s_off[(int64_t)x * P.nS + s];
     SEM_CHK(o < P.nbuf);
-    const double v = o < 0 ? part[s] : ll_load(mb_ll(c.local, o, epoch), (uint32_t)epoch, c.err);
+    const double v = o < 0 ? (OWN ? self : part[s])
+                           : ll_load(mb_ll(c.local, o, epoch), (uint32_t)epoch, c.err);
     tot = x == 0 ? v : tot + v;
   }
   if (apply_mask && P.s_mask[s]) tot = 0.0;
-  const int nl = P.s_nloc[s];
   for (int x = 0; x < nl; x++) u[P.s_slot[(int64_t)x * P.nS + s]] = tot;
 }
 
@@ -167,13 +179,37 @@ __global__ void __launch_bounds__(256) gs_exchange_p2p_kernel(const DevPlan P,
   const int npb = min((int)gridDim.x, (P.nS + (int)blockDim.x - 1) / (int)blockDim.x);
   const int nthp = npb * blockDim.x;
   const bool packer = blockIdx.x < npb;
-  if (packer)
+  // unpack by the non-packer blocks (they finish their local gs share first;
+  // the packers' share starts after the pack), each point once its packer block
+  // has released the epoch of its finished pack (the pack reads the slots the
+  // unpack overwrites); with no non-packer block the packers unpack their own
+  const int nun = (int)gridDim.x - npb;
+  const bool xun = SEM_XUNPACK && nun > 0 && c.xflag && npb <= P2P::kXflags;
+  if (packer) {
     for (int s = tid; s < P.nS; s += nthp) pack_point(P, u, part, c, epoch, s);
+    if (xun) {
+      // the block's slot reads have returned (their values went into the remote
+      // stores) before the barrier, so a plain flag store after it is enough for
+      // the unpacker's later overwrite; no fence (a fence here would wait for the
+      // NVLink stores: +4-5 us per pack measured).  The unpacker recomputes this
+      // rank's partial from the slots instead of reading part[].
+      __syncthreads();
+      if (threadIdx.x == 0)
+        *reinterpret_cast<volatile unsigned long long*>(&c.xflag[blockIdx.x]) = epoch;
+    }
+  }
   XTS(1);
   gs_local_body<n, SWEEP>(P, u, apply_mask, P.gs_ctr + 1, base, ce);
   XTS(2);
-  if (packer)
+  if (xun) {
+    if (!packer)
+      for (int s = (blockIdx.x - npb) * blockDim.x + threadIdx.x; s < P.nS; s += nun * blockDim.x) {
+        wait_flag(&c.xflag[(s % nthp) / blockDim.x], epoch, c.err);
+        unpack_point<true>(P, u, part, c, epoch, apply_mask, s);
+      }
+  } else if (packer) {
     for (int s = tid; s < P.nS; s += nthp) unpack_point(P, u, part, c, epoch, apply_mask, s);
+  }
   XTS(3);
   XTS(4);
 }
