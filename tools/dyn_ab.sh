@@ -1,3 +1,5 @@
+# HISTORICAL: the dynamic-unit and static variants measured here were removed after this A/B
+# (profiles/r02_experiments/dyn_units/README.md); the SEM_GS_DYN* macros no longer exist.
 # 2-GPU A/B of the exchange kernel's local gs schedule: dynamic units with
 # F = 2 (default build) / F = 1, and the static flat split (gpurun --gpus 2)
 O=gpurun_out/${DYN_TAG:-dyn1}
