@@ -302,10 +302,12 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    CUDA graph (cached per x / Jacobi operand) and replayed; 0 = stream
    launches.  Identical results. */
 #define SEM_OPT_PCG_GRAPH 14
-/* 1 (default) = on one rank, Jacobi-PCG fuses the p update p = dinv r + beta p
-   into the next iteration's Ax kernel (which streams p, r, dinv and writes p)
-   and x += alpha p into the r update: three kernels per iteration (Ax, gs,
-   update) instead of four; 0 = separate p kernel.  Same arithmetic (each
+/* 1 (default) = Jacobi-PCG fuses the p update p = dinv r + beta p into the
+   next iteration's Ax kernel (which streams p, r, dinv and writes p) and
+   x += alpha p into the r update: three kernels per iteration (Ax, gs or the
+   exchange kernel, update; at nranks > 1 over NCCL / loopback a one-thread
+   kernel ends the iteration after the allreduce) instead of four; 0 =
+   separate p kernel.  Same arithmetic (each
    value is computed by the same expression), iterates equal up to the
    sigma partial-sum order. */
 #define SEM_OPT_PCG_FUSE 15

@@ -267,7 +267,7 @@ class Context:
         _check(load().sem_set_option(self._h, 14, 1 if on else 0))
 
     def set_pcg_fuse(self, on: bool):
-        """One rank: p update fused into the next Ax kernel (default on)."""
+        """p update fused into the next Ax kernel, x into the r update (default on)."""
         _check(load().sem_set_option(self._h, 15, 1 if on else 0))
 
     def set_pcg_gsu(self, mode):

@@ -136,7 +136,7 @@ struct sem_ctx {
   sem::CoarseCg* d_ccg = nullptr;
   bool ax_pdl = true;      // SEM_OPT_AX_PDL (C2: 123.0 -> 121.6 us per PCG iteration)
   bool ax_pdl_now = false; // set around the PCG iteration's Ax launch
-  // SEM_OPT_PCG_FUSE: one-rank Jacobi-PCG with the p update fused into the Ax
+  // SEM_OPT_PCG_FUSE: Jacobi-PCG (every P) with the p update fused into the Ax
   // kernel (and x += alpha p into the CG update): three kernels per iteration
   bool pcg_fuse = true;
   bool pf_now = false;            // set around the PCG iteration's Ax launch
