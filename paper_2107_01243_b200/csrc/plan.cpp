@@ -96,6 +96,21 @@ static inline void ecoords(const sem_mesh& m, int64_t e, int64_t c[3]) {
   c[2] = e / ((int64_t)m.ex * m.ey);
 }
 
+// insertion sort of the <= 8 incidences / ranks of one entity (std::sort's
+// 16-element insertion threshold trips -Warray-bounds on the fixed arrays)
+template <typename T, typename Less>
+static void small_sort(T* a, int n, Less less) {
+  for (int x = 1; x < n; x++) {
+    T v = a[x];
+    int y = x - 1;
+    while (y >= 0 && less(v, a[y])) {
+      a[y + 1] = a[y];
+      y--;
+    }
+    a[y + 1] = v;
+  }
+}
+
 int64_t lattice_gid(const HostPlan& p, int64_t e, int i, int j, int k) {
   int64_t c[3];
   ecoords(p.m, e, c);
@@ -255,7 +270,7 @@ static int incidences(const sem_mesh& m, const int64_t c[3], const LocalEnt& L, 
         for (int a = 0; a < 3; a++) I.side[a] = K.side[a];
         I.lid = encode(K);
       }
-  std::sort(out, out + cnt, [](const Inc& a, const Inc& b) { return a.e < b.e; });
+  small_sort(out, cnt, [](const Inc& a, const Inc& b) { return a.e < b.e; });
   return cnt;
 }
 
@@ -429,7 +444,7 @@ int build_plan(const sem_mesh* mp, int N, HostPlan* P) {
           if (!seen) ranks[nr++] = r;
           if (inc[t].e >= p.e_lo && inc[t].e < p.e_hi) boundary[inc[t].e - p.e_lo] = 1;
         }
-        std::sort(ranks, ranks + nr);
+        small_sort(ranks, nr, [](int a, int b) { return a < b; });
         for (int pt = 0; pt < npts; pt++) {
           SP s{};
           s.nloc = 0;
