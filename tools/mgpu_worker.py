@@ -14,11 +14,53 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2107_01243_b200 as sem  # noqa: E402
 from mgpu_common import CASES, OracleRefs, case_field, check, rank_run, rank_slice  # noqa: E402
+from sem_inputs import random_field  # noqa: E402
+
+
+def bench_config_check(rank, P, comm):
+    """The bench's own multi-GPU configuration (C2 per GPU, weak-scaled along z,
+    peer-memory transport, graph-replayed PCG with device-side epochs): the
+    operator on a seeded random field normwise within 1e-12 of the oracle run
+    with the same number of ranks, and 3 fixed PCG iterations (tol 0) on b = A u
+    within 1e-10 of the oracle's iterate."""
+    from sem_inputs import CONFIGS, weak_scaled
+    spec = weak_scaled(CONFIGS["C2"][0], P)
+    N = CONFIGS["C2"][1]
+    u = random_field(spec.E * (N + 1) ** 3, seed=2024)
+    lo, hi = rank_slice(spec, N, rank, P)
+    fails = []
+    with sem.sem_setup(spec, N, rank=rank, nranks=P, nccl_comm=comm) as c:
+        du = torch.from_numpy(u[lo:hi]).cuda()
+        w = c.zeros()
+        c.apply(du, w)
+        x = c.zeros()
+        r = c.pcg_solve(w, x, 0.0, 3)
+        torch.cuda.synchronize()
+        out = {"w": w.cpu().numpy(), "x": x.cpu().numpy(), "iters": r["iters"]}
+    parts = [None] * P
+    dist.all_gather_object(parts, out)
+    if rank == 0:
+        import oracle as O
+        o = O.Oracle(spec, N, nranks=P)
+        wr = o.apply(u)
+        W = np.concatenate([p["w"] for p in parts])
+        e = np.abs(W - wr).max() / np.abs(wr).max()
+        if not e <= 1e-12:
+            fails.append(f"bench config P={P}: apply rel err {e:.2e}")
+        ref = o.pcg(wr, 0.0, 3)
+        X = np.concatenate([p["x"] for p in parts])
+        dx = np.abs(X - ref["x"]).max()
+        if parts[0]["iters"] != 3 or not dx <= 1e-10:
+            fails.append(f"bench config P={P}: 3 PCG iterations x diff {dx:.2e}")
+        print(f"bench config P={P} ({spec.ex}x{spec.ey}x{spec.ez}, N={N}): apply rel err {e:.2e}, "
+              f"3-iteration PCG max |dx| {dx:.2e}", flush=True)
+    return fails
 
 
 def failure_path(rank, P, comm):
@@ -75,6 +117,7 @@ def main():
                     fails += f
                     print(f"{tag}: {'FAIL' if f else 'ok'} pcg iters {out['r']['iters']} "
                           f"(oracle {ref.pcg['iters']})", flush=True)
+    fails += bench_config_check(rank, P, comm)
     fails += failure_path(rank, P, comm)
     sem.nccl_comm_destroy(comm)
     dist.barrier()
