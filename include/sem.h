@@ -327,6 +327,11 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    E-vector slots (also beyond 2^26 coarse slots).  Same iterates in exact
    arithmetic (reading Q35). */
 #define SEM_OPT_COARSE_ASM 17
+/* 1 (default) = on one rank with the flat gather-scatter schedule, the kernels
+   of each batch of 8 flexible-PCG (Schwarz) iterations, the coarse solve
+   included, are captured once into a CUDA graph and replayed; 0 = stream
+   launches.  Identical results. */
+#define SEM_OPT_SCHWARZ_GRAPH 18
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

@@ -297,6 +297,10 @@ class Context:
         (True / -1 auto, the default) or on the element operator + gs (False)."""
         _check(load().sem_set_option(self._h, 17, -1 if mode == -1 else (1 if mode else 0)))
 
+    def set_schwarz_graph(self, on: bool):
+        """One rank: replay 8-iteration Schwarz flexible-PCG batches as a CUDA graph (default on)."""
+        _check(load().sem_set_option(self._h, 18, 1 if on else 0))
+
     def set_coarse_iters(self, k: int):
         """Maximum CG iterations of the Schwarz coarse solve (default 10)."""
         _check(load().sem_set_option(self._h, 7, int(k)))

@@ -154,6 +154,13 @@ struct sem_ctx {
   bool pcg_graph = true;
   cudaGraphExec_t pg_exec = nullptr;
   double pg_key[4] = {0, 0, 0, 0};
+  // SEM_OPT_SCHWARZ_GRAPH: one-rank flexible-PCG (Schwarz) batches replayed as a
+  // CUDA graph (the coarse solve's kernels inlined into it)
+  bool sw_graph = true;
+  bool sw_capturing = false;
+  cudaGraphExec_t sw_exec = nullptr;
+  double sw_key[6] = {0, 0, 0, 0, 0, 0};
+  int64_t sw_launches = 0;
   int64_t pg_launches = 0;
   int g0_iters = -1;
   int64_t g0_launches = 0;
@@ -546,6 +553,7 @@ void free_ctx(sem_ctx* c) {
   if (c->c0) free_ctx(c->c0);
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
+  if (c->sw_exec) cudaGraphExecDestroy(c->sw_exec);
   if (c->d_gate) cudaFree(c->d_gate);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -1409,6 +1417,8 @@ static void schwarz_drop_coarse(sem_ctx* c) {
     if (p) cudaFree(p);
   c->d_b0 = c->d_x0 = c->d_dinv0 = nullptr;
   casm_free(c);
+  if (c->sw_exec) cudaGraphExecDestroy(c->sw_exec);
+  c->sw_exec = nullptr;
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   c->g0exec = nullptr;
   c->g0_iters = -1;
@@ -1452,7 +1462,9 @@ static int coarse_body(sem_ctx* c, const int* gate) {
 }
 
 static int coarse_solve(sem_ctx* c, const int* gate) {
-  if (c->c0->hp.nranks > 1 || !c->coarse_graph || c->timing) return coarse_body(c, gate);
+  // (inside the captured Schwarz batch the coarse kernels are captured inline)
+  if (c->c0->hp.nranks > 1 || !c->coarse_graph || c->timing || c->sw_capturing)
+    return coarse_body(c, gate);
   cudaStream_t s = c->stream;
   if (!c->g0exec || c->g0_iters != c->coarse_iters) {
     if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
@@ -1535,6 +1547,59 @@ static int schwarz_apply(sem_ctx* c, const double* r, double* z, int which, cons
 
 // flexible PCG with the Schwarz preconditioner (reading Q32); scalars stay on
 // the device, the host polls every kBatch iterations
+// One rank, flat gather-scatter schedule: the kernels of kBatch flexible-PCG
+// iterations (operator, gs, scalar and vector kernels, the preconditioner with
+// its coarse solve inlined) have fixed arguments, so the batch is captured once
+// and replayed (SEM_OPT_SCHWARZ_GRAPH); keyed by x and the preconditioner's
+// configuration.  nullptr: plain stream launches.
+template <class F>
+static cudaGraphExec_t schwarz_batch_graph(sem_ctx* c, double* x, F& iteration) {
+  if (!c->sw_graph || c->hp.nranks > 1 || c->timing || !sem::gs_flat(c->dp, c->gs_mode) ||
+      !c->c0 || c->c0->hp.nranks > 1 || !sem::gs_flat(c->c0->dp, c->c0->gs_mode))
+    return nullptr;
+  const double key[6] = {(double)(uintptr_t)x, (double)(uintptr_t)c->c0, (double)c->coarse_iters,
+                         c->fdm_tc ? 1.0 : 0.0, (c->casm_ok && c->coarse_asm != 0) ? 1.0 : 0.0,
+                         (double)(uintptr_t)c->d_b0};
+  if (c->sw_exec && std::memcmp(key, c->sw_key, sizeof(key)) == 0) return c->sw_exec;
+  if (c->sw_exec) cudaGraphExecDestroy(c->sw_exec);
+  c->sw_exec = nullptr;
+  if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaStream_t s_save = c->stream, s0_save = c->c0->stream;
+  c->stream = c->c0->stream = c->cap_stream;
+  c->sw_capturing = true;
+  const int64_t l_c = c->launches, l_c0 = c->c0->launches;
+  cudaGraph_t graph = nullptr;
+  int st = SEM_OK;
+  if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    for (int q = 0; q < kBatch && st == SEM_OK; q++) st = iteration();
+    if (cudaStreamEndCapture(c->cap_stream, &graph) != cudaSuccess) st = SEM_ECUDA;
+  } else {
+    st = SEM_ECUDA;
+  }
+  c->sw_capturing = false;
+  c->stream = s_save;
+  c->c0->stream = s0_save;
+  // kernels per replay (the coarse context's counted into this one's); the
+  // capture itself launched nothing
+  c->sw_launches = (c->launches - l_c) + (c->c0->launches - l_c0);
+  c->launches = l_c;
+  c->c0->launches = l_c0;
+  cudaGraphExec_t ge = nullptr;
+  if (st == SEM_OK && graph && cudaGraphInstantiate(&ge, graph, 0) != cudaSuccess) ge = nullptr;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (!ge) {
+    c->sw_graph = false;   // not capturable here: stream launches from now on
+    return nullptr;
+  }
+  c->sw_exec = ge;
+  std::memcpy(c->sw_key, key, sizeof(key));
+  return ge;
+}
+
 static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit,
                            sem_pcg_result* res) {
   if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
@@ -1571,9 +1636,8 @@ static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, i
   CUDA_TRY(sem::launch_fcg_scalar(0, st, c->d_hist, s));
   c->launches += 2;
   int hd = 0;
-  for (int it = 0; it < maxit && !hd; it += kBatch) {
-    const int nb = std::min(kBatch, maxit - it);
-    for (int q = 0; q < nb; q++) {
+  auto iteration = [&]() -> int {
+      cudaStream_t s = c->stream;   // (the capture stream while a batch is captured)
       if (!dist) {
         // w = A p with sigma = sum_l p_l (A_L p)_l reduced by the Ax kernel itself
         // (reading Q23: equals <p, w>_c for the continuous, masked p)
@@ -1600,6 +1664,16 @@ static int schwarz_pcg_run(sem_ctx* c, const double* b, double* x, double tol, i
       CUDA_TRY(sem::launch_fcg_scalar(3, st, c->d_hist, s));       // beta
       CUDA_TRY(sem::launch_xpay(n, p, z, st, sms, s));              // p = z + beta p
       c->launches += 7;
+      return SEM_OK;
+  };
+  for (int it = 0; it < maxit && !hd; it += kBatch) {
+    const int nb = std::min(kBatch, maxit - it);
+    cudaGraphExec_t ge = nb == kBatch ? schwarz_batch_graph(c, x, iteration) : nullptr;
+    if (ge) {
+      CUDA_TRY(cudaGraphLaunch(ge, s));
+      c->launches += c->sw_launches;
+    } else {
+      for (int q = 0; q < nb; q++) SEM_TRY(iteration());
     }
     CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, done, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -2175,6 +2249,13 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     c->pcg_fuse = value != 0;
     if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
     c->pg_exec = nullptr;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_SCHWARZ_GRAPH) {
+    cudaStreamSynchronize(c->stream);
+    c->sw_graph = value != 0;
+    if (c->sw_exec) cudaGraphExecDestroy(c->sw_exec);
+    c->sw_exec = nullptr;
     return SEM_OK;
   }
   if (option == SEM_OPT_PCG_GSU) {

@@ -328,3 +328,31 @@ def test_coarse_assembled_operator(spec, N):
         for asm, (rr, x) in res.items():
             assert rr["status"] == 0 and abs(rr["iters"] - ref["iters"]) <= 1, (asm, rr, ref["iters"])
             assert np.abs(x - ref["x"]).max() <= 1e-10, asm
+
+
+@pytest.mark.parametrize("spec,N", [(tgv_box(4, 3, 5, deform=1), 7), (unit_box(3, 2, 5, periodic=(1, 0, 0)), 7),
+                                    (CONFIGS["C1"][0], 3), (tgv_box(2, 2, 2), 1), (unit_box(2, 3, 2), 10)])
+def test_schwarz_graph_identical(spec, N):
+    """SEM_OPT_SCHWARZ_GRAPH: 8-iteration flexible-PCG batches captured once (the
+    coarse solve inlined) and replayed give bitwise the stream-launched iterates,
+    with either coarse form, and match the oracle."""
+    o = O.Oracle(spec, N)
+    b = _rhs(o)
+    ref = o.schwarz(10).pcg(b, 1e-10, 500)
+    with sem().sem_setup(spec, N) as c:
+        c.set_precond("schwarz")
+        for asm in (True, False):
+            c.set_coarse_asm(asm)
+            out = {}
+            for graph in (True, False):
+                c.set_schwarz_graph(graph)
+                x = c.zeros()
+                r = c.pcg_solve(dev(b), x, 1e-10, 500)
+                out[graph] = (host(x), r)
+            (x1, r1), (x0, r0) = out[True], out[False]
+            assert r1["iters"] == r0["iters"] and r1["res_final"] == r0["res_final"], (asm, r1, r0)
+            assert np.array_equal(x1, x0), asm
+            assert r1["status"] == 0 and abs(r1["iters"] - ref["iters"]) <= 1
+            assert np.abs(x1 - ref["x"]).max() <= 1e-10
+        c.set_coarse_asm(-1)
+        c.set_schwarz_graph(True)

@@ -144,6 +144,8 @@ def schwarz(cfgs=("C3", "C4")):
             n = c.n_local
             if os.environ.get("COARSE_ASM") == "0":   # A/B: element-operator coarse CG
                 c.set_coarse_asm(False)
+            if os.environ.get("SCHWARZ_GRAPH") == "0":   # A/B: stream-launched Schwarz batches
+                c.set_schwarz_graph(False)
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
