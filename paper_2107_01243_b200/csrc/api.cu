@@ -1220,6 +1220,9 @@ static bool coarse_replicated(const sem_ctx* c) {
 }
 
 static int coarse_assemble(sem_ctx* c);
+#ifndef SEM_COARSE_CLUSTER
+#define SEM_COARSE_CLUSTER 1   // small assembled coarse problems on one thread-block cluster
+#endif
 
 static int schwarz_setup(sem_ctx* c) {
   if (c->c0) return SEM_OK;
@@ -1439,8 +1442,12 @@ static int coarse_body(sem_ctx* c, const int* gate) {
   sem_ctx* c0 = c->c0;
   cudaStream_t s = c0->stream;
   if (c->casm_ok && c->coarse_asm != 0) {   // assembled operator on the unique vertices
-    CUDA_TRY(sem::launch_coarse_asm_solve(c->casm, c->d_b0, c->d_x0, gate, c->coarse_iters, 1e-12,
-                                          c->casm_grid, s, &c0->launches));
+    if (SEM_COARSE_CLUSTER && sem::coarse_asm_cluster_ok(c->casm.nu))   // one 8-CTA cluster
+      CUDA_TRY(sem::launch_coarse_asm_cluster(c->casm, c->d_b0, c->d_x0, gate, c->coarse_iters,
+                                              1e-12, s, &c0->launches));
+    else
+      CUDA_TRY(sem::launch_coarse_asm_solve(c->casm, c->d_b0, c->d_x0, gate, c->coarse_iters,
+                                            1e-12, c->casm_grid, s, &c0->launches));
     return SEM_OK;
   }
   SEM_TRY(gs_op(c0, c->d_b0, 1));

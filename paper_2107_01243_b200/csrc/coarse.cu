@@ -155,7 +155,136 @@ __global__ void __launch_bounds__(kCT) casm_scatter_kernel(const CoarseAsm A, do
   }
 }
 
+// ---- small coarse problems: the whole solve on ONE thread-block cluster
+// (SEM_COARSE_CLUSTER): kCC CTAs of kCT2 threads, hardware cluster barriers
+// between the phases, reductions through distributed shared memory (every CTA
+// sums the CTAs' partials in rank order, so all take the same scalars and the
+// same branch).  The unknowns' vectors stay in global memory (L2-resident).
+constexpr int kCC = 8, kCT2 = 1024;
+
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ double cl_ld_remote(const double* local, unsigned rank) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+  return v;
+}
+// cluster total of v (slot h of the partial array); identical in every CTA
+__device__ __forceinline__ double cl_reduce(double v, double* s_part, int h, double* scratch,
+                                            double* s_tot) {
+  const double bs = block_sum(v, scratch);
+  if (threadIdx.x == 0) s_part[h] = bs;
+  cl_sync();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned q = 0; q < kCC; q++) t += cl_ld_remote(&s_part[h], q);
+    *s_tot = t;
+  }
+  __syncthreads();
+  return *s_tot;
+}
+
+__global__ void __launch_bounds__(kCT2) casm_cluster_kernel(const CoarseAsm A, const double* __restrict__ b0,
+                                                            double* __restrict__ x0, const int* gate,
+                                                            int maxit, double rtol) {
+  __shared__ double scratch[32];
+  __shared__ double s_part[2];
+  __shared__ double s_tot;
+  if (gate && *gate) return;   // every CTA of the cluster alike
+  const int tid = (int)cl_rank() * blockDim.x + threadIdx.x, nth = kCC * blockDim.x;
+  int h = 0;
+  double s = 0.0;
+  for (int g = tid; g < A.nu; g += nth) {
+    const int q0 = A.u2s_ptr[g], q1 = A.u2s_ptr[g + 1];
+    SEM_CHK(q1 > q0 && q1 - q0 <= 8);
+    double v = b0[A.u2s[q0]];
+    for (int q = q0 + 1; q < q1; q++) v += b0[A.u2s[q]];
+    A.b[g] = v;
+    s += v;
+  }
+  const double sum = cl_reduce(s, s_part, h, scratch, &s_tot);
+  h ^= 1;
+  const double mean = A.periodic ? sum / (double)A.nu : 0.0;
+  double gg = 0.0;
+  for (int g = tid; g < A.nu; g += nth) {
+    const double r = A.b[g] - mean;
+    A.r[g] = r;
+    A.p[g] = r;
+    A.x[g] = 0.0;
+    gg = fma(r, r, gg);
+  }
+  double gamma = cl_reduce(gg, s_part, h, scratch, &s_tot);
+  h ^= 1;
+  const double tol = rtol * sqrt(gamma);
+  const bool run = !(sqrt(gamma) <= tol) && maxit > 0;
+  for (int it = 0; run && it < maxit; it++) {
+    double sg = 0.0;
+    for (int g = tid; g < A.nu; g += nth) {
+      double acc = 0.0;
+      for (int k = 0; k < A.K; k++) {
+        const int64_t e = (int64_t)k * A.nu + g;
+        acc = fma(A.val[e], A.p[A.col[e]], acc);
+      }
+      A.q[g] = acc;
+      sg = fma(A.p[g], acc, sg);
+    }
+    const double sigma = cl_reduce(sg, s_part, h, scratch, &s_tot);
+    h ^= 1;
+    if (!(sigma > 0.0)) break;   // breakdown: keep the current iterate
+    const double alpha = gamma / sigma;
+    double gn = 0.0;
+    for (int g = tid; g < A.nu; g += nth) {
+      A.x[g] = fma(alpha, A.p[g], A.x[g]);
+      const double r = fma(-alpha, A.q[g], A.r[g]);
+      A.r[g] = r;
+      gn = fma(r, r, gn);
+    }
+    const double gnew = cl_reduce(gn, s_part, h, scratch, &s_tot);
+    h ^= 1;
+    if (!(gnew == gnew) || sqrt(gnew) <= tol || it + 1 >= maxit) break;
+    const double beta = gnew / gamma;
+    gamma = gnew;
+    for (int g = tid; g < A.nu; g += nth) A.p[g] = fma(beta, A.p[g], A.r[g]);
+    cl_sync();   // p complete before the next product
+  }
+  cl_sync();     // x complete (and no CTA exits while others read its shared partials)
+  for (int64_t q = tid; q < A.n0; q += nth) {
+    const int g = A.uidx[q];
+    x0[q] = g >= 0 ? A.x[g] : 0.0;
+  }
+}
+
 }  // namespace dev
+
+bool coarse_asm_cluster_ok(int nu) { return nu <= kCoarseClusterMax; }
+
+cudaError_t launch_coarse_asm_cluster(const CoarseAsm& A, const double* b0, double* x0,
+                                      const int* gate, int maxit, double rtol, cudaStream_t s,
+                                      int64_t* launches) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(dev::kCC);
+  cfg.blockDim = dim3(dev::kCT2);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = dev::kCC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (launches) *launches += 1;
+  return cudaLaunchKernelEx(&cfg, dev::casm_cluster_kernel, A, b0, x0, gate, maxit, rtol);
+}
 
 int coarse_asm_grid(int nu, int num_sms) {
   const int g = (nu + dev::kCT - 1) / dev::kCT;

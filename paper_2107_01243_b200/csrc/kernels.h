@@ -249,6 +249,12 @@ struct CoarseAsm {
   CoarseCg* st = nullptr;
 };
 int coarse_asm_grid(int nu, int num_sms);
+// small coarse problems (nu <= kCoarseClusterMax): the whole solve on one 8-CTA cluster
+constexpr int kCoarseClusterMax = 1 << 14;   // C2 (8192): 0.232 -> 0.189 ms; C3 (32768): 0.315 -> 0.373, slower
+bool coarse_asm_cluster_ok(int nu);
+cudaError_t launch_coarse_asm_cluster(const CoarseAsm& A, const double* b0, double* x0,
+                                      const int* gate, int maxit, double rtol, cudaStream_t s,
+                                      int64_t* launches);
 // x0 = A0^-1 b0 by <= maxit CG steps on the assembled operator (b0, x0: E-vectors)
 cudaError_t launch_coarse_asm_solve(const CoarseAsm& A, const double* b0, double* x0,
                                     const int* gate, int maxit, double rtol, int grid,
