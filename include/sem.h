@@ -323,7 +323,9 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
 /* Schwarz coarse solve when the coarse level is single-rank (one rank, or
    the replicated level): -1 (default) / 1 = CG on the ASSEMBLED N = 1 operator
    over the unique unmasked vertices (ELL, built once at Schwarz setup from the
-   element matrices), 0 = CG on the element operator + gather-scatter over the
+   element matrices; up to 2^14 unknowns the whole solve runs on one 8-CTA
+   thread-block cluster), 2 = the assembled operator always with the
+   multi-kernel solve, 0 = CG on the element operator + gather-scatter over the
    E-vector slots (also beyond 2^26 coarse slots).  Same iterates in exact
    arithmetic (reading Q35). */
 #define SEM_OPT_COARSE_ASM 17

@@ -294,8 +294,10 @@ class Context:
 
     def set_coarse_asm(self, mode):
         """Single-rank Schwarz coarse level: CG on the assembled N = 1 operator
-        (True / -1 auto, the default) or on the element operator + gs (False)."""
-        _check(load().sem_set_option(self._h, 17, -1 if mode == -1 else (1 if mode else 0)))
+        (True / -1 auto, the default; small problems on one thread-block cluster),
+        2 = assembled with the multi-kernel solve, or on the element operator + gs (False)."""
+        v = mode if mode in (-1, 2) else (1 if mode else 0)
+        _check(load().sem_set_option(self._h, 17, v))
 
     def set_schwarz_graph(self, on: bool):
         """One rank: replay 8-iteration Schwarz flexible-PCG batches as a CUDA graph (default on)."""

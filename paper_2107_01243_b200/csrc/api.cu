@@ -1442,7 +1442,7 @@ static int coarse_body(sem_ctx* c, const int* gate) {
   sem_ctx* c0 = c->c0;
   cudaStream_t s = c0->stream;
   if (c->casm_ok && c->coarse_asm != 0) {   // assembled operator on the unique vertices
-    if (SEM_COARSE_CLUSTER && sem::coarse_asm_cluster_ok(c->casm.nu))   // one 8-CTA cluster
+    if (SEM_COARSE_CLUSTER && c->coarse_asm != 2 && sem::coarse_asm_cluster_ok(c->casm.nu))
       CUDA_TRY(sem::launch_coarse_asm_cluster(c->casm, c->d_b0, c->d_x0, gate, c->coarse_iters,
                                               1e-12, s, &c0->launches));
     else
@@ -2316,8 +2316,8 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     return SEM_OK;
   }
   if (option == SEM_OPT_COARSE_ASM) {
-    if (value < -1 || value > 1) {
-      sem::set_error("sem_set_option: SEM_OPT_COARSE_ASM must be -1, 0 or 1");
+    if (value < -1 || value > 2) {
+      sem::set_error("sem_set_option: SEM_OPT_COARSE_ASM must be -1, 0, 1 or 2");
       return SEM_EINVAL;
     }
     cudaStreamSynchronize(c->stream);

@@ -314,7 +314,7 @@ def test_coarse_assembled_operator(spec, N):
     with sem().sem_setup(spec, N) as c:
         c.set_precond("schwarz")
         zs, res = {}, {}
-        for asm in (True, False):
+        for asm in (True, 2, False):   # cluster (small problems), multi-kernel, element form
             c.set_coarse_asm(asm)
             z = c.zeros()
             c.schwarz_apply(dev(r), z, 2)
@@ -325,6 +325,7 @@ def test_coarse_assembled_operator(spec, N):
         c.set_coarse_asm(-1)
         scale = max(np.abs(zs[False]).max(), 1e-300)
         assert np.abs(zs[True] - zs[False]).max() <= 1e-12 * scale + 1e-300
+        assert np.abs(zs[2] - zs[False]).max() <= 1e-12 * scale + 1e-300
         for asm, (rr, x) in res.items():
             assert rr["status"] == 0 and abs(rr["iters"] - ref["iters"]) <= 1, (asm, rr, ref["iters"])
             assert np.abs(x - ref["x"]).max() <= 1e-10, asm
