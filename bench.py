@@ -108,8 +108,8 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, indices, settle=1.0):
-        self.indices, self.proc, self.settle = indices, None, settle
+    def __init__(self, indices, settle=0.5):
+        self.indices, self.proc, self.settle, self.first = indices, None, settle, []
 
     def __enter__(self):
         if not self.indices:
@@ -119,6 +119,12 @@ class Clocks:
                 ["nvidia-smi", "--id=" + ",".join(str(i) for i in self.indices),
                  f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # wait until the sampler has initialised (its first rows are out), so
+            # the NVML start-up cannot overlap the timed region
+            import select
+            if select.select([self.proc.stdout], [], [], 15.0)[0]:
+                for _ in self.indices:
+                    self.first.append(self.proc.stdout.readline())
             time.sleep(self.settle)
         except Exception:
             self.proc = None
@@ -135,7 +141,7 @@ class Clocks:
         except Exception:
             self.proc.kill()
             out = ""
-        for line in out.splitlines():
+        for line in self.first + out.splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 9:
                 self.rows.append(parts)
