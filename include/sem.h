@@ -334,6 +334,12 @@ int sem_p2p_write_bw(sem_ctx* c, int peer, int64_t bytes, int reps, double* gbps
    included, are captured once into a CUDA graph and replayed; 0 = stream
    launches.  Identical results. */
 #define SEM_OPT_SCHWARZ_GRAPH 18
+/* 1 (default) = on one rank with the flat gather-scatter schedule, each GMRES
+   restart cycle (restart residual, the m Arnoldi steps with their
+   preconditioner applications, the least-squares update) is captured once
+   into a CUDA graph and replayed; 0 = stream launches (polling every 8
+   steps).  Identical results. */
+#define SEM_OPT_GMRES_GRAPH 19
 int sem_set_option(sem_ctx* c, int option, int value);
 
 const char* sem_last_error(void);

@@ -303,6 +303,10 @@ class Context:
         """One rank: replay 8-iteration Schwarz flexible-PCG batches as a CUDA graph (default on)."""
         _check(load().sem_set_option(self._h, 18, 1 if on else 0))
 
+    def set_gmres_graph(self, on: bool):
+        """One rank: replay GMRES restart cycles as CUDA graphs (default on)."""
+        _check(load().sem_set_option(self._h, 19, 1 if on else 0))
+
     def set_coarse_iters(self, k: int):
         """Maximum CG iterations of the Schwarz coarse solve (default 10)."""
         _check(load().sem_set_option(self._h, 7, int(k)))

@@ -161,6 +161,11 @@ struct sem_ctx {
   cudaGraphExec_t sw_exec = nullptr;
   double sw_key[6] = {0, 0, 0, 0, 0, 0};
   int64_t sw_launches = 0;
+  // SEM_OPT_GMRES_GRAPH: one-rank GMRES restart cycles replayed as a CUDA graph
+  bool gm_graph = true;
+  cudaGraphExec_t gm_exec = nullptr;
+  double gm_key[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t gm_launches = 0;
   int64_t pg_launches = 0;
   int g0_iters = -1;
   int64_t g0_launches = 0;
@@ -554,6 +559,7 @@ void free_ctx(sem_ctx* c) {
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
   if (c->sw_exec) cudaGraphExecDestroy(c->sw_exec);
+  if (c->gm_exec) cudaGraphExecDestroy(c->gm_exec);
   if (c->d_gate) cudaFree(c->d_gate);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -1422,6 +1428,8 @@ static void schwarz_drop_coarse(sem_ctx* c) {
   casm_free(c);
   if (c->sw_exec) cudaGraphExecDestroy(c->sw_exec);
   c->sw_exec = nullptr;
+  if (c->gm_exec) cudaGraphExecDestroy(c->gm_exec);
+  c->gm_exec = nullptr;
   if (c->g0exec) cudaGraphExecDestroy(c->g0exec);
   c->g0exec = nullptr;
   c->g0_iters = -1;
@@ -1812,6 +1820,64 @@ static int gm_alloc(sem_ctx* c, int m) {
 }
 
 
+// One rank, flat gather-scatter schedules: a GMRES restart cycle (restart
+// residual, m Arnoldi steps with their preconditioner applications, the
+// least-squares update) has fixed kernel arguments, so it is captured once
+// (keyed by x, b, m and the preconditioner's configuration) and replayed per
+// cycle (SEM_OPT_GMRES_GRAPH); the steps after convergence are the same no-ops
+// as in stream mode.  nullptr: stream launches.
+template <class F>
+static cudaGraphExec_t gmres_cycle_graph(sem_ctx* c, double* x, const double* b, int m, bool schw,
+                                         F& cycle) {
+  if (!c->gm_graph || c->hp.nranks > 1 || c->timing || !sem::gs_flat(c->dp, c->gs_mode))
+    return nullptr;
+  if (schw && (!c->c0 || c->c0->hp.nranks > 1 || !sem::gs_flat(c->c0->dp, c->c0->gs_mode)))
+    return nullptr;
+  const double key[10] = {(double)(uintptr_t)x, (double)(uintptr_t)b, (double)m, schw ? 1.0 : 0.0,
+                          (double)(uintptr_t)c->d_V, (double)(uintptr_t)c->d_Zs,
+                          (double)(uintptr_t)c->c0, (double)c->coarse_iters,
+                          (c->fdm_tc ? 1.0 : 0.0) + ((c->casm_ok && c->coarse_asm != 0) ? 2.0 : 0.0) +
+                              (c->helm ? 4.0 : 0.0),
+                          c->helm ? c->h1 * 1e3 + c->h2 : 0.0};
+  if (c->gm_exec && std::memcmp(key, c->gm_key, sizeof(key)) == 0) return c->gm_exec;
+  if (c->gm_exec) cudaGraphExecDestroy(c->gm_exec);
+  c->gm_exec = nullptr;
+  if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaStream_t s_save = c->stream, s0_save = c->c0 ? c->c0->stream : nullptr;
+  c->stream = c->cap_stream;
+  if (c->c0) c->c0->stream = c->cap_stream;
+  c->sw_capturing = true;
+  const int64_t l_c = c->launches, l_c0 = c->c0 ? c->c0->launches : 0;
+  cudaGraph_t graph = nullptr;
+  int st = SEM_OK;
+  if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    st = cycle(false);
+    if (cudaStreamEndCapture(c->cap_stream, &graph) != cudaSuccess) st = SEM_ECUDA;
+  } else {
+    st = SEM_ECUDA;
+  }
+  c->sw_capturing = false;
+  c->stream = s_save;
+  if (c->c0) c->c0->stream = s0_save;
+  c->gm_launches = (c->launches - l_c) + (c->c0 ? c->c0->launches - l_c0 : 0);
+  c->launches = l_c;
+  if (c->c0) c->c0->launches = l_c0;
+  cudaGraphExec_t ge = nullptr;
+  if (st == SEM_OK && graph && cudaGraphInstantiate(&ge, graph, 0) != cudaSuccess) ge = nullptr;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (!ge) {
+    c->gm_graph = false;   // not capturable here: stream launches from now on
+    return nullptr;
+  }
+  c->gm_exec = ge;
+  std::memcpy(c->gm_key, key, sizeof(key));
+  return ge;
+}
+
 static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t maxit, int m,
                      sem_pcg_result* res) {
   if (maxit < 0 || !(tol >= 0.0)) { sem::set_error("bad tol/maxit"); return SEM_EINVAL; }
@@ -1851,7 +1917,10 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
   const int* done = &st->done;
   const int* cyc = &gs->cycle_done;
   int status_done = 0;
-  while (!status_done) {
+  // one restart cycle; poll: stop enqueuing once the cycle has finished (stream
+  // launches only; the captured cycle runs all m steps, finished ones no-ops)
+  auto cycle = [&](bool poll) -> int {
+    cudaStream_t s = c->stream;   // (the capture stream while a cycle is captured)
     // restart: V0 = (b - A x) / ||b - A x||_c, t = dinv V0
     {
       GateScope g(c, done);
@@ -1884,7 +1953,7 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
       CUDA_TRY(sem::launch_vnorm(n, w, Vn, schw ? nullptr : c->d_gt, dinv, gs, cyc, sms, s));
       c->launches += 6;
       if (schw && j + 1 < m) SEM_TRY(schwarz_apply(c, Vn, c->d_Zs + (size_t)(j + 1) * ld, 3, cyc, nullptr));
-      if ((j + 1) % kBatch == 0 && j + 1 < m) {   // poll: stop enqueuing a finished cycle
+      if (poll && (j + 1) % kBatch == 0 && j + 1 < m) {   // stop enqueuing a finished cycle
         int cd = 0;
         CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &gs->cycle_done, sizeof(int),
                                  cudaMemcpyDeviceToHost, s));
@@ -1903,6 +1972,16 @@ static int gmres_run(sem_ctx* c, const double* b, double* x, double tol, int32_t
                                  done, sms, s));
     CUDA_TRY(sem::launch_gm_end_cycle(gs, st, s));
     c->launches += 3;
+    return SEM_OK;
+  };
+  while (!status_done) {
+    cudaGraphExec_t ge = gmres_cycle_graph(c, x, b, m, schw, cycle);
+    if (ge) {
+      CUDA_TRY(cudaGraphLaunch(ge, s));
+      c->launches += c->gm_launches;
+    } else {
+      SEM_TRY(cycle(true));
+    }
     CUDA_TRY(cudaMemcpyAsync(&c->h_st->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     status_done = c->h_st->done;
@@ -2256,6 +2335,13 @@ extern "C" int sem_set_option(sem_ctx* c, int option, int value) {
     c->pcg_fuse = value != 0;
     if (c->pg_exec) cudaGraphExecDestroy(c->pg_exec);
     c->pg_exec = nullptr;
+    return SEM_OK;
+  }
+  if (option == SEM_OPT_GMRES_GRAPH) {
+    cudaStreamSynchronize(c->stream);
+    c->gm_graph = value != 0;
+    if (c->gm_exec) cudaGraphExecDestroy(c->gm_exec);
+    c->gm_exec = nullptr;
     return SEM_OK;
   }
   if (option == SEM_OPT_SCHWARZ_GRAPH) {

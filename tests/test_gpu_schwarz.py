@@ -357,3 +357,27 @@ def test_schwarz_graph_identical(spec, N):
             assert np.abs(x1 - ref["x"]).max() <= 1e-10
         c.set_coarse_asm(-1)
         c.set_schwarz_graph(True)
+
+
+@pytest.mark.parametrize("spec,N", [(tgv_box(4, 3, 5, deform=1), 7), (unit_box(3, 2, 5, periodic=(1, 0, 0)), 5),
+                                    (CONFIGS["C1"][0], 3), (tgv_box(2, 2, 2), 1)])
+def test_gmres_graph_identical(spec, N):
+    """SEM_OPT_GMRES_GRAPH: restart cycles captured once and replayed give bitwise
+    the stream-launched GMRES (Jacobi and Schwarz-flexible, restarts 30 and 5)."""
+    o = O.Oracle(spec, N)
+    b = _rhs(o)
+    with sem().sem_setup(spec, N) as c:
+        for pc in ("jacobi", "schwarz"):
+            c.set_precond(pc)
+            for m in (30, 5):
+                out = {}
+                for graph in (True, False):
+                    c.set_gmres_graph(graph)
+                    x = c.zeros()
+                    r = c.gmres_solve(dev(b), x, 1e-10, 2000, m)
+                    out[graph] = (host(x), r)
+                (x1, r1), (x0, r0) = out[True], out[False]
+                assert r1["status"] == 0 and r1["iters"] == r0["iters"], (pc, m, r1, r0)
+                assert r1["res_final"] == r0["res_final"] and np.array_equal(x1, x0), (pc, m)
+        c.set_gmres_graph(True)
+        c.set_precond("jacobi")

@@ -146,6 +146,8 @@ def schwarz(cfgs=("C3", "C4")):
                 c.set_coarse_asm(False)
             if os.environ.get("SCHWARZ_GRAPH") == "0":   # A/B: stream-launched Schwarz batches
                 c.set_schwarz_graph(False)
+            if os.environ.get("GMRES_GRAPH") == "0":     # A/B: stream-launched GMRES cycles
+                c.set_gmres_graph(False)
             X, Y, Z = c.coords()
             b = c.zeros()
             c.rhs(f_tgv(X, Y, Z, xp=torch), b)
