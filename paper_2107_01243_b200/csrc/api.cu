@@ -1476,9 +1476,16 @@ static int coarse_body(sem_ctx* c, const int* gate) {
   return SEM_OK;
 }
 
+static bool coarse_is_one_kernel(const sem_ctx* c) {
+  return SEM_COARSE_CLUSTER && c->casm_ok && c->coarse_asm != 0 && c->coarse_asm != 2 &&
+         sem::coarse_asm_cluster_ok(c->casm.nu);
+}
+
 static int coarse_solve(sem_ctx* c, const int* gate) {
-  // (inside the captured Schwarz batch the coarse kernels are captured inline)
-  if (c->c0->hp.nranks > 1 || !c->coarse_graph || c->timing || c->sw_capturing)
+  // (inside the captured Schwarz batch the coarse kernels are captured inline; a
+  // coarse solve that is a single cluster kernel needs no graph of its own)
+  if (c->c0->hp.nranks > 1 || !c->coarse_graph || c->timing || c->sw_capturing ||
+      coarse_is_one_kernel(c))
     return coarse_body(c, gate);
   cudaStream_t s = c->stream;
   if (!c->g0exec || c->g0_iters != c->coarse_iters) {
