@@ -381,3 +381,32 @@ def test_gmres_graph_identical(spec, N):
                 assert r1["res_final"] == r0["res_final"] and np.array_equal(x1, x0), (pc, m)
         c.set_gmres_graph(True)
         c.set_precond("jacobi")
+
+
+def test_coarse_iteration_counts_all_forms():
+    """SEM_OPT_COARSE_ITERS = 0 makes the coarse part of M r exactly zero and
+    = 1 a single CG step, identically (within rounding) in the three coarse
+    forms (one-cluster kernel, assembled multi-kernel, element operator)."""
+    spec, N = unit_box(3, 2, 5, periodic=(1, 0, 0)), 4
+    o = O.Oracle(spec, N)
+    r = assembled(o, 31)
+    with sem().sem_setup(spec, N) as c:
+        c.set_precond("schwarz")
+        for k in (0, 1, 3):
+            c.set_coarse_iters(k)
+            zs = {}
+            for asm in (True, 2, False):
+                c.set_coarse_asm(asm)
+                z = c.zeros()
+                c.schwarz_apply(dev(r), z, 2)
+                zs[asm] = host(z)
+            if k == 0:
+                for v in zs.values():
+                    assert float(np.abs(v).max()) == 0.0
+            else:
+                scale = max(np.abs(zs[False]).max(), 1e-300)
+                for asm in (True, 2):
+                    assert np.abs(zs[asm] - zs[False]).max() <= 1e-12 * scale, (k, asm)
+        c.set_coarse_iters(10)
+        c.set_coarse_asm(-1)
+        c.set_precond("jacobi")
