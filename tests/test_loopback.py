@@ -19,6 +19,7 @@ import os
 import sys
 import threading
 
+import numpy as np
 import pytest
 
 from conftest import ROOT, cuda_available
@@ -78,6 +79,66 @@ def test_loopback_multirank_parity(P, flags):
     finally:
         sem.loopback_destroy(world)
     assert not fails, fails
+
+
+@pytest.mark.gpu
+def test_loopback_bench_configuration():
+    """The bench's weak-scaled C2 workload at 2 ranks (8,192 elements of N = 7
+    per rank, 8.4 M slots) through the loopback transport: the operator on a
+    seeded random field within 1e-12 of the oracle run with 2 ranks (normwise),
+    and 3 fixed PCG iterations (tol 0, b = A u) within 1e-10 of its iterate."""
+    import threading
+
+    import torch
+
+    import oracle as O
+    import paper_2107_01243_b200 as sem
+    from mgpu_common import rank_slice
+    from sem_inputs import CONFIGS, random_field, weak_scaled
+    P = 2
+    spec, N = weak_scaled(CONFIGS["C2"][0], P), CONFIGS["C2"][1]
+    u = random_field(spec.E * (N + 1) ** 3, seed=2024)
+    outs, errs = [None] * P, [None] * P
+    world = sem.loopback_create(P, 0)
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                lo, hi = rank_slice(spec, N, r, P)
+                with sem.sem_setup(spec, N, rank=r, nranks=P, nccl_comm=sem.loopback_comm(world, r),
+                                   stream=st.cuda_stream) as c:
+                    du = torch.from_numpy(u[lo:hi]).cuda()
+                    w = c.zeros()
+                    c.apply(du, w)
+                    x = c.zeros()
+                    res = c.pcg_solve(w, x, 0.0, 3)
+                    st.synchronize()
+                    outs[r] = (w.cpu().numpy(), x.cpu().numpy(), res["iters"])
+        except BaseException as e:  # noqa: BLE001 -- reported by the main thread
+            errs[r] = e
+
+    try:
+        th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+        assert not any(t.is_alive() for t in th), "loopback ranks hung"
+    finally:
+        sem.loopback_destroy(world)
+    for e in errs:
+        if e is not None:
+            raise e
+    o = O.Oracle(spec, N, nranks=P)
+    wr = o.apply(u)
+    W = np.concatenate([q[0] for q in outs])
+    assert np.abs(W - wr).max() / np.abs(wr).max() <= 1e-12
+    ref = o.pcg(wr, 0.0, 3)
+    X = np.concatenate([q[1] for q in outs])
+    assert all(q[2] == 3 for q in outs)
+    assert np.abs(X - ref["x"]).max() <= 1e-10
 
 
 @pytest.mark.gpu
