@@ -146,6 +146,7 @@ struct sem_ctx {
   // -1 auto: when w exceeds the L2
   int pcg_gsu = -1;
   bool gsu_now = false;           // set around the PCG iteration's operator
+  bool gs_sigma_now = false;      // the gs kernel of this PCG iteration sums sigma
   int32_t* d_gu = nullptr;
   int pcg_variant = 0;     // SEM_OPT_PCG_VARIANT: 0 standard, 1 single-reduction (Chronopoulos-Gear)
   bool fdm_tc = true;   // SEM_OPT_FDM_TC: n = 8 local solves on the fp64 tensor cores (DMMA)
@@ -372,9 +373,19 @@ int exchange(sem_ctx* c) {
 
 // rank-local gather-scatter pass of the operator (masked slots are already
 // zero, so every masked entity point sums to zero)
+#ifndef SEM_GS_SIGMA
+#define SEM_GS_SIGMA 1   // one-rank fused PCG: sigma summed by the gs kernel's last block
+#endif
 int gs_pass(sem_ctx* c, double* w) {
   int tk = timer_begin(c, 4);
-  cudaError_t e = sem::launch_gs_local(c->dp, w, 0, &c->gs_base[0], c->gs_mode, c->stream);
+  sem::GsSigma sig;
+  if (c->gs_sigma_now) {
+    sig.part = c->d_partial_ax;
+    sig.count = c->d_nsig;
+    sig.st = c->d_st;
+  }
+  cudaError_t e = sem::launch_gs_local(c->dp, w, 0, &c->gs_base[0], c->gs_mode, c->stream,
+                                       c->gs_sigma_now ? &sig : nullptr);
   timer_end(c, tk);
   c->launches++;
   return check(e, "gs kernel");
@@ -940,10 +951,14 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
   c->pf_now = k.pf;
   c->pf_dinv = dinv;
   c->gsu_now = k.gu;
+  // one rank, separate gs kernel: sigma summed there, the update reads st->sigma
+  const bool gsig = SEM_GS_SIGMA && k.pf && !k.dist && !k.gu;
+  c->gs_sigma_now = gsig;
   const int sa = apply_op(c, c->d_p, c->d_wv, sem::AX_PCG);
   c->ax_pdl_now = false;
   c->pf_now = false;
   c->gsu_now = false;
+  c->gs_sigma_now = false;
   SEM_TRY(sa);
   if (k.pf) {   // r, x updates and (one rank, peer memory) the end of the iteration
     sem::PeerSync ps;
@@ -959,9 +974,9 @@ static int pcg_enqueue_iter(sem_ctx* c, const double* dinv, double* x, const Pcg
     const bool end_here = !k.dist || k.pp;
     int tk = timer_begin(c, 1);
     CUDA_TRY(sem::launch_cg_update(c->dp, c->d_mult, dinv, c->d_r, c->d_wv, c->d_partial, st,
-                                   k.rg_out, k.dist ? nullptr : c->d_partial_ax, c->d_nsig, ps,
-                                   c->red_grid, s, x, c->d_p, c->d_hist, end_here ? 1 : 0,
-                                   k.gu ? c->d_gu : nullptr));
+                                   k.rg_out, (k.dist || gsig) ? nullptr : c->d_partial_ax,
+                                   c->d_nsig, ps, c->red_grid, s, x, c->d_p, c->d_hist,
+                                   end_here ? 1 : 0, k.gu ? c->d_gu : nullptr));
     timer_end(c, tk);
     c->launches++;
     if (!end_here) {   // NCCL / loopback: reduce (rho', gamma), then end the iteration

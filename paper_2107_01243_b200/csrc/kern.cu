@@ -217,9 +217,19 @@ __global__ void mult_kernel(const DevPlan P, uint8_t* mult) {
 template <int n, bool SWEEP>
 __global__ void __launch_bounds__(256, SEM_GS_MINB) gs_local_kernel(const DevPlan P, double* __restrict__ u,
                                                        int apply_mask, unsigned long long base,
-                                                       int ce) {
+                                                       int ce, const GsSigma sig) {
   pdl_wait();
   pdl_trigger();
+  // one-rank PCG: sigma = the Ax kernel's per-CTA partials, summed here (off the
+  // CG update's critical path) by the last block, in the update's order
+  if (sig.part && blockIdx.x == gridDim.x - 1) {
+    __shared__ double scratch[32];
+    const int G = *sig.count;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(&sig.part[b]);
+    v = block_sum(v, scratch);
+    if (threadIdx.x == 0) sig.st->sigma = v;
+  }
   gs_local_body<n, SWEEP>(P, u, apply_mask, P.gs_ctr, base, ce);
 }
 
@@ -774,10 +784,11 @@ cudaError_t launch_sub_scalar(double* a, const double* scal, int64_t n, cudaStre
 }
 
 cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_t* base,
-                            int mode, cudaStream_t s) {
+                            int mode, cudaStream_t s, const GsSigma* sig_in) {
+  const GsSigma sig = sig_in ? *sig_in : GsSigma{};
   const int64_t N = P.N;
   const int64_t tot = P.nF * (N - 1) * (N - 1) + P.nEd * (N - 1) + P.nV;
-  if (tot == 0) return cudaSuccess;
+  if (tot == 0 && !sig.part) return cudaSuccess;
   // co-resident grid (x SEM_GS_GRIDX); chunk mode: blocks pull element chunks
   static std::atomic<int> cache[kMaxDev][2];
   const int dev = device_index();
@@ -804,9 +815,9 @@ cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_
   *base += (uint64_t)dev::gs_sweep_tickets(P.nloc, ce, g);
 #define GS_LAUNCH(k)                                                                        \
   return ce > 0 ? launch_k(dev::gs_local_kernel<k, true>, dim3(g), dim3(kThreads), 0, s, P, u, \
-                           apply_mask, b, ce)                                                  \
+                           apply_mask, b, ce, sig)                                             \
                 : launch_k(dev::gs_local_kernel<k, false>, dim3(g), dim3(kThreads), 0, s, P, u, \
-                           apply_mask, b, ce)
+                           apply_mask, b, ce, sig)
   switch (P.n) {
     case 2: GS_LAUNCH(2);
     case 3: GS_LAUNCH(3);

@@ -300,8 +300,15 @@ cudaError_t launch_export_mask(const DevPlan& P, uint8_t* m, cudaStream_t s);
 // gather-scatter (standalone)
 // *base: host copy of the chunk counter (advanced by the tickets the launch takes)
 // mode: 0 auto (flat while w fits in L2, else element-ordered chunks), 1 flat, 2 chunks
+// sig (one-rank PCG, SEM_GS_SIGMA): the gs kernel's last block also sums the Ax
+// kernel's sigma partials into st->sigma (the CG update's order and block size)
+struct GsSigma {
+  const double* part = nullptr;
+  const int* count = nullptr;
+  PcgState* st = nullptr;
+};
 cudaError_t launch_gs_local(const DevPlan& P, double* u, int apply_mask, uint64_t* base,
-                            int mode, cudaStream_t s);
+                            int mode, cudaStream_t s, const GsSigma* sig = nullptr);
 cudaError_t launch_gs_pack(const DevPlan& P, const double* u, double* part, double* sendbuf,
                            cudaStream_t s);
 cudaError_t launch_gs_unpack(const DevPlan& P, double* u, const double* part,
